@@ -1,0 +1,212 @@
+/*
+ * tm.h -- C ABI of the B200 hot path of arXiv 1509.04863 ("fast template
+ * matching"), Algorithm 1 FTM().
+ *
+ * Problem: given a signal x in R^N and a template t in R^K,
+ * find m = argmax_k (Tx)_k,  (Tx)_k = sum_{i<K} t_i x_{(k+i) mod N}.
+ * The method folds x through the subsampled circulant Phi for two co-prime
+ * moduli (Eq. 2, Alg. 1 step 3), correlates each fold with the template in
+ * the low-dimensional space (steps 4-6), takes the two argmaxes (step 7) and
+ * recovers the shift by the CRT (steps 8-9, Theorem 4).
+ *
+ * Conventions for every entry point
+ *   - All array arguments are DEVICE pointers on the current CUDA device,
+ *     owned by the caller (in practice torch tensors), unless the name ends
+ *     in _host.  The library never frees or retains them.
+ *   - `stream` is a cudaStream_t (0 = legacy default stream).  Every call only
+ *     enqueues work on `stream` and returns; nothing synchronises the host.
+ *   - Batches are row-major: pair b's signal starts at x + b*ldx elements.
+ *   - Return value: TM_OK, or an error code.  Argument errors are detected
+ *     synchronously before any launch and nothing is enqueued.  Asynchronous
+ *     kernel faults surface as TM_ECUDA on a later call.  tm_last_error()
+ *     returns a thread-local human-readable detail of the last failure.
+ *   - A failed match is data, not an error: k = -1 (NO_MATCH, reading C9 of
+ *     DESIGN.md) with the residues still reported.
+ *   - Plans are immutable after creation; one plan may be used concurrently
+ *     on several streams.
+ *
+ * Element types
+ *   TM_I8 : x, t int8;  y1, y2 int32 (exact);  r1, r2 int64 (exact).
+ *   TM_F32: x, t, y1, y2, r1, r2 float32.
+ *   residues int32 [batch][2];  k int64 [batch].
+ */
+#ifndef TM_H
+#define TM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tm_plan_s *tm_plan;
+
+enum { TM_I8 = 0, TM_F32 = 1 };
+
+enum {
+    TM_OK = 0,
+    TM_EINVAL = 1,        /* bad argument (see each call) */
+    TM_EUNSUPPORTED = 2,  /* valid for the paper, not supported by this build */
+    TM_ECUDA = 3,         /* CUDA error (launch or asynchronous fault) */
+};
+
+/* flags */
+#define TM_BINARY 1u  /* caller asserts every x and t entry is -1 or +1 (int8
+                         only): enables the packed +-1 fold kernel.  Passing
+                         other values with this flag gives unspecified y. */
+
+typedef struct {
+    int64_t N;          /* signal length */
+    int64_t K;          /* template length */
+    int64_t M1, M2;     /* co-prime moduli, M2 = M1 + 1 (Alg. 1 step 2) */
+    int64_t q1, q2;     /* ceil(N / Mj): terms per folded entry (Eq. 2) */
+    int64_t s1, s2;     /* qj*Mj - N: samples counted twice by the mod-N wrap (reading C5) */
+    int64_t len_y1;     /* M1 + K entries of y1 (strategy 1, D_{M+K}) */
+    int64_t len_y2;     /* M2 + K entries of y2 */
+    int64_t L1, L2;     /* transform lengths used for the correlation of y1 / y2 */
+    int32_t n_primes;   /* TM_I8: NTT primes used (1 or 2) for exact correlation */
+    int32_t dtype;      /* TM_I8 or TM_F32 */
+    uint32_t flags;
+    int32_t fast_fold;  /* 1 if the full-signal fold uses the packed +-1 kernel */
+    int64_t tf_bytes;   /* bytes of one folded template (tm_fold_template output) */
+    uint64_t seed;      /* seed of tm_generate */
+} tm_plan_info;
+
+/*
+ * tm_plan_create -- Alg. 1 step 2.
+ *   N      signal length, 1 <= N < 2^62.
+ *   K      template length, 1 <= K <= M1.
+ *   M      first modulus; 0 selects the paper's rule M1 = K.  M2 = M1 + 1.
+ *   seed   base seed of the synthetic generator tm_generate (Phi itself is
+ *          deterministic, r_k = 1 iff k mod M = 0).
+ *   dtype  TM_I8 or TM_F32.   flags  0 or TM_BINARY.
+ * Errors: TM_EINVAL if N < 1, K < 1, M1 < K, M1*M2 <= N (the minimal valid
+ * K is reported in tm_last_error), bad dtype/flags, out == NULL.
+ * TM_ECUDA if the CUDA device cannot be initialised.
+ * The plan holds only host scalars (plus one-time NTT root tables in static
+ * device memory of the library).
+ */
+int tm_plan_create(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t seed,
+                   int dtype, uint32_t flags);
+
+/* tm_plan_query -- fills *info.  TM_EINVAL on NULL arguments. */
+int tm_plan_query(tm_plan plan, tm_plan_info *info);
+
+/* Bytes of device workspace `ws` needed by tm_fold / tm_correlate / tm_run
+ * for `batch` pairs (256-byte aligned).  0 on invalid arguments. */
+size_t tm_workspace_bytes(tm_plan plan, int64_t batch);
+
+void tm_plan_destroy(tm_plan plan);
+
+/*
+ * tm_generate -- the paper's synthetic workload (section 3.5
+ * P:234-244): counter-based generator keyed by (seed, global pair index).
+ *   pair0, batch   global pair indices [pair0, pair0+batch).
+ *   noise          TM_I8: template bit-flip probability in [0,1];
+ *                  TM_F32: template Gaussian noise sigma >= 0.
+ *   offset, len    positions [offset, offset+len) of each signal to write to
+ *                  x (so a rank can generate only its chunk).  x may be NULL.
+ *   x [batch][ldx] signal chunk (ldx >= len).
+ *   t [batch][K]   template (may be NULL); k0 [batch] planted shift (may be NULL).
+ * int8 outputs are bit-identical to tmgen/ (host); fp32 outputs agree to
+ * float rounding of the same formula.
+ * Errors: TM_EINVAL on offset/len outside [0, N], ldx < len, batch < 0.
+ */
+int tm_generate(tm_plan plan, int64_t pair0, int64_t batch, double noise,
+                int64_t offset, int64_t len, void *x, int64_t ldx,
+                void *t, int64_t *k0, void *stream);
+
+/*
+ * tm_fold -- Eq. (2), Alg. 1 step 3 with D_{M+K}
+ * (strategy 1) and the mod-N index convention:
+ *     y_j[k] = sum_{i < ceil(N/Mj)} x[(k + i*Mj) mod N],  k < Mj + K, j = 1, 2,
+ * restricted to the global positions p in [offset, offset+len) (partial fold;
+ * offset = 0, len = N is the paper's fold).  x points at position `offset`
+ * of pair 0.  The sum of partial folds over any partition of [0, N) is the
+ * full fold (exactly for TM_I8) -- this is how a signal split over GPUs is
+ * folded (sum the partials with an all-reduce).
+ *   y1 [batch][M1+K], y2 [batch][M2+K]   int32 (TM_I8) or float32 (TM_F32).
+ *   accumulate     0: overwrite y; 1: add into y.
+ *   ws             workspace of tm_workspace_bytes(plan, batch) bytes.
+ * Errors: TM_EINVAL on NULL pointers, batch < 0, ldx < len, range outside
+ * [0, N].  x must be 16-byte aligned with ldx*elem a multiple of 16 for the
+ * fast kernels; otherwise a slower general kernel is used.
+ */
+int tm_fold(tm_plan plan, const void *x, int64_t ldx, int64_t batch,
+            int64_t offset, int64_t len, void *y1, void *y2, int accumulate,
+            void *ws, void *stream);
+
+/*
+ * tm_fold_template -- Alg. 1 step 4: t_M = [t 0] zero-padded, and the
+ * template half of step 5: the forward transform of the reversed padded
+ * template (reading C3: correlation, not convolution), in the layout
+ * tm_correlate consumes (TM_I8: NTT residues mod the plan's primes, bit-
+ * reversed order; TM_F32: the zero-padded template).
+ *   t  [batch][K];   tf  [batch] x tf_bytes (see tm_plan_query).
+ */
+int tm_fold_template(tm_plan plan, const void *t, int64_t batch, void *tf, void *stream);
+
+/*
+ * tm_correlate -- Alg. 1 steps 5-6 read as the correlation of
+ * P:61 (reading C3):  r_j[k] = sum_{i<K} t_i y_j[k+i],  k < Mj.
+ * Exact for TM_I8 (number-theoretic transform, exact CRT over n_primes);
+ * float32 for TM_F32.
+ *   y1, y2 from tm_fold; tf from tm_fold_template;
+ *   r1 [batch][M1], r2 [batch][M2]   int64 (TM_I8) or float32 (TM_F32).
+ */
+int tm_correlate(tm_plan plan, const void *y1, const void *y2, const void *tf,
+                 int64_t batch, void *r1, void *r2, void *ws, void *stream);
+
+/*
+ * tm_match -- Alg. 1 step 7: m~_j = the lowest index of max r_j over
+ * [0, Mj) (readings C6, C7); steps 8-9 by Theorem 4:
+ * z = the unique value in [0, M1*M2) with z = m~1 (mod M1), z = m~2 (mod M2);
+ * k = z if z < N else -1 (NO_MATCH, reading C9).
+ *   residues [batch][2] int32 (may be NULL);  k [batch] int64.
+ */
+int tm_match(tm_plan plan, const void *r1, const void *r2, int64_t batch,
+             int32_t *residues, int64_t *k, void *stream);
+
+/*
+ * tm_run -- the whole hot path, == tm_fold(offset 0, len N) o tm_fold_template
+ * o tm_correlate o tm_match, without materialising r (argmax fused into the
+ * correlation epilogue).  x [batch][ldx], t [batch][K].
+ */
+int tm_run(tm_plan plan, const void *x, int64_t ldx, const void *t, int64_t batch,
+           int32_t *residues, int64_t *k, void *ws, void *stream);
+
+/*
+ * tm_run_host -- tm_run on HOST buffers: copies x_host/t_host (pinned memory
+ * recommended) to the caller's device staging buffers in chunks of
+ * `chunk` pairs, overlapping the copy of chunk i+1 with the compute of chunk
+ * i, and copies residues/k back to residues_host/k_host.  Enqueues on
+ * `stream`; the results are valid after the stream synchronises.
+ *   dev_x   device buffer of 2*chunk*ldx elements (double buffer)
+ *   dev_t   device buffer of 2*chunk*K elements
+ *   dev_out device buffer of batch*(8 + 2*4) bytes for k and residues
+ *   ws      tm_workspace_bytes(plan, chunk) bytes
+ */
+int tm_run_host(tm_plan plan, const void *x_host, int64_t ldx, const void *t_host,
+                int64_t batch, int64_t chunk, int32_t *residues_host, int64_t *k_host,
+                void *dev_x, void *dev_t, void *dev_out, void *ws, void *stream);
+
+/*
+ * Instrumentation (not part of the method).
+ * tm_launch_count: number of CUDA kernels this library has launched in the
+ *   process (all threads), for launch accounting in benchmarks.
+ * tm_profile_events: make subsequent tm_run calls on the calling thread record
+ *   events[0..4] (cudaEvent_t) on their stream before the fold, after the fold,
+ *   after the template fold, after the correlation+argmax, after the CRT.
+ *   events = NULL disables.  TM_EINVAL if n < 5.
+ */
+uint64_t tm_launch_count(void);
+int tm_profile_events(void **events, int n);
+
+const char *tm_status_string(int status);
+const char *tm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TM_H */

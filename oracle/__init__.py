@@ -57,6 +57,8 @@ def lib():
         for n in ("or_argmax_i64", "or_argmax_f64"):
             getattr(L, n).restype = _i64
             getattr(L, n).argtypes = [_p, _i64]
+        L.or_fold_bins_i8.restype = None
+        L.or_fold_bins_i8.argtypes = [_p, _i64, _i64, _p, _i64, _p]
         L.or_crt.restype = _i64
         L.or_crt.argtypes = [_i64, _i64, _i64, _i64]
         L.or_crt_sets.restype = _i64
@@ -125,6 +127,16 @@ def fold(x: np.ndarray, M: int, K: int, lo: int = 0, length: int | None = None) 
         y = np.zeros(M + K, np.float64)
         lib().or_fold_f32(_ptr(x), N, M, K, lo, length, _ptr(y))
     return y
+
+
+def fold_bins(x: np.ndarray, M: int, bins) -> np.ndarray:
+    """Selected entries y[k] of the Eq. (2) fold (int8 data), one by one."""
+    x = _as_input(x)
+    assert _is_int(x)
+    bins = np.ascontiguousarray(np.asarray(bins, np.int64))
+    out = np.zeros(bins.shape[0], np.int64)
+    lib().or_fold_bins_i8(_ptr(x), x.shape[0], M, _ptr(bins), bins.shape[0], _ptr(out))
+    return out
 
 
 # --------------------------------------------------------------------------

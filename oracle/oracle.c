@@ -73,6 +73,19 @@ void or_fold_i8(const int8_t *x, int64_t N, int64_t M, int64_t K,
     }
 }
 
+/* One entry of Eq. (2): y_k = sum_{i<ceil(N/M)} x_{(k+iM) mod N} -- the fold
+ * evaluated bin by bin, for sampled checks at sizes where the whole fold is
+ * too slow for the oracle (N = 2^31).  Same formula, same order as or_fold. */
+void or_fold_bins_i8(const int8_t *x, int64_t N, int64_t M, const int64_t *bins, int64_t nb,
+                     int64_t *out) {
+    int64_t q = or_ceil_div(N, M);
+    for (int64_t b = 0; b < nb; ++b) {
+        int64_t s = 0;
+        for (int64_t i = 0; i < q; ++i) s += (int64_t)x[or_mod(bins[b] + i * M, N)];
+        out[b] = s;
+    }
+}
+
 void or_fold_f32(const float *x, int64_t N, int64_t M, int64_t K,
                  int64_t lo, int64_t len, double *y) {
     int64_t q = or_ceil_div(N, M);

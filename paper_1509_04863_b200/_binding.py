@@ -1,0 +1,245 @@
+"""ctypes binding of libtm.so (names follow include/tm.h; marshalling only)."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libtm.so")
+
+TM_I8, TM_F32 = 0, 1
+TM_BINARY = 1
+TM_OK, TM_EINVAL, TM_EUNSUPPORTED, TM_ECUDA = 0, 1, 2, 3
+
+EXPORTED_SYMBOLS = (
+    "tm_plan_create", "tm_plan_query", "tm_workspace_bytes", "tm_plan_destroy", "tm_generate",
+    "tm_fold", "tm_fold_template", "tm_correlate", "tm_match", "tm_run", "tm_run_host",
+    "tm_status_string", "tm_last_error", "tm_launch_count", "tm_profile_events",
+)
+
+_i64, _u64, _i32, _u32, _p, _d = (ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32,
+                                  ctypes.c_void_p, ctypes.c_double)
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("N", _i64), ("K", _i64), ("M1", _i64), ("M2", _i64), ("q1", _i64), ("q2", _i64),
+                ("s1", _i64), ("s2", _i64), ("len_y1", _i64), ("len_y2", _i64), ("L1", _i64),
+                ("L2", _i64), ("n_primes", _i32), ("dtype", _i32), ("flags", _u32),
+                ("fast_fold", _i32), ("tf_bytes", _i64), ("seed", _u64)]
+
+
+class TMError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        L = lib()
+        msg = L.tm_last_error().decode(errors="replace")
+        name = L.tm_status_string(status).decode()
+        super().__init__(f"{where}: {name}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libtm.so; raise loudly if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(there is no CPU fallback for the CUDA path)")
+        L = ctypes.CDLL(_LIB_PATH)
+        L.tm_plan_create.restype = ctypes.c_int
+        L.tm_plan_create.argtypes = [ctypes.POINTER(_p), _i64, _i64, _i64, _u64, ctypes.c_int, _u32]
+        L.tm_plan_query.restype = ctypes.c_int
+        L.tm_plan_query.argtypes = [_p, ctypes.POINTER(PlanInfo)]
+        L.tm_workspace_bytes.restype = ctypes.c_size_t
+        L.tm_workspace_bytes.argtypes = [_p, _i64]
+        L.tm_plan_destroy.restype = None
+        L.tm_plan_destroy.argtypes = [_p]
+        L.tm_generate.restype = ctypes.c_int
+        L.tm_generate.argtypes = [_p, _i64, _i64, _d, _i64, _i64, _p, _i64, _p, _p, _p]
+        L.tm_fold.restype = ctypes.c_int
+        L.tm_fold.argtypes = [_p, _p, _i64, _i64, _i64, _i64, _p, _p, ctypes.c_int, _p, _p]
+        L.tm_fold_template.restype = ctypes.c_int
+        L.tm_fold_template.argtypes = [_p, _p, _i64, _p, _p]
+        L.tm_correlate.restype = ctypes.c_int
+        L.tm_correlate.argtypes = [_p, _p, _p, _p, _i64, _p, _p, _p, _p]
+        L.tm_match.restype = ctypes.c_int
+        L.tm_match.argtypes = [_p, _p, _p, _i64, _p, _p, _p]
+        L.tm_run.restype = ctypes.c_int
+        L.tm_run.argtypes = [_p, _p, _i64, _p, _i64, _p, _p, _p, _p]
+        L.tm_run_host.restype = ctypes.c_int
+        L.tm_run_host.argtypes = [_p, _p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p]
+        L.tm_launch_count.restype = _u64
+        L.tm_launch_count.argtypes = []
+        L.tm_profile_events.restype = ctypes.c_int
+        L.tm_profile_events.argtypes = [ctypes.POINTER(_p), ctypes.c_int]
+        L.tm_status_string.restype = ctypes.c_char_p
+        L.tm_status_string.argtypes = [ctypes.c_int]
+        L.tm_last_error.restype = ctypes.c_char_p
+        L.tm_last_error.argtypes = []
+        _lib = L
+    return _lib
+
+
+def launch_count() -> int:
+    """Kernels launched by libtm in this process (tm_launch_count)."""
+    return int(lib().tm_launch_count())
+
+
+def profile_events(events):
+    """tm_profile_events: list of 5 torch.cuda.Event (enable_timing) or None."""
+    if events is None:
+        _check(lib().tm_profile_events(None, 0), "tm_profile_events")
+        return None
+    arr = (_p * len(events))(*[e.cuda_event for e in events])
+    _check(lib().tm_profile_events(arr, len(events)), "tm_profile_events")
+    return arr  # keep alive while in use
+
+
+def _check(rc: int, where: str):
+    if rc != TM_OK:
+        raise TMError(rc, where)
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+class Plan:
+    """tm_plan: Alg. 1 step 2 (M1 = M or K, M2 = M1 + 1).  dtype is "int8" or "float32"."""
+
+    def __init__(self, N: int, K: int, M: int = 0, seed: int = 0, dtype: str = "int8", binary: bool = True):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1509_04863_b200.Plan needs a CUDA device (no CPU fallback)")
+        self.dtype = {"int8": TM_I8, "float32": TM_F32}[str(dtype).replace("torch.", "")]
+        flags = TM_BINARY if (binary and self.dtype == TM_I8) else 0
+        h = _p()
+        _check(lib().tm_plan_create(ctypes.byref(h), N, K, M, seed, self.dtype, flags), "tm_plan_create")
+        self._h = h
+        info = PlanInfo()
+        _check(lib().tm_plan_query(h, ctypes.byref(info)), "tm_plan_query")
+        self.info = info
+        for f, _ in PlanInfo._fields_:
+            setattr(self, f, getattr(info, f))
+        self.x_dtype = torch.int8 if self.dtype == TM_I8 else torch.float32
+        self.y_dtype = torch.int32 if self.dtype == TM_I8 else torch.float32
+        self.r_dtype = torch.int64 if self.dtype == TM_I8 else torch.float32
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.tm_plan_destroy(h)
+            self._h = None
+
+    # ---- buffers (torch owns device memory) -------------------------------------
+    def workspace(self, batch: int, device="cuda"):
+        import torch
+        n = lib().tm_workspace_bytes(self._h, batch)
+        return torch.empty(max(int(n), 1), dtype=torch.uint8, device=device)
+
+    def _dev(self, t):
+        return t.device if t is not None else "cuda"
+
+    # ---- entry points --------------------------------------------------------------
+    def generate(self, pair0: int, batch: int, noise: float, offset: int = 0, length: int | None = None,
+                 x=None, t=None, k0=None, want_x=True, stream=None, device="cuda"):
+        import torch
+        length = self.N - offset if length is None else length
+        if want_x and x is None:
+            x = torch.empty((batch, length), dtype=self.x_dtype, device=device)
+        if t is None:
+            t = torch.empty((batch, self.K), dtype=self.x_dtype, device=device)
+        if k0 is None:
+            k0 = torch.empty(batch, dtype=torch.int64, device=device)
+        ldx = x.stride(0) if x is not None and x.dim() == 2 else length
+        _check(lib().tm_generate(self._h, pair0, batch, float(noise), offset, length, _ptr(x), ldx, _ptr(t),
+                                 _ptr(k0), _stream(stream)), "tm_generate")
+        return x, t, k0
+
+    def fold(self, x, offset: int = 0, length: int | None = None, y1=None, y2=None, accumulate=False,
+             ws=None, stream=None):
+        import torch
+        batch = x.shape[0]
+        length = x.shape[1] if length is None else length
+        if y1 is None:
+            y1 = torch.zeros((batch, self.len_y1), dtype=self.y_dtype, device=x.device)
+        if y2 is None:
+            y2 = torch.zeros((batch, self.len_y2), dtype=self.y_dtype, device=x.device)
+        if ws is None:
+            ws = self.workspace(batch, x.device)
+        _check(lib().tm_fold(self._h, _ptr(x), x.stride(0), batch, offset, length, _ptr(y1), _ptr(y2),
+                             int(accumulate), _ptr(ws), _stream(stream)), "tm_fold")
+        return y1, y2
+
+    def fold_template(self, t, tf=None, stream=None):
+        import torch
+        batch = t.shape[0]
+        if tf is None:
+            tf = torch.empty((batch, self.tf_bytes), dtype=torch.uint8, device=t.device)
+        _check(lib().tm_fold_template(self._h, _ptr(t), batch, _ptr(tf), _stream(stream)), "tm_fold_template")
+        return tf
+
+    def correlate(self, y1, y2, tf, r1=None, r2=None, stream=None):
+        import torch
+        batch = y1.shape[0]
+        if r1 is None:
+            r1 = torch.empty((batch, self.M1), dtype=self.r_dtype, device=y1.device)
+        if r2 is None:
+            r2 = torch.empty((batch, self.M2), dtype=self.r_dtype, device=y1.device)
+        _check(lib().tm_correlate(self._h, _ptr(y1), _ptr(y2), _ptr(tf), batch, _ptr(r1), _ptr(r2), None,
+                                  _stream(stream)), "tm_correlate")
+        return r1, r2
+
+    def match(self, r1, r2, residues=None, k=None, stream=None):
+        import torch
+        batch = r1.shape[0]
+        if residues is None:
+            residues = torch.empty((batch, 2), dtype=torch.int32, device=r1.device)
+        if k is None:
+            k = torch.empty(batch, dtype=torch.int64, device=r1.device)
+        _check(lib().tm_match(self._h, _ptr(r1), _ptr(r2), batch, _ptr(residues), _ptr(k), _stream(stream)),
+               "tm_match")
+        return residues, k
+
+    def run(self, x, t, residues=None, k=None, ws=None, stream=None):
+        import torch
+        batch = x.shape[0]
+        if residues is None:
+            residues = torch.empty((batch, 2), dtype=torch.int32, device=x.device)
+        if k is None:
+            k = torch.empty(batch, dtype=torch.int64, device=x.device)
+        if ws is None:
+            ws = self.workspace(batch, x.device)
+        _check(lib().tm_run(self._h, _ptr(x), x.stride(0), _ptr(t), batch, _ptr(residues), _ptr(k), _ptr(ws),
+                            _stream(stream)), "tm_run")
+        return residues, k
+
+    def run_host(self, x_host, t_host, chunk: int, residues_host, k_host, dev_x, dev_t, dev_out, ws, stream=None):
+        """tm_run_host: x_host/t_host/residues_host/k_host are (pinned) CPU tensors."""
+        batch = x_host.shape[0]
+        _check(lib().tm_run_host(self._h, _ptr(x_host), x_host.stride(0), _ptr(t_host), batch, chunk,
+                                 _ptr(residues_host), _ptr(k_host), _ptr(dev_x), _ptr(dev_t), _ptr(dev_out),
+                                 _ptr(ws), _stream(stream)), "tm_run_host")
+
+    def run_host_buffers(self, batch: int, chunk: int, device="cuda"):
+        """Device staging buffers for run_host (double-buffered chunks)."""
+        import torch
+        dev_x = torch.empty((2 * chunk, self.N), dtype=self.x_dtype, device=device)
+        dev_t = torch.empty((2 * chunk, self.K), dtype=self.x_dtype, device=device)
+        dev_out = torch.empty(((batch * 8 + 255) // 256 * 256) + batch * 8, dtype=torch.uint8, device=device)
+        return dev_x, dev_t, dev_out, self.workspace(chunk, device)

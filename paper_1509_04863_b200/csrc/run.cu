@@ -1,0 +1,113 @@
+// run.cu -- tm_run (the whole of Algorithm 1 FTM(), on
+// device buffers) and tm_run_host (the same on host buffers, with the
+// host->device copies of chunk i+1 overlapped with the compute of chunk i).
+#include "tm_internal.cuh"
+
+namespace {
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+struct RunWs {
+    char *fold_ws;   // tm_fold workspace (its own layout at offset 0)
+    void *y1, *y2;   // folded signal
+    void *tf;        // folded template
+    int32_t *resid;  // [batch][2]
+    void *tiles;     // fp32 argmax partials
+    size_t total;
+};
+
+RunWs run_ws(const tm_plan_s *p, int64_t batch, void *ws) {
+    tm_ws_layout F = tm_ws(p, batch);
+    RunWs r{};
+    char *base = (char *)ws;
+    size_t off = F.total;
+    r.fold_ws = base;
+    r.resid = (int32_t *)(base + F.resid);
+    r.tiles = base + F.f32_tiles;
+    const size_t ey = p->dtype == TM_I8 ? 4 : 4;
+    r.y1 = base + off; off += align256((size_t)batch * p->len_y1 * ey);
+    r.y2 = base + off; off += align256((size_t)batch * p->len_y2 * ey);
+    r.tf = base + off; off += align256((size_t)batch * p->tf_bytes);
+    r.total = off;
+    return r;
+}
+}  // namespace
+
+size_t tm_run_ws_bytes(const tm_plan_s *p, int64_t batch) { return run_ws(p, batch, nullptr).total; }
+
+extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const void *x, int64_t ldx, const void *t, int64_t batch, int32_t *residues,
+                      int64_t *k, void *ws, void *stream) {
+    if (!p) { tm_set_error("tm_run: NULL plan"); return TM_EINVAL; }
+    if (batch < 0) { tm_set_error("tm_run: batch < 0"); return TM_EINVAL; }
+    if (batch == 0) return TM_OK;
+    if (!x || !t || !k || !ws || ldx < p->N) { tm_set_error("tm_run: NULL pointer or ldx < N"); return TM_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    RunWs W = run_ws(p, batch, ws);
+    tm_prof_mark(0, s);
+    int rc = tm_fold_impl(p, x, ldx, batch, 0, p->N, W.y1, W.y2, 0, W.fold_ws, s);     // step 3
+    if (rc) return rc;
+    tm_prof_mark(1, s);
+    rc = tm_fold_template(p, t, batch, W.tf, stream);                                // step 4 (+5 for t)
+    if (rc) return rc;
+    tm_prof_mark(2, s);
+    rc = tm_correlate_impl(p, W.y1, W.y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, s);  // 5-7
+    if (rc) return rc;
+    tm_prof_mark(3, s);
+    rc = tm_crt_impl(p, W.resid, batch, residues, k, s);                              // steps 8-9
+    tm_prof_mark(4, s);
+    return rc;
+}
+
+extern "C" __attribute__((visibility("default"))) int tm_run_host(tm_plan p, const void *x_host, int64_t ldx, const void *t_host, int64_t batch,
+                           int64_t chunk, int32_t *residues_host, int64_t *k_host, void *dev_x, void *dev_t,
+                           void *dev_out, void *ws, void *stream) {
+    if (!p) { tm_set_error("tm_run_host: NULL plan"); return TM_EINVAL; }
+    if (batch < 0 || chunk < 1) { tm_set_error("tm_run_host: batch < 0 or chunk < 1"); return TM_EINVAL; }
+    if (batch == 0) return TM_OK;
+    if (!x_host || !t_host || !k_host || !dev_x || !dev_t || !dev_out || !ws || ldx < p->N) {
+        tm_set_error("tm_run_host: NULL pointer or ldx < N");
+        return TM_EINVAL;
+    }
+    const size_t ex = p->dtype == TM_I8 ? 1 : 4;
+    cudaStream_t s = (cudaStream_t)stream, sc = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return tm_cuda_status(e, "tm_run_host: stream");
+    cudaEvent_t copied[2], freed[2];
+    for (int i = 0; i < 2; ++i) {
+        cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming);
+    }
+    // the copy stream must not overwrite a slot the caller's stream still reads from a
+    // previous call: start after everything already queued on s
+    cudaEventRecord(freed[0], s);
+    cudaEventRecord(freed[1], s);
+    int64_t *dk = (int64_t *)dev_out;
+    int32_t *dres = (int32_t *)((char *)dev_out + ((size_t)batch * 8 + 255) / 256 * 256);
+    int rc = TM_OK;
+    const int64_t nchunks = (batch + chunk - 1) / chunk;
+    for (int64_t c = 0; c < nchunks && rc == TM_OK; ++c) {
+        const int slot = (int)(c & 1);
+        const int64_t b0 = c * chunk, nb = (batch - b0) < chunk ? (batch - b0) : chunk;
+        char *sx = (char *)dev_x + (size_t)slot * chunk * ldx * ex;
+        char *st = (char *)dev_t + (size_t)slot * chunk * p->K * ex;
+        cudaStreamWaitEvent(sc, freed[slot], 0);
+        e = cudaMemcpyAsync(sx, (const char *)x_host + (size_t)b0 * ldx * ex, (size_t)nb * ldx * ex,
+                            cudaMemcpyHostToDevice, sc);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(st, (const char *)t_host + (size_t)b0 * p->K * ex, (size_t)nb * p->K * ex,
+                                cudaMemcpyHostToDevice, sc);
+        if (e != cudaSuccess) { rc = tm_cuda_status(e, "tm_run_host: H2D"); break; }
+        cudaEventRecord(copied[slot], sc);
+        cudaStreamWaitEvent(s, copied[slot], 0);
+        rc = tm_run(p, sx, ldx, st, nb, dres + 2 * b0, dk + b0, ws, stream);
+        cudaEventRecord(freed[slot], s);
+    }
+    if (rc == TM_OK) {
+        e = cudaMemcpyAsync(k_host, dk, (size_t)batch * 8, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && residues_host)
+            e = cudaMemcpyAsync(residues_host, dres, (size_t)batch * 8, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) rc = tm_cuda_status(e, "tm_run_host: D2H");
+    }
+    for (int i = 0; i < 2; ++i) { cudaEventDestroy(copied[i]); cudaEventDestroy(freed[i]); }
+    cudaStreamDestroy(sc);
+    return rc;
+}

@@ -1,0 +1,67 @@
+// tm_internal.cuh -- private declarations of libtm (the B200 hot path of
+// arXiv 1509.04863, Algorithm 1).  Nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tm.h"
+
+#define TM_MAX_LOGL 18           // longest correlation transform: 2^18 (K <= 2^17)
+#define TM_NTT_SMEM_MAX_LOGL 14  // transforms up to 2^14 run fully in shared memory
+
+struct tm_plan_s {
+    int64_t N, K, M1, M2, q1, q2, s1, s2, len_y1, len_y2;
+    int64_t L1, L2;
+    int logL1, logL2;
+    int n_primes;
+    int dtype;
+    uint32_t flags;
+    int fast_fold;       // packed +-1 kernel eligible for full-row chunks
+    uint64_t seed;
+    int device;
+    int num_sms;
+    int64_t tf_elems;    // uint2 (value, shoup) elements per prime per pair (I8) / floats (F32)
+    int64_t tf_bytes;
+    uint32_t crt_inv;    // M1^{-1} mod M2
+};
+
+// ---- error plumbing (plan.cu) ----
+void tm_set_error(const char *fmt, ...);
+int tm_cuda_status(cudaError_t e, const char *what);
+void tm_count_launch();
+#define TM_CHECK_LAUNCH(what)                                                  \
+    do {                                                                       \
+        cudaError_t _e = cudaGetLastError();                                   \
+        if (_e != cudaSuccess) return tm_cuda_status(_e, what);                \
+        tm_count_launch();                                                     \
+    } while (0)
+// stage-boundary events of tm_run (tm_profile_events); NULL when disabled
+void tm_prof_mark(int stage, cudaStream_t s);
+
+// ---- NTT constants (ntt.cu) ----
+struct tm_ntt_tables {
+    const uint32_t *tw[2][2];   // [prime][dir] values,  per-length compact tables
+    const uint32_t *tws[2][2];  // Shoup companions floor(w * 2^32 / p)
+};
+int tm_ntt_tables_get(int device, tm_ntt_tables *out);
+extern const uint32_t TM_PRIMES[2];
+
+// ---- workspace layout (plan.cu) ----
+struct tm_ws_layout {
+    size_t fold_counts;   // int32 [batch][M1 + M2] base-bin accumulators
+    size_t fold_bytes;
+    size_t resid;         // int32 [batch][2] residues (tm_run)
+    size_t f32_tiles;     // fp32 per-tile argmax partials (tm_run, TM_F32)
+    size_t total;
+};
+tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch);
+size_t tm_run_ws_bytes(const tm_plan_s *p, int64_t batch);  // run.cu
+
+// ---- internal launchers ----
+int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset,
+                 int64_t len, void *y1, void *y2, int accumulate, void *ws, cudaStream_t s);
+int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const void *tf,
+                      int64_t batch, void *r1, void *r2, int32_t *resid, void *tile_scratch,
+                      cudaStream_t s);
+int tm_crt_impl(const tm_plan_s *p, const int32_t *resid, int64_t batch, int32_t *residues_out,
+                int64_t *k, cudaStream_t s);

@@ -99,6 +99,17 @@ def test_fold_invariants():
         np.testing.assert_array_equal(oracle.fold(np.ones(N, np.int8), M, K), np.full(M + K, q))
 
 
+def test_fold_bins_matches_fold():
+    rng = np.random.default_rng(14)
+    for _ in range(30):
+        N = int(rng.integers(2, 200))
+        K = int(rng.integers(1, N + 1))
+        M = int(rng.integers(K, N + 2))
+        x = rng.integers(-128, 128, N).astype(np.int8)
+        bins = rng.integers(0, M + K, 7)
+        np.testing.assert_array_equal(oracle.fold_bins(x, M, bins), oracle.fold(x, M, K)[bins])
+
+
 def test_partial_fold_additive():
     """The fold restricted to the positions of a chunk, summed over any partition
     of [0, N), is the full fold (the multi-GPU chunking identity)."""

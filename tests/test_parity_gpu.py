@@ -1,0 +1,253 @@
+"""GPU <-> oracle parity through the C ABI (libtm.so).
+
+Inputs come from the host generator (tmgen/) and are uploaded; expected values
+come only from oracle/.  Integer data: bit-exact y1, y2, r1, r2, residues, k.
+fp32 data: normwise 1e-5 on y and r (reading C15), identical residues unless
+the oracle's top-two gap is within that tolerance, and k = CRT(residues).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import tmgen
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def tm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1509_04863_b200 import _build
+    _build.build()
+    import paper_1509_04863_b200 as m
+    return m
+
+
+DEV = "cuda:0"
+
+
+def up(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def crt_closed(m1, M1, m2, M2, N):
+    z = oracle.crt(m1, M1, m2, M2)
+    return z if z < N else -1
+
+
+def check_int_pairs(tm, plan, x_h, t_h, pairs, staged=True, run=True):
+    """Full staged + fused comparison for the given pair indices."""
+    x = up(x_h)
+    t = up(t_h)
+    y1, y2 = plan.fold(x)
+    tf = plan.fold_template(t)
+    r1, r2 = plan.correlate(y1, y2, tf)
+    res, k = plan.match(r1, r2)
+    res_run, k_run = plan.run(x, t)
+    torch.cuda.synchronize()
+    y1h, y2h, r1h, r2h = (v.cpu().numpy() for v in (y1, y2, r1, r2))
+    resh, kh, res_runh, k_runh = res.cpu().numpy(), k.cpu().numpy(), res_run.cpu().numpy(), k_run.cpu().numpy()
+    for b in pairs:
+        o = oracle.ftm(x_h[b], t_h[b], M=plan.M1 if plan.M1 != plan.K else 0)
+        np.testing.assert_array_equal(y1h[b], o["y1"], err_msg=f"y1 pair {b}")
+        np.testing.assert_array_equal(y2h[b], o["y2"], err_msg=f"y2 pair {b}")
+        np.testing.assert_array_equal(r1h[b], o["r1"], err_msg=f"r1 pair {b}")
+        np.testing.assert_array_equal(r2h[b], o["r2"], err_msg=f"r2 pair {b}")
+        assert tuple(resh[b]) == o["residues"] == tuple(res_runh[b]), b
+        assert kh[b] == o["k"] == k_runh[b], b
+    return kh, k_runh
+
+
+# ------------------------------------------------------------- generator
+def test_device_generator_matches_host_int8(tm):
+    N, K = 3000, 200
+    plan = tm.Plan(N, K, M=0, seed=77)
+    for (off, ln) in ((0, N), (16, 1024), (5, 333), (2992, 8)):
+        x, t, k0 = plan.generate(3, 4, 0.3, offset=off, length=ln)
+        torch.cuda.synchronize()
+        for b in range(4):
+            np.testing.assert_array_equal(x[b].cpu().numpy(), tmgen.signal(77, 3 + b, N, lo=off, length=ln))
+            np.testing.assert_array_equal(t[b].cpu().numpy(), tmgen.template(77, 3 + b, N, K, 0.3))
+            assert int(k0[b]) == tmgen.k0(77, 3 + b, N)
+
+
+def test_device_generator_matches_host_f32(tm):
+    N, K = 4096, 300
+    plan = tm.Plan(N, K, seed=5, dtype="float32")
+    x, t, k0 = plan.generate(0, 2, 0.5)
+    torch.cuda.synchronize()
+    for b in range(2):
+        np.testing.assert_allclose(x[b].cpu().numpy(), tmgen.signal(5, b, N, dtype=np.float32), rtol=1e-6, atol=1e-6)
+        np.testing.assert_allclose(t[b].cpu().numpy(), tmgen.template(5, b, N, K, 0.5, dtype=np.float32),
+                                   rtol=1e-5, atol=1e-5)
+        assert int(k0[b]) == tmgen.k0(5, b, N)
+
+
+# ------------------------------------------------------------- cfg1 and small int cases
+def test_cfg1_exact(tm):
+    """BASELINE cfg1: N=4096, K=256, +-1, noiseless; many seeds (one pair each)."""
+    N, K = 4096, 256
+    plan = tm.Plan(N, K, seed=1)
+    x_h, t_h, k0 = tmgen.batch(1, 0, 64, N, K, 0.0)
+    kh, _ = check_int_pairs(tm, plan, x_h, t_h, range(64))
+    assert np.mean(kh == k0) > 0.5  # SURVEY measured 0.758 for this configuration
+
+
+@pytest.mark.parametrize("N,K,M", [(1000, 37, 0), (997, 40, 45), (64, 8, 0), (12, 3, 4), (5000, 71, 80)])
+def test_general_fold_wrap_cases(tm, N, K, M):
+    """M not dividing N (mod-N wrap, reading C5), M > K, tiny sizes: general kernels."""
+    rng = np.random.default_rng(N + K)
+    B = 5
+    plan = tm.Plan(N, K, M=M, seed=2, binary=False)
+    x_h = rng.integers(-128, 128, (B, N)).astype(np.int8)
+    t_h = np.stack([x_h[b][(np.arange(K) + 7 * b) % N] for b in range(B)]).astype(np.int8)
+    check_int_pairs(tm, plan, x_h, t_h, range(B))
+
+
+def test_two_prime_ntt(tm):
+    """|r| bound above p1/2 -> two NTT primes + CRT (general int8 data)."""
+    N, K = 100000, 400
+    plan = tm.Plan(N, K, seed=3, binary=False)
+    assert plan.n_primes == 2
+    rng = np.random.default_rng(3)
+    x_h = rng.integers(-128, 128, (3, N)).astype(np.int8)
+    x_h[0, :] = 127          # extreme values: |r| near K*q*128*127
+    t_h = np.full((3, K), 127, np.int8)
+    t_h[1] = rng.integers(-128, 128, K)
+    t_h[2] = -128
+    check_int_pairs(tm, plan, x_h, t_h, range(3))
+
+
+@pytest.mark.parametrize("N,K,B", [(2 ** 16, 1024, 6), (4096 * 37, 4096, 3), (8192 * 600, 8192, 1),
+                                   (2 ** 18, 4096, 4), (512 * 300, 512, 3)])
+def test_packed_pm1_fold(tm, N, K, B):
+    """The packed +-1 kernel: q not a multiple of 16, several column groups,
+    several row items per pair."""
+    plan = tm.Plan(N, K, seed=11)
+    assert plan.fast_fold == 1
+    x_h, t_h, _ = tmgen.batch(11, 0, B, N, K, 0.1)
+    check_int_pairs(tm, plan, x_h, t_h, range(B))
+
+
+def test_packed_pm1_extremes(tm):
+    """All-ones / all-minus-ones signals: the largest counts the SWAR lanes hold."""
+    N, K = 4096 * 64, 4096
+    plan = tm.Plan(N, K, seed=0)
+    x_h = np.ones((3, N), np.int8)
+    x_h[1] = -1
+    x_h[2, : N // 2] = -1
+    t_h = np.ones((3, K), np.int8)
+    check_int_pairs(tm, plan, x_h, t_h, range(3))
+
+
+def test_partial_folds_sum_to_full(tm):
+    """tm_fold over a partition of [0, N) with accumulate=1 == the full fold (the
+    multi-GPU chunking identity), for row-aligned (packed kernel) and unaligned
+    (general kernel) chunks; each partial also equals the oracle's partial fold."""
+    N, K = 4096 * 48, 4096
+    plan = tm.Plan(N, K, seed=21)
+    x_h, _, _ = tmgen.batch(21, 0, 2, N, K, 0.0)
+    x = up(x_h)
+    for cuts in ([0, 4096 * 16, 4096 * 17, N], [0, 1000, 77777, N]):
+        y1 = torch.zeros((2, plan.len_y1), dtype=torch.int32, device=DEV)
+        y2 = torch.zeros((2, plan.len_y2), dtype=torch.int32, device=DEV)
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            xc = x[:, a:b].contiguous()
+            p1, p2 = plan.fold(xc, offset=a, length=b - a)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(p1[0].cpu().numpy(), oracle.fold(x_h[0], plan.M1, K, a, b - a))
+            np.testing.assert_array_equal(p2[0].cpu().numpy(), oracle.fold(x_h[0], plan.M2, K, a, b - a))
+            plan.fold(xc, offset=a, length=b - a, y1=y1, y2=y2, accumulate=True)
+        torch.cuda.synchronize()
+        for bb in range(2):
+            np.testing.assert_array_equal(y1[bb].cpu().numpy(), oracle.fold(x_h[bb], plan.M1, K))
+            np.testing.assert_array_equal(y2[bb].cpu().numpy(), oracle.fold(x_h[bb], plan.M2, K))
+
+
+def test_empty_batch_and_errors(tm):
+    plan = tm.Plan(4096, 256, seed=0)
+    x = torch.empty((0, 4096), dtype=torch.int8, device=DEV)
+    t = torch.empty((0, 256), dtype=torch.int8, device=DEV)
+    res, k = plan.run(x, t)
+    assert k.numel() == 0
+    with pytest.raises(tm.TMError):
+        plan.fold(torch.zeros((1, 4096), dtype=torch.int8, device=DEV), offset=100)  # chunk beyond N
+    with pytest.raises(tm.TMError):
+        tm.Plan(1024, 16)  # 16*17 <= 1024
+
+
+# ------------------------------------------------------------- fp32 (cfg3 shape)
+def check_f32_pairs(tm, plan, x_h, t_h, pairs):
+    x, t = up(x_h), up(t_h)
+    y1, y2 = plan.fold(x)
+    tf = plan.fold_template(t)
+    r1, r2 = plan.correlate(y1, y2, tf)
+    res, k = plan.match(r1, r2)
+    res_run, k_run = plan.run(x, t)
+    torch.cuda.synchronize()
+    tol = 1e-5
+    for b in pairs:
+        o = oracle.ftm(x_h[b], t_h[b])
+        for name, g in (("y1", y1), ("y2", y2), ("r1", r1), ("r2", r2)):
+            ov = o[name]
+            gv = g[b].cpu().numpy().astype(np.float64)
+            assert np.max(np.abs(gv - ov)) <= tol * np.max(np.abs(ov)), (name, b)
+        for j, (name, M) in enumerate((("r1", plan.M1), ("r2", plan.M2))):
+            ov = o[name]
+            s = np.sort(ov)
+            gap = s[-1] - s[-2]
+            if gap > tol * np.max(np.abs(ov)):
+                assert int(res[b, j]) == o["residues"][j] == int(res_run[b, j]), (b, j)
+        m1, m2 = int(res[b, 0]), int(res[b, 1])
+        assert int(k[b]) == crt_closed(m1, plan.M1, m2, plan.M2, plan.N)
+        if (m1, m2) == o["residues"]:
+            assert int(k[b]) == o["k"]
+
+
+def test_f32_small(tm):
+    N, K = 2 ** 16, 512
+    plan = tm.Plan(N, K, seed=31, dtype="float32")
+    x_h, t_h, _ = tmgen.batch(31, 0, 4, N, K, 0.5, dtype=np.float32)
+    check_f32_pairs(tm, plan, x_h, t_h, range(4))
+
+
+def test_f32_ragged(tm):
+    N, K = 30011, 250   # M1 does not divide N
+    plan = tm.Plan(N, K, M=260, seed=32, dtype="float32")
+    x_h, t_h, _ = tmgen.batch(32, 0, 3, N, K, 0.5, dtype=np.float32)
+    check_f32_pairs(tm, plan, x_h, t_h, range(3))
+
+
+# ------------------------------------------------------------- BASELINE sizes
+def test_cfg2_full_batch_sampled(tm):
+    """cfg2 at full size (N=2^20, K=4096, 1024 pairs, 10% flips), tm_run on the whole
+    batch as bench.py launches it; oracle on 24 sampled pairs; k of every pair equals
+    CRT of its residues; success rate reported."""
+    N, K, B = 2 ** 20, 4096, 1024
+    plan = tm.Plan(N, K, seed=2)
+    x_h, t_h, k0 = tmgen.batch(2, 0, B, N, K, 0.1)
+    kh, kr = check_int_pairs(tm, plan, x_h, t_h, list(range(0, B, 43)) + [B - 1])
+    np.testing.assert_array_equal(kh, kr)
+    rate = float(np.mean(kh == k0))
+    print(f"cfg2 success rate {rate:.3f}")
+    assert 0.02 < rate < 0.3   # SURVEY: 0.093 over 300 trials
+
+
+@pytest.mark.parametrize("K", [4096, 8192, 16384])
+def test_cfg4_full_batch_sampled(tm, K):
+    N, B = 2 ** 24, 64
+    plan = tm.Plan(N, K, seed=4)
+    x_h, t_h, k0 = tmgen.batch(4, 0, B, N, K, 0.2)
+    check_int_pairs(tm, plan, x_h, t_h, [0, 31, 63] if K < 16384 else [0, 63])
+
+
+def test_cfg3_full_batch_sampled(tm):
+    N, K, B = 2 ** 22, 8192, 256
+    plan = tm.Plan(N, K, seed=3, dtype="float32")
+    x_h, t_h, _ = tmgen.batch(3, 0, B, N, K, 0.5, dtype=np.float32)
+    check_f32_pairs(tm, plan, x_h, t_h, [0, 255])
