@@ -218,6 +218,9 @@ def main():
 
     # ---- timed region: K steps, stage events per step (tm_profile_events)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for e5 in ev:          # torch creates the CUDA event lazily on first record
+        for e in e5:
+            e.record(stream)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()

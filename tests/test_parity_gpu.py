@@ -192,7 +192,7 @@ def check_f32_pairs(tm, plan, x_h, t_h, pairs):
     torch.cuda.synchronize()
     tol = 1e-5
     for b in pairs:
-        o = oracle.ftm(x_h[b], t_h[b])
+        o = oracle.ftm(x_h[b], t_h[b], M=plan.M1 if plan.M1 != plan.K else 0)
         for name, g in (("y1", y1), ("y2", y2), ("r1", r1), ("r2", r2)):
             ov = o[name]
             gv = g[b].cpu().numpy().astype(np.float64)
