@@ -62,7 +62,7 @@ int tm_ntt_tables_get(int device, tm_ntt_tables *out) {
     DevTables &D = g_tabs[device];
     if (!D.ready) {
         const size_t n = size_t(1) << TM_MAX_LOGL;  // entries per table (sum of n/2 over lengths)
-        std::vector<uint32_t> h(8 * n, 0u);
+        std::vector<uint32_t> h(16 * n, 0u);  // 8n separate (value | companion) + 8n interleaved
         for (int pi = 0; pi < 2; ++pi) {
             const uint64_t p = TM_PRIMES[pi];
             for (int dir = 0; dir < 2; ++dir) {
@@ -73,9 +73,12 @@ int tm_ntt_tables_get(int device, tm_ntt_tables *out) {
                     uint64_t w = powmod(TM_GENERATORS[pi], (p - 1) / len, p);
                     if (dir) w = powmod(w, p - 2, p);
                     uint64_t cur = 1;
+                    uint32_t *il = h.data() + 8 * n + (size_t)(pi * 2 + dir) * 2 * n;
                     for (uint64_t j = 0; j < len / 2; ++j) {
                         val[len / 2 - 1 + j] = (uint32_t)cur;
                         sh[len / 2 - 1 + j] = (uint32_t)(((unsigned __int128)cur << 32) / p);
+                        il[2 * (len / 2 - 1 + j)] = val[len / 2 - 1 + j];
+                        il[2 * (len / 2 - 1 + j) + 1] = sh[len / 2 - 1 + j];
                         cur = (unsigned __int128)cur * w % p;
                     }
                 }
@@ -91,6 +94,7 @@ int tm_ntt_tables_get(int device, tm_ntt_tables *out) {
             for (int dir = 0; dir < 2; ++dir) {
                 D.t.tw[pi][dir] = d + (size_t)(pi * 2 + dir) * 2 * n;
                 D.t.tws[pi][dir] = d + (size_t)(pi * 2 + dir) * 2 * n + n;
+                D.t.tw2[pi][dir] = reinterpret_cast<const uint2 *>(d + 8 * n + (size_t)(pi * 2 + dir) * 2 * n);
             }
         D.ready = true;
     }
@@ -215,6 +219,7 @@ __global__ void __launch_bounds__(1024) template_ntt_kernel(TfArgs A) {
 struct CorrArgs {
     const int32_t *y[2];
     int64_t len_y[2];
+    int64_t nload[2];
     int64_t M[2];
     int64_t K;
     int logL[2];
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(1024) corr_ntt_kernel(CorrArgs A) {
     uint32_t *a = A.use_smem ? sm : A.scratch + (b * 2 + j) * A.scratch_stride;
     uint32_t *keep = a + L;  // residues of prime 0 (two-prime case)
     const int32_t *y = A.y[j] + b * A.len_y[j];
-    const int64_t nload = M + A.K - 1;  // y[0 .. M+K-2]; y[M+K-1] is never needed
+    const int64_t nload = A.nload[j];  // y[0 .. M+K-2] (y[M+K-1] is never needed), or M (cyclic y1)
     for (int pi = 0; pi < A.n_primes; ++pi) {
         const uint32_t p = pi ? 998244353u : 2013265921u;
         for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
@@ -475,6 +480,7 @@ extern "C" __attribute__((visibility("default"))) int tm_fold_template(tm_plan p
         return TM_OK;
     }
     if (batch > 0x7FFFFFFF) { tm_set_error("tm_fold_template: batch too large"); return TM_EUNSUPPORTED; }
+    if (p->fast_corr) return tm_fast_template(p, t, batch, tf, s);
     TfArgs A;
     A.t = (const int8_t *)t; A.K = p->K;
     A.logL[0] = p->logL1; A.logL[1] = p->logL2;
@@ -521,6 +527,7 @@ int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const 
         }
         return TM_OK;
     }
+    if (p->fast_corr) return tm_fast_correlate(p, y1, y2, nullptr, tf, batch, r1, r2, resid, s);
     if (!corr_in_smem(p)) {
         tm_set_error("tm_correlate: transform length %lld x %d primes exceeds shared memory (large path not built)",
                      (long long)(p->L1 > p->L2 ? p->L1 : p->L2), p->n_primes);
@@ -529,6 +536,7 @@ int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const 
     CorrArgs A;
     A.y[0] = (const int32_t *)y1; A.y[1] = (const int32_t *)y2;
     A.len_y[0] = p->len_y1; A.len_y[1] = p->len_y2;
+    A.nload[0] = p->nload1; A.nload[1] = p->nload2;
     A.M[0] = p->M1; A.M[1] = p->M2; A.K = p->K;
     A.logL[0] = p->logL1; A.logL[1] = p->logL2;
     A.tf_slot[0] = 0; A.tf_slot[1] = (p->L1 == p->L2) ? 0 : (int)p->L1;

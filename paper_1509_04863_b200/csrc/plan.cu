@@ -97,7 +97,11 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
                      (long long)M1, (long long)M2, (long long)N, (long long)kmin);
         return TM_EINVAL;
     }
-    int64_t L1 = int64_t(1) << ilog2_ceil(M1 + K - 1);
+    // y1 is M1-periodic when M1 | N (y1[M1 + c] = y1[c]): then a cyclic transform of
+    // length exactly M1 suffices if M1 is a power of two; otherwise zero-pad to
+    // L >= M + K - 1 so that no needed term wraps.
+    const bool cyc1 = (N % M1 == 0) && ((M1 & (M1 - 1)) == 0);
+    int64_t L1 = cyc1 ? M1 : int64_t(1) << ilog2_ceil(M1 + K - 1);
     int64_t L2 = int64_t(1) << ilog2_ceil(M2 + K - 1);
     if (ilog2_ceil(M2 + K - 1) > TM_MAX_LOGL) {
         tm_set_error("tm_plan_create: correlation length %lld exceeds this build's 2^%d", (long long)L2, TM_MAX_LOGL);
@@ -117,7 +121,9 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
     p->s1 = p->q1 * M1 - N; p->s2 = p->q2 * M2 - N;
     p->len_y1 = M1 + K; p->len_y2 = M2 + K;
     p->L1 = L1; p->L2 = L2;
-    p->logL1 = ilog2_ceil(M1 + K - 1); p->logL2 = ilog2_ceil(M2 + K - 1);
+    p->logL1 = ilog2_ceil(L1); p->logL2 = ilog2_ceil(L2);
+    p->nload1 = cyc1 ? M1 : M1 + K - 1;
+    p->nload2 = M2 + K - 1;
     p->dtype = dtype; p->flags = flags; p->seed = seed;
     p->device = dev; p->num_sms = sms;
     p->crt_inv = inv_mod(M1, M2);
@@ -129,9 +135,15 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
         double tmax = (flags & TM_BINARY) ? 1.0 : 128.0;
         double bound = (double)K * tmax * (double)(p->q1 > p->q2 ? p->q1 : p->q2) * tmax;
         p->n_primes = (bound < (double)(TM_PRIMES[0] / 2) - 1.0) ? 1 : 2;
-        int64_t per_prime = L1 + (L2 != L1 ? L2 : 0);
-        p->tf_elems = per_prime;
-        p->tf_bytes = per_prime * p->n_primes * 8;  // uint2 (value, Shoup companion)
+        p->fast_corr = tm_fast_corr_ok(p);
+        if (p->fast_corr) {  // u32 Montgomery spectra in the fast kernel's register order
+            p->tf_elems = L1 + L2;
+            p->tf_bytes = (L1 + L2) * p->n_primes * 4;
+        } else {             // uint2 (value, Shoup companion), natural bit-reversed order
+            int64_t per_prime = L1 + (L2 != L1 ? L2 : 0);
+            p->tf_elems = per_prime;
+            p->tf_bytes = per_prime * p->n_primes * 8;
+        }
         tm_ntt_tables t;
         int rc = tm_ntt_tables_get(dev, &t);
         if (rc != TM_OK) { free(p); return rc; }

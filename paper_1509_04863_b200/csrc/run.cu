@@ -46,11 +46,19 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
     int rc = tm_fold_impl(p, x, ldx, batch, 0, p->N, W.y1, W.y2, 0, W.fold_ws, s);     // step 3
     if (rc) return rc;
     tm_prof_mark(1, s);
-    rc = tm_fold_template(p, t, batch, W.tf, stream);                                // step 4 (+5 for t)
-    if (rc) return rc;
-    tm_prof_mark(2, s);
-    rc = tm_correlate_impl(p, W.y1, W.y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, s);  // 5-7
-    if (rc) return rc;
+    if (p->fast_corr) {
+        // steps 4-7 in one kernel per modulus: the template spectrum is computed in
+        // registers next to the signal's (no tf round trip through HBM)
+        tm_prof_mark(2, s);
+        rc = tm_fast_correlate(p, W.y1, W.y2, t, nullptr, batch, nullptr, nullptr, W.resid, s);
+        if (rc) return rc;
+    } else {
+        rc = tm_fold_template(p, t, batch, W.tf, stream);                            // step 4 (+5 for t)
+        if (rc) return rc;
+        tm_prof_mark(2, s);
+        rc = tm_correlate_impl(p, W.y1, W.y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, s);  // 5-7
+        if (rc) return rc;
+    }
     tm_prof_mark(3, s);
     rc = tm_crt_impl(p, W.resid, batch, residues, k, s);                              // steps 8-9
     tm_prof_mark(4, s);

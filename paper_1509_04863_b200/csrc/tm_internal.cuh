@@ -13,6 +13,8 @@ struct tm_plan_s {
     int64_t N, K, M1, M2, q1, q2, s1, s2, len_y1, len_y2;
     int64_t L1, L2;
     int logL1, logL2;
+    int64_t nload1, nload2;  // entries of y_j the correlation reads (cyclic y1: M1)
+    int fast_corr;       // register-resident NTT kernels (corr_fast.cu) usable
     int n_primes;
     int dtype;
     uint32_t flags;
@@ -42,6 +44,7 @@ void tm_prof_mark(int stage, cudaStream_t s);
 struct tm_ntt_tables {
     const uint32_t *tw[2][2];   // [prime][dir] values,  per-length compact tables
     const uint32_t *tws[2][2];  // Shoup companions floor(w * 2^32 / p)
+    const uint2 *tw2[2][2];     // the same, interleaved (value, companion)
 };
 int tm_ntt_tables_get(int device, tm_ntt_tables *out);
 extern const uint32_t TM_PRIMES[2];
@@ -58,6 +61,10 @@ tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch);
 size_t tm_run_ws_bytes(const tm_plan_s *p, int64_t batch);  // run.cu
 
 // ---- internal launchers ----
+bool tm_fast_corr_ok(const tm_plan_s *p);
+int tm_fast_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf, cudaStream_t s);
+int tm_fast_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, const void *tf,
+                      int64_t batch, void *r1, void *r2, int32_t *resid, cudaStream_t s);
 int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset,
                  int64_t len, void *y1, void *y2, int accumulate, void *ws, cudaStream_t s);
 int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const void *tf,
