@@ -25,6 +25,8 @@
 //    extension entries k in [M, M+K) (strategy 1, D_{M+K}):
 //      y[M + c] = y[c] - x[c] + x[(c + s) mod N]  (exact identity of Eq. 2).
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "tm_internal.cuh"
 
@@ -225,11 +227,13 @@ __global__ void __launch_bounds__(PM_WARPS * 32, 2) fold_pm1(PmArgs a) {
     // ---- M2 counts: unwrapped diagonal d -> bin (d - (row0 + ra)) mod M2
     int32_t *c2 = a.counts + b * (a.M1 + a.M2) + a.M1;
     const int64_t g0 = a.row0 + ra;
+    int64_t bin0 = (d_min - g0) % a.M2;   // once per CTA
+    if (bin0 < 0) bin0 += a.M2;
     for (int i = threadIdx.x; i < n_sm; i += blockDim.x) {
         int v = sm_y2[i];
         if (v) {
-            int64_t bin = (d_min + i - g0) % a.M2;
-            if (bin < 0) bin += a.M2;
+            int64_t bin = bin0 + i;
+            while (bin >= a.M2) bin -= a.M2;
             atomicAdd(&c2[bin], v);
         }
     }
@@ -250,9 +254,11 @@ __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t
         int64_t rel = pos - offset;
         return (rel >= 0 && rel < len) ? (int32_t)xb[rel] : 0;
     };
-    // base bin of M2 k: elements = rows - [the row g* = (M1 - k) mod M2 is in the chunk]
+    // base bin of M2 k < M2: elements = rows - [the row g* = (M1 - k) mod M2 is in the chunk]
+    // (M1 - k lies in [-1, M1], so the reduction is one conditional add: no division)
+    const int64_t s2 = q2 * M2 - N;
     auto base2 = [&](int64_t k) -> int32_t {
-        int64_t gs = (M1 - k) % M2;
+        int64_t gs = M1 - k;
         if (gs < 0) gs += M2;
         int32_t n = (int32_t)rows - ((gs >= row0 && gs < row0 + rows) ? 1 : 0);
         int32_t v = n - c2[k];
@@ -272,7 +278,9 @@ __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t
             v = base2(k);
         } else {
             int64_t c = k - M2;                  // extension: y2[M2+c] = y2[c] - x[c] + x[c+s2]
-            v = base2(c) - xat(c) + xat((c + (q2 * M2 - N)) % N);
+            int64_t e = c + s2;
+            if (e >= N) e -= N;
+            v = base2(c) - xat(c) + xat(e);
         }
         if (accumulate) o2[k] += v; else o2[k] = v;
     }
@@ -299,7 +307,33 @@ int pick_row_chunks(const tm_plan_s *p, int64_t batch, int64_t rows, int64_t n_g
     return (int)best;
 }
 
+// Work split for the persistent TMA kernel (one CTA per SM): the fewest row
+// chunks per (pair, column group) whose item count spreads over the SMs with
+// < 5% imbalance (items are equal-sized), rows per item in [128, 1024].
+void pick_rows_tma(const tm_plan_s *p, int64_t batch, int64_t rows, int64_t n_groups, int64_t *R_out,
+                   int64_t *nrc_out) {
+    const int64_t slots = p->num_sms;
+    int64_t bestR = 0, bestN = 0;
+    double best_eff = -1.0;
+    for (int64_t n = (rows + 1023) / 1024; n <= rows; ++n) {
+        const int64_t R = ((rows + n - 1) / n + 15) / 16 * 16;
+        const int64_t nrc = (rows + R - 1) / R;
+        if (nrc != n && n > 1) continue;
+        const int64_t items = batch * n_groups * nrc;
+        const int64_t g = items < slots ? items : slots;
+        const double eff = ((double)items / (double)g) / (double)((items + g - 1) / g) * ((double)g / slots);
+        if (eff > best_eff + 1e-9) { best_eff = eff; bestR = R; bestN = nrc; }
+        if (eff >= 0.95 || (R < 128 && bestN)) break;
+    }
+    *R_out = bestR;
+    *nrc_out = bestN;
+}
+
 }  // namespace
+
+int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
+                void *y1, void *y2, int accumulate, void *ws, int64_t R, int64_t n_rc, cudaStream_t s,
+                bool *used_counts);
 
 int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset,
                  int64_t len, void *y1, void *y2, int accumulate, void *ws, cudaStream_t s) {
@@ -307,6 +341,24 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
     const bool aligned = ((uintptr_t)x % 16 == 0) && (ldx % 16 == 0);
     const bool fast = p->fast_fold && aligned && (offset % p->M1 == 0) && (len % p->M1 == 0) &&
                       batch <= (int64_t(1) << 31) / 64;
+    static const bool use_regs = getenv("TM_FOLD_KERNEL") && !strcmp(getenv("TM_FOLD_KERNEL"), "regs");
+    if (fast && len > 0 && !use_regs) {
+        int64_t R = 0, nrc = 0;
+        const int64_t rows = len / p->M1, n_groups = (p->M1 + PM_COLS - 1) / PM_COLS;
+        pick_rows_tma(p, batch, rows, n_groups, &R, &nrc);
+        bool used_counts = false;
+        int rc = tm_fold_tma(p, x, ldx, batch, offset, len, y1, y2, accumulate, ws, R, nrc, s, &used_counts);
+        if (rc != TM_EUNSUPPORTED) {
+            if (rc != TM_OK || !used_counts) return rc;
+            tm_ws_layout L = tm_ws(p, batch);
+            int64_t gx = (p->M2 + p->K + 255) / 256;
+            fold_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(
+                (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, offset / p->M1, rows,
+                (const int32_t *)((char *)ws + L.fold_counts), (int32_t *)y1, (int32_t *)y2, accumulate);
+            TM_CHECK_LAUNCH("tm_fold: fold_finalize");
+            return TM_OK;
+        }
+    }
     if (fast && len > 0) {
         tm_ws_layout L = tm_ws(p, batch);
         int32_t *counts = (int32_t *)((char *)ws + L.fold_counts);

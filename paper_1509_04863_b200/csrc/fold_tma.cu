@@ -1,0 +1,458 @@
+// fold_tma.cu -- the packed +-1 fold (Algorithm 1 step 3, Eq. 2,
+// P:117-120) as a persistent, warp-specialised kernel fed by bulk-async (TMA)
+// copies through a shared-memory ring.
+//
+// Arithmetic is the one documented in fold.cu (fold_pm1): rows of M1 columns,
+// M1 bin = column, M2 bin = (column - row) mod M2 (anti-diagonal), counts of
+// negatives two at a time in byte lanes (b & 0x02), class accumulators by row
+// mod 4 with one funnel-shift combine per 16-row tile, systolic lane -> lane+1
+// hand-off of finished 16-bin blocks.
+//
+// What changes here is the memory side:
+//  * one CTA per SM loops over work items (pair, 4096-column group, row range);
+//  * warp 8 (one elected lane) streams 8-row stages of the item into a 4-stage
+//    ring with cp.async.bulk + mbarrier transaction counts, running ahead across
+//    item boundaries, so HBM reads never wait for the consumers' arithmetic or
+//    for the per-item flush;
+//  * warps 0-7 read their 16x16-byte tiles with LDS.128 and release each stage
+//    as soon as it is in registers;
+//  * when an item is a whole pair (M1 <= 4096, full fold) the consumers write
+//    the finished y1/y2 directly (counts -> values, the mod-N wrap and the
+//    strategy-1 extension), so no workspace, memset or second kernel is needed.
+#include "tm_internal.cuh"
+
+namespace {
+
+constexpr int TW = 8;                 // consumer warps, one 512-column strip each
+constexpr int TCOLS = TW * 512;       // columns per CTA group
+constexpr int SROWS = 8;              // rows per ring stage
+constexpr int NST = 4;                // ring stages
+constexpr int STAGE_BYTES = SROWS * TCOLS;
+
+struct TmaArgs {
+    const int8_t *x;
+    int64_t ldx;
+    int64_t N, M1, M2, K, q2;
+    int64_t rows;        // rows in the chunk
+    int64_t row0;        // global row of the chunk's first row
+    int64_t R;           // rows per item
+    int64_t n_rc, n_groups, n_items;
+    int owner;           // items are whole pairs of a full fold: write y directly
+    int accumulate;
+    int acc_words;       // y2 accumulator words reserved in shared memory
+    int priv_stride;     // words per warp-private anti-diagonal array (512 + 16 ceil(R/16))
+    int32_t *counts;     // non-owner: [batch][M1 + M2]
+    int32_t *y1, *y2;    // owner outputs
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(TW * 32) : "memory"); }
+
+__device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, int sh) { return __funnelshift_r(lo, hi, sh); }
+
+struct Item {
+    int64_t b, gi, ra, nrow, cs_cta, width;
+};
+__device__ __forceinline__ Item decode(const TmaArgs &a, int64_t item) {
+    Item it;
+    const int64_t rc = item % a.n_rc;
+    item /= a.n_rc;
+    it.gi = item % a.n_groups;
+    it.b = item / a.n_groups;
+    it.ra = rc * a.R;
+    const int64_t rb = (it.ra + a.R < a.rows) ? it.ra + a.R : a.rows;
+    it.nrow = rb - it.ra;
+    it.cs_cta = it.gi * TCOLS;
+    it.width = (a.M1 - it.cs_cta < TCOLS) ? a.M1 - it.cs_cta : TCOLS;
+    return it;
+}
+
+constexpr int NE = 4;  // epilogue warps
+
+// comb(d): total count of unwrapped diagonal d (relative to the CTA's first column)
+// from the warp-private arrays of one buffer: only the <= 3 warps whose strip
+// [512 w - 16 ntile, 512 w + 511] contains d contribute.
+__device__ __forceinline__ int32_t comb_at(const int32_t *pv, int stride, int d, int ntile, int width) {
+    const int pad = 16 * ntile;
+    int wlo = (d - 511 + 511 + 512 * 64) / 512 - 64;  // ceil((d - 511) / 512)
+    if (wlo < 0) wlo = 0;
+    int whi = (d + pad) >> 9;                          // floor((d + pad) / 512)
+    const int wmax = (width >> 9) - 1;
+    if (whi > wmax) whi = wmax;
+    int32_t v = 0;
+    for (int w = wlo; w <= whi; ++w) {
+        const int j = d - 512 * w + pad;
+        if (j >= 0 && j < 512 + pad) v += pv[w * stride + j];
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *ring = smem;
+    int32_t *privb = reinterpret_cast<int32_t *>(smem + NST * STAGE_BYTES);  // [2][TW][priv_stride]
+    uint64_t *full = reinterpret_cast<uint64_t *>(privb + 2 * TW * a.priv_stride);
+    uint64_t *empty = full + NST;
+    uint64_t *pfull = empty + NST;   // [2]: consumers -> epilogue (count TW)
+    uint64_t *pempty = pfull + 2;    // [2]: epilogue -> consumers (count NE)
+    uint4 *xs = reinterpret_cast<uint4 *>(pempty + 2);  // owner epilogue: x[0 .. K + q)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], TW);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&pfull[b], TW);
+            mbar_init(&pempty[b], NE);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == TW) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+                const Item it = decode(a, item);
+                const int8_t *base = a.x + it.b * a.ldx + it.ra * a.M1 + it.cs_cta;
+                for (int64_t r0 = 0; r0 < it.nrow; r0 += SROWS) {
+                    const int nr = (int)((it.nrow - r0) < SROWS ? (it.nrow - r0) : SROWS);
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_expect_tx(&full[s], (uint32_t)(nr * it.width));
+                    uint8_t *dst = ring + s * STAGE_BYTES;
+                    if (it.width == a.M1) {  // rows are contiguous in global memory
+                        bulk_g2s(dst, base + r0 * a.M1, (uint32_t)(nr * it.width), &full[s]);
+                    } else {
+                        for (int r = 0; r < nr; ++r)
+                            bulk_g2s(dst + r * it.width, base + (r0 + r) * a.M1, (uint32_t)it.width, &full[s]);
+                    }
+                    if (++s == NST) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+        return;
+    }
+
+    if (warp > TW) {
+        // ------------------------------------------------------------ epilogue
+        const int et = threadIdx.x - (TW + 1) * 32;  // 0 .. NE*32-1
+        int pb = 0;
+        uint32_t pph = 0;
+        for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+            const Item it = decode(a, item);
+            const int ntile = (int)((it.nrow + 15) / 16);
+            const int width = (int)it.width;
+            mbar_wait(&pfull[pb], pph);
+            const int32_t *pv = privb + pb * TW * a.priv_stride;
+            if (a.owner) {
+                // whole pair, full fold: counts -> values, + wrap + extension, store y2
+                const int q = (int)it.nrow;  // = q1 = q2 (M1 | N)
+                // stage x[0 .. K + q) (all the wrap/extension terms read) with coalesced
+                // 16-byte loads: one memory latency per pair instead of one per bin
+                {
+                    const int nx = (int)((a.K + q + 15) / 16);
+                    const uint4 *src = reinterpret_cast<const uint4 *>(a.x + it.b * a.ldx);
+                    uint4 *dst = reinterpret_cast<uint4 *>(xs);
+                    for (int i = et; i < nx; i += NE * 32) dst[i] = src[i];
+                    asm volatile("bar.sync 2, %0;" ::"n"(NE * 32) : "memory");
+                }
+                const int8_t *xb = reinterpret_cast<const int8_t *>(xs);
+                int32_t *o2 = a.y2 + it.b * (a.M2 + a.K);
+                const int M2 = (int)a.M2, M1 = (int)a.M1, K = (int)a.K;
+                const int dlo = -16 * ntile;
+                for (int k = et; k < M2; k += NE * 32) {
+                    // bin k collects the unwrapped diagonals d = k and d = k - M2 (d >= dlo)
+                    int32_t C = comb_at(pv, a.priv_stride, k, ntile, width);
+                    if (k - M2 >= dlo) C += comb_at(pv, a.priv_stride, k - M2, ntile, width);
+                    int gs = M1 - k;
+                    if (gs < 0) gs += M2;
+                    int32_t v = q - (gs < q ? 1 : 0) - C;
+                    const int j = k - (M2 - q);  // mod-N wrap: bin M2 - q + j gets x[j]
+                    if (j >= 0) v += xb[j];
+                    if (a.accumulate) o2[k] += v; else o2[k] = v;
+                    if (k < K) {                 // y2[M2 + k] = y2[k] - x[k] + x[k + q]  (s2 = q)
+                        const int32_t e = v - xb[k] + xb[k + q];
+                        if (a.accumulate) o2[M2 + k] += e; else o2[M2 + k] = e;
+                    }
+                }
+                asm volatile("bar.sync 2, %0;" ::"n"(NE * 32) : "memory");  // xs reuse
+            } else {
+                int32_t *c2 = a.counts + it.b * (a.M1 + a.M2) + a.M1;
+                const int64_t g0 = a.row0 + it.ra;
+                const int dlo = -16 * ntile;
+                int64_t bin0 = ((int64_t)dlo + it.cs_cta - g0) % a.M2;
+                if (bin0 < 0) bin0 += a.M2;
+                for (int i = et; i < width - dlo; i += NE * 32) {
+                    const int v = comb_at(pv, a.priv_stride, dlo + i, ntile, width);
+                    if (v) {
+                        int64_t bin = bin0 + i;
+                        while (bin >= a.M2) bin -= a.M2;
+                        atomicAdd(&c2[bin], v);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pempty[pb]);
+            if (++pb == 2) { pb = 0; pph ^= 1; }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    // Per-warp private anti-diagonal arrays priv[w][0 .. 512 + 16*ntile): warp w's
+    // unwrapped diagonal d (relative to its strip start cs_w) lives at index
+    // d + 16*ntile.  Every index is written exactly once: lane 31's finished block
+    // of tile t (the chain output) and, after the last tile, each lane's low block
+    // plus its left neighbour's pending carry.  No atomics, no zero-fill.  The two
+    // buffers alternate between items; the epilogue warps turn one into y2 while
+    // the consumers fill the other.
+    int s = 0;
+    uint32_t ph = 0;
+    int pb = 0;
+    uint32_t pph = 0;
+    const uint32_t ring_u32 = smem_u32(ring);
+    for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+        const Item it = decode(a, item);
+        const int nrow = (int)it.nrow;
+        const int ntile = (nrow + 15) / 16;
+        const int width = (int)it.width;
+        const bool active = warp * 512 < width;
+        const int colb = warp * 512 + 16 * lane;  // byte column inside a stage row
+        int32_t *priv = privb + (pb * TW + warp) * a.priv_stride;
+        mbar_wait(&pempty[pb], pph ^ 1);
+        uint32_t y1w[8], carry[8], W[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { y1w[i] = 0; carry[i] = 0; W[i] = 0; }
+        uint32_t a1[4] = {0, 0, 0, 0};
+        for (int t = 0; t < ntile; ++t) {
+            uint32_t m[16][4];
+            const bool full_tile = (t * 16 + 16 <= nrow) && width == TCOLS;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const int rbase = t * 16 + half * 8;
+                if (rbase < nrow) {
+                    mbar_wait(&full[s], ph);
+                    const uint32_t st = ring_u32 + s * STAGE_BYTES + colb;
+                    if (full_tile) {
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            uint4 v;
+                            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                         : "r"(st + r * TCOLS));
+                            m[half * 8 + r][0] = v.x & 0x02020202u; m[half * 8 + r][1] = v.y & 0x02020202u;
+                            m[half * 8 + r][2] = v.z & 0x02020202u; m[half * 8 + r][3] = v.w & 0x02020202u;
+                        }
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            uint4 v = make_uint4(0, 0, 0, 0);
+                            if (active && rbase + r < nrow)
+                                asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                             : "r"(st + r * width));
+                            m[half * 8 + r][0] = v.x & 0x02020202u; m[half * 8 + r][1] = v.y & 0x02020202u;
+                            m[half * 8 + r][2] = v.z & 0x02020202u; m[half * 8 + r][3] = v.w & 0x02020202u;
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[s]);
+                    if (++s == NST) { s = 0; ph ^= 1; }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        m[half * 8 + r][0] = m[half * 8 + r][1] = m[half * 8 + r][2] = m[half * 8 + r][3] = 0u;
+                }
+            }
+            if (!active) continue;
+            // ---- M1: column sums in byte lanes
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                uint32_t sacc = a1[w];
+#pragma unroll
+                for (int r = 0; r < 16; r += 2) sacc = sacc + m[r][w] + m[r + 1][w];
+                a1[w] = sacc;
+            }
+            if ((t & 3) == 3 || t == ntile - 1) {
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    y1w[2 * w] += __byte_perm(a1[w], 0, 0x4140);
+                    y1w[2 * w + 1] += __byte_perm(a1[w], 0, 0x4342);
+                    a1[w] = 0;
+                }
+            }
+            // ---- M2: anti-diagonals (row r = 4 al + rho: byte j -> window byte 16 - r + j)
+            uint32_t A[4][8];
+#pragma unroll
+            for (int rho = 0; rho < 4; ++rho)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) A[rho][i] = 0;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int al = r >> 2, rho = r & 3;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) A[rho][4 - al + w] += m[r][w];
+            }
+            uint32_t Wn[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { Wn[i] = 0; Wn[4 + i] = W[i]; }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                uint32_t v = Wn[i] + A[0][i];
+                v += fsr(A[1][i], i < 7 ? A[1][i + 1] : 0u, 8);
+                v += fsr(A[2][i], i < 7 ? A[2][i + 1] : 0u, 16);
+                v += fsr(A[3][i], i < 7 ? A[3][i + 1] : 0u, 24);
+                W[i] = v;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, carry[i], 1);
+                const uint32_t add = __byte_perm(W[4 + (i >> 1)], 0, (i & 1) ? 0x4342 : 0x4140);
+                carry[i] = (lane ? v : 0u) + add;
+            }
+            if (lane == 31) {  // finished block of the whole warp: bins cs_w + 496 - 16 t + [0, 16)
+                int4 *dst = reinterpret_cast<int4 *>(priv + 496 - 16 * t + 16 * ntile);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    dst[i] = make_int4((int)(carry[2 * i] & 0xFFFFu), (int)(carry[2 * i] >> 16),
+                                       (int)(carry[2 * i + 1] & 0xFFFFu), (int)(carry[2 * i + 1] >> 16));
+            }
+        }
+        const int64_t c0 = it.cs_cta + warp * 512 + 16 * lane;
+        if (active) {
+            // drain: lane l's low block (bins 16 l - 16 ntile + [0,16)) + lane l-1's pending carry
+            uint32_t lo[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t c = __shfl_up_sync(0xffffffffu, carry[i], 1);
+                lo[i] = __byte_perm(W[i >> 1], 0, (i & 1) ? 0x4342 : 0x4140) + ((lane && ntile) ? c : 0u);
+            }
+            int4 *dst = reinterpret_cast<int4 *>(priv + 16 * lane);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                dst[i] = make_int4((int)(lo[2 * i] & 0xFFFFu), (int)(lo[2 * i] >> 16),
+                                   (int)(lo[2 * i + 1] & 0xFFFFu), (int)(lo[2 * i + 1] >> 16));
+            // M1 bins are owned by this lane: write them now
+            if (a.owner) {
+                const int32_t q = nrow;
+                int32_t v[16];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    v[2 * i] = q - (int32_t)(y1w[i] & 0xFFFFu);
+                    v[2 * i + 1] = q - (int32_t)(y1w[i] >> 16);
+                }
+                int32_t *o1 = a.y1 + it.b * (a.M1 + a.K);
+#pragma unroll
+                for (int rep = 0; rep < 2; ++rep) {  // y1[c] and y1[M1 + c] = y1[c] (M1 | N), c < K
+                    const int64_t base = rep ? a.M1 + c0 : c0;
+                    if (rep && c0 >= a.K) break;
+                    if (!rep || c0 + 16 <= a.K) {
+                        if ((((uintptr_t)(o1 + base)) & 15) == 0) {
+                            int4 *d0 = reinterpret_cast<int4 *>(o1 + base);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                int4 w = make_int4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                                if (a.accumulate) {
+                                    const int4 o = d0[i];
+                                    w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+                                }
+                                d0[i] = w;
+                            }
+                            continue;
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        if (rep && c0 + i >= a.K) break;
+                        if (a.accumulate) o1[base + i] += v[i]; else o1[base + i] = v[i];
+                    }
+                }
+            } else {
+                int32_t *cnt = a.counts + it.b * (a.M1 + a.M2);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    atomicAdd(&cnt[c0 + 2 * i], (int)(y1w[i] & 0xFFFFu));
+                    atomicAdd(&cnt[c0 + 2 * i + 1], (int)(y1w[i] >> 16));
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[pb]);
+        if (++pb == 2) { pb = 0; pph ^= 1; }
+    }
+}
+
+}  // namespace
+
+// Returns TM_OK after enqueueing, or TM_EUNSUPPORTED when the shape is not covered
+// (the caller then uses the register-streaming fold_pm1).
+int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
+                void *y1, void *y2, int accumulate, void *ws, int64_t R, int64_t n_rc, cudaStream_t s,
+                bool *used_counts) {
+    TmaArgs a{};
+    a.x = (const int8_t *)x; a.ldx = ldx;
+    a.N = p->N; a.M1 = p->M1; a.M2 = p->M2; a.K = p->K; a.q2 = p->q2;
+    a.rows = len / p->M1; a.row0 = offset / p->M1;
+    a.n_groups = (p->M1 + TCOLS - 1) / TCOLS;
+    a.R = R; a.n_rc = n_rc;
+    a.n_items = batch * a.n_groups * a.n_rc;
+    a.owner = (a.n_groups == 1 && a.n_rc == 1 && offset == 0 && len == p->N) ? 1 : 0;
+    a.accumulate = accumulate;
+    if (R > 1024) return TM_EUNSUPPORTED;
+    a.priv_stride = (int)(512 + (R + 15) / 16 * 16);
+    a.acc_words = TW * a.priv_stride;
+    tm_ws_layout L = tm_ws(p, batch);
+    a.counts = (int32_t *)((char *)ws + L.fold_counts);
+    a.y1 = (int32_t *)y1; a.y2 = (int32_t *)y2;
+    *used_counts = !a.owner;
+    if (!a.owner) {
+        cudaError_t e = cudaMemsetAsync(a.counts, 0, (size_t)batch * (p->M1 + p->M2) * 4, s);
+        if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: memset");
+    }
+    const size_t xs_bytes = a.owner ? (size_t)((p->K + R + 15) / 16 * 16) : 0;
+    const size_t smem = (size_t)NST * STAGE_BYTES + (size_t)2 * a.acc_words * 4 + (2 * NST + 4) * 8 + xs_bytes;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fold_pm1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    if (smem > 227 * 1024) return TM_EUNSUPPORTED;
+    int64_t grid = a.n_items < p->num_sms ? a.n_items : p->num_sms;
+    fold_pm1_tma<<<(unsigned)grid, (TW + 1 + NE) * 32, smem, s>>>(a);
+    TM_CHECK_LAUNCH("tm_fold: fold_pm1_tma");
+    return TM_OK;
+}

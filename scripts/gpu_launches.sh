@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q -x -rf > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+for w in ${WLS:-cfg2 cfg4a cfg4}; do
+timeout 300 python bench.py --workload $w --steps 100 --warmup 10 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_$w.log 2>&1; echo bench $w rc=$?
+done
+for w in ${WLS:-cfg2 cfg4a cfg4}; do
+CMD="python bench.py --workload $w --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
+$CMD > gpurun_out/plain_$w.log 2>&1 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_$w.csv $CMD > gpurun_out/ncu_$w.log 2>&1; echo ncu $w rc=$?
+done
