@@ -20,7 +20,7 @@
 
 namespace {
 
-constexpr uint32_t P1 = 2013265921u, P2 = 998244353u;
+constexpr uint32_t P1 = TM_P1, P2 = TM_P2;
 
 struct FastArgs {
     const int32_t *y;      // [batch][ldy]
@@ -53,14 +53,21 @@ __device__ __forceinline__ uint32_t mul_shoup(uint32_t a, uint32_t w, uint32_t w
     uint32_t r = a * w - q * p;
     return r >= p ? r - p : r;
 }
+// Lazy (Harvey) arithmetic, valid because 4p < 2^32:
+//   red2(s)  : [0, 4p) -> [0, 2p)        (one unsigned min)
+//   shoup_lz : a * w mod p into [0, 2p), any a < 2^32, w < p
+//   montmul  : a * b * 2^-32 mod p into [0, 2p) for a, b < 2p
+__device__ __forceinline__ uint32_t red2(uint32_t s, uint32_t p2) { return min(s, s - p2); }
+__device__ __forceinline__ uint32_t shoup_lz(uint32_t a, uint32_t w, uint32_t ws, uint32_t p) {
+    return a * w - __umulhi(a, ws) * p;
+}
 template <int PI>
 __device__ __forceinline__ uint32_t montmul(uint32_t a, uint32_t b) {
     constexpr uint32_t p = PI ? P2 : P1;
-    constexpr uint32_t pinv = PI ? 998244351u : 2013265919u;  // -p^{-1} mod 2^32 (checked on host)
+    constexpr uint32_t pinv = PI ? TM_P2_PINV : TM_P1_PINV;
     uint64_t t = (uint64_t)a * b;
     uint32_t m = (uint32_t)t * pinv;
-    uint32_t u = (uint32_t)((t + (uint64_t)m * p) >> 32);
-    return u >= p ? u - p : u;
+    return (uint32_t)((t + (uint64_t)m * p) >> 32);
 }
 
 // twiddle load; volatile so the compiler neither merges it with the identical load
@@ -117,9 +124,9 @@ __device__ __forceinline__ void dif(uint32_t (&v)[1 << LOGE], uint32_t *buf, int
             for (int m = 0; m < E; ++m) {
                 if (m & h) continue;
                 const uint2 w = wv[m & (h - 1)];
-                const uint32_t X = v[m], Y = v[m | h];
-                v[m] = add_p(X, Y, p);
-                v[m | h] = mul_shoup(X + p - Y, w.x, w.y, p);
+                const uint32_t X = v[m], Y = v[m | h];  // both in [0, 2p)
+                v[m] = red2(X + Y, 2 * p);
+                v[m | h] = shoup_lz(X + 2 * p - Y, w.x, w.y, p);
             }
         }
         transpose<LOGL, LOGE>(v, buf, t, k, k + 1);
@@ -134,8 +141,8 @@ __device__ __forceinline__ void dif(uint32_t (&v)[1 << LOGE], uint32_t *buf, int
         for (int m = 0; m < E; ++m) {
             const uint32_t o = __shfl_xor_sync(0xffffffffu, v[m], 1 << sb);
             const uint2 w = ldtw(tab + ((tl << LOGE) | m));
-            const uint32_t a = upper ? o + p - v[m] : v[m] + o;
-            v[m] = upper ? mul_shoup(a, w.x, w.y, p) : (a >= p ? a - p : a);
+            const uint32_t a = upper ? o + 2 * p - v[m] : v[m] + o;
+            v[m] = upper ? shoup_lz(a, w.x, w.y, p) : red2(a, 2 * p);
         }
     }
 #pragma unroll
@@ -150,8 +157,8 @@ __device__ __forceinline__ void dif(uint32_t (&v)[1 << LOGE], uint32_t *buf, int
             if (m & h) continue;
             const uint2 w = wv[m & (h - 1)];
             const uint32_t X = v[m], Y = v[m | h];
-            v[m] = add_p(X, Y, p);
-            v[m | h] = mul_shoup(X + p - Y, w.x, w.y, p);
+            v[m] = red2(X + Y, 2 * p);
+            v[m | h] = shoup_lz(X + 2 * p - Y, w.x, w.y, p);
         }
     }
 }
@@ -173,10 +180,10 @@ __device__ __forceinline__ void dit(uint32_t (&v)[1 << LOGE], uint32_t *buf, int
         for (int m = 0; m < E; ++m) {
             if (m & h) continue;
             const uint2 w = wv[m & (h - 1)];
-            const uint32_t X = v[m];
-            const uint32_t Yw = mul_shoup(v[m | h], w.x, w.y, p);
-            v[m] = add_p(X, Yw, p);
-            v[m | h] = sub_p(X, Yw, p);
+            const uint32_t X = red2(v[m], 2 * p);               // inputs in [0, 4p)
+            const uint32_t Yw = shoup_lz(v[m | h], w.x, w.y, p);
+            v[m] = X + Yw;                                       // outputs in [0, 4p)
+            v[m | h] = X + 2 * p - Yw;
         }
     }
 #pragma unroll
@@ -188,9 +195,9 @@ __device__ __forceinline__ void dit(uint32_t (&v)[1 << LOGE], uint32_t *buf, int
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const uint2 w = ldtw(tab + ((tl << LOGE) | m));
-            const uint32_t send = upper ? mul_shoup(v[m], w.x, w.y, p) : v[m];
+            const uint32_t send = upper ? shoup_lz(v[m], w.x, w.y, p) : red2(v[m], 2 * p);
             const uint32_t o = __shfl_xor_sync(0xffffffffu, send, 1 << sb);
-            v[m] = upper ? sub_p(o, send, p) : add_p(send, o, p);
+            v[m] = upper ? o + 2 * p - send : send + o;
         }
     }
 #pragma unroll
@@ -209,10 +216,10 @@ __device__ __forceinline__ void dit(uint32_t (&v)[1 << LOGE], uint32_t *buf, int
             for (int m = 0; m < E; ++m) {
                 if (m & h) continue;
                 const uint2 w = wv[m & (h - 1)];
-                const uint32_t X = v[m];
-                const uint32_t Yw = mul_shoup(v[m | h], w.x, w.y, p);
-                v[m] = add_p(X, Yw, p);
-                v[m | h] = sub_p(X, Yw, p);
+                const uint32_t X = red2(v[m], 2 * p);
+                const uint32_t Yw = shoup_lz(v[m | h], w.x, w.y, p);
+                v[m] = X + Yw;
+                v[m | h] = X + 2 * p - Yw;
             }
         }
     }
@@ -237,7 +244,7 @@ __device__ __forceinline__ void template_spectrum(uint32_t (&T)[1 << LOGE], uint
     }
     dif<LOGL, LOGE>(T, buf, t, A.twf[PI], p);
 #pragma unroll
-    for (int m = 0; m < G::E; ++m) T[m] = mul_shoup(T[m], A.cL[PI], A.cLs[PI], p);
+    for (int m = 0; m < G::E; ++m) T[m] = shoup_lz(T[m], A.cL[PI], A.cLs[PI], p);  // [0, 2p)
 }
 
 // separate register allocation for the template transform (noinline)
@@ -270,8 +277,13 @@ __device__ __forceinline__ void correlate_one_prime(uint32_t (&v)[1 << LOGE], ui
     dif<LOGL, LOGE>(v, buf, t, A.twf[PI], p);
     const uint32_t *src = FROM_T ? Ts : A.tf + (b * A.np + PI) * A.tf_prime + A.tf_off;
 #pragma unroll
-    for (int m = 0; m < G::E; ++m) v[m] = montmul<PI>(v[m], src[m * G::NT + t]);
+    for (int m = 0; m < G::E; ++m) v[m] = montmul<PI>(v[m], src[m * G::NT + t]);  // [0, 2p)
     dit<LOGL, LOGE>(v, buf, t, A.twi[PI], p);
+#pragma unroll
+    for (int m = 0; m < G::E; ++m) {  // [0, 4p) -> [0, p)
+        const uint32_t r = red2(v[m], 2 * p);
+        v[m] = min(r, r - p);
+    }
 }
 
 __device__ __forceinline__ void amax(int64_t &bv, int32_t &bi, int64_t v, int32_t i) {
@@ -312,7 +324,7 @@ __global__ void __launch_bounds__(1 << (LOGL - LOGE), min_blocks<LOGL, LOGE>()) 
             // r = a1 + p1 * ((a2 - a1) p1^{-1} mod p2), centred in (-p1 p2 / 2, p1 p2 / 2]
             const uint64_t a1 = keep[m * G::NT + t], a2 = v[m];
             const uint64_t d = (a2 + P2 - (a1 % P2)) % P2;
-            const uint64_t u = (d * 49499719ull) % P2;
+            const uint64_t u = (d * TM_P1_INV_MOD_P2) % P2;
             const uint64_t z = a1 + (uint64_t)P1 * u;
             const uint64_t PP = (uint64_t)P1 * P2;
             val = z > PP / 2 ? (int64_t)(z - PP) : (int64_t)z;

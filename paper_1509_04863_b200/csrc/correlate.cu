@@ -7,7 +7,7 @@
 //
 // Integer data (TM_I8) is correlated EXACTLY with a number-theoretic
 // transform: cyclic correlation of length L_j >= M_j + K - 1 (so no needed
-// term wraps) modulo p1 = 15*2^27+1 and, when the bound |r| <= K*max|t|*
+// term wraps) modulo p1 = 479*2^21+1 and, when the bound |r| <= K*max|t|*
 // max|y| reaches p1/2, also p2 = 119*2^23+1 with an exact CRT combine.
 // Forward transforms are decimation-in-frequency (natural in, bit-reversed
 // out), the inverse is decimation-in-time (bit-reversed in, natural out), so
@@ -25,8 +25,8 @@
 
 #include "tm_internal.cuh"
 
-const uint32_t TM_PRIMES[2] = {2013265921u, 998244353u};  // 15*2^27+1, 119*2^23+1
-static const uint32_t TM_GENERATORS[2] = {31u, 3u};
+const uint32_t TM_PRIMES[2] = {TM_P1, TM_P2};
+static const uint32_t TM_GENERATORS[2] = {3u, 3u};
 
 namespace {
 
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(1024) template_ntt_kernel(TfArgs A) {
     if (li >= A.n_len) return;
     const int logL = A.logL[li];
     const int64_t L = int64_t(1) << logL;
-    const uint32_t p = pi ? 998244353u : 2013265921u;
+    const uint32_t p = pi ? TM_P2 : TM_P1;
     uint32_t *a = A.use_smem ? sm
                              : A.scratch + ((b * A.n_primes + pi) * 2 + li) * (int64_t(1) << A.logL[A.n_len - 1]);
     const int8_t *t = A.t + b * A.K;
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(1024) corr_ntt_kernel(CorrArgs A) {
     const int32_t *y = A.y[j] + b * A.len_y[j];
     const int64_t nload = A.nload[j];  // y[0 .. M+K-2] (y[M+K-1] is never needed), or M (cyclic y1)
     for (int pi = 0; pi < A.n_primes; ++pi) {
-        const uint32_t p = pi ? 998244353u : 2013265921u;
+        const uint32_t p = pi ? TM_P2 : TM_P1;
         for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
             int32_t v = (i < nload) ? y[i] : 0;
             int64_t m = (int64_t)v % (int64_t)p;
@@ -275,8 +275,8 @@ __global__ void __launch_bounds__(1024) corr_ntt_kernel(CorrArgs A) {
     // signed reconstruction, output, argmax
     int64_t bv = INT64_MIN, bi = INT64_MAX;
     int64_t *rout = A.r[j] ? A.r[j] + b * M : nullptr;
-    const uint64_t p1 = 2013265921u, p2 = 998244353u;
-    const uint64_t inv_p1_mod_p2 = 49499719u;   // p1^{-1} mod p2 (tests/test_abi.py checks it)
+    const uint64_t p1 = TM_P1, p2 = TM_P2;
+    const uint64_t inv_p1_mod_p2 = TM_P1_INV_MOD_P2;
     for (int64_t k = threadIdx.x; k < M; k += blockDim.x) {
         int64_t v;
         if (A.n_primes == 1) {

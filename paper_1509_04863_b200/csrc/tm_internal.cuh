@@ -40,7 +40,15 @@ void tm_count_launch();
 // stage-boundary events of tm_run (tm_profile_events); NULL when disabled
 void tm_prof_mark(int stage, cudaStream_t s);
 
-// ---- NTT constants (ntt.cu) ----
+// ---- NTT constants ----
+// Two NTT-friendly primes below 2^30 (so that 4p < 2^32 and butterflies can keep
+// residues lazily in [0, 2p) / [0, 4p)): p1 = 479*2^21+1 (transforms up to 2^21),
+// p2 = 119*2^23+1; both have primitive root 3.  tests/test_abi.py re-derives them.
+#define TM_P1 1004535809u
+#define TM_P2 998244353u
+#define TM_P1_PINV 1004535807u   // -p1^{-1} mod 2^32 (Montgomery)
+#define TM_P2_PINV 998244351u    // -p2^{-1} mod 2^32
+#define TM_P1_INV_MOD_P2 332747959ull
 struct tm_ntt_tables {
     const uint32_t *tw[2][2];   // [prime][dir] values,  per-length compact tables
     const uint32_t *tws[2][2];  // Shoup companions floor(w * 2^32 / p)

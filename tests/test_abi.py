@@ -65,12 +65,21 @@ def test_plan_create_rejects_invalid_without_gpu(libtm):
 
 
 def test_ntt_constants():
-    """Host-side check of the constants the NTT kernels hard-code."""
-    src = open(os.path.join(ROOT, "paper_1509_04863_b200", "csrc", "correlate.cu")).read()
-    p1, p2 = 2013265921, 998244353
-    assert p1 == 15 * 2 ** 27 + 1 and p2 == 119 * 2 ** 23 + 1
-    assert "49499719u" in src and pow(p1, -1, p2) == 49499719
-    for g, p in ((31, p1), (3, p2)):
+    """Host-side check of the constants the NTT kernels hard-code (tm_internal.cuh)."""
+    src = open(os.path.join(ROOT, "paper_1509_04863_b200", "csrc", "tm_internal.cuh")).read()
+    consts = dict(re.findall(r"#define (TM_P\w+) (\d+)u", src))
+    p1, p2 = int(consts["TM_P1"]), int(consts["TM_P2"])
+    assert p1 == 479 * 2 ** 21 + 1 and p2 == 119 * 2 ** 23 + 1
+    assert p1 < 2 ** 30 and p2 < 2 ** 30          # lazy reduction needs 4p < 2^32
+    assert int(consts["TM_P1_PINV"]) == (-pow(p1, -1, 2 ** 32)) % 2 ** 32
+    assert int(consts["TM_P2_PINV"]) == (-pow(p2, -1, 2 ** 32)) % 2 ** 32
+    assert int(re.search(r"TM_P1_INV_MOD_P2 (\d+)ull", src).group(1)) == pow(p1, -1, p2)
+    for p, fs in ((p1, (2, 479)), (p2, (2, 7, 17))):
+        assert all((p - 1) % f == 0 for f in fs)
         n = p - 1
-        fs = {f for f in (2, 3, 5, 7, 17) if n % f == 0}
-        assert all(pow(g, n // f, p) != 1 for f in fs)
+        m = n
+        for f in fs:
+            while m % f == 0:
+                m //= f
+        assert m == 1                                # complete factorisation of p - 1
+        assert all(pow(3, n // f, p) != 1 for f in fs)  # 3 is a primitive root
