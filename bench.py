@@ -38,6 +38,10 @@ WORKLOADS = {
                   desc="cfg4: N=2^24, K=8192, batch 64, +-1 int8, 20% flips"),
     "cfg4": dict(N=2 ** 24, K=16384, B=64, dtype="int8", noise=0.2, seed=4,
                  desc="cfg4: N=2^24, K=16384, batch 64, +-1 int8, 20% flips"),
+    # one signal split into contiguous row-aligned chunks over the ranks (strong scaling)
+    "cfg5": dict(N=2 ** 31, K=65536, B=1, dtype="int8", noise=0.05, seed=5, single=True,
+                 desc="cfg5: one signal N=2^31 (+-1 int8, 2 GiB), K=65536, 5% flips, split over the GPUs; "
+                      "partial folds summed by one NCCL all-reduce"),
 }
 METRIC = "signal Gsamples/s matched (1/2/4/8 B200) and % of HBM roofline; match success rate"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
@@ -199,6 +203,8 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if wl.get("single"):
+        return run_single_signal(args, wl, rank, world, local, dev)
     N, K, B = wl["N"], wl["K"], wl["B"]
     plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"])
     stream = torch.cuda.current_stream()
@@ -328,6 +334,127 @@ def main():
         "gpu_launches": launches,
     }
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_single_signal(args, wl, rank, world, local, dev):
+    """cfg5: each rank folds its chunk of the one signal (global positions), the
+    partial folds are summed with one all-reduce, every rank correlates/matches."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1509_04863_b200 as tm
+    from paper_1509_04863_b200 import dist as tmdist
+
+    N, K = wl["N"], wl["K"]
+    plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"])
+    stream = torch.cuda.current_stream()
+    off, ln = tmdist.signal_chunks(N, plan.M1, world)[rank]
+    x, t, k0 = plan.generate(0, 1, wl["noise"], offset=off, length=ln, device=dev)
+    ws = plan.workspace(1, dev)
+    y1 = torch.empty((1, plan.len_y1), dtype=torch.int32, device=dev)
+    y2 = torch.empty((1, plan.len_y2), dtype=torch.int32, device=dev)
+    res = torch.empty((1, 2), dtype=torch.int32, device=dev)
+    k = torch.empty(1, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize()
+
+    def step(ev=None):
+        if ev: ev[0].record(stream)
+        plan.fold(x, offset=off, length=ln, y1=y1, y2=y2, accumulate=False, ws=ws, stream=stream)
+        if ev: ev[1].record(stream)
+        if world > 1:
+            tmdist.allreduce_folds(y1, y2)
+        if ev: ev[2].record(stream)
+        plan.correlate_match(y1, y2, t, residues=res, k=k, ws=ws, stream=stream)
+        if ev: ev[3].record(stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = tm.launch_count()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for i in range(args.steps):
+            step(ev[i])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    launches = tm.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    ms_max = tmdist.max_over_ranks(start.elapsed_time(stop), device=dev)
+    st = [statistics.mean(e[i].elapsed_time(e[i + 1]) for e in ev) for i in range(3)]
+    fold_ms = tmdist.max_over_ranks(st[0], device=dev)
+    # e2e: the chunk copied from pinned host memory every step, k read back
+    e2e = None
+    if args.e2e_steps > 0:
+        xh = torch.empty((1, ln), dtype=torch.int8, pin_memory=True)
+        xh.copy_(x.cpu())
+        xd = torch.empty_like(x)
+        kh = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            xd.copy_(xh, non_blocking=True)
+            plan.fold(xd, offset=off, length=ln, y1=y1, y2=y2, ws=ws, stream=stream)
+            if world > 1:
+                tmdist.allreduce_folds(y1, y2)
+            plan.correlate_match(y1, y2, t, residues=res, k=k, ws=ws, stream=stream)
+            kh.copy_(k, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = tmdist.max_over_ranks(e0.elapsed_time(e1), device=dev)
+        e2e = {"value": N * args.e2e_steps / (e_ms * 1e-3) / 1e9, "unit": "Gsamples/s",
+               "h2d_bytes_per_step": ln, "d2h_bytes_per_step": 8, "steps": args.e2e_steps}
+        del xh, xd
+    success = float((k == k0).double().item())
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        fold_bytes = ln + (plan.len_y1 + plan.len_y2) * 4
+        achieved = fold_bytes / (fold_ms * 1e-3) / 1e9
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            # the oracle's Eq. 2 fold of cfg5 alone is minutes of CPU: report the
+            # oracle on a bounded sample (the fold of 2^-6 of the signal's rows)
+            import numpy as np
+            import time as _t
+            import oracle
+            import tmgen
+            n_s = N // 64
+            xs = tmgen.signal(wl["seed"], 0, N, lo=0, length=n_s)
+            t0 = _t.perf_counter()
+            oracle.fold(xs, plan.M1, K)
+            oracle.fold(xs, plan.M2, K)
+            dt = _t.perf_counter() - t0
+            cpu = {"value": n_s / dt / 1e9, "unit": "Gsamples/s", "cores": 1, "kind": "oracle",
+                   "sample": f"oracle Eq. 2 folds (M1 and M2) of the first 2^25 samples of the cfg5 signal "
+                             f"taken as a signal of length 2^25 (correlation excluded: K=65536 is minutes of "
+                             f"CPU), {dt:.1f} s"}
+        line = {
+            "metric": METRIC, "value": N * args.steps / (ms_max * 1e-3) / 1e9, "unit": "Gsamples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i8",
+            "data": "synthetic (seeded counter-based generator, chunks generated on each rank's device)",
+            "config": {"workload": wl["desc"], "N": N, "K": K, "M1": plan.M1, "M2": plan.M2, "chunk_samples": ln,
+                       "parallelism": f"sequence split over {world} rank(s) + NCCL all-reduce of y1||y2 "
+                                      f"({(plan.len_y1 + plan.len_y2) * 4} B)",
+                       "l2": "no flush: per-rank input > 126 MB L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "kernel": "tm_fold (fold_pm1_tma + fold_finalize)",
+                         "algorithmic_bytes_per_launch": fold_bytes, "peak_source": peak_src, "fold_ms": fold_ms},
+            "stage_ms": {"fold": st[0], "allreduce": st[1], "correlate_match": st[2]},
+            "success_rate": success, "k": int(k.item()), "k0": int(k0.item()),
+            "cpu_baseline": cpu, "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

@@ -177,6 +177,15 @@ int tm_run(tm_plan plan, const void *x, int64_t ldx, const void *t, int64_t batc
            int32_t *residues, int64_t *k, void *ws, void *stream);
 
 /*
+ * tm_correlate_match -- Alg. 1 steps 4-9 on already-folded vectors (the part
+ * of tm_run after the fold): used after partial folds of one signal split over
+ * several GPUs have been summed (all-reduce).  y1, y2 as produced by tm_fold
+ * over the whole of [0, N); t [batch][K]; outputs as tm_match; ws as tm_run.
+ */
+int tm_correlate_match(tm_plan plan, const void *y1, const void *y2, const void *t, int64_t batch,
+                       int32_t *residues, int64_t *k, void *ws, void *stream);
+
+/*
  * tm_run_host -- tm_run on HOST buffers: copies x_host/t_host (pinned memory
  * recommended) to the caller's device staging buffers in chunks of
  * `chunk` pairs, overlapping the copy of chunk i+1 with the compute of chunk

@@ -13,7 +13,7 @@ TM_OK, TM_EINVAL, TM_EUNSUPPORTED, TM_ECUDA = 0, 1, 2, 3
 
 EXPORTED_SYMBOLS = (
     "tm_plan_create", "tm_plan_query", "tm_workspace_bytes", "tm_plan_destroy", "tm_generate",
-    "tm_fold", "tm_fold_template", "tm_correlate", "tm_match", "tm_run", "tm_run_host",
+    "tm_fold", "tm_fold_template", "tm_correlate", "tm_match", "tm_run", "tm_run_host", "tm_correlate_match",
     "tm_status_string", "tm_last_error", "tm_launch_count", "tm_profile_events",
 )
 
@@ -72,6 +72,8 @@ def lib():
         L.tm_match.argtypes = [_p, _p, _p, _i64, _p, _p, _p]
         L.tm_run.restype = ctypes.c_int
         L.tm_run.argtypes = [_p, _p, _i64, _p, _i64, _p, _p, _p, _p]
+        L.tm_correlate_match.restype = ctypes.c_int
+        L.tm_correlate_match.argtypes = [_p, _p, _p, _p, _i64, _p, _p, _p, _p]
         L.tm_run_host.restype = ctypes.c_int
         L.tm_run_host.argtypes = [_p, _p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p]
         L.tm_launch_count.restype = _u64
@@ -201,7 +203,8 @@ class Plan:
             r1 = torch.empty((batch, self.M1), dtype=self.r_dtype, device=y1.device)
         if r2 is None:
             r2 = torch.empty((batch, self.M2), dtype=self.r_dtype, device=y1.device)
-        _check(lib().tm_correlate(self._h, _ptr(y1), _ptr(y2), _ptr(tf), batch, _ptr(r1), _ptr(r2), None,
+        ws = self.workspace(batch, y1.device)
+        _check(lib().tm_correlate(self._h, _ptr(y1), _ptr(y2), _ptr(tf), batch, _ptr(r1), _ptr(r2), _ptr(ws),
                                   _stream(stream)), "tm_correlate")
         return r1, r2
 
@@ -227,6 +230,20 @@ class Plan:
             ws = self.workspace(batch, x.device)
         _check(lib().tm_run(self._h, _ptr(x), x.stride(0), _ptr(t), batch, _ptr(residues), _ptr(k), _ptr(ws),
                             _stream(stream)), "tm_run")
+        return residues, k
+
+    def correlate_match(self, y1, y2, t, residues=None, k=None, ws=None, stream=None):
+        """tm_correlate_match: steps 4-9 on already-folded (e.g. all-reduced) y1, y2."""
+        import torch
+        batch = y1.shape[0]
+        if residues is None:
+            residues = torch.empty((batch, 2), dtype=torch.int32, device=y1.device)
+        if k is None:
+            k = torch.empty(batch, dtype=torch.int64, device=y1.device)
+        if ws is None:
+            ws = self.workspace(batch, y1.device)
+        _check(lib().tm_correlate_match(self._h, _ptr(y1), _ptr(y2), _ptr(t), batch, _ptr(residues), _ptr(k),
+                                        _ptr(ws), _stream(stream)), "tm_correlate_match")
         return residues, k
 
     def run_host(self, x_host, t_host, chunk: int, residues_host, k_host, dev_x, dev_t, dev_out, ws, stream=None):

@@ -41,18 +41,6 @@ struct FastArgs {
     int jmod;              // 0 or 1 (column in resid)
 };
 
-__device__ __forceinline__ uint32_t add_p(uint32_t a, uint32_t b, uint32_t p) {
-    uint32_t s = a + b;
-    return s >= p ? s - p : s;
-}
-__device__ __forceinline__ uint32_t sub_p(uint32_t a, uint32_t b, uint32_t p) {
-    return a >= b ? a - b : a + p - b;
-}
-__device__ __forceinline__ uint32_t mul_shoup(uint32_t a, uint32_t w, uint32_t ws, uint32_t p) {
-    uint32_t q = __umulhi(a, ws);
-    uint32_t r = a * w - q * p;
-    return r >= p ? r - p : r;
-}
 // Lazy (Harvey) arithmetic, valid because 4p < 2^32:
 //   red2(s)  : [0, 4p) -> [0, 2p)        (one unsigned min)
 //   shoup_lz : a * w mod p into [0, 2p), any a < 2^32, w < p

@@ -481,6 +481,7 @@ extern "C" __attribute__((visibility("default"))) int tm_fold_template(tm_plan p
     }
     if (batch > 0x7FFFFFFF) { tm_set_error("tm_fold_template: batch too large"); return TM_EUNSUPPORTED; }
     if (p->fast_corr) return tm_fast_template(p, t, batch, tf, s);
+    if (p->big_corr) return tm_gntt_template(p, t, batch, tf, s);
     TfArgs A;
     A.t = (const int8_t *)t; A.K = p->K;
     A.logL[0] = p->logL1; A.logL[1] = p->logL2;
@@ -506,7 +507,7 @@ extern "C" __attribute__((visibility("default"))) int tm_fold_template(tm_plan p
 }
 
 int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const void *tf, int64_t batch,
-                      void *r1, void *r2, int32_t *resid, void *tile_scratch, cudaStream_t s) {
+                      void *r1, void *r2, int32_t *resid, void *tile_scratch, void *gntt_scratch, cudaStream_t s) {
     if (batch == 0) return TM_OK;
     if (p->dtype == TM_F32) {
         const int nt1 = (int)((p->M1 + F_TK - 1) / F_TK), nt2 = (int)((p->M2 + F_TK - 1) / F_TK);
@@ -528,6 +529,7 @@ int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const 
         return TM_OK;
     }
     if (p->fast_corr) return tm_fast_correlate(p, y1, y2, nullptr, tf, batch, r1, r2, resid, s);
+    if (p->big_corr) return tm_gntt_correlate(p, y1, y2, nullptr, tf, batch, r1, r2, resid, gntt_scratch, s);
     if (!corr_in_smem(p)) {
         tm_set_error("tm_correlate: transform length %lld x %d primes exceeds shared memory (large path not built)",
                      (long long)(p->L1 > p->L2 ? p->L1 : p->L2), p->n_primes);
@@ -557,11 +559,12 @@ int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const 
 
 extern "C" __attribute__((visibility("default"))) int tm_correlate(tm_plan p, const void *y1, const void *y2, const void *tf, int64_t batch, void *r1,
                             void *r2, void *ws, void *stream) {
-    (void)ws;
     if (!p) { tm_set_error("tm_correlate: NULL plan"); return TM_EINVAL; }
     if (batch < 0) { tm_set_error("tm_correlate: batch < 0"); return TM_EINVAL; }
     if (batch > 0 && (!y1 || !y2 || !tf || !r1 || !r2)) { tm_set_error("tm_correlate: NULL pointer"); return TM_EINVAL; }
-    return tm_correlate_impl(p, y1, y2, tf, batch, r1, r2, nullptr, nullptr, (cudaStream_t)stream);
+    if (p->big_corr && !ws) { tm_set_error("tm_correlate: workspace required for this plan"); return TM_EINVAL; }
+    void *g = ws ? (char *)ws + tm_ws(p, batch).gntt : nullptr;
+    return tm_correlate_impl(p, y1, y2, tf, batch, r1, r2, nullptr, nullptr, g, (cudaStream_t)stream);
 }
 
 int tm_crt_impl(const tm_plan_s *p, const int32_t *resid, int64_t batch, int32_t *residues_out, int64_t *k,

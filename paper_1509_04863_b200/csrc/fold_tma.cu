@@ -77,7 +77,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(TW * 32) : "memory"); }
 
 __device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, int sh) { return __funnelshift_r(lo, hi, sh); }
 

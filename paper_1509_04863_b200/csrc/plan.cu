@@ -136,7 +136,11 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
         double bound = (double)K * tmax * (double)(p->q1 > p->q2 ? p->q1 : p->q2) * tmax;
         p->n_primes = (bound < (double)(TM_PRIMES[0] / 2) - 1.0) ? 1 : 2;
         p->fast_corr = tm_fast_corr_ok(p);
-        if (p->fast_corr) {  // u32 Montgomery spectra in the fast kernel's register order
+        p->big_corr = !p->fast_corr && p->logL2 > 14;
+        if (p->big_corr) {   // u32 natural bit-reversed spectra at L2 (first L1 serve y1)
+            p->tf_elems = L2;
+            p->tf_bytes = L2 * p->n_primes * 4;
+        } else if (p->fast_corr) {  // u32 Montgomery spectra in the fast kernel's register order
             p->tf_elems = L1 + L2;
             p->tf_bytes = (L1 + L2) * p->n_primes * 4;
         } else {             // uint2 (value, Shoup companion), natural bit-reversed order
@@ -181,6 +185,8 @@ tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch) {
     off += align256((size_t)batch * 2 * 4);
     w.f32_tiles = off;
     if (p->dtype == TM_F32) off += align256((size_t)batch * 2 * ((p->M2 + 1023) / 1024) * 8);
+    w.gntt = off;
+    if (p->big_corr) off += align256(tm_gntt_scratch_bytes(p, batch));
     w.total = off;
     return w;
 }

@@ -12,6 +12,7 @@ struct RunWs {
     void *tf;        // folded template
     int32_t *resid;  // [batch][2]
     void *tiles;     // fp32 argmax partials
+    void *gntt;      // grid-pass NTT scratch
     size_t total;
 };
 
@@ -23,6 +24,7 @@ RunWs run_ws(const tm_plan_s *p, int64_t batch, void *ws) {
     r.fold_ws = base;
     r.resid = (int32_t *)(base + F.resid);
     r.tiles = base + F.f32_tiles;
+    r.gntt = base + F.gntt;
     const size_t ey = p->dtype == TM_I8 ? 4 : 4;
     r.y1 = base + off; off += align256((size_t)batch * p->len_y1 * ey);
     r.y2 = base + off; off += align256((size_t)batch * p->len_y2 * ey);
@@ -52,17 +54,46 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
         tm_prof_mark(2, s);
         rc = tm_fast_correlate(p, W.y1, W.y2, t, nullptr, batch, nullptr, nullptr, W.resid, s);
         if (rc) return rc;
+    } else if (p->big_corr) {
+        tm_prof_mark(2, s);
+        rc = tm_gntt_correlate(p, W.y1, W.y2, t, nullptr, batch, nullptr, nullptr, W.resid, W.gntt, s);
+        if (rc) return rc;
     } else {
         rc = tm_fold_template(p, t, batch, W.tf, stream);                            // step 4 (+5 for t)
         if (rc) return rc;
         tm_prof_mark(2, s);
-        rc = tm_correlate_impl(p, W.y1, W.y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, s);  // 5-7
+        rc = tm_correlate_impl(p, W.y1, W.y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, nullptr, s);  // 5-7
         if (rc) return rc;
     }
     tm_prof_mark(3, s);
     rc = tm_crt_impl(p, W.resid, batch, residues, k, s);                              // steps 8-9
     tm_prof_mark(4, s);
     return rc;
+}
+
+// steps 4-9 on already-folded vectors (e.g. after an all-reduce of partial folds)
+extern "C" __attribute__((visibility("default"))) int tm_correlate_match(tm_plan p, const void *y1, const void *y2,
+                                                                         const void *t, int64_t batch,
+                                                                         int32_t *residues, int64_t *k, void *ws,
+                                                                         void *stream) {
+    if (!p) { tm_set_error("tm_correlate_match: NULL plan"); return TM_EINVAL; }
+    if (batch < 0) { tm_set_error("tm_correlate_match: batch < 0"); return TM_EINVAL; }
+    if (batch == 0) return TM_OK;
+    if (!y1 || !y2 || !t || !k || !ws) { tm_set_error("tm_correlate_match: NULL pointer"); return TM_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    RunWs W = run_ws(p, batch, ws);
+    int rc;
+    if (p->fast_corr) {
+        rc = tm_fast_correlate(p, y1, y2, t, nullptr, batch, nullptr, nullptr, W.resid, s);
+    } else if (p->big_corr) {
+        rc = tm_gntt_correlate(p, y1, y2, t, nullptr, batch, nullptr, nullptr, W.resid, W.gntt, s);
+    } else {
+        rc = tm_fold_template(p, t, batch, W.tf, stream);
+        if (rc == TM_OK)
+            rc = tm_correlate_impl(p, y1, y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, nullptr, s);
+    }
+    if (rc) return rc;
+    return tm_crt_impl(p, W.resid, batch, residues, k, s);
 }
 
 extern "C" __attribute__((visibility("default"))) int tm_run_host(tm_plan p, const void *x_host, int64_t ldx, const void *t_host, int64_t batch,

@@ -15,6 +15,7 @@ struct tm_plan_s {
     int logL1, logL2;
     int64_t nload1, nload2;  // entries of y_j the correlation reads (cyclic y1: M1)
     int fast_corr;       // register-resident NTT kernels (corr_fast.cu) usable
+    int big_corr;        // grid-pass NTT (gntt.cu) for transforms longer than 2^14
     int n_primes;
     int dtype;
     uint32_t flags;
@@ -63,6 +64,7 @@ struct tm_ws_layout {
     size_t fold_bytes;
     size_t resid;         // int32 [batch][2] residues (tm_run)
     size_t f32_tiles;     // fp32 per-tile argmax partials (tm_run, TM_F32)
+    size_t gntt;          // grid-pass NTT scratch (big_corr plans)
     size_t total;
 };
 tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch);
@@ -70,6 +72,10 @@ size_t tm_run_ws_bytes(const tm_plan_s *p, int64_t batch);  // run.cu
 
 // ---- internal launchers ----
 bool tm_fast_corr_ok(const tm_plan_s *p);
+size_t tm_gntt_scratch_bytes(const tm_plan_s *p, int64_t batch);
+int tm_gntt_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, const void *tf,
+                      int64_t batch, void *r1, void *r2, int32_t *resid, void *scratch, cudaStream_t s);
+int tm_gntt_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf, cudaStream_t s);
 int tm_fast_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf, cudaStream_t s);
 int tm_fast_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, const void *tf,
                       int64_t batch, void *r1, void *r2, int32_t *resid, cudaStream_t s);
@@ -77,6 +83,6 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
                  int64_t len, void *y1, void *y2, int accumulate, void *ws, cudaStream_t s);
 int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const void *tf,
                       int64_t batch, void *r1, void *r2, int32_t *resid, void *tile_scratch,
-                      cudaStream_t s);
+                      void *gntt_scratch, cudaStream_t s);
 int tm_crt_impl(const tm_plan_s *p, const int32_t *resid, int64_t batch, int32_t *residues_out,
                 int64_t *k, cudaStream_t s);

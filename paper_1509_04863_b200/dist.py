@@ -1,0 +1,55 @@
+"""Host-side multi-GPU logic (one process per GPU, torch.distributed).
+
+* Batches of independent pairs shard with no data-path collective: rank r owns
+  global pairs [r*B, (r+1)*B) (weak scaling) -- `pair_range`.
+* One huge signal is split into contiguous, row-aligned chunks (rows of M1
+  samples, so every chunk can use the packed fold kernel) -- `signal_chunks`;
+  each rank folds its chunk with global-position semantics (tm_fold(offset,
+  len)) and the partial folds are summed with ONE all-reduce of the
+  concatenated y1 || y2 vector -- `allreduce_folds`.  The fold of Eq. 2 is
+  additive over any partition of the positions (pinned in tests), so the sum
+  is exactly the full fold.
+No arithmetic of the method lives here.
+"""
+from __future__ import annotations
+
+
+def pair_range(batch_per_rank: int, rank: int) -> tuple[int, int]:
+    """Global pair indices [first, first + batch) owned by `rank`."""
+    return rank * batch_per_rank, batch_per_rank
+
+
+def signal_chunks(N: int, M1: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous row-aligned chunks (offset, length) covering [0, N), one per rank.
+    Rows (M1 samples) are dealt as evenly as possible; requires M1 | N."""
+    if N % M1:
+        raise ValueError("row-aligned chunks need M1 | N")
+    rows = N // M1
+    base, extra = divmod(rows, world)
+    out, r0 = [], 0
+    for r in range(world):
+        nr = base + (1 if r < extra else 0)
+        out.append((r0 * M1, nr * M1))
+        r0 += nr
+    return out
+
+
+def allreduce_folds(y1, y2, group=None):
+    """Sum partial folds across ranks with one collective (SUM over int32 or fp32).
+    Returns (y1, y2) holding the full fold on every rank."""
+    import torch
+    import torch.distributed as dist
+    n1 = y1.numel()
+    flat = torch.cat([y1.reshape(-1), y2.reshape(-1)])
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    return flat[:n1].view_as(y1), flat[n1:].view_as(y2)
+
+
+def max_over_ranks(value: float, device=None, group=None) -> float:
+    """Max of a per-rank timing across ranks (the slowest rank defines the step)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

@@ -1,0 +1,90 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): the partition of one signal
+into row-aligned chunks, the all-reduce of partial folds (partial folds computed
+by the oracle stand in for tm_fold on each rank), batch sharding by global pair
+index, and the max-over-ranks timing reduction."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1509_04863_b200 import dist as tmdist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_signal_chunks_partition():
+    for N, M1, G in ((2 ** 31, 65536, 8), (4096 * 37, 4096, 3), (4096, 256, 5), (1024, 256, 4)):
+        ch = tmdist.signal_chunks(N, M1, G)
+        assert len(ch) == G
+        pos = 0
+        for off, ln in ch:
+            assert off == pos and off % M1 == 0 and ln % M1 == 0
+            pos += ln
+        assert pos == N
+        lens = [ln for _, ln in ch]
+        assert max(lens) - min(lens) <= M1
+    with pytest.raises(ValueError):
+        tmdist.signal_chunks(1000, 64, 2)
+
+
+def test_pair_range():
+    assert tmdist.pair_range(1024, 0) == (0, 1024)
+    assert tmdist.pair_range(1024, 3) == (3072, 1024)
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import tmgen
+        N, K = 64 * 48, 64           # M1 = 64, M2 = 65, q = 48
+        M1, M2 = oracle.moduli(N, K)
+        x = tmgen.signal(9, 0, N)
+        off, ln = tmdist.signal_chunks(N, M1, world)[rank]
+        y1 = torch.from_numpy(oracle.fold(x, M1, K, off, ln))
+        y2 = torch.from_numpy(oracle.fold(x, M2, K, off, ln))
+        y1, y2 = tmdist.allreduce_folds(y1, y2)
+        ok_fold = np.array_equal(y1.numpy(), oracle.fold(x, M1, K)) and np.array_equal(y2.numpy(), oracle.fold(x, M2, K))
+        # every rank then matches the same full fold -> identical k on all ranks
+        t = tmgen.template(9, 0, N, K, 0.0)
+        r1 = oracle.correlate(y1.numpy(), M1, t)
+        r2 = oracle.correlate(y2.numpy(), M2, t)
+        z = oracle.crt(oracle.argmax(r1), M1, oracle.argmax(r2), M2)
+        k = z if z < N else -1
+        ks = [None] * world
+        dist.all_gather_object(ks, k)
+        tmax = tmdist.max_over_ranks(1.0 + rank)
+        q.put((rank, ok_fold, ks, k == oracle.ftm(x, t)["k"], tmax))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_of_partial_folds_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok_fold, ks, ok_k, tmax in res:
+        assert ok_fold, rank
+        assert len(set(ks)) == 1
+        assert ok_k
+        assert tmax == 2.0

@@ -251,3 +251,61 @@ def test_cfg3_full_batch_sampled(tm):
     plan = tm.Plan(N, K, seed=3, dtype="float32")
     x_h, t_h, _ = tmgen.batch(3, 0, B, N, K, 0.5, dtype=np.float32)
     check_f32_pairs(tm, plan, x_h, t_h, [0, 255])
+
+
+# ------------------------------------------------------------- long transforms (grid-pass NTT)
+def test_gntt_one_prime_L2_2e15(tm):
+    """K = 16384 (cfg4's largest): L1 = 2^14 cyclic, L2 = 2^15 -> grid-pass NTT."""
+    N, K = 2 ** 20, 16384
+    plan = tm.Plan(N, K, seed=41)
+    assert plan.n_primes == 1 and plan.L2 == 2 ** 15
+    x_h, t_h, _ = tmgen.batch(41, 0, 2, N, K, 0.2)
+    check_int_pairs(tm, plan, x_h, t_h, range(2))
+
+
+def test_gntt_two_primes_cfg5_lengths(tm):
+    """The transform lengths and prime count of cfg5 (L1 = 2^16, L2 = 2^17, two
+    NTT primes + CRT) at a size the oracle finishes: K = 65536, q = 64, general
+    int8 data (the |r| bound exceeds p1/2)."""
+    N, K = 2 ** 22, 65536
+    plan = tm.Plan(N, K, seed=5, binary=False)
+    assert plan.n_primes == 2 and plan.L1 == 2 ** 16 and plan.L2 == 2 ** 17
+    rng = np.random.default_rng(5)
+    x_h = rng.integers(-128, 128, (1, N)).astype(np.int8)
+    t_h = x_h[:, 1000:1000 + K].copy()
+    check_int_pairs(tm, plan, x_h, t_h, [0])
+
+
+def test_cfg5_full_size_fold_and_chunks(tm):
+    """cfg5 at full size (N = 2^31, K = 65536, one +-1 pair, 5% flips): tm_run;
+    y1/y2 on 96 sampled bins (incl. the wrap bins [M2-q, M2) and extension bins)
+    equal the oracle's Eq. 2 evaluated bin by bin; folding the signal as 2, 4 and
+    8 row-aligned chunks (the multi-GPU partition) and summing gives bit-identical
+    y; k equals the CRT of the residues."""
+    N, K = 2 ** 31, 65536
+    plan = tm.Plan(N, K, seed=5)
+    assert plan.fast_fold == 1 and plan.n_primes == 2
+    x_h = tmgen.signal(5, 0, N)
+    t_h = tmgen.template(5, 0, N, K, 0.05)
+    x = torch.from_numpy(x_h).view(1, N).to(DEV)
+    t = torch.from_numpy(t_h).view(1, K).to(DEV)
+    y1, y2 = plan.fold(x)
+    res, k = plan.run(x, t)
+    torch.cuda.synchronize()
+    q = plan.q2
+    rng = np.random.default_rng(0)
+    b2 = np.unique(np.concatenate([rng.integers(0, plan.M2 + K, 64), np.arange(plan.M2 - q, plan.M2 - q + 8),
+                                   np.arange(plan.M2 - 8, plan.M2 + 8), [plan.M2 + K - 1]]))
+    b1 = np.unique(np.concatenate([rng.integers(0, plan.M1 + K, 64), [0, plan.M1 - 1, plan.M1, plan.M1 + K - 1]]))
+    np.testing.assert_array_equal(y1[0].cpu().numpy()[b1], oracle.fold_bins(x_h, plan.M1, b1))
+    np.testing.assert_array_equal(y2[0].cpu().numpy()[b2], oracle.fold_bins(x_h, plan.M2, b2))
+    m1, m2 = int(res[0, 0]), int(res[0, 1])
+    assert int(k[0]) == crt_closed(m1, plan.M1, m2, plan.M2, N)
+    for G in (2, 4, 8):
+        a1 = torch.zeros_like(y1)
+        a2 = torch.zeros_like(y2)
+        step = N // G
+        for r in range(G):
+            plan.fold(x[:, r * step:(r + 1) * step], offset=r * step, length=step, y1=a1, y2=a2, accumulate=True)
+        torch.cuda.synchronize()
+        assert torch.equal(a1, y1) and torch.equal(a2, y2), G
