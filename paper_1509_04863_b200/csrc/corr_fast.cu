@@ -16,6 +16,8 @@
 //
 // Twiddles: stage with span h uses the length-2h table w_{2h}^j (uint2 value +
 // Shoup companion, per-length compact tables in global memory, L1-resident).
+#include <cstdlib>
+
 #include "tm_internal.cuh"
 
 namespace {
@@ -39,6 +41,11 @@ struct FastArgs {
     int64_t *r;            // [batch][M] or NULL
     int32_t *resid;        // [batch][2] or NULL
     int jmod;              // 0 or 1 (column in resid)
+    // pair kernel (both moduli in one CTA)
+    const int32_t *y1, *y2;
+    int64_t ldy1, ldy2, nload1, nload2, M1, M2;
+    int64_t *r1, *r2;
+    uint32_t cL1, cL1s;    // L1^{-1} * 2^32 mod p1 and companion
 };
 
 // Lazy (Harvey) arithmetic, valid because 4p < 2^32:
@@ -217,6 +224,22 @@ __device__ __forceinline__ uint32_t to_residue(int32_t v, uint32_t p) {
     return v >= 0 ? (uint32_t)v : (uint32_t)((int64_t)p + v);
 }
 
+// template spectrum (unscaled, distribution Df, lazily in [0, 2p)) of t_rev[i] = t[(L - i) mod L]
+template <int LOGL, int LOGE, int PI>
+__device__ __forceinline__ void template_spectrum_raw(uint32_t (&T)[1 << LOGE], uint32_t *buf, int t,
+                                                      const FastArgs &A, int64_t b) {
+    using G = Geo<LOGL, LOGE>;
+    constexpr uint32_t p = PI ? P2 : P1;
+    const int8_t *tb = A.t + b * A.K;
+#pragma unroll
+    for (int m = 0; m < G::E; ++m) {
+        const int i = G::idx(0, t, m);
+        const int src = i == 0 ? 0 : G::L - i;
+        T[m] = to_residue(src < A.K ? (int32_t)tb[src] : 0, p);
+    }
+    dif<LOGL, LOGE>(T, buf, t, A.twf[PI], p);
+}
+
 // template spectrum (Montgomery-scaled, distribution Df) of t_rev[i] = t[(L - i) mod L]
 template <int LOGL, int LOGE, int PI>
 __device__ __forceinline__ void template_spectrum(uint32_t (&T)[1 << LOGE], uint32_t *buf, int t, const FastArgs &A,
@@ -276,6 +299,37 @@ __device__ __forceinline__ void correlate_one_prime(uint32_t (&v)[1 << LOGE], ui
 
 __device__ __forceinline__ void amax(int64_t &bv, int32_t &bi, int64_t v, int32_t i) {
     if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+}
+
+// block-wide (value, lowest index) max; thread 0 stores the index to *out (if non-NULL).
+// Uses buf as scratch (synchronises before and after).
+template <int NT>
+__device__ __forceinline__ void block_argmax_store(int64_t bv, int32_t bi, uint32_t *buf, int32_t *out) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        amax(bv, bi, ov, oi);
+    }
+    __syncthreads();
+    int64_t *sv = reinterpret_cast<int64_t *>(buf);
+    int32_t *si = reinterpret_cast<int32_t *>(sv + 32);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { sv[w] = bv; si[w] = bi; }
+    __syncthreads();
+    if (w == 0) {
+        constexpr int NW = (NT + 31) / 32;
+        bv = l < NW ? sv[l] : INT64_MIN;
+        bi = l < NW ? si[l] : 0x7FFFFFFF;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            amax(bv, bi, ov, oi);
+        }
+        if (l == 0 && out) *out = bi;
+    }
+    __syncthreads();
 }
 
 template <int LOGL, int LOGE>
@@ -370,6 +424,181 @@ __global__ void __launch_bounds__(1 << (LOGL - LOGE), min_blocks<LOGL, LOGE>()) 
     }
 }
 
+// ---------------------------------------------------------------------------
+// One CTA per PAIR (both moduli) for the paper's shape: y1 cyclic with L1 = M1 and
+// L2 = 2 L1 (M = K, K | N, K a power of two).  The template is transformed once,
+// at L2: the first L1 entries of its bit-reversed spectrum are exactly the
+// length-L1 spectrum of t reversed mod L1 (even frequencies, support of t_rev
+// does not collide when folded since K <= L1).  NT = L2/16 = L1/8 threads:
+// y2 uses 16 residues per thread (Geo<L2,4>), y1 uses 8 (Geo<L1,3>).
+// Template spectra live in shared memory in the order each transform reads
+// them: Ts2[m * NT + t] (register order of Geo<L2,4>), Ts1[i] natural
+// bit-reversed index (read as Ts1[(t << 3) | m], two LDS.128 per thread).
+// FROM_T = false reads the same two arrays from tf ([batch][L2 + L1] u32).
+// ---------------------------------------------------------------------------
+template <int LOGL2>
+__device__ __noinline__ void pair_template_to_smem(uint32_t *buf, uint32_t *Ts2, uint32_t *Ts1, int t,
+                                                   const FastArgs &A, int64_t b) {
+    constexpr int LOGL1 = LOGL2 - 1;
+    constexpr int NT = Geo<LOGL2, 4>::NT;
+    uint32_t T[16];
+    template_spectrum_raw<LOGL2, 4, 0>(T, buf, t, A, b);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        Ts2[m * NT + t] = shoup_lz(T[m], A.cL[0], A.cLs[0], P1);      // * L2^{-1} R
+        const int i = (t << 4) | m;                                    // bit-reversed index
+        if (i < (1 << LOGL1)) Ts1[i] = shoup_lz(T[m], A.cL1, A.cL1s, P1);  // * L1^{-1} R
+    }
+}
+
+template <int LOGL2>
+__device__ __noinline__ void pair_modulus2(uint32_t *buf, const uint32_t *ts2, int t, const FastArgs &A, int64_t b) {
+    using G2 = Geo<LOGL2, 4>;
+    constexpr int NT = G2::NT;
+    constexpr uint32_t p = P1;
+    int64_t bv = INT64_MIN;
+    int32_t bi = 0x7FFFFFFF;
+    uint32_t v[16];
+    const int32_t *yb = A.y2 + b * A.ldy2;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const int i = G2::idx(0, t, m);
+        v[m] = to_residue(i < A.nload2 ? yb[i] : 0, p);
+    }
+    dif<LOGL2, 4>(v, buf, t, A.twf[0], p);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = montmul<0>(v[m], ts2[m * NT + t]);
+    dit<LOGL2, 4>(v, buf, t, A.twi[0], p);
+    int64_t *rout = A.r2 ? A.r2 + b * A.M2 : nullptr;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const uint32_t r0 = red2(v[m], 2 * p), u = min(r0, r0 - p);
+        const int i = G2::idx(0, t, m);
+        const int64_t val = u > p / 2 ? (int64_t)u - (int64_t)p : (int64_t)u;
+        if (i < A.M2) {
+            if (rout) rout[i] = val;
+            amax(bv, bi, val, i);
+        }
+    }
+    block_argmax_store<NT>(bv, bi, buf, A.resid ? A.resid + b * 2 + 1 : nullptr);
+}
+
+template <int LOGL2>
+__device__ __noinline__ void pair_modulus1(uint32_t *buf, const uint32_t *ts1, int t, const FastArgs &A, int64_t b) {
+    constexpr int LOGL1 = LOGL2 - 1;
+    using G1 = Geo<LOGL1, 3>;
+    constexpr int NT = G1::NT;
+    constexpr uint32_t p = P1;
+    int64_t bv = INT64_MIN;
+    int32_t bi = 0x7FFFFFFF;
+    uint32_t v[8];
+    const int32_t *yb = A.y1 + b * A.ldy1;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int i = G1::idx(0, t, m);
+        v[m] = to_residue(i < A.nload1 ? yb[i] : 0, p);
+    }
+    dif<LOGL1, 3>(v, buf, t, A.twf[0], p);
+    const uint4 *tv = reinterpret_cast<const uint4 *>(ts1 + (t << 3));
+    const uint4 ta = tv[0], tb = tv[1];
+    const uint32_t tt[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
+#pragma unroll
+    for (int m = 0; m < 8; ++m) v[m] = montmul<0>(v[m], tt[m]);
+    dit<LOGL1, 3>(v, buf, t, A.twi[0], p);
+    int64_t *rout = A.r1 ? A.r1 + b * A.M1 : nullptr;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const uint32_t r0 = red2(v[m], 2 * p), u = min(r0, r0 - p);
+        const int i = G1::idx(0, t, m);
+        const int64_t val = u > p / 2 ? (int64_t)u - (int64_t)p : (int64_t)u;
+        if (i < A.M1) {
+            if (rout) rout[i] = val;
+            amax(bv, bi, val, i);
+        }
+    }
+    block_argmax_store<NT>(bv, bi, buf, A.resid ? A.resid + b * 2 + 0 : nullptr);
+}
+
+template <int LOGL2, bool FROM_T>
+__global__ void __launch_bounds__(1 << (LOGL2 - 4), min_blocks<LOGL2, 4>()) corr_pair_kernel(FastArgs A) {
+    constexpr int LOGL1 = LOGL2 - 1;
+    using G2 = Geo<LOGL2, 4>;
+    static_assert(G2::NT == Geo<LOGL1, 3>::NT, "thread counts must match");
+    extern __shared__ uint32_t buf[];
+    uint32_t *Ts2 = buf + G2::L;
+    uint32_t *Ts1 = Ts2 + G2::L;
+    const int t = threadIdx.x;
+    const int64_t b = blockIdx.x;
+    const uint32_t *ts2, *ts1;
+    if constexpr (FROM_T) {
+        pair_template_to_smem<LOGL2>(buf, Ts2, Ts1, t, A, b);
+        __syncthreads();
+        ts2 = Ts2;
+        ts1 = Ts1;
+    } else {
+        ts2 = A.tf + b * A.tf_prime;
+        ts1 = ts2 + G2::L;
+    }
+    pair_modulus2<LOGL2>(buf, ts2, t, A, b);
+    pair_modulus1<LOGL2>(buf, ts1, t, A, b);
+}
+
+// tm_fold_template for pair-kernel plans: [batch][L2 (register order, * L2^-1 R) + L1 (br order, * L1^-1 R)]
+template <int LOGL2>
+__global__ void __launch_bounds__(1 << (LOGL2 - 4), min_blocks<LOGL2, 4>()) template_pair_kernel(FastArgs A) {
+    constexpr int LOGL1 = LOGL2 - 1;
+    using G2 = Geo<LOGL2, 4>;
+    constexpr int NT = G2::NT;
+    extern __shared__ uint32_t buf[];
+    const int t = threadIdx.x;
+    const int64_t b = blockIdx.x;
+    uint32_t T[16];
+    template_spectrum_raw<LOGL2, 4, 0>(T, buf, t, A, b);
+    uint32_t *dst = A.tf_out + b * A.tf_prime;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        dst[m * NT + t] = shoup_lz(T[m], A.cL[0], A.cLs[0], P1);
+        const int i = (t << 4) | m;
+        if (i < (1 << LOGL1)) dst[G2::L + i] = shoup_lz(T[m], A.cL1, A.cL1s, P1);
+    }
+}
+
+template <int LOGL2>
+int launch_pair(const FastArgs &A, int64_t batch, bool from_t, bool template_only, cudaStream_t s) {
+    using G2 = Geo<LOGL2, 4>;
+    if (template_only) {
+        const size_t smem = (size_t)G2::L * 4;
+        auto k = template_pair_kernel<LOGL2>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<(unsigned)batch, G2::NT, smem, s>>>(A);
+        TM_CHECK_LAUNCH("tm_fold_template: template_pair_kernel");
+        return TM_OK;
+    }
+    const size_t smem = (size_t)G2::L * 4 * (from_t ? 2 : 1) + (from_t ? (size_t)G2::L * 2 : 0);
+    if (from_t) {
+        auto k = corr_pair_kernel<LOGL2, true>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<(unsigned)batch, G2::NT, smem, s>>>(A);
+    } else {
+        auto k = corr_pair_kernel<LOGL2, false>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<(unsigned)batch, G2::NT, smem, s>>>(A);
+    }
+    TM_CHECK_LAUNCH("tm_correlate: corr_pair_kernel");
+    return TM_OK;
+}
+
+int dispatch_pair(int logL2, const FastArgs &A, int64_t batch, bool from_t, bool template_only, cudaStream_t s) {
+    switch (logL2) {
+        case 10: return launch_pair<10>(A, batch, from_t, template_only, s);
+        case 11: return launch_pair<11>(A, batch, from_t, template_only, s);
+        case 12: return launch_pair<12>(A, batch, from_t, template_only, s);
+        case 13: return launch_pair<13>(A, batch, from_t, template_only, s);
+        case 14: return launch_pair<14>(A, batch, from_t, template_only, s);
+        default: tm_set_error("pair NTT: unsupported length 2^%d", logL2); return TM_EUNSUPPORTED;
+    }
+}
+
 template <int LOGL, int LOGE, int NP>
 int launch_corr(const FastArgs &A, int64_t batch, bool from_t, cudaStream_t s) {
     using G = Geo<LOGL, LOGE>;
@@ -444,6 +673,22 @@ void fill_common(const tm_plan_s *p, int logL, FastArgs &A) {
 
 }  // namespace
 
+// the paper's shape (M = K | N, K a power of two): one CTA per pair, shared template
+static bool pair_ok(const tm_plan_s *p) {
+    return p->n_primes == 1 && p->logL2 == p->logL1 + 1 && p->nload1 == p->M1 && p->L1 == p->M1 &&
+           p->logL2 >= 10 && p->logL2 <= 14;
+}
+
+static void fill_pair(const tm_plan_s *p, FastArgs &A) {
+    fill_common(p, p->logL2, A);
+    const uint64_t P = TM_P1;
+    uint64_t Linv = 1, base = ((uint64_t)1 << p->logL1) % P, e = P - 2;
+    while (e) { if (e & 1) Linv = (unsigned __int128)Linv * base % P; base = (unsigned __int128)base * base % P; e >>= 1; }
+    const uint64_t c = (unsigned __int128)Linv * (((unsigned __int128)1 << 32) % P) % P;
+    A.cL1 = (uint32_t)c;
+    A.cL1s = (uint32_t)(((unsigned __int128)c << 32) / P);
+}
+
 bool tm_fast_corr_ok(const tm_plan_s *p) {
     return p->dtype == TM_I8 && p->logL1 >= 9 && p->logL1 <= 14 && p->logL2 >= 9 && p->logL2 <= 14 &&
            p->n_primes >= 1 && p->n_primes <= 2;
@@ -451,6 +696,13 @@ bool tm_fast_corr_ok(const tm_plan_s *p) {
 
 // tf layout (fast plans): u32 [batch][n_primes][L1 + L2]; slot 0 = y1's length, slot 1 = y2's
 int tm_fast_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf, cudaStream_t s) {
+    if (pair_ok(p)) {
+        FastArgs A{};
+        fill_pair(p, A);
+        A.t = (const int8_t *)t; A.K = p->K;
+        A.tf_out = (uint32_t *)tf;
+        return dispatch_pair(p->logL2, A, batch, false, true, s);
+    }
     for (int j = 0; j < 2; ++j) {
         const int logL = j ? p->logL2 : p->logL1;
         FastArgs A{};
@@ -466,6 +718,20 @@ int tm_fast_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf,
 
 int tm_fast_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, const void *tf,
                       int64_t batch, void *r1, void *r2, int32_t *resid, cudaStream_t s) {
+    static const bool no_pair = getenv("TM_NO_PAIR_KERNEL") != nullptr;
+    if (pair_ok(p) && !no_pair) {
+        FastArgs A{};
+        fill_pair(p, A);
+        A.y1 = (const int32_t *)y1; A.y2 = (const int32_t *)y2;
+        A.ldy1 = p->len_y1; A.ldy2 = p->len_y2;
+        A.nload1 = p->nload1; A.nload2 = p->nload2;
+        A.M1 = p->M1; A.M2 = p->M2;
+        A.r1 = (int64_t *)r1; A.r2 = (int64_t *)r2;
+        A.resid = resid;
+        A.t = (const int8_t *)t; A.K = p->K;
+        A.tf = (const uint32_t *)tf;
+        return dispatch_pair(p->logL2, A, batch, t != nullptr, false, s);
+    }
     for (int j = 0; j < 2; ++j) {
         const int logL = j ? p->logL2 : p->logL1;
         FastArgs A{};

@@ -258,84 +258,63 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a)
         for (int i = 0; i < 8; ++i) { y1w[i] = 0; carry[i] = 0; W[i] = 0; }
         uint32_t a1[4] = {0, 0, 0, 0};
         for (int t = 0; t < ntile; ++t) {
-            uint32_t m[16][4];
+            // the finished low block of the previous tile becomes this tile's high block
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { W[4 + i] = W[i]; W[i] = 0; }
             const bool full_tile = (t * 16 + 16 <= nrow) && width == TCOLS;
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 const int rbase = t * 16 + half * 8;
-                if (rbase < nrow) {
-                    mbar_wait(&full[s], ph);
-                    const uint32_t st = ring_u32 + s * STAGE_BYTES + colb;
-                    if (full_tile) {
+                if (rbase >= nrow) break;
+                mbar_wait(&full[s], ph);
+                const uint32_t st = ring_u32 + s * STAGE_BYTES + colb;
 #pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            uint4 v;
+                for (int g = 0; g < 2; ++g) {
+                    // 4 rows r = 8 half + 4 g + rho, rho = 0..3 (alpha = r >> 2 = 2 half + g)
+                    uint32_t m[4][4];
+#pragma unroll
+                    for (int rho = 0; rho < 4; ++rho) {
+                        const int rr = g * 4 + rho;
+                        uint4 v = make_uint4(0, 0, 0, 0);
+                        if (full_tile || (active && rbase + rr < nrow))
                             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                                          : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                                         : "r"(st + r * TCOLS));
-                            m[half * 8 + r][0] = v.x & 0x02020202u; m[half * 8 + r][1] = v.y & 0x02020202u;
-                            m[half * 8 + r][2] = v.z & 0x02020202u; m[half * 8 + r][3] = v.w & 0x02020202u;
-                        }
-                    } else {
-#pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            uint4 v = make_uint4(0, 0, 0, 0);
-                            if (active && rbase + r < nrow)
-                                asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                                             : "r"(st + r * width));
-                            m[half * 8 + r][0] = v.x & 0x02020202u; m[half * 8 + r][1] = v.y & 0x02020202u;
-                            m[half * 8 + r][2] = v.z & 0x02020202u; m[half * 8 + r][3] = v.w & 0x02020202u;
-                        }
+                                         : "r"(st + rr * (full_tile ? TCOLS : width)));
+                        m[rho][0] = v.x & 0x02020202u; m[rho][1] = v.y & 0x02020202u;
+                        m[rho][2] = v.z & 0x02020202u; m[rho][3] = v.w & 0x02020202u;
                     }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[s]);
-                    if (++s == NST) { s = 0; ph ^= 1; }
-                } else {
+                    if (!active) continue;
+                    // M1: column sums in byte lanes
 #pragma unroll
-                    for (int r = 0; r < 8; ++r)
-                        m[half * 8 + r][0] = m[half * 8 + r][1] = m[half * 8 + r][2] = m[half * 8 + r][3] = 0u;
+                    for (int w = 0; w < 4; ++w) a1[w] = a1[w] + (m[0][w] + m[1][w]) + (m[2][w] + m[3][w]);
+                    // M2: row r, byte j -> window byte 16 - r + j.  With alpha = r >> 2 and
+                    // rho = r & 3, window word 4 - alpha + k' (k' = -1..3) receives
+                    // funnelshift_r(m[k'], m[k'+1], 8 rho) (m[-1] = m[4] = 0).
+                    const int alpha = half * 2 + g;
+#pragma unroll
+                    for (int kk = -1; kk < 4; ++kk) {
+                        uint32_t add = (kk >= 0) ? m[0][kk] : 0u;
+#pragma unroll
+                        for (int rho = 1; rho < 4; ++rho) {
+                            const uint32_t lo = (kk >= 0) ? m[rho][kk] : 0u;
+                            const uint32_t hi = (kk + 1 < 4) ? m[rho][kk + 1] : 0u;
+                            add += fsr(lo, hi, 8 * rho);
+                        }
+                        W[4 - alpha + kk] += add;
+                    }
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if (++s == NST) { s = 0; ph ^= 1; }
             }
             if (!active) continue;
-            // ---- M1: column sums in byte lanes
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                uint32_t sacc = a1[w];
-#pragma unroll
-                for (int r = 0; r < 16; r += 2) sacc = sacc + m[r][w] + m[r + 1][w];
-                a1[w] = sacc;
-            }
-            if ((t & 3) == 3 || t == ntile - 1) {
+            if ((t & 3) == 3 || t == ntile - 1) {  // widen byte counters before they can overflow
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
                     y1w[2 * w] += __byte_perm(a1[w], 0, 0x4140);
                     y1w[2 * w + 1] += __byte_perm(a1[w], 0, 0x4342);
                     a1[w] = 0;
                 }
-            }
-            // ---- M2: anti-diagonals (row r = 4 al + rho: byte j -> window byte 16 - r + j)
-            uint32_t A[4][8];
-#pragma unroll
-            for (int rho = 0; rho < 4; ++rho)
-#pragma unroll
-                for (int i = 0; i < 8; ++i) A[rho][i] = 0;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const int al = r >> 2, rho = r & 3;
-#pragma unroll
-                for (int w = 0; w < 4; ++w) A[rho][4 - al + w] += m[r][w];
-            }
-            uint32_t Wn[8];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { Wn[i] = 0; Wn[4 + i] = W[i]; }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                uint32_t v = Wn[i] + A[0][i];
-                v += fsr(A[1][i], i < 7 ? A[1][i + 1] : 0u, 8);
-                v += fsr(A[2][i], i < 7 ? A[2][i + 1] : 0u, 16);
-                v += fsr(A[3][i], i < 7 ? A[3][i + 1] : 0u, 24);
-                W[i] = v;
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {

@@ -85,6 +85,33 @@ int main() {
     }
     printf("tma_read 6x32KB/SM: %.1f GB/s\n", chunk * sms / best / 1e6);
   }
+  // per-SM ceiling: fewer CTAs (1 per SM), deeper rings
+  for (int ncta : {32, 48, 64, 96, 128}) {
+    constexpr int NST = 6, STAGE = 32768;
+    auto k = tma_read<NST, STAGE>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, NST * STAGE + 128);
+    size_t chunk = bytes / ncta / STAGE * STAGE;
+    if (chunk > (size_t(256) << 20)) chunk = size_t(256) << 20;
+    best = 1e9;
+    for (int it = 0; it < 5; ++it) {
+      cudaEventRecord(a); k<<<ncta, 64, NST * STAGE + 128>>>(d, chunk, o); cudaEventRecord(b);
+      cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
+    }
+    printf("tma_read 6x32KB, %3d CTAs: %.1f GB/s total, %.1f GB/s per SM\n", ncta, chunk * ncta / best / 1e6, chunk / best / 1e6);
+  }
+  for (int ncta : {32, 64}) {
+    constexpr int NST = 3, STAGE = 65536;
+    auto k = tma_read<NST, STAGE>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, NST * STAGE + 128);
+    size_t chunk = bytes / ncta / STAGE * STAGE;
+    if (chunk > (size_t(128) << 20)) chunk = size_t(128) << 20;
+    best = 1e9;
+    for (int it = 0; it < 5; ++it) {
+      cudaEventRecord(a); k<<<ncta, 64, NST * STAGE + 128>>>(d, chunk, o); cudaEventRecord(b);
+      cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
+    }
+    printf("tma_read 3x64KB, %3d CTAs: %.1f GB/s total, %.1f GB/s per SM\n", ncta, chunk * ncta / best / 1e6, chunk / best / 1e6);
+  }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
