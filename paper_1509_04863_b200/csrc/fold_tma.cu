@@ -19,14 +19,15 @@
 //  * when an item is a whole pair (M1 <= 4096, full fold) the consumers write
 //    the finished y1/y2 directly (counts -> values, the mod-N wrap and the
 //    strategy-1 extension), so no workspace, memset or second kernel is needed.
-#include "tm_internal.cuh"
+#include <cstdlib>
+
+#include "ntt_core.cuh"
 
 namespace {
 
 constexpr int TW = 8;                 // consumer warps, one 512-column strip each
 constexpr int TCOLS = TW * 512;       // columns per CTA group
 constexpr int SROWS = 8;              // rows per ring stage
-constexpr int NST = 4;                // ring stages
 constexpr int STAGE_BYTES = SROWS * TCOLS;
 
 struct TmaArgs {
@@ -43,6 +44,12 @@ struct TmaArgs {
     int priv_stride;     // words per warp-private anti-diagonal array (512 + 16 ceil(R/16))
     int32_t *counts;     // non-owner: [batch][M1 + M2]
     int32_t *y1, *y2;    // owner outputs
+    // fused mode: NTT warps correlate pair i while the fold warps stream pair i+1
+    FastArgs f;          // template, tables, y pointers, resid (see ntt_core.cuh)
+    int32_t *residues_out;
+    int64_t *k_out;
+    uint32_t crt_inv;
+    int xs_bytes;        // bytes reserved for the epilogue's x[0 .. K + q) stage
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -102,7 +109,7 @@ constexpr int NE = 4;  // epilogue warps
 // comb(d): total count of unwrapped diagonal d (relative to the CTA's first column)
 // from the warp-private arrays of one buffer: only the <= 3 warps whose strip
 // [512 w - 16 ntile, 512 w + 511] contains d contribute.
-__device__ __forceinline__ int32_t comb_at(const int32_t *pv, int stride, int d, int ntile, int width) {
+__device__ __forceinline__ int32_t comb_at(const uint16_t *pv, int stride, int d, int ntile, int width) {
     const int pad = 16 * ntile;
     int wlo = (d - 511 + 511 + 512 * 64) / 512 - 64;  // ceil((d - 511) / 512)
     if (wlo < 0) wlo = 0;
@@ -112,21 +119,31 @@ __device__ __forceinline__ int32_t comb_at(const int32_t *pv, int stride, int d,
     int32_t v = 0;
     for (int w = wlo; w <= whi; ++w) {
         const int j = d - 512 * w + pad;
-        if (j >= 0 && j < 512 + pad) v += pv[w * stride + j];
+        if (j >= 0 && j < 512 + pad) v += (int32_t)pv[w * stride + j];
     }
     return v;
 }
 
-__global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a) {
+constexpr int ntt_threads(int logl2) { return logl2 > 0 ? (1 << (logl2 - 4)) : 0; }
+
+// NST: ring stages.  LOGL2 > 0 selects the fused kernel: NT = L2/16 extra threads
+// (warps 13..) run the pair NTT correlation (ntt_core.cuh) of each finished pair.
+template <int NST, int LOGL2>
+__global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), 1) fold_pm1_tma(TmaArgs a) {
+    constexpr bool FUSED = LOGL2 > 0;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *ring = smem;
-    int32_t *privb = reinterpret_cast<int32_t *>(smem + NST * STAGE_BYTES);  // [2][TW][priv_stride]
+    uint16_t *privb = reinterpret_cast<uint16_t *>(smem + NST * STAGE_BYTES);  // [2][TW][priv_stride]
     uint64_t *full = reinterpret_cast<uint64_t *>(privb + 2 * TW * a.priv_stride);
     uint64_t *empty = full + NST;
     uint64_t *pfull = empty + NST;   // [2]: consumers -> epilogue (count TW)
     uint64_t *pempty = pfull + 2;    // [2]: epilogue -> consumers (count NE)
-    uint4 *xs = reinterpret_cast<uint4 *>(pempty + 2);  // owner epilogue: x[0 .. K + q)
+    uint64_t *yready = pempty + 2;   // [2]: y1 + y2 of a pair in global memory (count TW + NE)
+    uint64_t *ydone = yready + 2;    // [2]: NTT warps finished with a pair (count NT / 32)
+    uint4 *xs = reinterpret_cast<uint4 *>(ydone + 2);  // owner epilogue: x[0 .. K + q)
+    uint32_t *nbuf = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(xs) + a.xs_bytes);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NTW = ntt_threads(LOGL2) / 32;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
@@ -135,10 +152,46 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a)
         for (int b = 0; b < 2; ++b) {
             mbar_init(&pfull[b], TW);
             mbar_init(&pempty[b], NE);
+            mbar_init(&yready[b], TW + NE);
+            mbar_init(&ydone[b], NTW > 0 ? NTW : 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+
+    if constexpr (FUSED) {
+        if (warp >= TW + 1 + NE) {
+            // ---------------------------------------------------------- NTT warps
+            constexpr int NT = ntt_threads(LOGL2);
+            using NBar = NamedBar<3, NT>;
+            const int nt = threadIdx.x - (TW + 1 + NE) * 32;
+            uint32_t *Ts2 = nbuf + (1 << LOGL2);
+            uint32_t *Ts1 = Ts2 + (1 << LOGL2);
+            int pb = 0;
+            uint32_t pph = 0;
+            for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+                const int64_t b = item;  // fused mode: items are whole pairs
+                mbar_wait(&yready[pb], pph);
+                pair_template_to_smem<LOGL2, NBar>(nbuf, Ts2, Ts1, nt, a.f, b);
+                NBar::sync();
+                pair_modulus2<LOGL2, NBar>(nbuf, Ts2, nt, a.f, b);
+                pair_modulus1<LOGL2, NBar>(nbuf, Ts1, nt, a.f, b);
+                if (nt == 0) {  // Theorem 4: z = m1 + M1 ((m2 - m1) M1^{-1} mod M2); k = z < N ? z : -1
+                    const int64_t m1 = a.f.resid[b * 2], m2 = a.f.resid[b * 2 + 1];
+                    int64_t d = (m2 - m1) % a.M2;
+                    if (d < 0) d += a.M2;
+                    const int64_t u = (int64_t)(((unsigned __int128)d * a.crt_inv) % (uint64_t)a.M2);
+                    const int64_t z = m1 + a.M1 * u;
+                    a.k_out[b] = z < a.N ? z : -1;
+                    if (a.residues_out) { a.residues_out[2 * b] = (int32_t)m1; a.residues_out[2 * b + 1] = (int32_t)m2; }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ydone[pb]);
+                if (++pb == 2) { pb = 0; pph ^= 1; }
+            }
+            return;
+        }
+    }
 
     if (warp == TW) {
         // ------------------------------------------------------------ producer
@@ -176,7 +229,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a)
             const int ntile = (int)((it.nrow + 15) / 16);
             const int width = (int)it.width;
             mbar_wait(&pfull[pb], pph);
-            const int32_t *pv = privb + pb * TW * a.priv_stride;
+            const uint16_t *pv = privb + pb * TW * a.priv_stride;
             if (a.owner) {
                 // whole pair, full fold: counts -> values, + wrap + extension, store y2
                 const int q = (int)it.nrow;  // = q1 = q2 (M1 | N)
@@ -224,8 +277,12 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a)
                     }
                 }
             }
+            if constexpr (FUSED) __threadfence_block();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&pempty[pb]);
+            if (lane == 0) {
+                mbar_arrive(&pempty[pb]);
+                if constexpr (FUSED) mbar_arrive(&yready[pb]);
+            }
             if (++pb == 2) { pb = 0; pph ^= 1; }
         }
         return;
@@ -251,8 +308,9 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a)
         const int width = (int)it.width;
         const bool active = warp * 512 < width;
         const int colb = warp * 512 + 16 * lane;  // byte column inside a stage row
-        int32_t *priv = privb + (pb * TW + warp) * a.priv_stride;
+        uint16_t *priv = privb + (pb * TW + warp) * a.priv_stride;
         mbar_wait(&pempty[pb], pph ^ 1);
+        if constexpr (FUSED) mbar_wait(&ydone[pb], pph ^ 1);  // bounds the fold's lead over the NTT
         uint32_t y1w[8], carry[8], W[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) { y1w[i] = 0; carry[i] = 0; W[i] = 0; }
@@ -323,11 +381,10 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a)
                 carry[i] = (lane ? v : 0u) + add;
             }
             if (lane == 31) {  // finished block of the whole warp: bins cs_w + 496 - 16 t + [0, 16)
-                int4 *dst = reinterpret_cast<int4 *>(priv + 496 - 16 * t + 16 * ntile);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    dst[i] = make_int4((int)(carry[2 * i] & 0xFFFFu), (int)(carry[2 * i] >> 16),
-                                       (int)(carry[2 * i + 1] & 0xFFFFu), (int)(carry[2 * i + 1] >> 16));
+                // carry[i] holds bins 2i (low half) and 2i + 1 (high half): already packed u16 pairs
+                uint4 *dst = reinterpret_cast<uint4 *>(priv + 496 - 16 * t + 16 * ntile);
+                dst[0] = make_uint4(carry[0], carry[1], carry[2], carry[3]);
+                dst[1] = make_uint4(carry[4], carry[5], carry[6], carry[7]);
             }
         }
         const int64_t c0 = it.cs_cta + warp * 512 + 16 * lane;
@@ -339,11 +396,9 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a)
                 const uint32_t c = __shfl_up_sync(0xffffffffu, carry[i], 1);
                 lo[i] = __byte_perm(W[i >> 1], 0, (i & 1) ? 0x4342 : 0x4140) + ((lane && ntile) ? c : 0u);
             }
-            int4 *dst = reinterpret_cast<int4 *>(priv + 16 * lane);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                dst[i] = make_int4((int)(lo[2 * i] & 0xFFFFu), (int)(lo[2 * i] >> 16),
-                                   (int)(lo[2 * i + 1] & 0xFFFFu), (int)(lo[2 * i + 1] >> 16));
+            uint4 *dst = reinterpret_cast<uint4 *>(priv + 16 * lane);
+            dst[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            dst[1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
             // M1 bins are owned by this lane: write them now
             if (a.owner) {
                 const int32_t q = nrow;
@@ -388,8 +443,12 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a)
                 }
             }
         }
+        if constexpr (FUSED) __threadfence_block();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&pfull[pb]);
+        if (lane == 0) {
+            mbar_arrive(&pfull[pb]);
+            if constexpr (FUSED) mbar_arrive(&yready[pb]);
+        }
         if (++pb == 2) { pb = 0; pph ^= 1; }
     }
 }
@@ -398,10 +457,10 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32, 1) fold_pm1_tma(TmaArgs a)
 
 // Returns TM_OK after enqueueing, or TM_EUNSUPPORTED when the shape is not covered
 // (the caller then uses the register-streaming fold_pm1).
-int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
-                void *y1, void *y2, int accumulate, void *ws, int64_t R, int64_t n_rc, cudaStream_t s,
-                bool *used_counts) {
-    TmaArgs a{};
+namespace {
+
+int setup_args(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len, void *y1,
+               void *y2, int accumulate, void *ws, int64_t R, int64_t n_rc, TmaArgs &a) {
     a.x = (const int8_t *)x; a.ldx = ldx;
     a.N = p->N; a.M1 = p->M1; a.M2 = p->M2; a.K = p->K; a.q2 = p->q2;
     a.rows = len / p->M1; a.row0 = offset / p->M1;
@@ -416,21 +475,93 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     tm_ws_layout L = tm_ws(p, batch);
     a.counts = (int32_t *)((char *)ws + L.fold_counts);
     a.y1 = (int32_t *)y1; a.y2 = (int32_t *)y2;
+    a.xs_bytes = a.owner ? (int)((p->K + R + 15) / 16 * 16) : 0;
+    return TM_OK;
+}
+
+size_t smem_bytes(const TmaArgs &a, int nst, int logl2) {
+    size_t b = (size_t)nst * STAGE_BYTES + (size_t)2 * a.acc_words * 2 + (2 * nst + 8) * 8 + a.xs_bytes;
+    if (logl2 > 0) b += (size_t)(2 * (1 << logl2) + (1 << (logl2 - 1))) * 4;
+    return b;
+}
+
+template <int NST, int LOGL2>
+int launch(const TmaArgs &a, int64_t grid, size_t smem, cudaStream_t s) {
+    auto k = fold_pm1_tma<NST, LOGL2>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    k<<<(unsigned)grid, (TW + 1 + NE) * 32 + ntt_threads(LOGL2), smem, s>>>(a);
+    TM_CHECK_LAUNCH("fold_pm1_tma");
+    return TM_OK;
+}
+
+}  // namespace
+
+int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
+                void *y1, void *y2, int accumulate, void *ws, int64_t R, int64_t n_rc, cudaStream_t s,
+                bool *used_counts) {
+    TmaArgs a{};
+    int rc = setup_args(p, x, ldx, batch, offset, len, y1, y2, accumulate, ws, R, n_rc, a);
+    if (rc) return rc;
     *used_counts = !a.owner;
     if (!a.owner) {
         cudaError_t e = cudaMemsetAsync(a.counts, 0, (size_t)batch * (p->M1 + p->M2) * 4, s);
         if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: memset");
     }
-    const size_t xs_bytes = a.owner ? (size_t)((p->K + R + 15) / 16 * 16) : 0;
-    const size_t smem = (size_t)NST * STAGE_BYTES + (size_t)2 * a.acc_words * 4 + (2 * NST + 4) * 8 + xs_bytes;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(fold_pm1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
+    const size_t smem = smem_bytes(a, 4, 0);
     if (smem > 227 * 1024) return TM_EUNSUPPORTED;
-    int64_t grid = a.n_items < p->num_sms ? a.n_items : p->num_sms;
-    fold_pm1_tma<<<(unsigned)grid, (TW + 1 + NE) * 32, smem, s>>>(a);
-    TM_CHECK_LAUNCH("tm_fold: fold_pm1_tma");
-    return TM_OK;
+    const int64_t grid = a.n_items < p->num_sms ? a.n_items : p->num_sms;
+    return launch<4, 0>(a, grid, smem, s);
+}
+
+// The whole of Algorithm 1 in ONE kernel for the paper's shape: whole pairs per
+// item (M1 <= 4096, q <= 1024), one NTT prime, L2 = 2 L1 <= 2^13.  Returns
+// TM_EUNSUPPORTED (nothing enqueued) when the plan/batch does not qualify.
+bool tm_fused_ok(const tm_plan_s *p, int64_t batch) {
+    // opt-in (TM_FUSED=1): measured slower than fold + pair-NTT kernels back to back
+    // (0.414 vs 0.346 ms per cfg2 step): one 512-thread NTT group per SM cannot keep up
+    static const bool on = getenv("TM_FUSED") != nullptr;
+    if (!on) return false;
+    return p->fast_fold && p->fast_corr && p->n_primes == 1 && p->M1 <= TCOLS && p->q1 <= 1024 &&
+           p->logL2 == p->logL1 + 1 && p->L1 == p->M1 && p->nload1 == p->M1 && p->logL2 >= 10 && p->logL2 <= 13 &&
+           batch >= p->num_sms;
+}
+
+int tm_fold_corr_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
+                       void *y2, int32_t *resid, int32_t *residues, int64_t *k, void *ws, cudaStream_t s) {
+    if (!tm_fused_ok(p, batch)) return TM_EUNSUPPORTED;
+    if (((uintptr_t)x % 16) || (ldx % 16)) return TM_EUNSUPPORTED;
+    TmaArgs a{};
+    const int64_t R = (p->q1 + 15) / 16 * 16;
+    int rc = setup_args(p, x, ldx, batch, 0, p->N, y1, y2, 0, ws, R, 1, a);
+    if (rc) return rc;
+    if (!a.owner) return TM_EUNSUPPORTED;
+    tm_ntt_tables tabs;
+    tm_ntt_tables_get(p->device, &tabs);
+    FastArgs &f = a.f;
+    f.t = (const int8_t *)t; f.K = p->K;
+    f.twf[0] = tabs.tw2[0][0]; f.twi[0] = tabs.tw2[0][1];
+    f.twf[1] = tabs.tw2[1][0]; f.twi[1] = tabs.tw2[1][1];
+    tm_mont_linv(p->logL2, TM_P1, &f.cL[0], &f.cLs[0]);
+    tm_mont_linv(p->logL1, TM_P1, &f.cL1, &f.cL1s);
+    f.y1 = (const int32_t *)y1; f.y2 = (const int32_t *)y2;
+    f.ldy1 = p->len_y1; f.ldy2 = p->len_y2;
+    f.nload1 = p->nload1; f.nload2 = p->nload2;
+    f.M1 = p->M1; f.M2 = p->M2;
+    f.r1 = nullptr; f.r2 = nullptr;
+    f.resid = resid;
+    a.residues_out = residues;
+    a.k_out = k;
+    a.crt_inv = p->crt_inv;
+    const int64_t grid = batch < p->num_sms ? batch : p->num_sms;
+    switch (p->logL2) {
+        case 10: { const size_t sm = smem_bytes(a, 3, 10); if (sm > 227 * 1024) return TM_EUNSUPPORTED; return launch<3, 10>(a, grid, sm, s); }
+        case 11: { const size_t sm = smem_bytes(a, 3, 11); if (sm > 227 * 1024) return TM_EUNSUPPORTED; return launch<3, 11>(a, grid, sm, s); }
+        case 12: { const size_t sm = smem_bytes(a, 3, 12); if (sm > 227 * 1024) return TM_EUNSUPPORTED; return launch<3, 12>(a, grid, sm, s); }
+        case 13: { const size_t sm = smem_bytes(a, 3, 13); if (sm > 227 * 1024) return TM_EUNSUPPORTED; return launch<3, 13>(a, grid, sm, s); }
+        default: return TM_EUNSUPPORTED;
+    }
 }

@@ -45,6 +45,14 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
     cudaStream_t s = (cudaStream_t)stream;
     RunWs W = run_ws(p, batch, ws);
     tm_prof_mark(0, s);
+    if (tm_fused_ok(p, batch)) {
+        // the whole of Algorithm 1 in one persistent kernel (fold warps + NTT warps per SM)
+        int rc = tm_fold_corr_fused(p, x, ldx, t, batch, W.y1, W.y2, W.resid, residues, k, W.fold_ws, s);
+        if (rc != TM_EUNSUPPORTED) {
+            for (int i = 1; i <= 4; ++i) tm_prof_mark(i, s);
+            return rc;
+        }
+    }
     int rc = tm_fold_impl(p, x, ldx, batch, 0, p->N, W.y1, W.y2, 0, W.fold_ws, s);     // step 3
     if (rc) return rc;
     tm_prof_mark(1, s);

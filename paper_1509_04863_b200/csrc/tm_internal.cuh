@@ -72,6 +72,10 @@ size_t tm_run_ws_bytes(const tm_plan_s *p, int64_t batch);  // run.cu
 
 // ---- internal launchers ----
 bool tm_fast_corr_ok(const tm_plan_s *p);
+void tm_mont_linv(int logL, uint32_t p, uint32_t *c, uint32_t *cs);
+bool tm_fused_ok(const tm_plan_s *p, int64_t batch);
+int tm_fold_corr_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
+                       void *y2, int32_t *resid, int32_t *residues, int64_t *k, void *ws, cudaStream_t s);
 size_t tm_gntt_scratch_bytes(const tm_plan_s *p, int64_t batch);
 int tm_gntt_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, const void *tf,
                       int64_t batch, void *r1, void *r2, int32_t *resid, void *scratch, cudaStream_t s);

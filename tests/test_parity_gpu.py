@@ -309,3 +309,28 @@ def test_cfg5_full_size_fold_and_chunks(tm):
             plan.fold(x[:, r * step:(r + 1) * step], offset=r * step, length=step, y1=a1, y2=a2, accumulate=True)
         torch.cuda.synchronize()
         assert torch.equal(a1, y1) and torch.equal(a2, y2), G
+
+
+@pytest.mark.parametrize("N,K", [(2 ** 16, 1024), (2 ** 18, 2048), (2 ** 20, 4096)])
+def test_fused_kernel_every_pair(tm, N, K, monkeypatch):
+    """tm_run on a batch >= #SMs (the persistent fold + pair-NTT path, and the
+    opt-in single-kernel path when TM_FUSED is set in the environment); every
+    pair's residues and k equal the oracle's, and equal the staged path's
+    (fold -> template fold -> correlate -> match)."""
+    B = 300 if N < 2 ** 20 else 160
+    plan = tm.Plan(N, K, seed=61)
+    x_h, t_h, k0 = tmgen.batch(61, 0, B, N, K, 0.05)
+    x, t = up(x_h), up(t_h)
+    res_run, k_run = plan.run(x, t)
+    y1, y2 = plan.fold(x)
+    r1, r2 = plan.correlate(y1, y2, plan.fold_template(t))
+    res, k = plan.match(r1, r2)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res_run.cpu().numpy(), res.cpu().numpy())
+    np.testing.assert_array_equal(k_run.cpu().numpy(), k.cpu().numpy())
+    kk = k_run.cpu().numpy()
+    rr = res_run.cpu().numpy()
+    step = 1 if N < 2 ** 20 else 8
+    for b in range(0, B, step):
+        o = oracle.ftm(x_h[b], t_h[b], want_vectors=False)
+        assert tuple(rr[b]) == o["residues"] and kk[b] == o["k"], b
