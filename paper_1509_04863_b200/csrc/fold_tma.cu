@@ -50,6 +50,7 @@ struct TmaArgs {
     int64_t *k_out;
     uint32_t crt_inv;
     int xs_bytes;        // bytes reserved for the epilogue's x[0 .. K + q) stage
+    int *work_counter;   // non-NULL: dynamic item assignment (atomic counter, zeroed per launch)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -128,8 +129,10 @@ constexpr int ntt_threads(int logl2) { return logl2 > 0 ? (1 << (logl2 - 4)) : 0
 
 // NST: ring stages.  LOGL2 > 0 selects the fused kernel: NT = L2/16 extra threads
 // (warps 13..) run the pair NTT correlation (ntt_core.cuh) of each finished pair.
-template <int NST, int LOGL2>
-__global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), 1) fold_pm1_tma(TmaArgs a) {
+// MINB = 2 caps registers (<= 78/thread) so that a pair-NTT CTA can share the SM
+// (overlap mode of tm_run).
+template <int NST, int LOGL2, int MINB = 1>
+__global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), MINB) fold_pm1_tma(TmaArgs a) {
     constexpr bool FUSED = LOGL2 > 0;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *ring = smem;
@@ -140,7 +143,9 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), 1) fo
     uint64_t *pempty = pfull + 2;    // [2]: epilogue -> consumers (count NE)
     uint64_t *yready = pempty + 2;   // [2]: y1 + y2 of a pair in global memory (count TW + NE)
     uint64_t *ydone = yready + 2;    // [2]: NTT warps finished with a pair (count NT / 32)
-    uint4 *xs = reinterpret_cast<uint4 *>(ydone + 2);  // owner epilogue: x[0 .. K + q)
+    int64_t *item_q = reinterpret_cast<int64_t *>(ydone + 2);  // [8] producer -> consumers: item of seq
+    int64_t *pitem = item_q + 8;     // [2] consumers -> epilogue / NTT warps: item of a buffer (-1 = end)
+    uint4 *xs = reinterpret_cast<uint4 *>(pitem + 2);  // owner epilogue: x[0 .. K + q)
     uint32_t *nbuf = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(xs) + a.xs_bytes);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int NTW = ntt_threads(LOGL2) / 32;
@@ -169,9 +174,10 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), 1) fo
             uint32_t *Ts1 = Ts2 + (1 << LOGL2);
             int pb = 0;
             uint32_t pph = 0;
-            for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
-                const int64_t b = item;  // fused mode: items are whole pairs
+            for (;;) {
                 mbar_wait(&yready[pb], pph);
+                const int64_t b = pitem[pb];  // fused mode: items are whole pairs
+                if (b < 0) break;
                 pair_template_to_smem<LOGL2, NBar>(nbuf, Ts2, Ts1, nt, a.f, b);
                 NBar::sync();
                 pair_modulus2<LOGL2, NBar>(nbuf, Ts2, nt, a.f, b);
@@ -198,7 +204,15 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), 1) fo
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+            for (int64_t seq = 0;; ++seq) {
+                int64_t item = a.work_counter ? (int64_t)atomicAdd(a.work_counter, 1) : blockIdx.x + seq * gridDim.x;
+                if (item >= a.n_items) item = -1;
+                item_q[seq & 7] = item;  // published by the arrive on the item's first stage
+                if (item < 0) {          // end: complete one more stage phase with no data
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_arrive(&full[s]);
+                    break;
+                }
                 const Item it = decode(a, item);
                 const int8_t *base = a.x + it.b * a.ldx + it.ra * a.M1 + it.cs_cta;
                 for (int64_t r0 = 0; r0 < it.nrow; r0 += SROWS) {
@@ -224,11 +238,19 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), 1) fo
         const int et = threadIdx.x - (TW + 1) * 32;  // 0 .. NE*32-1
         int pb = 0;
         uint32_t pph = 0;
-        for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+        for (;;) {
+            mbar_wait(&pfull[pb], pph);
+            const int64_t item = pitem[pb];
+            if (item < 0) {
+                if constexpr (FUSED) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&yready[pb]);
+                }
+                break;
+            }
             const Item it = decode(a, item);
             const int ntile = (int)((it.nrow + 15) / 16);
             const int width = (int)it.width;
-            mbar_wait(&pfull[pb], pph);
             const uint16_t *pv = privb + pb * TW * a.priv_stride;
             if (a.owner) {
                 // whole pair, full fold: counts -> values, + wrap + extension, store y2
@@ -301,7 +323,20 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), 1) fo
     int pb = 0;
     uint32_t pph = 0;
     const uint32_t ring_u32 = smem_u32(ring);
-    for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+    for (int64_t seq = 0;; ++seq) {
+        mbar_wait(&full[s], ph);  // first stage of the next item (or the end marker)
+        const int64_t item = item_q[seq & 7];
+        mbar_wait(&pempty[pb], pph ^ 1);
+        if constexpr (FUSED) mbar_wait(&ydone[pb], pph ^ 1);  // bounds the fold's lead over the NTT
+        if (item < 0) {  // tell the epilogue (and the NTT warps) to stop
+            if (lane == 0 && warp == 0) pitem[pb] = -1;
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&pfull[pb]);
+                if constexpr (FUSED) mbar_arrive(&yready[pb]);
+            }
+            break;
+        }
         const Item it = decode(a, item);
         const int nrow = (int)it.nrow;
         const int ntile = (nrow + 15) / 16;
@@ -309,8 +344,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), 1) fo
         const bool active = warp * 512 < width;
         const int colb = warp * 512 + 16 * lane;  // byte column inside a stage row
         uint16_t *priv = privb + (pb * TW + warp) * a.priv_stride;
-        mbar_wait(&pempty[pb], pph ^ 1);
-        if constexpr (FUSED) mbar_wait(&ydone[pb], pph ^ 1);  // bounds the fold's lead over the NTT
+        if (lane == 0 && warp == 0) pitem[pb] = item;
         uint32_t y1w[8], carry[8], W[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) { y1w[i] = 0; carry[i] = 0; W[i] = 0; }
@@ -480,14 +514,14 @@ int setup_args(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, in
 }
 
 size_t smem_bytes(const TmaArgs &a, int nst, int logl2) {
-    size_t b = (size_t)nst * STAGE_BYTES + (size_t)2 * a.acc_words * 2 + (2 * nst + 8) * 8 + a.xs_bytes;
+    size_t b = (size_t)nst * STAGE_BYTES + (size_t)2 * a.acc_words * 2 + (2 * nst + 8) * 8 + 10 * 8 + a.xs_bytes;
     if (logl2 > 0) b += (size_t)(2 * (1 << logl2) + (1 << (logl2 - 1))) * 4;
     return b;
 }
 
-template <int NST, int LOGL2>
+template <int NST, int LOGL2, int MINB = 1>
 int launch(const TmaArgs &a, int64_t grid, size_t smem, cudaStream_t s) {
-    auto k = fold_pm1_tma<NST, LOGL2>;
+    auto k = fold_pm1_tma<NST, LOGL2, MINB>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -515,6 +549,36 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     if (smem > 227 * 1024) return TM_EUNSUPPORTED;
     const int64_t grid = a.n_items < p->num_sms ? a.n_items : p->num_sms;
     return launch<4, 0>(a, grid, smem, s);
+}
+
+// Overlap mode of tm_run: the owner-mode fold of a chunk of pairs with dynamic item
+// assignment, a 3-stage ring and <= 78 registers, so that pair-NTT CTAs of the
+// previous chunk (another stream) co-reside on the same SMs.
+bool tm_overlap_ok(const tm_plan_s *p, int64_t batch) {
+    // opt-in (TM_OVERLAP=1): measured slower than the serial fold -> pair-NTT sequence
+    // (cfg2: 0.40-0.59 ms vs 0.342 ms per step with 2-6 chunks)
+    static const bool on = getenv("TM_OVERLAP") != nullptr;
+    if (!on) return false;
+    return p->fast_fold && p->fast_corr && p->n_primes == 1 && p->M1 <= TCOLS && p->q1 <= 1024 &&
+           p->logL2 == p->logL1 + 1 && p->L1 == p->M1 && p->nload1 == p->M1 && p->logL2 >= 10 && p->logL2 <= 14 &&
+           batch >= 2 * p->num_sms;
+}
+
+int tm_fold_overlap(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, void *y1, void *y2, void *ws,
+                    int *counter, cudaStream_t s) {
+    if (((uintptr_t)x % 16) || (ldx % 16)) return TM_EUNSUPPORTED;
+    TmaArgs a{};
+    const int64_t R = (p->q1 + 15) / 16 * 16;
+    int rc = setup_args(p, x, ldx, batch, 0, p->N, y1, y2, 0, ws, R, 1, a);
+    if (rc) return rc;
+    if (!a.owner) return TM_EUNSUPPORTED;
+    cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
+    if (e != cudaSuccess) return tm_cuda_status(e, "tm_run: counter reset");
+    a.work_counter = counter;
+    const size_t sm = smem_bytes(a, 3, 0);
+    if (sm > 227 * 1024) return TM_EUNSUPPORTED;
+    const int64_t grid = batch < p->num_sms ? batch : p->num_sms;
+    return launch<3, 0, 2>(a, grid, sm, s);
 }
 
 // The whole of Algorithm 1 in ONE kernel for the paper's shape: whole pairs per

@@ -171,7 +171,15 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_query(tm_plan plan
     return TM_OK;
 }
 
-extern "C" __attribute__((visibility("default"))) void tm_plan_destroy(tm_plan plan) { free(plan); }
+extern "C" __attribute__((visibility("default"))) void tm_plan_destroy(tm_plan plan) {
+    if (!plan) return;
+    if (plan->aux_stream) {
+        cudaStreamDestroy(plan->aux_stream);
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 16; ++j) cudaEventDestroy(plan->aux_ev[i][j]);
+    }
+    free(plan);
+}
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
@@ -187,6 +195,8 @@ tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch) {
     if (p->dtype == TM_F32) off += align256((size_t)batch * 2 * ((p->M2 + 1023) / 1024) * 8);
     w.gntt = off;
     if (p->big_corr) off += align256(tm_gntt_scratch_bytes(p, batch));
+    w.counters = off;
+    off += 256;
     w.total = off;
     return w;
 }

@@ -1,6 +1,8 @@
 // run.cu -- tm_run (the whole of Algorithm 1 FTM(), on
 // device buffers) and tm_run_host (the same on host buffers, with the
 // host->device copies of chunk i+1 overlapped with the compute of chunk i).
+#include <cstdlib>
+
 #include "tm_internal.cuh"
 
 namespace {
@@ -36,6 +38,55 @@ RunWs run_ws(const tm_plan_s *p, int64_t batch, void *ws) {
 
 size_t tm_run_ws_bytes(const tm_plan_s *p, int64_t batch) { return run_ws(p, batch, nullptr).total; }
 
+#include <mutex>
+static std::mutex g_aux_mu;
+
+// Overlap mode: the batch is cut into chunks; the fold of chunk c+1 (caller's
+// stream) runs while the pair-NTT kernel of chunk c runs on an internal stream,
+// so the HBM-bound fold and the ALU-bound correlation share the SMs.
+static int run_overlap(const tm_plan_s *pc, const void *x, int64_t ldx, const void *t, int64_t batch,
+                       int32_t *residues, int64_t *k, const RunWs &W, void *counters, cudaStream_t s) {
+    tm_plan_s *p = const_cast<tm_plan_s *>(pc);  // lazily created internal stream/events only
+    {
+        std::lock_guard<std::mutex> lk(g_aux_mu);
+        if (!p->aux_stream) {
+            if (cudaStreamCreateWithFlags(&p->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
+                return TM_EUNSUPPORTED;
+            for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 16; ++j) cudaEventCreateWithFlags(&p->aux_ev[i][j], cudaEventDisableTiming);
+        }
+    }
+    static const int env_chunks = getenv("TM_OVERLAP_CHUNKS") ? atoi(getenv("TM_OVERLAP_CHUNKS")) : 0;
+    int C = env_chunks > 0 ? env_chunks : 4;
+    if (C > 16) C = 16;
+    while (C > 1 && batch / C < p->num_sms) --C;
+    const int64_t per = (batch + C - 1) / C;
+    cudaStream_t s2 = p->aux_stream;
+    int *cnt = (int *)counters;
+    // the aux stream must not start before work already queued on s (e.g. inputs)
+    cudaEventRecord(p->aux_ev[1][15], s);
+    cudaStreamWaitEvent(s2, p->aux_ev[1][15], 0);
+    for (int c = 0; c < C; ++c) {
+        const int64_t b0 = c * per, nb = (batch - b0) < per ? (batch - b0) : per;
+        if (nb <= 0) break;
+        int32_t *y1c = (int32_t *)W.y1 + b0 * p->len_y1;
+        int32_t *y2c = (int32_t *)W.y2 + b0 * p->len_y2;
+        int rc = tm_fold_overlap(p, (const int8_t *)x + b0 * ldx, ldx, nb, y1c, y2c, W.fold_ws, cnt + c, s);
+        if (rc) return rc;
+        cudaEventRecord(p->aux_ev[0][c], s);
+        cudaStreamWaitEvent(s2, p->aux_ev[0][c], 0);
+        rc = tm_fast_correlate(p, y1c, y2c, (const int8_t *)t + b0 * p->K, nullptr, nb, nullptr, nullptr,
+                               W.resid + 2 * b0, s2);
+        if (rc) return rc;
+    }
+    cudaEventRecord(p->aux_ev[1][0], s2);
+    cudaStreamWaitEvent(s, p->aux_ev[1][0], 0);
+    for (int i = 1; i <= 3; ++i) tm_prof_mark(i, s);
+    int rc = tm_crt_impl(p, W.resid, batch, residues, k, s);
+    tm_prof_mark(4, s);
+    return rc;
+}
+
 extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const void *x, int64_t ldx, const void *t, int64_t batch, int32_t *residues,
                       int64_t *k, void *ws, void *stream) {
     if (!p) { tm_set_error("tm_run: NULL plan"); return TM_EINVAL; }
@@ -52,6 +103,10 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
             for (int i = 1; i <= 4; ++i) tm_prof_mark(i, s);
             return rc;
         }
+    }
+    if (tm_overlap_ok(p, batch)) {
+        int rc = run_overlap(p, x, ldx, t, batch, residues, k, W, (char *)ws + tm_ws(p, batch).counters, s);
+        if (rc != TM_EUNSUPPORTED) return rc;
     }
     int rc = tm_fold_impl(p, x, ldx, batch, 0, p->N, W.y1, W.y2, 0, W.fold_ws, s);     // step 3
     if (rc) return rc;

@@ -24,6 +24,8 @@ struct tm_plan_s {
     int device;
     int num_sms;
     int64_t tf_elems;    // uint2 (value, shoup) elements per prime per pair (I8) / floats (F32)
+    cudaStream_t aux_stream;    // internal stream of tm_run's overlap mode (created lazily)
+    cudaEvent_t aux_ev[2][16];  // fold-done / ntt-done events per chunk
     int64_t tf_bytes;
     uint32_t crt_inv;    // M1^{-1} mod M2
 };
@@ -65,6 +67,7 @@ struct tm_ws_layout {
     size_t resid;         // int32 [batch][2] residues (tm_run)
     size_t f32_tiles;     // fp32 per-tile argmax partials (tm_run, TM_F32)
     size_t gntt;          // grid-pass NTT scratch (big_corr plans)
+    size_t counters;      // int32 work counters (tm_run overlap mode, one per chunk)
     size_t total;
 };
 tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch);
@@ -74,6 +77,9 @@ size_t tm_run_ws_bytes(const tm_plan_s *p, int64_t batch);  // run.cu
 bool tm_fast_corr_ok(const tm_plan_s *p);
 void tm_mont_linv(int logL, uint32_t p, uint32_t *c, uint32_t *cs);
 bool tm_fused_ok(const tm_plan_s *p, int64_t batch);
+bool tm_overlap_ok(const tm_plan_s *p, int64_t batch);
+int tm_fold_overlap(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, void *y1, void *y2, void *ws,
+                    int *counter, cudaStream_t s);
 int tm_fold_corr_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
                        void *y2, int32_t *resid, int32_t *residues, int64_t *k, void *ws, cudaStream_t s);
 size_t tm_gntt_scratch_bytes(const tm_plan_s *p, int64_t batch);

@@ -334,3 +334,36 @@ def test_fused_kernel_every_pair(tm, N, K, monkeypatch):
     for b in range(0, B, step):
         o = oracle.ftm(x_h[b], t_h[b], want_vectors=False)
         assert tuple(rr[b]) == o["residues"] and kk[b] == o["k"], b
+
+
+# ------------------------------------------------------------- paper scale (NEXT f1)
+TABLE1 = {int(a): float(b) for a, b in (r.split() for r in __import__("conftest").golden("table1.txt"))}
+
+
+@pytest.mark.parametrize("logN,trials", [(23, 400), (24, 400), (25, 300), (26, 200), (27, 100)])
+def test_table1_reproduction_on_gpu(tm, logN, trials):
+    """PAPER.md Table 1: success of Algorithm 1 with K = N/2^10,
+    noiseless +-1 codes, M1 = K, M2 = K+1, run through the CUDA path at the
+    paper's sizes (device-generated inputs, global pair = trial index).  The
+    success count must fall in a binomial band around the printed value: the
+    0.999 two-sided interval for p = printed, widened by 0.03 for the paper's own
+    1000-trial sampling error (and for 0.05 vs our reading)."""
+    from scipy.stats import binom
+    N = 2 ** logN
+    K = N >> 10
+    plan = tm.Plan(N, K, seed=1509)
+    B = max(1, min(trials, (1 << 31) // N))
+    ok = 0
+    done = 0
+    while done < trials:
+        nb = min(B, trials - done)
+        x, t, k0 = plan.generate(done, nb, 0.0)
+        _, k = plan.run(x, t)
+        ok += int((k == k0).sum())
+        done += nb
+        del x, t
+    p = TABLE1[logN]
+    lo = binom.ppf(0.0005, trials, max(p - 0.03, 0.0))
+    hi = binom.ppf(0.9995, trials, min(p + 0.03, 1.0))
+    print(f"Table 1 N=2^{logN}: {ok}/{trials} = {ok / trials:.3f} (paper {p})")
+    assert lo <= ok <= hi, (ok, trials, p)
