@@ -55,6 +55,14 @@ enum {
 #define TM_BINARY 1u  /* caller asserts every x and t entry is -1 or +1 (int8
                          only): enables the packed +-1 fold kernel.  Passing
                          other values with this flag gives unspecified y. */
+#define TM_CORR_NTT 2u  /* TM_I8 correlation engine: number-theoretic transform
+                           (CUDA cores).  Default: the tensor-core engine when
+                           the plan is eligible for it, else the NTT. */
+#define TM_CORR_TC 4u   /* TM_I8 correlation engine: int8 tensor cores
+                           (tcgen05.mma kind::i8, exact int32 accumulation of
+                           4-bit limbs of y); TM_EUNSUPPORTED if the plan is not
+                           eligible (|y| bound > 32767, K > 65536, shared
+                           memory).  The two engines give identical results. */
 
 typedef struct {
     int64_t N;          /* signal length */
@@ -71,6 +79,7 @@ typedef struct {
     int32_t fast_fold;  /* 1 if the full-signal fold uses the packed +-1 kernel */
     int64_t tf_bytes;   /* bytes of one folded template (tm_fold_template output) */
     uint64_t seed;      /* seed of tm_generate */
+    int32_t corr_engine; /* TM_I8: 1 = tensor-core correlation (TM_CORR_TC), 0 = NTT */
 } tm_plan_info;
 
 /*

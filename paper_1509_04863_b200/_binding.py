@@ -9,6 +9,8 @@ _LIB_PATH = os.path.join(_HERE, "libtm.so")
 
 TM_I8, TM_F32 = 0, 1
 TM_BINARY = 1
+TM_CORR_NTT, TM_CORR_TC = 2, 4
+_ENGINES = {None: 0, "auto": 0, "ntt": TM_CORR_NTT, "tc": TM_CORR_TC}
 TM_OK, TM_EINVAL, TM_EUNSUPPORTED, TM_ECUDA = 0, 1, 2, 3
 
 EXPORTED_SYMBOLS = (
@@ -25,7 +27,8 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("N", _i64), ("K", _i64), ("M1", _i64), ("M2", _i64), ("q1", _i64), ("q2", _i64),
                 ("s1", _i64), ("s2", _i64), ("len_y1", _i64), ("len_y2", _i64), ("L1", _i64),
                 ("L2", _i64), ("n_primes", _i32), ("dtype", _i32), ("flags", _u32),
-                ("fast_fold", _i32), ("tf_bytes", _i64), ("seed", _u64)]
+                ("fast_fold", _i32), ("tf_bytes", _i64), ("seed", _u64),
+                ("corr_engine", _i32)]
 
 
 class TMError(RuntimeError):
@@ -122,14 +125,18 @@ def _ptr(t):
 
 
 class Plan:
-    """tm_plan: Alg. 1 step 2 (M1 = M or K, M2 = M1 + 1).  dtype is "int8" or "float32"."""
+    """tm_plan: Alg. 1 step 2 (M1 = M or K, M2 = M1 + 1).  dtype is "int8" or "float32".
+    engine (int8 only): None/"auto" (tensor cores when eligible), "ntt" or "tc"."""
 
-    def __init__(self, N: int, K: int, M: int = 0, seed: int = 0, dtype: str = "int8", binary: bool = True):
+    def __init__(self, N: int, K: int, M: int = 0, seed: int = 0, dtype: str = "int8", binary: bool = True,
+                 engine: str | None = None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1509_04863_b200.Plan needs a CUDA device (no CPU fallback)")
         self.dtype = {"int8": TM_I8, "float32": TM_F32}[str(dtype).replace("torch.", "")]
         flags = TM_BINARY if (binary and self.dtype == TM_I8) else 0
+        if self.dtype == TM_I8:
+            flags |= _ENGINES[engine]
         h = _p()
         _check(lib().tm_plan_create(ctypes.byref(h), N, K, M, seed, self.dtype, flags), "tm_plan_create")
         self._h = h

@@ -480,6 +480,7 @@ extern "C" __attribute__((visibility("default"))) int tm_fold_template(tm_plan p
         return TM_OK;
     }
     if (batch > 0x7FFFFFFF) { tm_set_error("tm_fold_template: batch too large"); return TM_EUNSUPPORTED; }
+    if (p->use_tc) return tm_tc_template(p, t, batch, tf, s);
     if (p->fast_corr) return tm_fast_template(p, t, batch, tf, s);
     if (p->big_corr) return tm_gntt_template(p, t, batch, tf, s);
     TfArgs A;
@@ -528,6 +529,7 @@ int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const 
         }
         return TM_OK;
     }
+    if (p->use_tc) return tm_tc_correlate(p, y1, y2, tf, p->tf_bytes, batch, r1, r2, resid, nullptr, nullptr, s);
     if (p->fast_corr) return tm_fast_correlate(p, y1, y2, nullptr, tf, batch, r1, r2, resid, s);
     if (p->big_corr) return tm_gntt_correlate(p, y1, y2, nullptr, tf, batch, r1, r2, resid, gntt_scratch, s);
     if (!corr_in_smem(p)) {

@@ -84,7 +84,9 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
     if (N < 1 || N >= (int64_t(1) << 62)) { tm_set_error("tm_plan_create: N=%lld out of range", (long long)N); return TM_EINVAL; }
     if (K < 1) { tm_set_error("tm_plan_create: K=%lld < 1", (long long)K); return TM_EINVAL; }
     if (dtype != TM_I8 && dtype != TM_F32) { tm_set_error("tm_plan_create: bad dtype %d", dtype); return TM_EINVAL; }
-    if (flags & ~TM_BINARY) { tm_set_error("tm_plan_create: unknown flags 0x%x", flags); return TM_EINVAL; }
+    if (flags & ~(TM_BINARY | TM_CORR_NTT | TM_CORR_TC)) { tm_set_error("tm_plan_create: unknown flags 0x%x", flags); return TM_EINVAL; }
+    if ((flags & TM_CORR_NTT) && (flags & TM_CORR_TC)) { tm_set_error("tm_plan_create: TM_CORR_NTT and TM_CORR_TC are exclusive"); return TM_EINVAL; }
+    if ((flags & (TM_CORR_NTT | TM_CORR_TC)) && dtype != TM_I8) { tm_set_error("tm_plan_create: TM_CORR_* needs TM_I8"); return TM_EINVAL; }
     if ((flags & TM_BINARY) && dtype != TM_I8) { tm_set_error("tm_plan_create: TM_BINARY needs TM_I8"); return TM_EINVAL; }
     int64_t M1 = M ? M : K, M2 = M1 + 1;
     if (M1 < K) { tm_set_error("tm_plan_create: M1=%lld < K=%lld (Alg. 1 step 2 needs M1 >= K)", (long long)M1, (long long)K); return TM_EINVAL; }
@@ -151,6 +153,25 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
         tm_ntt_tables t;
         int rc = tm_ntt_tables_get(dev, &t);
         if (rc != TM_OK) { free(p); return rc; }
+        // correlation engine: tensor cores when eligible (TM_CORR=ntt in the
+        // environment forces the NTT for A/B measurements of the default)
+        tm_tc_plan(p);
+        static const char *env = getenv("TM_CORR");
+        const bool env_ntt = env && strcmp(env, "ntt") == 0;
+        if (flags & TM_CORR_TC) {
+            if (!p->tc_ok) {
+                free(p);
+                tm_set_error("tm_plan_create: TM_CORR_TC: plan not eligible for the tensor-core engine");
+                return TM_EUNSUPPORTED;
+            }
+            p->use_tc = 1;
+        } else {
+            p->use_tc = p->tc_ok && !(flags & TM_CORR_NTT) && !env_ntt;
+        }
+        if (p->use_tc) {  // the folded template is the int8 template itself, 16-byte rows
+            p->tf_bytes = (K + 15) / 16 * 16;
+            p->tf_elems = p->tf_bytes;
+        }
     } else {
         p->n_primes = 0;
         p->tf_elems = K;
@@ -168,6 +189,7 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_query(tm_plan plan
     info->L1 = plan->L1; info->L2 = plan->L2;
     info->n_primes = plan->n_primes; info->dtype = plan->dtype; info->flags = plan->flags;
     info->fast_fold = plan->fast_fold; info->tf_bytes = plan->tf_bytes; info->seed = plan->seed;
+    info->corr_engine = plan->use_tc;
     return TM_OK;
 }
 

@@ -96,6 +96,17 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
     cudaStream_t s = (cudaStream_t)stream;
     RunWs W = run_ws(p, batch, ws);
     tm_prof_mark(0, s);
+    if (p->use_tc) {
+        // step 3, then steps 4-9 in one tensor-core kernel (argmax + CRT in its epilogue)
+        int rc = tm_fold_impl(p, x, ldx, batch, 0, p->N, W.y1, W.y2, 0, W.fold_ws, s);
+        if (rc) return rc;
+        tm_prof_mark(1, s);
+        tm_prof_mark(2, s);
+        rc = tm_tc_correlate(p, W.y1, W.y2, t, p->K, batch, nullptr, nullptr, nullptr, residues, k, s);
+        tm_prof_mark(3, s);
+        tm_prof_mark(4, s);
+        return rc;
+    }
     if (tm_fused_ok(p, batch)) {
         // the whole of Algorithm 1 in one persistent kernel (fold warps + NTT warps per SM)
         int rc = tm_fold_corr_fused(p, x, ldx, t, batch, W.y1, W.y2, W.resid, residues, k, W.fold_ws, s);
@@ -146,6 +157,7 @@ extern "C" __attribute__((visibility("default"))) int tm_correlate_match(tm_plan
     cudaStream_t s = (cudaStream_t)stream;
     RunWs W = run_ws(p, batch, ws);
     int rc;
+    if (p->use_tc) return tm_tc_correlate(p, y1, y2, t, p->K, batch, nullptr, nullptr, nullptr, residues, k, s);
     if (p->fast_corr) {
         rc = tm_fast_correlate(p, y1, y2, t, nullptr, batch, nullptr, nullptr, W.resid, s);
     } else if (p->big_corr) {

@@ -28,6 +28,11 @@ struct tm_plan_s {
     cudaEvent_t aux_ev[2][16];  // fold-done / ntt-done events per chunk
     int64_t tf_bytes;
     uint32_t crt_inv;    // M1^{-1} mod M2
+    // tensor-core correlation engine (corr_tc.cu)
+    int use_tc;          // tm_run / tm_correlate use corr_tc_kernel
+    int tc_ok;           // plan shape eligible for it
+    int tc_NA[2], tc_NMC, tc_R, tc_NC, tc_JA, tc_lmax;
+    uint32_t tc_ncols, tc_offB, tc_offTp, tc_offMisc, tc_smem;
 };
 
 // ---- error plumbing (plan.cu) ----
@@ -94,5 +99,9 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
 int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const void *tf,
                       int64_t batch, void *r1, void *r2, int32_t *resid, void *tile_scratch,
                       void *gntt_scratch, cudaStream_t s);
+void tm_tc_plan(tm_plan_s *p);
+int tm_tc_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt, int64_t batch,
+                    void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k, cudaStream_t s);
+int tm_tc_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf, cudaStream_t s);
 int tm_crt_impl(const tm_plan_s *p, const int32_t *resid, int64_t batch, int32_t *residues_out,
                 int64_t *k, cudaStream_t s);

@@ -89,21 +89,27 @@ def test_device_generator_matches_host_f32(tm):
 
 
 # ------------------------------------------------------------- cfg1 and small int cases
-def test_cfg1_exact(tm):
+ENGINES = ["auto", "ntt"]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_cfg1_exact(tm, engine):
     """BASELINE cfg1: N=4096, K=256, +-1, noiseless; many seeds (one pair each)."""
     N, K = 4096, 256
-    plan = tm.Plan(N, K, seed=1)
+    plan = tm.Plan(N, K, seed=1, engine=engine)
+    assert plan.corr_engine == (engine == "auto")
     x_h, t_h, k0 = tmgen.batch(1, 0, 64, N, K, 0.0)
     kh, _ = check_int_pairs(tm, plan, x_h, t_h, range(64))
     assert np.mean(kh == k0) > 0.5  # SURVEY measured 0.758 for this configuration
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("N,K,M", [(1000, 37, 0), (997, 40, 45), (64, 8, 0), (12, 3, 4), (5000, 71, 80)])
-def test_general_fold_wrap_cases(tm, N, K, M):
+def test_general_fold_wrap_cases(tm, N, K, M, engine):
     """M not dividing N (mod-N wrap, reading C5), M > K, tiny sizes: general kernels."""
     rng = np.random.default_rng(N + K)
     B = 5
-    plan = tm.Plan(N, K, M=M, seed=2, binary=False)
+    plan = tm.Plan(N, K, M=M, seed=2, binary=False, engine=engine)
     x_h = rng.integers(-128, 128, (B, N)).astype(np.int8)
     t_h = np.stack([x_h[b][(np.arange(K) + 7 * b) % N] for b in range(B)]).astype(np.int8)
     check_int_pairs(tm, plan, x_h, t_h, range(B))
@@ -123,12 +129,13 @@ def test_two_prime_ntt(tm):
     check_int_pairs(tm, plan, x_h, t_h, range(3))
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("N,K,B", [(2 ** 16, 1024, 6), (4096 * 37, 4096, 3), (8192 * 600, 8192, 1),
                                    (2 ** 18, 4096, 4), (512 * 300, 512, 3)])
-def test_packed_pm1_fold(tm, N, K, B):
+def test_packed_pm1_fold(tm, N, K, B, engine):
     """The packed +-1 kernel: q not a multiple of 16, several column groups,
     several row items per pair."""
-    plan = tm.Plan(N, K, seed=11)
+    plan = tm.Plan(N, K, seed=11, engine=engine)
     assert plan.fast_fold == 1
     x_h, t_h, _ = tmgen.batch(11, 0, B, N, K, 0.1)
     check_int_pairs(tm, plan, x_h, t_h, range(B))
@@ -224,18 +231,54 @@ def test_f32_ragged(tm):
 
 
 # ------------------------------------------------------------- BASELINE sizes
-def test_cfg2_full_batch_sampled(tm):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_cfg2_full_batch_sampled(tm, engine):
     """cfg2 at full size (N=2^20, K=4096, 1024 pairs, 10% flips), tm_run on the whole
     batch as bench.py launches it; oracle on 24 sampled pairs; k of every pair equals
     CRT of its residues; success rate reported."""
     N, K, B = 2 ** 20, 4096, 1024
-    plan = tm.Plan(N, K, seed=2)
+    plan = tm.Plan(N, K, seed=2, engine=engine)
+    assert plan.corr_engine == (engine == "auto")
     x_h, t_h, k0 = tmgen.batch(2, 0, B, N, K, 0.1)
     kh, kr = check_int_pairs(tm, plan, x_h, t_h, list(range(0, B, 43)) + [B - 1])
     np.testing.assert_array_equal(kh, kr)
     rate = float(np.mean(kh == k0))
     print(f"cfg2 success rate {rate:.3f}")
     assert 0.02 < rate < 0.3   # SURVEY: 0.093 over 300 trials
+
+
+# ------------------------------------------------------------- tensor-core engine specifics
+@pytest.mark.parametrize("N,K,M,B", [(2 ** 14, 200, 0, 3),      # K not a multiple of 16 / 128
+                                     (30000, 300, 333, 3),      # M1, M2 ragged vs the 128-row blocks
+                                     (2 ** 16, 1024, 1100, 2),  # M > K, leftover > 8 -> extra block
+                                     (4096, 256, 0, 2)])
+def test_tc_engine_limbs_and_ragged_shapes(tm, N, K, M, B):
+    """TM_CORR_TC on general int8 data: |y| up to 128 q needs 2-3 four-bit limbs
+    (pair 0: all +127 -> the largest |y|; pair 1: random; pair 2: +-1), ragged
+    M, K not a multiple of 16; bit-exact against the oracle."""
+    plan = tm.Plan(N, K, M=M, seed=5, binary=False, engine="tc")
+    assert plan.corr_engine == 1
+    rng = np.random.default_rng(N ^ K)
+    x_h = rng.integers(-128, 128, (B, N)).astype(np.int8)
+    x_h[0] = 127
+    if B > 2:
+        x_h[2] = rng.choice(np.array([-1, 1], np.int8), N)
+    t_h = rng.integers(-128, 128, (B, K)).astype(np.int8)
+    t_h[0, : K // 2] = -128
+    check_int_pairs(tm, plan, x_h, t_h, range(B))
+
+
+def test_tc_and_ntt_engines_agree_on_cfg2(tm):
+    """Every pair of a full cfg2 batch: residues and k from the two exact engines
+    are identical (both are pinned to the oracle on sampled pairs above)."""
+    N, K, B = 2 ** 20, 4096, 1024
+    x, t, _ = tm.Plan(N, K, seed=9).generate(0, B, 0.1)
+    out = {}
+    for engine in ("tc", "ntt"):
+        plan = tm.Plan(N, K, seed=9, engine=engine)
+        out[engine] = [v.cpu().numpy() for v in plan.run(x, t)]
+    np.testing.assert_array_equal(out["tc"][0], out["ntt"][0])
+    np.testing.assert_array_equal(out["tc"][1], out["ntt"][1])
 
 
 @pytest.mark.parametrize("K", [4096, 8192, 16384])
