@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "ntt_core.cuh"
+#include "tc_core.cuh"
 
 namespace {
 
@@ -51,6 +52,10 @@ struct TmaArgs {
     uint32_t crt_inv;
     int xs_bytes;        // bytes reserved for the epilogue's x[0 .. K + q) stage
     int *work_counter;   // non-NULL: dynamic item assignment (atomic counter, zeroed per launch)
+    // tensor-core fused mode: 8 warps correlate pair i (tc_core.cuh) while the fold streams pair i+1
+    tc::TcArgs tca;
+    uint32_t tc_off;     // shared-memory offset of the tensor-core group's region
+    int64_t ldy1, ldy2;  // owner outputs: row strides of y1, y2 (>= M + K)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -131,9 +136,12 @@ constexpr int ntt_threads(int logl2) { return logl2 > 0 ? (1 << (logl2 - 4)) : 0
 // (warps 13..) run the pair NTT correlation (ntt_core.cuh) of each finished pair.
 // MINB = 2 caps registers (<= 78/thread) so that a pair-NTT CTA can share the SM
 // (overlap mode of tm_run).
-template <int NST, int LOGL2, int MINB = 1>
-__global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), MINB) fold_pm1_tma(TmaArgs a) {
-    constexpr bool FUSED = LOGL2 > 0;
+constexpr int TC_GROUP = 5;  // named barrier of the tensor-core warps
+
+template <int NST, int LOGL2, int MINB = 1, bool TCM = false>
+__global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM ? tc::NTHR : 0), MINB)
+    fold_pm1_tma(TmaArgs a) {
+    constexpr bool FUSED = LOGL2 > 0 || TCM;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *ring = smem;
     uint16_t *privb = reinterpret_cast<uint16_t *>(smem + NST * STAGE_BYTES);  // [2][TW][priv_stride]
@@ -148,8 +156,13 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), MINB)
     uint4 *xs = reinterpret_cast<uint4 *>(pitem + 2);  // owner epilogue: x[0 .. K + q)
     uint32_t *nbuf = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(xs) + a.xs_bytes);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int NTW = ntt_threads(LOGL2) / 32;
+    constexpr int NTW = TCM ? tc::NTHR / 32 : ntt_threads(LOGL2) / 32;
     if (threadIdx.x == 0) {
+        if constexpr (TCM) {
+            mbar_init(reinterpret_cast<uint64_t *>(smem + a.tc_off + a.tca.offMisc), 1);  // MMA passes
+            for (int b = 0; b < 2; ++b)  // pbegin: consumers -> tensor-core warps, pair of a buffer known
+                mbar_init(reinterpret_cast<uint64_t *>(smem + a.tc_off + a.tca.offMisc + tc::MISC_PBEGIN) + b, 1);
+        }
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], TW);
@@ -164,7 +177,47 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), MINB)
     }
     __syncthreads();
 
-    if constexpr (FUSED) {
+    if constexpr (TCM) {
+        if (warp >= TW + 1 + NE) {
+            // ------------------------------------------------- tensor-core warps
+            // steps 4-9 of each finished pair (tc_core.cuh), one pair behind the fold
+            using GS = tc::GroupSync<TC_GROUP>;
+            const int gt = threadIdx.x - (TW + 1 + NE) * 32;
+            uint8_t *tsm = smem + a.tc_off;
+            uint32_t *tslot = reinterpret_cast<uint32_t *>(tsm + a.tca.offMisc + 8);
+            if (gt < 32) {
+                asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                                 smem_u32(tslot)),
+                             "r"(a.tca.ncols));
+                asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            GS::sync();
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t tbase = *tslot;
+            uint32_t mph = 0;
+            int pb = 0;
+            uint32_t pph = 0;
+            uint64_t *pbegin = reinterpret_cast<uint64_t *>(tsm + a.tca.offMisc + tc::MISC_PBEGIN);
+            for (;;) {
+                mbar_wait(&pbegin[pb], pph);
+                const int64_t b = pitem[pb];  // fused mode: items are whole pairs
+                if (b < 0) break;
+                tc::tc_pre<GS>(a.tca, tsm, b, gt);  // template side while the pair is being folded
+                mbar_wait(&yready[pb], pph);
+                tc::tc_main<GS>(a.tca, tsm, b, gt, warp & 3, tbase, mph);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ydone[pb]);
+                if (++pb == 2) { pb = 0; pph ^= 1; }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            GS::sync();
+            if (gt < 32)
+                asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(a.tca.ncols));
+            return;
+        }
+    }
+    if constexpr (LOGL2 > 0) {
         if (warp >= TW + 1 + NE) {
             // ---------------------------------------------------------- NTT warps
             constexpr int NT = ntt_threads(LOGL2);
@@ -265,7 +318,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), MINB)
                     asm volatile("bar.sync 2, %0;" ::"n"(NE * 32) : "memory");
                 }
                 const int8_t *xb = reinterpret_cast<const int8_t *>(xs);
-                int32_t *o2 = a.y2 + it.b * (a.M2 + a.K);
+                int32_t *o2 = a.y2 + it.b * a.ldy2;
                 const int M2 = (int)a.M2, M1 = (int)a.M1, K = (int)a.K;
                 const int dlo = -16 * ntile;
                 for (int k = et; k < M2; k += NE * 32) {
@@ -328,8 +381,11 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), MINB)
         const int64_t item = item_q[seq & 7];
         mbar_wait(&pempty[pb], pph ^ 1);
         if constexpr (FUSED) mbar_wait(&ydone[pb], pph ^ 1);  // bounds the fold's lead over the NTT
-        if (item < 0) {  // tell the epilogue (and the NTT warps) to stop
-            if (lane == 0 && warp == 0) pitem[pb] = -1;
+        if (item < 0) {  // tell the epilogue (and the NTT / tensor-core warps) to stop
+            if (lane == 0 && warp == 0) {
+                pitem[pb] = -1;
+                if constexpr (TCM) mbar_arrive(reinterpret_cast<uint64_t *>(smem + a.tc_off + a.tca.offMisc + tc::MISC_PBEGIN) + pb);
+            }
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&pfull[pb]);
@@ -344,7 +400,10 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), MINB)
         const bool active = warp * 512 < width;
         const int colb = warp * 512 + 16 * lane;  // byte column inside a stage row
         uint16_t *priv = privb + (pb * TW + warp) * a.priv_stride;
-        if (lane == 0 && warp == 0) pitem[pb] = item;
+        if (lane == 0 && warp == 0) {
+            pitem[pb] = item;
+            if constexpr (TCM) mbar_arrive(reinterpret_cast<uint64_t *>(smem + a.tc_off + a.tca.offMisc + tc::MISC_PBEGIN) + pb);
+        }
         uint32_t y1w[8], carry[8], W[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) { y1w[i] = 0; carry[i] = 0; W[i] = 0; }
@@ -442,7 +501,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2), MINB)
                     v[2 * i] = q - (int32_t)(y1w[i] & 0xFFFFu);
                     v[2 * i + 1] = q - (int32_t)(y1w[i] >> 16);
                 }
-                int32_t *o1 = a.y1 + it.b * (a.M1 + a.K);
+                int32_t *o1 = a.y1 + it.b * a.ldy1;
 #pragma unroll
                 for (int rep = 0; rep < 2; ++rep) {  // y1[c] and y1[M1 + c] = y1[c] (M1 | N), c < K
                     const int64_t base = rep ? a.M1 + c0 : c0;
@@ -509,6 +568,7 @@ int setup_args(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, in
     tm_ws_layout L = tm_ws(p, batch);
     a.counts = (int32_t *)((char *)ws + L.fold_counts);
     a.y1 = (int32_t *)y1; a.y2 = (int32_t *)y2;
+    a.ldy1 = p->M1 + p->K; a.ldy2 = p->M2 + p->K;
     a.xs_bytes = a.owner ? (int)((p->K + R + 15) / 16 * 16) : 0;
     return TM_OK;
 }
@@ -519,15 +579,16 @@ size_t smem_bytes(const TmaArgs &a, int nst, int logl2) {
     return b;
 }
 
-template <int NST, int LOGL2, int MINB = 1>
+template <int NST, int LOGL2, int MINB = 1, bool TCM = false>
 int launch(const TmaArgs &a, int64_t grid, size_t smem, cudaStream_t s) {
-    auto k = fold_pm1_tma<NST, LOGL2, MINB>;
+    auto k = fold_pm1_tma<NST, LOGL2, MINB, TCM>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         attr = true;
     }
-    k<<<(unsigned)grid, (TW + 1 + NE) * 32 + ntt_threads(LOGL2), smem, s>>>(a);
+    k<<<(unsigned)grid, (TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM ? tc::NTHR : 0), smem, s>>>(a);
     TM_CHECK_LAUNCH("fold_pm1_tma");
     return TM_OK;
 }
@@ -562,6 +623,17 @@ bool tm_overlap_ok(const tm_plan_s *p, int64_t batch) {
     return p->fast_fold && p->fast_corr && p->n_primes == 1 && p->M1 <= TCOLS && p->q1 <= 1024 &&
            p->logL2 == p->logL1 + 1 && p->L1 == p->M1 && p->nload1 == p->M1 && p->logL2 >= 10 && p->logL2 <= 14 &&
            batch >= 2 * p->num_sms;
+}
+
+// Tensor-core two-stream overlap mode of tm_run (run.cu): opt-in (TM_OVERLAP=1);
+// measured slower than the fused kernel and than fold -> correlation in sequence
+// (cfg2: 0.36-0.72 ms vs 0.277 ms per step with 4-16 chunks).
+bool tm_overlap_tc_ok(const tm_plan_s *p, int64_t batch) {
+    static const char *env = getenv("TM_OVERLAP");
+    static const bool on = env && env[0] == '1';
+    if (!on) return false;
+    return p->use_tc && p->fast_fold && p->M1 <= TCOLS && p->q1 <= 1024 && batch >= 2 * 64 &&
+           p->N % 16 == 0 && p->N == p->M1 * p->q1;
 }
 
 int tm_fold_overlap(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, void *y1, void *y2, void *ws,
@@ -628,4 +700,42 @@ int tm_fold_corr_fused(const tm_plan_s *p, const void *x, int64_t ldx, const voi
         case 13: { const size_t sm = smem_bytes(a, 3, 13); if (sm > 227 * 1024) return TM_EUNSUPPORTED; return launch<3, 13>(a, grid, sm, s); }
         default: return TM_EUNSUPPORTED;
     }
+}
+
+// The whole of Algorithm 1 in ONE persistent kernel with the tensor-core
+// correlation: per SM, the fold warps stream pair i+1 while 8 tensor-core
+// warps correlate pair i (tc_core.cuh).  Whole pairs per item (M1 <= 4096,
+// q <= 1024).  Returns TM_EUNSUPPORTED (nothing enqueued) when the plan/batch
+// does not qualify.
+bool tm_fused_tc_ok(const tm_plan_s *p, int64_t batch) {
+    static const char *env = getenv("TM_FUSED_TC");
+    static const bool off = env && env[0] == '0';
+    if (off) return false;
+    return p->use_tc && p->fast_fold && p->M1 <= TCOLS && p->q1 <= 1024 && p->N == p->M1 * p->q1 && batch >= 1;
+}
+
+int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
+                     void *y2, int32_t *residues, int64_t *k, void *ws, int *counter, cudaStream_t s) {
+    if (!tm_fused_tc_ok(p, batch)) return TM_EUNSUPPORTED;
+    if (((uintptr_t)x % 16) || (ldx % 16)) return TM_EUNSUPPORTED;
+    TmaArgs a{};
+    const int64_t R = (p->q1 + 15) / 16 * 16;
+    int rc = setup_args(p, x, ldx, batch, 0, p->N, y1, y2, 0, ws, R, 1, a);
+    if (rc) return rc;
+    if (!a.owner) return TM_EUNSUPPORTED;
+    tm_tc_fill_args(p, y1, y2, t, p->K, nullptr, nullptr, nullptr, residues, k, a.tca);
+    a.tca.dbg = tm_tc_dbg_buffer();
+    // y is scratch here: 128-byte rows, dropped from L2 without write-back once correlated
+    a.ldy1 = a.tca.ldy[0] = p->ldy1_run;
+    a.ldy2 = a.tca.ldy[1] = p->ldy2_run;
+    a.tca.discard_y = 1;
+    const size_t base = (smem_bytes(a, 3, 0) + 1023) / 1024 * 1024;
+    a.tc_off = (uint32_t)base;
+    const size_t sm = base + p->tc_smem;
+    if (sm > 227 * 1024) return TM_EUNSUPPORTED;
+    cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
+    if (e != cudaSuccess) return tm_cuda_status(e, "tm_run: counter reset");
+    a.work_counter = counter;
+    const int64_t grid = batch < p->num_sms ? batch : p->num_sms;
+    return launch<3, 0, 1, true>(a, grid, sm, s);
 }

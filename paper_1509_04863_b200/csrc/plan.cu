@@ -122,6 +122,7 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
     p->q1 = ceil_div(N, M1); p->q2 = ceil_div(N, M2);
     p->s1 = p->q1 * M1 - N; p->s2 = p->q2 * M2 - N;
     p->len_y1 = M1 + K; p->len_y2 = M2 + K;
+    p->ldy1_run = (p->len_y1 + 31) / 32 * 32; p->ldy2_run = (p->len_y2 + 31) / 32 * 32;
     p->L1 = L1; p->L2 = L2;
     p->logL1 = ilog2_ceil(L1); p->logL2 = ilog2_ceil(L2);
     p->nload1 = cyc1 ? M1 : M1 + K - 1;

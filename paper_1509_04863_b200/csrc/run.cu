@@ -28,8 +28,8 @@ RunWs run_ws(const tm_plan_s *p, int64_t batch, void *ws) {
     r.tiles = base + F.f32_tiles;
     r.gntt = base + F.gntt;
     const size_t ey = p->dtype == TM_I8 ? 4 : 4;
-    r.y1 = base + off; off += align256((size_t)batch * p->len_y1 * ey);
-    r.y2 = base + off; off += align256((size_t)batch * p->len_y2 * ey);
+    r.y1 = base + off; off += align256((size_t)batch * p->ldy1_run * ey);  // >= every path's stride
+    r.y2 = base + off; off += align256((size_t)batch * p->ldy2_run * ey);
     r.tf = base + off; off += align256((size_t)batch * p->tf_bytes);
     r.total = off;
     return r;
@@ -87,6 +87,52 @@ static int run_overlap(const tm_plan_s *pc, const void *x, int64_t ldx, const vo
     return rc;
 }
 
+// Tensor-core overlap mode: the fold of chunk c+1 (caller's stream, 3-stage ring,
+// dynamic item assignment) runs while corr_tc_kernel correlates chunk c on an
+// internal stream; a fold CTA (~127 KB shared memory) and a tensor-core CTA
+// (~90 KB, TMEM for its accumulators) co-reside on each SM, so the HBM-bound
+// fold and the tensor-core correlation overlap.
+static int run_overlap_tc(const tm_plan_s *pc, const void *x, int64_t ldx, const void *t, int64_t batch,
+                          int32_t *residues, int64_t *k, const RunWs &W, void *counters, cudaStream_t s) {
+    tm_plan_s *p = const_cast<tm_plan_s *>(pc);  // lazily created internal stream/events only
+    {
+        std::lock_guard<std::mutex> lk(g_aux_mu);
+        if (!p->aux_stream) {
+            if (cudaStreamCreateWithFlags(&p->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
+                return TM_EUNSUPPORTED;
+            for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 16; ++j) cudaEventCreateWithFlags(&p->aux_ev[i][j], cudaEventDisableTiming);
+        }
+    }
+    static const int env_chunks = getenv("TM_OVERLAP_CHUNKS") ? atoi(getenv("TM_OVERLAP_CHUNKS")) : 0;
+    int C = env_chunks > 0 ? env_chunks : 8;
+    if (C > 16) C = 16;
+    while (C > 1 && batch / C < 64) --C;
+    const int64_t per = (batch + C - 1) / C;
+    cudaStream_t s2 = p->aux_stream;
+    int *cnt = (int *)counters;
+    cudaEventRecord(p->aux_ev[1][15], s);  // the aux stream starts after work already queued on s
+    cudaStreamWaitEvent(s2, p->aux_ev[1][15], 0);
+    tm_prof_mark(1, s);
+    for (int c = 0; c < C; ++c) {
+        const int64_t b0 = c * per, nb = (batch - b0) < per ? (batch - b0) : per;
+        if (nb <= 0) break;
+        int32_t *y1c = (int32_t *)W.y1 + b0 * p->len_y1;
+        int32_t *y2c = (int32_t *)W.y2 + b0 * p->len_y2;
+        int rc = tm_fold_overlap(p, (const int8_t *)x + b0 * ldx, ldx, nb, y1c, y2c, W.fold_ws, cnt + c, s);
+        if (rc) return rc;
+        cudaEventRecord(p->aux_ev[0][c], s);
+        cudaStreamWaitEvent(s2, p->aux_ev[0][c], 0);
+        rc = tm_tc_correlate(p, y1c, y2c, (const int8_t *)t + b0 * p->K, p->K, nb, nullptr, nullptr, nullptr,
+                             residues ? residues + 2 * b0 : nullptr, k + b0, s2);
+        if (rc) return rc;
+    }
+    cudaEventRecord(p->aux_ev[1][0], s2);
+    cudaStreamWaitEvent(s, p->aux_ev[1][0], 0);
+    for (int i = 2; i <= 4; ++i) tm_prof_mark(i, s);
+    return TM_OK;
+}
+
 extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const void *x, int64_t ldx, const void *t, int64_t batch, int32_t *residues,
                       int64_t *k, void *ws, void *stream) {
     if (!p) { tm_set_error("tm_run: NULL plan"); return TM_EINVAL; }
@@ -97,6 +143,18 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
     RunWs W = run_ws(p, batch, ws);
     tm_prof_mark(0, s);
     if (p->use_tc) {
+        if (tm_fused_tc_ok(p, batch)) {  // the whole path in one persistent kernel
+            int rc = tm_fold_tc_fused(p, x, ldx, t, batch, W.y1, W.y2, residues, k, W.fold_ws,
+                                      (int *)((char *)ws + tm_ws(p, batch).counters), s);
+            if (rc != TM_EUNSUPPORTED) {
+                for (int i = 1; i <= 4; ++i) tm_prof_mark(i, s);
+                return rc;
+            }
+        }
+        if (tm_overlap_tc_ok(p, batch)) {
+            int rc = run_overlap_tc(p, x, ldx, t, batch, residues, k, W, (char *)ws + tm_ws(p, batch).counters, s);
+            if (rc != TM_EUNSUPPORTED) return rc;
+        }
         // step 3, then steps 4-9 in one tensor-core kernel (argmax + CRT in its epilogue)
         int rc = tm_fold_impl(p, x, ldx, batch, 0, p->N, W.y1, W.y2, 0, W.fold_ws, s);
         if (rc) return rc;

@@ -11,6 +11,7 @@
 
 struct tm_plan_s {
     int64_t N, K, M1, M2, q1, q2, s1, s2, len_y1, len_y2;
+    int64_t ldy1_run, ldy2_run;  // y row strides inside tm_run's workspace (multiples of 32 entries)
     int64_t L1, L2;
     int logL1, logL2;
     int64_t nload1, nload2;  // entries of y_j the correlation reads (cyclic y1: M1)
@@ -83,6 +84,10 @@ bool tm_fast_corr_ok(const tm_plan_s *p);
 void tm_mont_linv(int logL, uint32_t p, uint32_t *c, uint32_t *cs);
 bool tm_fused_ok(const tm_plan_s *p, int64_t batch);
 bool tm_overlap_ok(const tm_plan_s *p, int64_t batch);
+bool tm_overlap_tc_ok(const tm_plan_s *p, int64_t batch);
+bool tm_fused_tc_ok(const tm_plan_s *p, int64_t batch);
+int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
+                     void *y2, int32_t *residues, int64_t *k, void *ws, int *counter, cudaStream_t s);
 int tm_fold_overlap(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, void *y1, void *y2, void *ws,
                     int *counter, cudaStream_t s);
 int tm_fold_corr_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,

@@ -10,7 +10,10 @@ dbg = torch.zeros(B * 8 + 256, dtype=torch.int64, device='cuda')
 L.tm_debug_tc_timestamps.argtypes = [ctypes.c_void_p]
 for it in range(3):
     L.tm_debug_tc_timestamps(dbg.data_ptr() if it == 2 else None)
-    plan.correlate_match(y1, y2, t)
+    if len(sys.argv) > 1 and sys.argv[1] == 'run':
+        plan.run(x, t)
+    else:
+        plan.correlate_match(y1, y2, t)
 torch.cuda.synchronize()
 L.tm_debug_tc_timestamps(None)
 dd = dbg.cpu().numpy()
@@ -21,4 +24,12 @@ names = ['tmpl', 'stage_y', 'buildA', 'mma', 'epi']
 for i, n in enumerate(names):
     print(f'{n:8s} mean {ph[:, i].mean():9.0f} p50 {np.median(ph[:, i]):9.0f} max {ph[:, i].max():9.0f}')
 tot = d[:, 5] - d[:, 0]
-print('cta lifetime mean', tot.mean(), 'span per SM', [(d[d[:,6]==s,5].max()-d[d[:,6]==s,0].min()) for s in range(3)])
+print('pair lifetime mean', tot.mean(), 'span per SM', [(d[d[:,6]==s,5].max()-d[d[:,6]==s,0].min()) for s in range(3)])
+t0 = d[:, 0].min()
+sms = np.unique(d[:, 6])
+first = np.array([d[d[:, 6] == s, 0].min() - t0 for s in sms]) / 1e3
+last = np.array([d[d[:, 6] == s, 5].max() - t0 for s in sms]) / 1e3
+print('(ns stamps) first TC start per SM us: min %.1f p50 %.1f max %.1f' % (first.min(), np.median(first), first.max()))
+print('last TC end per SM us: min %.1f p50 %.1f max %.1f' % (last.min(), np.median(last), last.max()))
+cnt = np.array([(d[:, 6] == s).sum() for s in sms])
+print('pairs per SM', np.bincount(cnt))
