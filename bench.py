@@ -296,14 +296,24 @@ def main():
 
     bx = x.element_size()
     peak, peak_src = measured_peaks()
-    # fold kernel algorithmic bytes per launch: read x once + write y1, y2 once
-    fold_bytes = B * N * bx + B * (plan.len_y1 + plan.len_y2) * 4
+    path = plan.run_path(B)
+    if path == 2:
+        # fused kernel = the whole step: algorithmic bytes = x and t read once, k and
+        # residues written once (y never needs to leave the chip)
+        kernel = "fold_pm1_tma<3,0,1,TC> (fused fold + tensor-core correlation + argmax + CRT)"
+        fold_bytes = B * (N + K) * bx + B * (8 + 8)
+        tkey = args.workload + ":fused_tc"
+    else:
+        # fold kernel algorithmic bytes per launch: read x once + write y1, y2 once
+        kernel = "fold_pm1_tma<4,0,1> (fold)"
+        fold_bytes = B * N * bx + B * (plan.len_y1 + plan.len_y2) * 4
+        tkey = args.workload
     achieved = fold_bytes / (fold_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(args.workload)
+            traffic = json.load(f).get(tkey)
     cpu = None
     if not args.no_cpu_baseline:
         cores, model = cpu_info()
@@ -321,9 +331,10 @@ def main():
                    "parallelism": f"dp{world} (independent pairs)",
                    "l2": f"no flush: per-step input {B * N * bx / 2**30:.2f} GiB > 126 MB L2"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "tm_fold (fold_pm1 + fold_finalize)",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": kernel,
                      "algorithmic_bytes_per_launch": fold_bytes, "peak_source": peak_src,
-                     "fold_ms": fold_ms},
+                     "kernel_ms": fold_ms},
+        "run_path": tm.RUN_PATHS.get(path, str(path)),
         "stage_ms": {"fold": stage_mean[0], "fold_template": stage_mean[1], "correlate_argmax": stage_mean[2],
                      "crt": stage_mean[3]},
         "step_hbm_frac": (B * N * bx / (ms_max / args.steps * 1e-3) / 1e9) / peak,

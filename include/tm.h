@@ -220,6 +220,15 @@ int tm_run_host(tm_plan plan, const void *x_host, int64_t ldx, const void *t_hos
  */
 uint64_t tm_launch_count(void);
 int tm_profile_events(void **events, int n);
+/* tm_run_path: the kernel sequence tm_run(plan, batch) launches, -1 on bad
+ * arguments.  TM_PATH_FUSED_TC: one persistent kernel (packed fold warps +
+ * tensor-core correlation warps, argmax and CRT in its epilogue);
+ * TM_PATH_STAGED_TC: fold kernel, then the tensor-core correlation kernel;
+ * TM_PATH_STAGED: fold, then the NTT (or fp32) correlation and the CRT kernel;
+ * TM_PATH_FUSED_NTT / TM_PATH_OVERLAP: opt-in experimental modes. */
+enum { TM_PATH_STAGED = 0, TM_PATH_STAGED_TC = 1, TM_PATH_FUSED_TC = 2, TM_PATH_FUSED_NTT = 3,
+       TM_PATH_OVERLAP = 4 };
+int tm_run_path(tm_plan plan, int64_t batch);
 
 const char *tm_status_string(int status);
 const char *tm_last_error(void);

@@ -16,8 +16,10 @@ TM_OK, TM_EINVAL, TM_EUNSUPPORTED, TM_ECUDA = 0, 1, 2, 3
 EXPORTED_SYMBOLS = (
     "tm_plan_create", "tm_plan_query", "tm_workspace_bytes", "tm_plan_destroy", "tm_generate",
     "tm_fold", "tm_fold_template", "tm_correlate", "tm_match", "tm_run", "tm_run_host", "tm_correlate_match",
-    "tm_status_string", "tm_last_error", "tm_launch_count", "tm_profile_events",
+    "tm_status_string", "tm_last_error", "tm_launch_count", "tm_profile_events", "tm_run_path",
 )
+RUN_PATHS = {0: "staged (fold -> NTT/fp32 correlation -> CRT)", 1: "staged (fold -> tensor-core correlation)",
+             2: "fused (fold + tensor-core correlation in one kernel)", 3: "fused (fold + NTT)", 4: "overlap"}
 
 _i64, _u64, _i32, _u32, _p, _d = (ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32,
                                   ctypes.c_void_p, ctypes.c_double)
@@ -83,6 +85,8 @@ def lib():
         L.tm_launch_count.argtypes = []
         L.tm_profile_events.restype = ctypes.c_int
         L.tm_profile_events.argtypes = [ctypes.POINTER(_p), ctypes.c_int]
+        L.tm_run_path.restype = ctypes.c_int
+        L.tm_run_path.argtypes = [_p, _i64]
         L.tm_status_string.restype = ctypes.c_char_p
         L.tm_status_string.argtypes = [ctypes.c_int]
         L.tm_last_error.restype = ctypes.c_char_p
@@ -252,6 +256,10 @@ class Plan:
         _check(lib().tm_correlate_match(self._h, _ptr(y1), _ptr(y2), _ptr(t), batch, _ptr(residues), _ptr(k),
                                         _ptr(ws), _stream(stream)), "tm_correlate_match")
         return residues, k
+
+    def run_path(self, batch: int) -> int:
+        """tm_run_path: which kernel sequence tm_run launches for this batch (instrumentation)."""
+        return int(lib().tm_run_path(self._h, batch))
 
     def run_host(self, x_host, t_host, chunk: int, residues_host, k_host, dev_x, dev_t, dev_out, ws, stream=None):
         """tm_run_host: x_host/t_host/residues_host/k_host are (pinned) CPU tensors."""

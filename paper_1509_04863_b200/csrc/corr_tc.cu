@@ -100,8 +100,9 @@ void tm_tc_plan(tm_plan_s *p) {
     uint32_t ncols = 32;
     while (ncols < cols) ncols *= 2;
     const int R = NMC + NC - 1;
-    const int JA = 8 * (NC - 1) + 15;
-    uint32_t off = 256u * JA;   // A
+    const int JA = 8 * (NC - 1) + 15;            // 16-byte chunks of the whole padded template
+    const int CCH = NC > 17 ? (NC + 1) / 2 : NC;  // A operand built in chunks of CCH template blocks
+    uint32_t off = 256u * (8 * (CCH - 1) + 15);  // A (one chunk)
     p->tc_offB = off;
     off += 256u * R;            // B (one limb): 8 chunk columns x 2 R rows x 16 B
     p->tc_offTp = off;
@@ -114,6 +115,7 @@ void tm_tc_plan(tm_plan_s *p) {
     p->tc_NMC = NMC; p->tc_R = R;
     p->tc_NC = NC;
     p->tc_JA = JA;
+    p->tc_CCH = CCH;
     p->tc_lmax = lmax;
     p->tc_ncols = ncols;
     p->tc_ok = 1;
@@ -129,7 +131,7 @@ void tm_tc_fill_args(const tm_plan_s *p, const void *y1, const void *y2, const v
     a.M[0] = p->M1; a.M[1] = p->M2;
     a.NA[0] = p->tc_NA[0]; a.NA[1] = p->tc_NA[1];
     a.NMC = p->tc_NMC; a.R = p->tc_R;
-    a.NC = p->tc_NC; a.JA = p->tc_JA; a.LMAX = p->tc_lmax; a.ncols = p->tc_ncols;
+    a.NC = p->tc_NC; a.JA = p->tc_JA; a.CCH = p->tc_CCH; a.LMAX = p->tc_lmax; a.ncols = p->tc_ncols;
     a.offB = p->tc_offB; a.offTp = p->tc_offTp; a.offMisc = p->tc_offMisc;
     a.r[0] = (int64_t *)r1; a.r[1] = (int64_t *)r2;
     a.resid = resid; a.residues_out = residues_out; a.k_out = k;

@@ -83,6 +83,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
+// x is streamed exactly once: its L2 lines are marked evict-first so that the
+// folded vectors (written, then read back by the correlation) stay in L2
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s_ef(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                            uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -200,11 +215,11 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             uint32_t pph = 0;
             uint64_t *pbegin = reinterpret_cast<uint64_t *>(tsm + a.tca.offMisc + tc::MISC_PBEGIN);
             for (;;) {
-                mbar_wait(&pbegin[pb], pph);
+                tc::group_wait<GS>(&pbegin[pb], pph, gt >> 5);
                 const int64_t b = pitem[pb];  // fused mode: items are whole pairs
                 if (b < 0) break;
                 tc::tc_pre<GS>(a.tca, tsm, b, gt);  // template side while the pair is being folded
-                mbar_wait(&yready[pb], pph);
+                tc::group_wait<GS>(&yready[pb], pph, gt >> 5);
                 tc::tc_main<GS>(a.tca, tsm, b, gt, warp & 3, tbase, mph);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&ydone[pb]);
@@ -257,6 +272,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
+            const uint64_t pol = l2_evict_first_policy();
             for (int64_t seq = 0;; ++seq) {
                 int64_t item = a.work_counter ? (int64_t)atomicAdd(a.work_counter, 1) : blockIdx.x + seq * gridDim.x;
                 if (item >= a.n_items) item = -1;
@@ -274,10 +290,10 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                     mbar_expect_tx(&full[s], (uint32_t)(nr * it.width));
                     uint8_t *dst = ring + s * STAGE_BYTES;
                     if (it.width == a.M1) {  // rows are contiguous in global memory
-                        bulk_g2s(dst, base + r0 * a.M1, (uint32_t)(nr * it.width), &full[s]);
+                        bulk_g2s_ef(dst, base + r0 * a.M1, (uint32_t)(nr * it.width), &full[s], pol);
                     } else {
                         for (int r = 0; r < nr; ++r)
-                            bulk_g2s(dst + r * it.width, base + (r0 + r) * a.M1, (uint32_t)it.width, &full[s]);
+                            bulk_g2s_ef(dst + r * it.width, base + (r0 + r) * a.M1, (uint32_t)it.width, &full[s], pol);
                     }
                     if (++s == NST) { s = 0; ph ^= 1; }
                 }
@@ -729,7 +745,11 @@ int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void 
     a.ldy1 = a.tca.ldy[0] = p->ldy1_run;
     a.ldy2 = a.tca.ldy[1] = p->ldy2_run;
     a.tca.discard_y = 1;
-    const size_t base = (smem_bytes(a, 3, 0) + 1023) / 1024 * 1024;
+    // 4-stage ring when the tensor-core region fits next to it, else 3 stages
+    const size_t base4 = (smem_bytes(a, 4, 0) + 1023) / 1024 * 1024;
+    const size_t base3 = (smem_bytes(a, 3, 0) + 1023) / 1024 * 1024;
+    const int nst = (base4 + p->tc_smem <= 227 * 1024) ? 4 : 3;
+    const size_t base = nst == 4 ? base4 : base3;
     a.tc_off = (uint32_t)base;
     const size_t sm = base + p->tc_smem;
     if (sm > 227 * 1024) return TM_EUNSUPPORTED;
@@ -737,5 +757,6 @@ int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void 
     if (e != cudaSuccess) return tm_cuda_status(e, "tm_run: counter reset");
     a.work_counter = counter;
     const int64_t grid = batch < p->num_sms ? batch : p->num_sms;
+    if (nst == 4) return launch<4, 0, 1, true>(a, grid, sm, s);
     return launch<3, 0, 1, true>(a, grid, sm, s);
 }

@@ -203,6 +203,19 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
     return rc;
 }
 
+// Instrumentation: which kernel sequence tm_run(plan, batch) launches.
+extern "C" __attribute__((visibility("default"))) int tm_run_path(tm_plan p, int64_t batch) {
+    if (!p || batch <= 0) return -1;
+    if (p->use_tc) {
+        if (tm_fused_tc_ok(p, batch)) return TM_PATH_FUSED_TC;
+        if (tm_overlap_tc_ok(p, batch)) return TM_PATH_OVERLAP;
+        return TM_PATH_STAGED_TC;
+    }
+    if (tm_fused_ok(p, batch)) return TM_PATH_FUSED_NTT;
+    if (tm_overlap_ok(p, batch)) return TM_PATH_OVERLAP;
+    return TM_PATH_STAGED;
+}
+
 // steps 4-9 on already-folded vectors (e.g. after an all-reduce of partial folds)
 extern "C" __attribute__((visibility("default"))) int tm_correlate_match(tm_plan p, const void *y1, const void *y2,
                                                                          const void *t, int64_t batch,

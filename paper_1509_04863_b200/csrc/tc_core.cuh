@@ -14,9 +14,11 @@ namespace tc {
 constexpr int P = 128;
 constexpr int NTHR = 256;
 constexpr int MAXLEFT = 8;  // outputs k in [P*NA, M) done by warp dot products
-// misc area (offMisc): mbarrier | TMEM slot | sv[16] | sk[16] | lv[2][MAXLEFT] | pbegin[2] (fused kernel)
-constexpr int MISC_PBEGIN = 16 + 2 * 16 * 8 + 2 * MAXLEFT * 8;
-constexpr int MISC_BYTES = MISC_PBEGIN + 16;
+// misc area (offMisc): mbarrier | TMEM slot | sv[16] | sk[16] | pbegin[2] (fused kernel) |
+// leftover partial sums [8 warps][2 MAXLEFT]
+constexpr int MISC_PBEGIN = 16 + 2 * 16 * 8;
+constexpr int MISC_LEFT = MISC_PBEGIN + 16;
+constexpr int MISC_BYTES = MISC_LEFT + (NTHR / 32) * 2 * MAXLEFT * 8;
 
 struct TcArgs {
     const int8_t *t;
@@ -27,6 +29,7 @@ struct TcArgs {
     int NMC;     // blocks per modulus in the MMA (multiple of 16, >= NA)
     int R;       // B blocks staged (NMC + NC - 1)
     int NC, JA, LMAX;
+    int CCH;     // template blocks per A-operand chunk (the A buffer holds one chunk)
     uint32_t ncols;
     uint32_t offB, offTp, offMisc;
     int64_t *r[2];
@@ -90,6 +93,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
     } while (!done);
+}
+
+// the whole group waits for an mbarrier phase: warp 0 polls, the other warps block
+// in the group barrier (no issue slots taken from co-resident warps)
+template <class Sync>
+__device__ __forceinline__ void group_wait(uint64_t *bar, uint32_t parity, int warp) {
+    if (warp == 0) mbar_wait(bar, parity);
+    Sync::sync();
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t *v) {
@@ -211,9 +222,28 @@ struct GroupSync {
     }
 };
 
-// Steps 4 (template side) for pair b: the zero-padded template and its 16
-// byte-shifted copies (the MMA's A operand) in shared memory.  Needs only t, so
-// the fused kernel runs it while the pair is still being folded.
+// A operand for the template blocks c in [c0, c1): chunk (J, s) of the buffer =
+// tp[16 (J + 8 c0) + s + 1 + e], J < 8 (c1 - c0 - 1) + 15.
+__device__ __forceinline__ void build_a(const TcArgs &a, uint8_t *sm, int c0, int c1, int tid) {
+    const uint8_t *tp = sm + a.offTp + 128 * c0;
+    const int n = (8 * (c1 - c0 - 1) + 15) * 16;
+    for (int c = tid; c < n; c += NTHR) {
+        const int J = c >> 4, sg = c & 15;
+        const int sh = sg + 1, m = sh >> 2, r = 8 * (sh & 3);
+        const uint32_t *w = reinterpret_cast<const uint32_t *>(tp + 16 * J) + m;
+        const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
+        uint4 o;
+        o.x = __funnelshift_r(w0, w1, r);
+        o.y = __funnelshift_r(w1, w2, r);
+        o.z = __funnelshift_r(w2, w3, r);
+        o.w = __funnelshift_r(w3, w4, r);
+        reinterpret_cast<uint4 *>(sm)[c] = o;
+    }
+}
+
+// Step 4 (template side) for pair b: the zero-padded template and the A operand
+// of its first CCH blocks in shared memory.  Needs only t, so the fused kernel
+// runs it while the pair is still being folded.
 template <class Sync>
 __device__ __forceinline__ void tc_pre(const TcArgs &a, uint8_t *sm, int64_t b, int tid) {
     uint8_t *tp = sm + a.offTp;
@@ -233,21 +263,8 @@ __device__ __forceinline__ void tc_pre(const TcArgs &a, uint8_t *sm, int64_t b, 
             tp[i] = (j >= 0 && j < a.K) ? (uint8_t)tr[j] : 0;
         }
     }
-
     Sync::sync();
-    // ---- A: 16 byte-shifted copies of tp, chunk (J, s) = tp[16 J + s + 1 + e] ----
-    for (int c = tid; c < a.JA * 16; c += NTHR) {
-        const int J = c >> 4, sg = c & 15;
-        const int sh = sg + 1, m = sh >> 2, r = 8 * (sh & 3);
-        const uint32_t *w = reinterpret_cast<const uint32_t *>(tp + 16 * J) + m;
-        const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
-        uint4 o;
-        o.x = __funnelshift_r(w0, w1, r);
-        o.y = __funnelshift_r(w1, w2, r);
-        o.z = __funnelshift_r(w2, w3, r);
-        o.w = __funnelshift_r(w3, w4, r);
-        reinterpret_cast<uint4 *>(sm)[c] = o;
-    }
+    build_a(a, sm, 0, min(a.NC, a.CCH), tid);
 }
 
 // Steps 5-9 for pair b (after tc_pre): y_1, y_2 -> B, MMAs, argmax, CRT.
@@ -263,10 +280,10 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
     long long tstamp[6];
     tstamp[0] = gtime();
     tstamp[1] = tstamp[0];
-    uint64_t *mdone = reinterpret_cast<uint64_t *>(sm + a.offMisc);   // MMAs of a limb pass done
+    uint64_t *mdone = reinterpret_cast<uint64_t *>(sm + a.offMisc);   // MMAs of a pass done
     int64_t *sv = reinterpret_cast<int64_t *>(sm + a.offMisc + 16);   // [8 warps][2]
     int64_t *sk = sv + 16;                                             // [8][2]
-    int64_t *lv = sk + 16;                                             // [2][MAXLEFT]
+    int64_t *lp = reinterpret_cast<int64_t *>(sm + a.offMisc + MISC_LEFT);  // [8 warps][2 MAXLEFT]
     uint8_t *B = sm + a.offB;
     uint8_t *tp = sm + a.offTp;
 
@@ -280,71 +297,74 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
         Sync::sync();
         stage_y(a, B, b, 0, nl, warp, lane);
     }
-
     tstamp[2] = gtime();
-    tstamp[3] = gtime();
+    tstamp[3] = tstamp[2];
 
-    // ---- MMAs, one pass per limb (the B buffer holds one limb): warp 0 issues,
-    // descriptors precomputed, only start addresses move.  D columns of limb l:
+    // ---- MMA passes over (A chunk of CCH template blocks) x (limb): the B buffer
+    // holds one limb, the A buffer one chunk; before a pass rewrites either, the
+    // previous pass's MMAs must have completed.  Warp 0 issues; descriptors are
+    // precomputed, only start addresses move.  D columns of limb l:
     // [2 NMC l, 2 NMC (l + 1)), n = 2 a + j.
     const int nsp = 2 * a.NMC > 256 ? a.NMC : 2 * a.NMC;  // N <= 256 per MMA
     const int nsplit = 2 * a.NMC / nsp;
-    for (int l = 0; l < nl; ++l) {
-        if (l > 0) {  // the previous pass must have finished reading B
-            mbar_wait(mdone, (mph + (uint32_t)(l - 1)) & 1u);
+    uint32_t pass = 0;
+    int staged = 0;  // limb in B
+    for (int c0 = 0; c0 < a.NC; c0 += a.CCH) {
+        const int c1 = min(a.NC, c0 + a.CCH);
+        for (int l = 0; l < nl; ++l) {
+            if (pass > 0) {
+                group_wait<Sync>(mdone, (mph + pass - 1) & 1u, warp);
+                if (l == 0) build_a(a, sm, c0, c1, tid);
+                if (l != staged) { stage_y(a, B, b, l, nl, warp, lane); staged = l; }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             Sync::sync();
-            stage_y(a, B, b, l, nl, warp, lane);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        Sync::sync();
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (warp == 0) {
-            const uint32_t lbo = 32u * a.R;
-            const uint64_t ad0 = sdesc(smem_u32(sm), 256, 128);
-            const uint64_t bd0 = sdesc(smem_u32(B), lbo, 128);
-            const uint32_t id = idesc_i8(nsp);
-            for (int sp = 0; sp < nsplit; ++sp) {
-                const uint32_t dcol = tbase + 2 * a.NMC * l + sp * nsp;
-                for (int c = 0; c < a.NC; ++c) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (warp == 0) {
+                const uint32_t lbo = 32u * a.R;
+                const uint64_t ad0 = sdesc(smem_u32(sm), 256, 128);
+                const uint64_t bd0 = sdesc(smem_u32(B), lbo, 128);
+                const uint32_t id = idesc_i8(nsp);
+                for (int sp = 0; sp < nsplit; ++sp) {
+                    const uint32_t dcol = tbase + 2 * a.NMC * l + sp * nsp;
+                    for (int c = c0; c < c1; ++c) {
 #pragma unroll
-                    for (int ks = 0; ks < P / 32; ++ks) {
-                        // A: +2048 B per c, +512 B per k-step.  B: +32 B per c (2 rows),
-                        // +2 LBO per k-step, + nsp rows per split
-                        const uint64_t ad = ad0 + (uint64_t)(128u * c + 32u * ks);
-                        const uint64_t bd = bd0 + (uint64_t)(2u * c + (lbo >> 3) * ks + (uint32_t)(sp * nsp));
-                        mma_i8(dcol, ad, bd, id, (c | ks) ? 1u : 0u);
+                        for (int ks = 0; ks < P / 32; ++ks) {
+                            // A: +2048 B per c (chunk-relative), +512 B per k-step.  B: +32 B
+                            // per c (2 rows), +2 LBO per k-step, + nsp rows per split
+                            const uint64_t ad = ad0 + (uint64_t)(128u * (c - c0) + 32u * ks);
+                            const uint64_t bd = bd0 + (uint64_t)(2u * c + (lbo >> 3) * ks + (uint32_t)(sp * nsp));
+                            mma_i8(dcol, ad, bd, id, (c | ks) ? 1u : 0u);
+                        }
                     }
                 }
+                umma_commit(mdone);
             }
-            umma_commit(mdone);
+            ++pass;
         }
     }
 
-    // ---- leftover outputs k in [P NA_j, M_j): one warp per output, overlapping the MMAs ----
-    {
-        const int nleft0 = (int)max((int64_t)0, a.M[0] - (int64_t)P * a.NA[0]);
-        const int nleft1 = (int)max((int64_t)0, a.M[1] - (int64_t)P * a.NA[1]);
-        for (int w = warp; w < nleft0 + nleft1; w += NTHR / 32) {
-            const int j = w < nleft0 ? 0 : 1;
-            const int q = j ? w - nleft0 : w;
-            const int64_t k = (int64_t)P * a.NA[j] + q;
-            const int32_t *yr = a.y[j] + b * a.ldy[j] + k;
-            int64_t s = 0;
-            for (int64_t i = lane; i < a.K; i += 32) s += (int64_t)(int8_t)tp[128 + i] * yr[i];
+    // ---- leftover outputs k in [P NA_j, M_j) (at most MAXLEFT per modulus): every
+    // thread takes K / NTHR terms (independent loads), partial sums per warp ----
+    const int nleft0 = (int)max((int64_t)0, a.M[0] - (int64_t)P * a.NA[0]);
+    const int nleft1 = (int)max((int64_t)0, a.M[1] - (int64_t)P * a.NA[1]);
+    for (int q = 0; q < nleft0 + nleft1; ++q) {
+        const int j = q < nleft0 ? 0 : 1;
+        const int64_t k = (int64_t)P * a.NA[j] + (j ? q - nleft0 : q);
+        const int32_t *yr = a.y[j] + b * a.ldy[j] + k;
+        int64_t s = 0;
+#pragma unroll 8
+        for (int i = tid; i < a.K; i += NTHR) s += (int64_t)(int8_t)tp[128 + i] * yr[i];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) {
-                lv[j * MAXLEFT + q] = s;
-                if (a.r[j]) a.r[j][b * a.M[j] + k] = s;
-            }
-        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) lp[warp * 2 * MAXLEFT + q] = s;
     }
 
     // ---- epilogue: warp w reads TMEM lanes 32 (w & 3) + [0, 32) (rows b'),
     // output blocks [hw NMC/2, (hw + 1) NMC/2) of both moduli (hw = w >> 2) ----
-    mbar_wait(mdone, (mph + (uint32_t)(nl - 1)) & 1u);
-    mph += (uint32_t)nl;
+    group_wait<Sync>(mdone, (mph + pass - 1) & 1u, warp);
+    mph += pass;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     tstamp[4] = gtime();
     {
@@ -383,8 +403,14 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
         for (int j = 0; j < 2; ++j) {
             int64_t v = INT64_MIN, kk = INT64_MAX;
             for (int w = 0; w < NTHR / 32; ++w) amax(v, kk, sv[2 * w + j], sk[2 * w + j]);
-            const int nleft = (int)max((int64_t)0, a.M[j] - (int64_t)P * a.NA[j]);
-            for (int q = 0; q < nleft; ++q) amax(v, kk, lv[j * MAXLEFT + q], (int64_t)P * a.NA[j] + q);
+            const int nleft = j ? nleft1 : nleft0;
+            for (int q = 0; q < nleft; ++q) {
+                int64_t r = 0;
+                for (int w = 0; w < NTHR / 32; ++w) r += lp[w * 2 * MAXLEFT + (j ? nleft0 : 0) + q];
+                const int64_t k = (int64_t)P * a.NA[j] + q;
+                if (a.r[j]) a.r[j][b * a.M[j] + k] = r;
+                amax(v, kk, r, k);
+            }
             m[j] = kk;
         }
         if (a.resid) { a.resid[2 * b] = (int32_t)m[0]; a.resid[2 * b + 1] = (int32_t)m[1]; }

@@ -32,7 +32,7 @@ struct tm_plan_s {
     // tensor-core correlation engine (corr_tc.cu)
     int use_tc;          // tm_run / tm_correlate use corr_tc_kernel
     int tc_ok;           // plan shape eligible for it
-    int tc_NA[2], tc_NMC, tc_R, tc_NC, tc_JA, tc_lmax;
+    int tc_NA[2], tc_NMC, tc_R, tc_NC, tc_JA, tc_CCH, tc_lmax;
     uint32_t tc_ncols, tc_offB, tc_offTp, tc_offMisc, tc_smem;
 };
 

@@ -1,0 +1,28 @@
+"""Summarise an ncu --set full report (ncu -i X.ncu-rep --page raw --csv) into a
+small JSON of the metrics DESIGN.md / bench.py cite, one entry per kernel.
+usage: python scripts/ncu_summary.py raw.csv out.json"""
+import csv
+import json
+import sys
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum",
+        "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active",
+        "lts__t_bytes.sum", "launch__shared_mem_per_block_dynamic"]
+rows = list(csv.reader(open(sys.argv[1])))
+hdr, units = rows[0], rows[1]
+out = {}
+for r in rows[2:]:
+    name = r[hdr.index("Kernel Name")] if "Kernel Name" in hdr else f"kernel{len(out)}"
+    d = {}
+    for w in WANT:
+        if w in hdr:
+            d[w] = [r[hdr.index(w)], units[hdr.index(w)]]
+    out[name if name not in out else f"{name} #{len(out)}"] = d
+json.dump(out, open(sys.argv[2], "w"), indent=1)
+print(json.dumps(out, indent=1)[:3000])
