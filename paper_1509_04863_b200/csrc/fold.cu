@@ -390,6 +390,11 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
         TM_CHECK_LAUNCH("tm_fold: fold_finalize");
         return TM_OK;
     }
+    if (p->dtype == TM_F32 && ws && len > 0) {  // strip kernel + fixed-order finalize
+        tm_ws_layout L = tm_ws(p, batch);
+        int rc = tm_fold_f32(p, x, ldx, batch, offset, len, y1, y2, accumulate, (char *)ws + L.fold_counts, s);
+        if (rc != TM_EUNSUPPORTED) return rc;
+    }
     if (batch > 65535) { tm_set_error("tm_fold: general kernel supports batch <= 65535"); return TM_EUNSUPPORTED; }
     int64_t gx = (p->M2 + p->K + 255) / 256;
     if (gx > 65535) gx = 65535;
@@ -420,6 +425,9 @@ extern "C" __attribute__((visibility("default"))) int tm_fold(tm_plan p, const v
         tm_set_error("tm_fold: NULL pointer or ldx < len");
         return TM_EINVAL;
     }
-    if (batch > 0 && p->fast_fold && !ws) { tm_set_error("tm_fold: workspace required"); return TM_EINVAL; }
+    if (batch > 0 && (p->fast_fold || tm_fold_f32_ok(p)) && !ws) {
+        tm_set_error("tm_fold: workspace required");
+        return TM_EINVAL;
+    }
     return tm_fold_impl(p, x, ldx, batch, offset, len, y1, y2, accumulate, ws, (cudaStream_t)stream);
 }

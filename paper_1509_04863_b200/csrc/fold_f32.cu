@@ -1,0 +1,195 @@
+// fold_f32.cu -- the fold of real-valued signals (Algorithm 1 step 3, PAPER.md
+// Eq. 2) at HBM speed, deterministic fp32 accumulation.
+//
+// Same factorisation as the packed +-1 kernel: with K | N
+// and the row view x[g][c] = x[g M1 + c], the M1 bin of (g, c) is c (a column
+// sum) and the M2 = M1 + 1 bin is (c - g) mod M2 (an anti-diagonal).  A warp
+// owns a strip of 128 columns (lane l: columns 4l .. 4l+3, one 16-byte load per
+// row) and streams a chunk of R rows:
+//   * column sums: 4 registers per lane, rows added in order;
+//   * anti-diagonals: 4 registers per lane hold the diagonals d = 4l + e - g of
+//     the current row; after each row the window moves one column to the right
+//     (registers e -> e+1, lane l's register 3 -> lane l+1's register 0 by one
+//     warp shuffle), lane 31's register 3 leaves the strip and is written to a
+//     per-warp shared-memory list, and after the last row the 128 registers are.
+// Every (strip, row chunk) thus produces R + 127 diagonal partial sums and 128
+// column partial sums, written once to the workspace; fold_f32_finalize adds
+// them per bin in a fixed order (chunks, then strips ascending), applies the
+// mod-N wrap and the strategy-1 extension (as fold_finalize does for counts),
+// and writes y1, y2.  Summation order never depends on scheduling, so results
+// are bit-reproducible run to run.
+#include "tm_internal.cuh"
+
+namespace {
+
+constexpr int FW = 8;          // warps per CTA (strips of 128 columns)
+constexpr int FCOLS = FW * 128;
+constexpr int RMAX = 1024;     // rows per chunk
+constexpr int UR = 8;          // rows in flight per warp
+
+struct F32Args {
+    const float *x;
+    int64_t ldx;
+    int64_t M1, M2, K, N, q2;
+    int64_t rows, row0;        // rows of the chunk [offset, offset + len) and its first global row
+    int64_t R, nrc;            // rows per item, row chunks
+    int64_t n_strips, n_groups;
+    float *parts;              // [batch][nrc][M1 + n_strips (R + 127)]
+};
+
+__device__ __forceinline__ int64_t part_stride(const F32Args &a) { return a.M1 + a.n_strips * (a.R + 127); }
+
+__global__ void __launch_bounds__(FW * 32) fold_f32_strips(F32Args a) {
+    extern __shared__ float emit[];  // [FW][RMAX + 127]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t item = blockIdx.x;
+    const int64_t rc = item % a.nrc;
+    const int64_t grp = (item / a.nrc) % a.n_groups;
+    const int64_t b = item / a.nrc / a.n_groups;
+    const int64_t strip = grp * FW + warp;
+    if (strip >= a.n_strips) return;
+    const int64_t r0 = rc * a.R;
+    const int nrow = (int)((a.rows - r0) < a.R ? (a.rows - r0) : a.R);
+    const int64_t c0 = strip * 128 + 4 * lane;
+    const float *xp = a.x + b * a.ldx + r0 * a.M1 + c0;
+    float *em = emit + warp * (RMAX + 127);
+    const int R = (int)a.R;
+    float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int g0 = 0; g0 < nrow; g0 += UR) {
+        float4 v[UR];
+#pragma unroll
+        for (int u = 0; u < UR; ++u)
+            v[u] = (g0 + u < nrow) ? __ldcs(reinterpret_cast<const float4 *>(xp + (int64_t)(g0 + u) * a.M1))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+            const int g = g0 + u;
+            if (g >= nrow) break;
+            s1[0] += v[u].x; s1[1] += v[u].y; s1[2] += v[u].z; s1[3] += v[u].w;
+            s2[0] += v[u].x; s2[1] += v[u].y; s2[2] += v[u].z; s2[3] += v[u].w;
+            if (g == nrow - 1) break;  // the final window is written below
+            // diagonal 127 - g (relative to the strip) leaves it: index (127 - g) + R - 1
+            if (lane == 31) em[127 - g + R - 1] = s2[3];
+            const float in = __shfl_up_sync(0xffffffffu, s2[3], 1);
+            s2[3] = s2[2]; s2[2] = s2[1]; s2[1] = s2[0];
+            s2[0] = lane ? in : 0.f;
+        }
+    }
+    // after row nrow-1: register e of lane l holds diagonal 4l + e - (nrow - 1)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) em[4 * lane + e - (nrow - 1) + R - 1] = s2[e];
+    __syncwarp();
+    float *pp = a.parts + (b * a.nrc + rc) * part_stride(a);
+    // column partial sums
+    *reinterpret_cast<float4 *>(pp + c0) = make_float4(s1[0], s1[1], s1[2], s1[3]);
+    // diagonal partials: indices [R - nrow, R + 127) were written (shorter chunks leave a zero head)
+    float *dp = pp + a.M1 + strip * (a.R + 127);
+    for (int i = lane; i < R + 127; i += 32) dp[i] = (i >= R - nrow) ? em[i] : 0.f;
+}
+
+// bin sums, wrap and extension; x read only for the wrap/extension terms
+__global__ void fold_f32_finalize(F32Args a, int64_t offset, int64_t len, float *__restrict__ y1,
+                                  float *__restrict__ y2, int accumulate) {
+    const int64_t b = blockIdx.y;
+    const float *xb = a.x + b * a.ldx;
+    const float *pb = a.parts + b * a.nrc * part_stride(a);
+    float *o1 = y1 + b * (a.M1 + a.K), *o2 = y2 + b * (a.M2 + a.K);
+    auto xat = [&](int64_t pos) -> float {  // x at a global position, 0 outside the chunk
+        const int64_t rel = pos - offset;
+        return (rel >= 0 && rel < len) ? xb[rel] : 0.f;
+    };
+    const int64_t R = a.R;
+    // sum of the anti-diagonal partials of bin k (over chunks, then strips, in order)
+    auto base2 = [&](int64_t k) -> float {
+        float acc = 0.f;
+        for (int64_t rc = 0; rc < a.nrc; ++rc) {
+            const float *pp = pb + rc * part_stride(a) + a.M1;
+            const int64_t G0 = a.row0 + rc * R;          // global row of the chunk's row 0
+            // c - g_rel = u  with  (u - G0) mod M2 = k,  u in [-(R - 1), M1 - 1]
+            for (int64_t u = (k + G0) % a.M2; u >= -(R - 1); u -= a.M2) {
+                if (u > a.M1 - 1) continue;
+                // strips s with 128 s - (R - 1) <= u <= 128 s + 127, partial index u - 128 s + R - 1
+                int64_t slo = (u - 127 + 128 * 4096) / 128 - 4096;
+                if (128 * slo < u - 127) ++slo;
+                if (slo < 0) slo = 0;
+                int64_t shi = (u + R - 1) >= 0 ? (u + R - 1) / 128 : -1;
+                if (shi > a.n_strips - 1) shi = a.n_strips - 1;
+                for (int64_t s = slo; s <= shi; ++s) acc += pp[s * (R + 127) + (u - 128 * s + R - 1)];
+            }
+        }
+        const int64_t j = k - (a.M2 - a.q2);  // the mod-N wrap: bin M2 - q + j gets x[j]
+        if (j >= 0 && j < a.q2) acc += xat(j);
+        return acc;
+    };
+    const int64_t s2 = a.q2 * a.M2 - a.N;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.M2 + a.K;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (k < a.M1 + a.K) {
+            const int64_t c = k < a.M1 ? k : k - a.M1;   // M1 | N: y1[M1 + c] = y1[c]
+            float v = 0.f;
+            for (int64_t rc = 0; rc < a.nrc; ++rc) v += pb[rc * part_stride(a) + c];
+            if (accumulate) o1[k] += v; else o1[k] = v;
+        }
+        float v;
+        if (k < a.M2) {
+            v = base2(k);
+        } else {
+            const int64_t c = k - a.M2;                  // extension: y2[M2+c] = y2[c] - x[c] + x[c+s2]
+            int64_t e = c + s2;
+            if (e >= a.N) e -= a.N;
+            v = base2(c) - xat(c) + xat(e);
+        }
+        if (accumulate) o2[k] += v; else o2[k] = v;
+    }
+}
+
+void geometry(const tm_plan_s *p, int64_t rows, int64_t *R, int64_t *nrc) {
+    *nrc = (rows + RMAX - 1) / RMAX;
+    if (*nrc < 1) *nrc = 1;
+    *R = (rows + *nrc - 1) / *nrc;
+    if (*R < 1) *R = 1;
+}
+
+}  // namespace
+
+bool tm_fold_f32_ok(const tm_plan_s *p) {
+    return p->dtype == TM_F32 && p->N % p->M1 == 0 && p->M1 % 128 == 0 && p->M1 + 1 == p->M2;
+}
+
+size_t tm_fold_f32_ws_bytes(const tm_plan_s *p, int64_t batch) {
+    if (!tm_fold_f32_ok(p)) return 0;
+    int64_t R, nrc;
+    geometry(p, p->N / p->M1, &R, &nrc);
+    return (size_t)batch * nrc * (p->M1 + (p->M1 / 128) * (R + 127)) * 4;
+}
+
+// TM_EUNSUPPORTED (nothing enqueued) when the chunk or alignment does not qualify.
+int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
+                void *y1, void *y2, int accumulate, void *parts, cudaStream_t s) {
+    if (!tm_fold_f32_ok(p) || !parts) return TM_EUNSUPPORTED;
+    if (((uintptr_t)x % 16) || (ldx % 4) || (offset % p->M1) || (len % p->M1) || len == 0) return TM_EUNSUPPORTED;
+    F32Args a{};
+    a.x = (const float *)x; a.ldx = ldx;
+    a.M1 = p->M1; a.M2 = p->M2; a.K = p->K; a.N = p->N; a.q2 = p->q2;
+    a.rows = len / p->M1; a.row0 = offset / p->M1;
+    geometry(p, a.rows, &a.R, &a.nrc);
+    a.n_strips = p->M1 / 128;
+    a.n_groups = (a.n_strips + FW - 1) / FW;
+    a.parts = (float *)parts;
+    const int64_t items = batch * a.n_groups * a.nrc;
+    if (items > 0x7FFFFFFF || batch > 65535) return TM_EUNSUPPORTED;
+    const size_t smem = (size_t)FW * (RMAX + 127) * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fold_f32_strips, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    fold_f32_strips<<<(unsigned)items, FW * 32, smem, s>>>(a);
+    TM_CHECK_LAUNCH("tm_fold: fold_f32_strips");
+    int64_t gx = (p->M2 + p->K + 255) / 256;
+    if (gx > 65535) gx = 65535;
+    fold_f32_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(a, offset, len, (float *)y1, (float *)y2,
+                                                                           accumulate);
+    TM_CHECK_LAUNCH("tm_fold: fold_f32_finalize");
+    return TM_OK;
+}

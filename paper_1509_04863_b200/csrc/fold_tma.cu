@@ -172,6 +172,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
     uint32_t *nbuf = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(xs) + a.xs_bytes);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int NTW = TCM ? tc::NTHR / 32 : ntt_threads(LOGL2) / 32;
+    long long t_entry = 0;
+    if constexpr (TCM) t_entry = tc::gtime();
     if (threadIdx.x == 0) {
         if constexpr (TCM) {
             mbar_init(reinterpret_cast<uint64_t *>(smem + a.tc_off + a.tca.offMisc), 1);  // MMA passes
@@ -214,6 +216,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             int pb = 0;
             uint32_t pph = 0;
             uint64_t *pbegin = reinterpret_cast<uint64_t *>(tsm + a.tca.offMisc + tc::MISC_PBEGIN);
+            if (a.tca.dbg && gt == 0) a.tca.dbg[8 * a.n_items + 2 * blockIdx.x] = t_entry;
             for (;;) {
                 tc::group_wait<GS>(&pbegin[pb], pph, gt >> 5);
                 const int64_t b = pitem[pb];  // fused mode: items are whole pairs
@@ -227,6 +230,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             GS::sync();
+            if (a.tca.dbg && gt == 0) a.tca.dbg[8 * a.n_items + 2 * blockIdx.x + 1] = tc::gtime();
             if (gt < 32)
                 asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(a.tca.ncols));
             return;

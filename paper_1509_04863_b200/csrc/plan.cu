@@ -211,6 +211,8 @@ tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch) {
     size_t off = 0;
     w.fold_counts = off;
     w.fold_bytes = align256((size_t)batch * (size_t)(p->M1 + p->M2) * 4);
+    const size_t f32 = align256(tm_fold_f32_ws_bytes(p, batch));  // fp32 fold partial sums
+    if (f32 > w.fold_bytes) w.fold_bytes = f32;
     off += w.fold_bytes;
     w.resid = off;
     off += align256((size_t)batch * 2 * 4);
