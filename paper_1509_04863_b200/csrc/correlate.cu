@@ -475,6 +475,7 @@ extern "C" __attribute__((visibility("default"))) int tm_fold_template(tm_plan p
     if (!t || !tf) { tm_set_error("tm_fold_template: NULL pointer"); return TM_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
     if (p->dtype == TM_F32) {
+        if (tm_fft_f32_ok(p)) return tm_fft_f32_template(p, t, p->K, batch, tf, s);
         cudaError_t e = cudaMemcpyAsync(tf, t, (size_t)batch * p->K * 4, cudaMemcpyDeviceToDevice, s);
         if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold_template: copy");
         return TM_OK;
@@ -510,6 +511,8 @@ extern "C" __attribute__((visibility("default"))) int tm_fold_template(tm_plan p
 int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const void *tf, int64_t batch,
                       void *r1, void *r2, int32_t *resid, void *tile_scratch, void *gntt_scratch, cudaStream_t s) {
     if (batch == 0) return TM_OK;
+    if (p->dtype == TM_F32 && tm_fft_f32_ok(p))
+        return tm_fft_f32_correlate(p, y1, y2, tf, batch, r1, r2, resid, s);
     if (p->dtype == TM_F32) {
         const int nt1 = (int)((p->M1 + F_TK - 1) / F_TK), nt2 = (int)((p->M2 + F_TK - 1) / F_TK);
         const int nt = nt2;

@@ -1,0 +1,367 @@
+// fft_f32.cu -- correlation + argmax for real-valued (float32) pairs
+// (Algorithm 1 steps 4-7, read as the correlation of P:61,
+// reading C3) with register-resident complex fp32 FFTs.
+//
+// Both folded signals share one complex transform: with z = y1 + i y2 (each
+// zero beyond its Mj + K - 1 entries read, reading C4) and T the spectrum of
+// the reversed, zero-padded template t_rev[i] = t[(L - i) mod L],
+//     IFFT(FFT(z) . T) = r1 + i r2,
+// because the correlation is linear in the signal and r1, r2 are real (the
+// real part is y1's correlation, the imaginary part y2's); L = 2^ceil(log2(
+// M2 + K - 1)) >= Mj + K - 1, so no needed term wraps.  Per pair: one forward
+// transform of the template (tm_fold_template, kept in HBM in the transform's
+// register order) and one forward + one inverse transform of z.
+//
+// Transform layout (the NTT kernels' scheme, corr_fast.cu): L = 2^LOGL, each of
+// NT = L / 16 threads holds 16 complex values in registers; index bits are
+// processed 4 at a time in registers with XOR-swizzled shared-memory
+// transposes (two float planes) between phases, leftover bits by warp
+// shuffles.  Forward = decimation in frequency (natural -> bit-reversed),
+// inverse = decimation in time (bit-reversed -> natural).  Twiddles: float2
+// tables built in double precision on the host, w_n^j at offset n/2 - 1.
+// Error: O(log2 L) fp32 roundings per output, ~1e-6 of max |r| at cfg3 sizes,
+// inside reading C15's 1e-5 normwise tolerance (test_f32_*, test_cfg3_*).
+#include <cmath>
+#include <mutex>
+#include <vector>
+
+#include "tm_internal.cuh"
+
+namespace {
+
+constexpr int LOGE = 4, E = 1 << LOGE;
+constexpr int FFT_MAX_LOGL = 14;
+
+template <int LOGL>
+struct FGeo {
+    static constexpr int L = 1 << LOGL, NT = L >> LOGE;
+    static constexpr int H = (LOGL - LOGE) / LOGE, S = (LOGL - LOGE) % LOGE;
+    static __device__ __forceinline__ int idx(int k, int t, int m) {
+        if (k == H) return (t << LOGE) | m;
+        const int blo = LOGL - (k + 1) * LOGE;
+        return ((t >> blo) << (blo + LOGE)) | (m << blo) | (t & ((1 << blo) - 1));
+    }
+    static __device__ __forceinline__ int swz(int i) { return i ^ ((i >> LOGE) & 31); }
+};
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+template <int LOGL>
+__device__ __forceinline__ void ftranspose(float2 (&v)[E], float *br, float *bi, int t, int kf, int kt) {
+    using G = FGeo<LOGL>;
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int i = G::swz(G::idx(kf, t, m));
+        br[i] = v[m].x;
+        bi[i] = v[m].y;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int i = G::swz(G::idx(kt, t, m));
+        v[m] = make_float2(br[i], bi[i]);
+    }
+}
+
+// forward DIF: natural (D0) -> bit-reversed (Df: index (t << LOGE) | m)
+template <int LOGL>
+__device__ __forceinline__ void fdif(float2 (&v)[E], float *br, float *bi, int t, const float2 *__restrict__ tw) {
+    using G = FGeo<LOGL>;
+#pragma unroll
+    for (int k = 0; k < G::H; ++k) {
+        const int blo = LOGL - (k + 1) * LOGE;
+        const int tlow = t & ((1 << blo) - 1);
+#pragma unroll
+        for (int u = LOGE - 1; u >= 0; --u) {
+            const int h = 1 << u;
+            const float2 *tab = tw + ((1 << (blo + u)) - 1);
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                if (m & h) continue;
+                const float2 w = __ldg(tab + (((m & (h - 1)) << blo) | tlow));
+                const float2 X = v[m], Y = v[m | h];
+                v[m] = cadd(X, Y);
+                v[m | h] = cmul(csub(X, Y), w);
+            }
+        }
+        ftranspose<LOGL>(v, br, bi, t, k, k + 1);
+    }
+#pragma unroll
+    for (int sb = G::S - 1; sb >= 0; --sb) {
+        const float2 *tab = tw + ((1 << (LOGE + sb)) - 1);
+        const bool upper = (t >> sb) & 1;
+        const int tl = t & ((1 << sb) - 1);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const float ox = __shfl_xor_sync(0xffffffffu, v[m].x, 1 << sb);
+            const float oy = __shfl_xor_sync(0xffffffffu, v[m].y, 1 << sb);
+            const float2 o = make_float2(ox, oy);
+            if (upper) v[m] = cmul(csub(o, v[m]), __ldg(tab + ((tl << LOGE) | m)));
+            else v[m] = cadd(v[m], o);
+        }
+    }
+#pragma unroll
+    for (int u = LOGE - 1; u >= 0; --u) {
+        const int h = 1 << u;
+        const float2 *tab = tw + (h - 1);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            if (m & h) continue;
+            const float2 w = __ldg(tab + (m & (h - 1)));
+            const float2 X = v[m], Y = v[m | h];
+            v[m] = cadd(X, Y);
+            v[m | h] = cmul(csub(X, Y), w);
+        }
+    }
+}
+
+// inverse DIT: bit-reversed (Df) -> natural (D0), unscaled
+template <int LOGL>
+__device__ __forceinline__ void fdit(float2 (&v)[E], float *br, float *bi, int t, const float2 *__restrict__ tw) {
+    using G = FGeo<LOGL>;
+#pragma unroll
+    for (int u = 0; u < LOGE; ++u) {
+        const int h = 1 << u;
+        const float2 *tab = tw + (h - 1);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            if (m & h) continue;
+            const float2 Yw = cmul(v[m | h], __ldg(tab + (m & (h - 1))));
+            const float2 X = v[m];
+            v[m] = cadd(X, Yw);
+            v[m | h] = csub(X, Yw);
+        }
+    }
+#pragma unroll
+    for (int sb = 0; sb < G::S; ++sb) {
+        const float2 *tab = tw + ((1 << (LOGE + sb)) - 1);
+        const bool upper = (t >> sb) & 1;
+        const int tl = t & ((1 << sb) - 1);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const float2 send = upper ? cmul(v[m], __ldg(tab + ((tl << LOGE) | m))) : v[m];
+            const float ox = __shfl_xor_sync(0xffffffffu, send.x, 1 << sb);
+            const float oy = __shfl_xor_sync(0xffffffffu, send.y, 1 << sb);
+            const float2 o = make_float2(ox, oy);
+            v[m] = upper ? csub(o, send) : cadd(send, o);
+        }
+    }
+#pragma unroll
+    for (int k = G::H - 1; k >= 0; --k) {
+        ftranspose<LOGL>(v, br, bi, t, k + 1, k);
+        const int blo = LOGL - (k + 1) * LOGE;
+        const int tlow = t & ((1 << blo) - 1);
+#pragma unroll
+        for (int u = 0; u < LOGE; ++u) {
+            const int h = 1 << u;
+            const float2 *tab = tw + ((1 << (blo + u)) - 1);
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                if (m & h) continue;
+                const float2 Yw = cmul(v[m | h], __ldg(tab + (((m & (h - 1)) << blo) | tlow)));
+                const float2 X = v[m];
+                v[m] = cadd(X, Yw);
+                v[m | h] = csub(X, Yw);
+            }
+        }
+    }
+}
+
+struct FftArgs {
+    const float *t;          // [batch][ldt] templates (tf_template) or NULL
+    int64_t ldt, K;
+    const float2 *twf, *twi;
+    float2 *tf;              // [batch][L] spectra in register order (m * NT + t), scaled by 1/L
+    const float *y1, *y2;
+    int64_t ldy1, ldy2, nload1, nload2, M1, M2;
+    float *r1, *r2;          // [batch][Mj] or NULL
+    int32_t *resid;          // [batch][2] or NULL
+};
+
+template <int LOGL>
+__global__ void __launch_bounds__(FGeo<LOGL>::NT, 1) fft_template_f32(FftArgs a) {
+    using G = FGeo<LOGL>;
+    extern __shared__ float fsm[];
+    float *br = fsm, *bi = fsm + G::L;
+    const int t = threadIdx.x;
+    const int64_t b = blockIdx.x;
+    const float *tb = a.t + b * a.ldt;
+    float2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int i = G::idx(0, t, m);
+        const int src = i == 0 ? 0 : G::L - i;  // t_rev[i] = t[(L - i) mod L] (reading C3)
+        v[m] = make_float2(src < a.K ? tb[src] : 0.f, 0.f);
+    }
+    fdif<LOGL>(v, br, bi, t, a.twf);
+    const float s = 1.0f / (float)G::L;
+    float2 *o = a.tf + b * G::L;
+#pragma unroll
+    for (int m = 0; m < E; ++m) o[m * G::NT + t] = make_float2(v[m].x * s, v[m].y * s);
+}
+
+__device__ __forceinline__ void fmax_idx(float &bv, int &bi, float v, int i) {
+    if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+}
+
+template <int LOGL>
+__global__ void __launch_bounds__(FGeo<LOGL>::NT, 1) fft_corr_f32(FftArgs a) {
+    using G = FGeo<LOGL>;
+    extern __shared__ float fsm[];
+    float *br = fsm, *bi = fsm + G::L;
+    const int t = threadIdx.x;
+    const int64_t b = blockIdx.x;
+    const float *y1 = a.y1 + b * a.ldy1, *y2 = a.y2 + b * a.ldy2;
+    float2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int i = G::idx(0, t, m);
+        v[m] = make_float2(i < a.nload1 ? y1[i] : 0.f, i < a.nload2 ? y2[i] : 0.f);
+    }
+    fdif<LOGL>(v, br, bi, t, a.twf);
+    const float2 *T = a.tf + b * G::L;
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = cmul(v[m], T[m * G::NT + t]);
+    fdit<LOGL>(v, br, bi, t, a.twi);
+    // natural order: element idx(0, t, m) = r1 (real part) + i r2 (imaginary part)
+    float b1 = -INFINITY, b2 = -INFINITY;
+    int i1 = 0x7FFFFFFF, i2 = 0x7FFFFFFF;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int i = G::idx(0, t, m);
+        if (i < a.M1) {
+            if (a.r1) a.r1[b * a.M1 + i] = v[m].x;
+            fmax_idx(b1, i1, v[m].x, i);
+        }
+        if (i < a.M2) {
+            if (a.r2) a.r2[b * a.M2 + i] = v[m].y;
+            fmax_idx(b2, i2, v[m].y, i);
+        }
+    }
+    if (!a.resid) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        fmax_idx(b1, i1, __shfl_xor_sync(0xffffffffu, b1, o), __shfl_xor_sync(0xffffffffu, i1, o));
+        fmax_idx(b2, i2, __shfl_xor_sync(0xffffffffu, b2, o), __shfl_xor_sync(0xffffffffu, i2, o));
+    }
+    __syncthreads();  // br/bi reuse
+    const int w = t >> 5, l = t & 31;
+    if (l == 0) { br[w] = b1; bi[w] = b2; reinterpret_cast<int *>(br + 32)[w] = i1; reinterpret_cast<int *>(bi + 32)[w] = i2; }
+    __syncthreads();
+    if (w == 0) {
+        constexpr int NW = (G::NT + 31) / 32;
+        b1 = l < NW ? br[l] : -INFINITY;
+        b2 = l < NW ? bi[l] : -INFINITY;
+        i1 = l < NW ? reinterpret_cast<int *>(br + 32)[l] : 0x7FFFFFFF;
+        i2 = l < NW ? reinterpret_cast<int *>(bi + 32)[l] : 0x7FFFFFFF;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            fmax_idx(b1, i1, __shfl_xor_sync(0xffffffffu, b1, o), __shfl_xor_sync(0xffffffffu, i1, o));
+            fmax_idx(b2, i2, __shfl_xor_sync(0xffffffffu, b2, o), __shfl_xor_sync(0xffffffffu, i2, o));
+        }
+        if (l == 0) { a.resid[2 * b] = i1; a.resid[2 * b + 1] = i2; }
+    }
+}
+
+std::mutex g_fmu;
+struct FTabs {
+    bool ready = false;
+    float2 *d = nullptr;
+};
+FTabs g_ftabs[64];
+
+// w_n^j = exp(-+2 pi i j / n), j < n/2, at offset n/2 - 1, for n = 2 .. 2^FFT_MAX_LOGL
+int ftables(int device, const float2 **twf, const float2 **twi) {
+    if (device < 0 || device >= 64) return TM_EUNSUPPORTED;
+    std::lock_guard<std::mutex> lk(g_fmu);
+    FTabs &F = g_ftabs[device];
+    if (!F.ready) {
+        const size_t n = size_t(1) << FFT_MAX_LOGL;
+        std::vector<float2> h(2 * n);
+        for (int dir = 0; dir < 2; ++dir)
+            for (int l = 1; l <= FFT_MAX_LOGL; ++l) {
+                const size_t len = size_t(1) << l;
+                for (size_t j = 0; j < len / 2; ++j) {
+                    const double ang = (dir ? 2.0 : -2.0) * M_PI * (double)j / (double)len;
+                    h[dir * n + len / 2 - 1 + j] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+                }
+            }
+        cudaError_t e = cudaMalloc(&F.d, h.size() * sizeof(float2));
+        if (e != cudaSuccess) return tm_cuda_status(e, "tm: FFT table allocation");
+        e = cudaMemcpy(F.d, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return tm_cuda_status(e, "tm: FFT table upload");
+        F.ready = true;
+    }
+    *twf = F.d;
+    *twi = F.d + (size_t(1) << FFT_MAX_LOGL);
+    return TM_OK;
+}
+
+template <int LOGL>
+int launch_pair(bool templ, const FftArgs &A, int64_t batch, cudaStream_t s) {
+    using G = FGeo<LOGL>;
+    const size_t smem = (size_t)2 * G::L * 4;
+    if (templ) {
+        auto k = fft_template_f32<LOGL>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<(unsigned)batch, G::NT, smem, s>>>(A);
+        TM_CHECK_LAUNCH("fft_template_f32");
+    } else {
+        auto k = fft_corr_f32<LOGL>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<(unsigned)batch, G::NT, smem, s>>>(A);
+        TM_CHECK_LAUNCH("fft_corr_f32");
+    }
+    return TM_OK;
+}
+
+int dispatch(int logL, bool templ, const FftArgs &A, int64_t batch, cudaStream_t s) {
+    switch (logL) {
+        case 9: return launch_pair<9>(templ, A, batch, s);
+        case 10: return launch_pair<10>(templ, A, batch, s);
+        case 11: return launch_pair<11>(templ, A, batch, s);
+        case 12: return launch_pair<12>(templ, A, batch, s);
+        case 13: return launch_pair<13>(templ, A, batch, s);
+        case 14: return launch_pair<14>(templ, A, batch, s);
+        default: return TM_EUNSUPPORTED;
+    }
+}
+
+}  // namespace
+
+// float32 plans whose transform length fits the register kernel (L2 <= 2^14)
+bool tm_fft_f32_ok(const tm_plan_s *p) { return p->dtype == TM_F32 && p->logL2 >= 9 && p->logL2 <= FFT_MAX_LOGL; }
+
+// tf [batch][L2] float2: the template spectrum (tm_fold_template for these plans)
+int tm_fft_f32_template(const tm_plan_s *p, const void *t, int64_t ldt, int64_t batch, void *tf, cudaStream_t s) {
+    if (!tm_fft_f32_ok(p)) return TM_EUNSUPPORTED;
+    if (batch > 0x7FFFFFFF) return TM_EUNSUPPORTED;
+    FftArgs A{};
+    int rc = ftables(p->device, &A.twf, &A.twi);
+    if (rc) return rc;
+    A.t = (const float *)t; A.ldt = ldt; A.K = p->K;
+    A.tf = (float2 *)tf;
+    return dispatch(p->logL2, true, A, batch, s);
+}
+
+int tm_fft_f32_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *tf, int64_t batch,
+                         void *r1, void *r2, int32_t *resid, cudaStream_t s) {
+    if (!tm_fft_f32_ok(p)) return TM_EUNSUPPORTED;
+    if (batch > 0x7FFFFFFF) return TM_EUNSUPPORTED;
+    FftArgs A{};
+    int rc = ftables(p->device, &A.twf, &A.twi);
+    if (rc) return rc;
+    A.tf = (float2 *)const_cast<void *>(tf);
+    A.y1 = (const float *)y1; A.y2 = (const float *)y2;
+    A.ldy1 = p->len_y1; A.ldy2 = p->len_y2;
+    A.nload1 = p->M1 + p->K - 1; A.nload2 = p->M2 + p->K - 1;  // reading C4
+    A.M1 = p->M1; A.M2 = p->M2;
+    A.r1 = (float *)r1; A.r2 = (float *)r2;
+    A.resid = resid;
+    return dispatch(p->logL2, false, A, batch, s);
+}

@@ -175,8 +175,13 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
         }
     } else {
         p->n_primes = 0;
-        p->tf_elems = K;
-        p->tf_bytes = K * 4;
+        if (tm_fft_f32_ok(p)) {  // complex spectrum of the reversed template (fft_f32.cu)
+            p->tf_elems = p->L2;
+            p->tf_bytes = p->L2 * 8;
+        } else {                 // the template itself (direct correlation)
+            p->tf_elems = K;
+            p->tf_bytes = K * 4;
+        }
     }
     *out = p;
     return TM_OK;
