@@ -63,9 +63,13 @@ def lib():
         L.or_crt.argtypes = [_i64, _i64, _i64, _i64]
         L.or_crt_sets.restype = _i64
         L.or_crt_sets.argtypes = [_i64, _i64, _i64, _i64, _i64]
+        L.or_crt_sets_modN.restype = _i64
+        L.or_crt_sets_modN.argtypes = [_i64, _i64, _i64, _i64, _i64]
+        L.or_resolve.restype = _i64
+        L.or_resolve.argtypes = [_i64, _i64, _i64, _i64, _i64, ctypes.c_int]
         for n in ("or_ftm_i8", "or_ftm_f32"):
             getattr(L, n).restype = _i64
-            getattr(L, n).argtypes = [_p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p]
+            getattr(L, n).argtypes = [_p, _i64, _p, _i64, _i64, ctypes.c_int, _p, _p, _p, _p, _p]
         for n in ("or_full_corr_i8", "or_full_corr_f32"):
             getattr(L, n).restype = None
             getattr(L, n).argtypes = [_p, _i64, _p, _i64, _p]
@@ -184,12 +188,22 @@ def crt_sets(m1: int, M1: int, m2: int, M2: int, N: int) -> int:
     return lib().or_crt_sets(m1, M1, m2, M2, N)
 
 
+def crt_sets_modN(m1: int, M1: int, m2: int, M2: int, N: int) -> int:
+    """Steps 8-9 with the candidate sets reduced mod N (reading C10's repair)."""
+    return lib().or_crt_sets_modN(m1, M1, m2, M2, N)
+
+
+def resolve(m1: int, M1: int, m2: int, M2: int, N: int, alias_repair: bool = False) -> int:
+    return lib().or_resolve(m1, M1, m2, M2, N, int(alias_repair))
+
+
 # --------------------------------------------------------------------------
 # O6  Algorithm 1 end to end
 # --------------------------------------------------------------------------
-def ftm(x: np.ndarray, t: np.ndarray, M: int = 0, want_vectors: bool = True) -> dict:
+def ftm(x: np.ndarray, t: np.ndarray, M: int = 0, want_vectors: bool = True, alias_repair: bool = False) -> dict:
     """Run FTM() on one (signal, template) pair.  Returns a dict with k
-    (-1 = NO_MATCH), residues, and (optionally) y1, y2, r1, r2."""
+    (-1 = NO_MATCH), residues, and (optionally) y1, y2, r1, r2.  alias_repair:
+    steps 8-9 with the candidate sets reduced mod N (reading C10)."""
     x = _as_input(x)
     t = _as_input(t)
     N, K = x.shape[0], t.shape[0]
@@ -206,10 +220,10 @@ def ftm(x: np.ndarray, t: np.ndarray, M: int = 0, want_vectors: bool = True) -> 
     if want_vectors:
         y1 = np.zeros(M1 + K, dt); y2 = np.zeros(M2 + K, dt)
         r1 = np.zeros(M1, dt); r2 = np.zeros(M2, dt)
-        k = fn(_ptr(x), N, _ptr(t), K, M, _ptr(res), _ptr(y1), _ptr(y2), _ptr(r1), _ptr(r2))
+        k = fn(_ptr(x), N, _ptr(t), K, M, int(alias_repair), _ptr(res), _ptr(y1), _ptr(y2), _ptr(r1), _ptr(r2))
         return dict(k=k, residues=(int(res[0]), int(res[1])), M1=M1, M2=M2,
                     y1=y1, y2=y2, r1=r1, r2=r2)
-    k = fn(_ptr(x), N, _ptr(t), K, M, _ptr(res), None, None, None, None)
+    k = fn(_ptr(x), N, _ptr(t), K, M, int(alias_repair), _ptr(res), None, None, None, None)
     return dict(k=k, residues=(int(res[0]), int(res[1])), M1=M1, M2=M2)
 
 

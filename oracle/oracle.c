@@ -191,12 +191,61 @@ int64_t or_crt_sets(int64_t m1, int64_t M1, int64_t m2, int64_t M2, int64_t N) {
 }
 
 /* ------------------------------------------------------------------ */
+/* O5'' Alg. 1 steps 8-9 with the candidate sets taken modulo N (the      */
+/*     paper's index convention (x)_i = (x)_{i mod N}): reading C10's */
+/*     alias repair (opt-in).                             */
+/*       S_Mj mod N = { (m~j + i Mj) mod N : i = 0 .. ceil(N/Mj)-1 }       */
+/*     Returns the single common element, -1 if empty, -2 if several.      */
+/*     S_M2 mod N is sorted once and every element of S_M1 mod N is looked */
+/*     up by bisection: O(q log q), usable at every BASELINE size.        */
+/* ------------------------------------------------------------------ */
+static int or_cmp_i64(const void *a, const void *b) {
+    int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+    return (x > y) - (x < y);
+}
+
+int64_t or_crt_sets_modN(int64_t m1, int64_t M1, int64_t m2, int64_t M2, int64_t N) {
+    int64_t q1 = or_ceil_div(N, M1), q2 = or_ceil_div(N, M2);
+    int64_t *s2 = (int64_t *)malloc(sizeof(int64_t) * q2);
+    for (int64_t j = 0; j < q2; ++j) s2[j] = or_mod(m2 + j * M2, N);
+    qsort(s2, (size_t)q2, sizeof(int64_t), or_cmp_i64);
+    int64_t found = -1, count = 0;
+    for (int64_t i = 0; i < q1; ++i) {
+        int64_t a = or_mod(m1 + i * M1, N);
+        int64_t lo = 0, hi = q2;  /* first index with s2[idx] >= a */
+        while (lo < hi) {
+            int64_t mid = (lo + hi) / 2;
+            if (s2[mid] < a) lo = mid + 1; else hi = mid;
+        }
+        if (lo < q2 && s2[lo] == a) {  /* a common element; count distinct values */
+            if (count == 0) { found = a; count = 1; }
+            else if (a != found) count = 2;
+        }
+    }
+    free(s2);
+    if (count > 1) return -2;
+    return found;
+}
+
+/* Steps 8-9 resolution used by FTM(): the literal unreduced sets (reading C9,
+   computed by Theorem 4: k = z if z < N, else NO_MATCH), or, with repair, the
+   mod-N sets above (NO_MATCH if they do not meet in exactly one element). */
+int64_t or_resolve(int64_t m1, int64_t M1, int64_t m2, int64_t M2, int64_t N, int repair) {
+    int64_t z = or_crt(m1, M1, m2, M2);
+    if (z >= 0 && z < N) return z;
+    if (!repair) return -1;
+    int64_t v = or_crt_sets_modN(m1, M1, m2, M2, N);
+    return v >= 0 ? v : -1;
+}
+
+/* ------------------------------------------------------------------ */
 /* O6  Algorithm 1, FTM(), end to end.                        */
-/*     k^ = z if z < N else -1 (NO_MATCH, reading C9).                    */
+/*     k^ = z if z < N else -1 (NO_MATCH, reading C9); repair != 0: the   */
+/*     mod-N reading of steps 8-9 (or_resolve).                           */
 /*     Optional outputs (NULL to skip): residues[2], y1[M1+K], y2[M2+K],  */
 /*     r1[M1], r2[M2].  Returns k^, or -3 on invalid arguments.           */
 /* ------------------------------------------------------------------ */
-int64_t or_ftm_i8(const int8_t *x, int64_t N, const int8_t *t, int64_t K, int64_t M,
+int64_t or_ftm_i8(const int8_t *x, int64_t N, const int8_t *t, int64_t K, int64_t M, int repair,
                   int64_t *residues, int64_t *y1o, int64_t *y2o,
                   int64_t *r1o, int64_t *r2o) {
     int64_t M1, M2;
@@ -211,8 +260,7 @@ int64_t or_ftm_i8(const int8_t *x, int64_t N, const int8_t *t, int64_t K, int64_
     or_correlate_i64(y2, M2, K, t, r2);
     int64_t m1 = or_argmax_i64(r1, M1);                              /* step 7 */
     int64_t m2 = or_argmax_i64(r2, M2);
-    int64_t z = or_crt(m1, M1, m2, M2);                              /* steps 8-9 */
-    int64_t k = (z >= 0 && z < N) ? z : -1;
+    int64_t k = or_resolve(m1, M1, m2, M2, N, repair);               /* steps 8-9 */
     if (residues) { residues[0] = m1; residues[1] = m2; }
     if (y1o) memcpy(y1o, y1, sizeof(int64_t) * (M1 + K));
     if (y2o) memcpy(y2o, y2, sizeof(int64_t) * (M2 + K));
@@ -222,7 +270,7 @@ int64_t or_ftm_i8(const int8_t *x, int64_t N, const int8_t *t, int64_t K, int64_
     return k;
 }
 
-int64_t or_ftm_f32(const float *x, int64_t N, const float *t, int64_t K, int64_t M,
+int64_t or_ftm_f32(const float *x, int64_t N, const float *t, int64_t K, int64_t M, int repair,
                    int64_t *residues, double *y1o, double *y2o,
                    double *r1o, double *r2o) {
     int64_t M1, M2;
@@ -237,8 +285,7 @@ int64_t or_ftm_f32(const float *x, int64_t N, const float *t, int64_t K, int64_t
     or_correlate_f64(y2, M2, K, t, r2);
     int64_t m1 = or_argmax_f64(r1, M1);
     int64_t m2 = or_argmax_f64(r2, M2);
-    int64_t z = or_crt(m1, M1, m2, M2);
-    int64_t k = (z >= 0 && z < N) ? z : -1;
+    int64_t k = or_resolve(m1, M1, m2, M2, N, repair);
     if (residues) { residues[0] = m1; residues[1] = m2; }
     if (y1o) memcpy(y1o, y1, sizeof(double) * (M1 + K));
     if (y2o) memcpy(y2o, y2, sizeof(double) * (M2 + K));

@@ -361,3 +361,51 @@ def test_table1_small_column():
     # "works" would not land near 0.05; a broken pipeline gives 0 which is
     # also inside the band, so the deterministic pins above carry that case.
     assert ok <= 6
+
+
+def test_crt_sets_modN_closed_form():
+    """Reading C10's repair: steps 8-9 with the candidate sets
+    reduced mod N.  With M1 | N the mod-N intersection is exactly
+    z if z < N, z - N if N <= z < N + s2 (s2 = ceil(N/M2) M2 - N: the wrapped
+    element of S_M2), else empty -- the closed form the CUDA path uses.
+    Exhaustive over small K, every N = q K with K (K+1) > N, all residues."""
+    for K in range(2, 13):
+        M1, M2 = K, K + 1
+        for q in range(1, K + 1):
+            N = q * K
+            s2 = -(-N // M2) * M2 - N
+            for m1 in range(M1):
+                for m2 in range(M2):
+                    z = oracle.crt(m1, M1, m2, M2)
+                    want = z if z < N else (z - N if z < N + s2 else -1)
+                    assert oracle.crt_sets_modN(m1, M1, m2, M2, N) == want, (K, N, m1, m2)
+                    assert oracle.resolve(m1, M1, m2, M2, N, True) == want
+                    assert oracle.resolve(m1, M1, m2, M2, N, False) == (z if z < N else -1)
+
+
+def test_alias_repair_recovers_wrapped_peaks():
+    """cfg1 shape (N = 4096, K = 256, s2 = 16) with the planted shift k0 < s2:
+    the literal reading loses the trials whose M2 peak lands in the wrap bin
+    k0 + M2 - s2 (z = k0 + N, NO_MATCH); the mod-N reading returns k0 for
+    exactly those and agrees with the literal reading everywhere else
+    (1732/1732 alias hits recovered)."""
+    N, K = 4096, 256
+    rng = np.random.default_rng(1510)
+    lit_ok = rep_ok = alias = 0
+    for trial in range(300):
+        k0 = trial % 16
+        x = (1 - 2 * rng.integers(0, 2, N)).astype(np.int8)
+        t = x[(k0 + np.arange(K)) % N].copy()
+        a = oracle.ftm(x, t, want_vectors=False)
+        b = oracle.ftm(x, t, want_vectors=False, alias_repair=True)
+        assert a["residues"] == b["residues"]
+        if a["k"] >= 0:
+            assert b["k"] == a["k"]
+        else:
+            m1, m2 = a["residues"]
+            if b["k"] == k0:
+                alias += 1
+                assert m1 == k0 and m2 == k0 + (K + 1) - 16  # the wrap bin of Eq. 2
+        lit_ok += a["k"] == k0
+        rep_ok += b["k"] == k0
+    assert alias > 10 and rep_ok == lit_ok + alias
