@@ -58,6 +58,12 @@ enum {
 #define TM_CORR_NTT 2u  /* TM_I8 correlation engine: number-theoretic transform
                            (CUDA cores).  Default: the tensor-core engine when
                            the plan is eligible for it, else the NTT. */
+#define TM_ALIAS_REPAIR 8u  /* steps 8-9 with the candidate sets reduced mod N
+                               (reading C10 of DESIGN.md): when M1 | N and
+                               N <= z < N + s2, k = z - N instead of NO_MATCH
+                               (a true peak m < s2 that the mod-N wrap of Eq. 2
+                               moved into bin m + M2 - s2).  Default: off, the
+                               literal unreduced sets of P:104-105 (C9). */
 #define TM_CORR_TC 4u   /* TM_I8 correlation engine: int8 tensor cores
                            (tcgen05.mma kind::i8, exact int32 accumulation of
                            4-bit limbs of y); TM_EUNSUPPORTED if the plan is not

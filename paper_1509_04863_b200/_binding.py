@@ -10,6 +10,7 @@ _LIB_PATH = os.path.join(_HERE, "libtm.so")
 TM_I8, TM_F32 = 0, 1
 TM_BINARY = 1
 TM_CORR_NTT, TM_CORR_TC = 2, 4
+TM_ALIAS_REPAIR = 8
 _ENGINES = {None: 0, "auto": 0, "ntt": TM_CORR_NTT, "tc": TM_CORR_TC}
 TM_OK, TM_EINVAL, TM_EUNSUPPORTED, TM_ECUDA = 0, 1, 2, 3
 
@@ -133,7 +134,7 @@ class Plan:
     engine (int8 only): None/"auto" (tensor cores when eligible), "ntt" or "tc"."""
 
     def __init__(self, N: int, K: int, M: int = 0, seed: int = 0, dtype: str = "int8", binary: bool = True,
-                 engine: str | None = None):
+                 engine: str | None = None, alias_repair: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1509_04863_b200.Plan needs a CUDA device (no CPU fallback)")
@@ -141,6 +142,8 @@ class Plan:
         flags = TM_BINARY if (binary and self.dtype == TM_I8) else 0
         if self.dtype == TM_I8:
             flags |= _ENGINES[engine]
+        if alias_repair:
+            flags |= TM_ALIAS_REPAIR
         h = _p()
         _check(lib().tm_plan_create(ctypes.byref(h), N, K, M, seed, self.dtype, flags), "tm_plan_create")
         self._h = h

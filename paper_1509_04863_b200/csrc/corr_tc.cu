@@ -135,7 +135,7 @@ void tm_tc_fill_args(const tm_plan_s *p, const void *y1, const void *y2, const v
     a.offB = p->tc_offB; a.offTp = p->tc_offTp; a.offMisc = p->tc_offMisc;
     a.r[0] = (int64_t *)r1; a.r[1] = (int64_t *)r2;
     a.resid = resid; a.residues_out = residues_out; a.k_out = k;
-    a.N = p->N; a.M1 = p->M1; a.M2 = p->M2; a.crt_inv = p->crt_inv;
+    a.N = p->N; a.M1 = p->M1; a.M2 = p->M2; a.crt_inv = p->crt_inv; a.crt_wrap = p->crt_wrap;
 }
 
 // r1/r2 (may be NULL), resid (may be NULL), k (NULL: no CRT).  t is int8 [batch][ldt].

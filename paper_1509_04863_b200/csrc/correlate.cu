@@ -440,17 +440,13 @@ __global__ void argmax_kernel(const T *__restrict__ r1, const T *__restrict__ r2
     }
 }
 
-// Theorem 4: z = m1 + M1 * ((m2 - m1) * M1^{-1} mod M2);  k = z < N ? z : -1
+// steps 8-9 (tm_resolve)
 __global__ void crt_kernel(const int32_t *__restrict__ resid, int64_t batch, int64_t M1, int64_t M2,
-                           uint32_t inv, int64_t N, int32_t *residues_out, int64_t *k) {
+                           uint32_t inv, int64_t N, int64_t wrap, int32_t *residues_out, int64_t *k) {
     int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= batch) return;
     int64_t m1 = resid[2 * b], m2 = resid[2 * b + 1];
-    int64_t d = (m2 - m1) % M2;
-    if (d < 0) d += M2;
-    int64_t u = (int64_t)(((unsigned __int128)d * inv) % (uint64_t)M2);
-    int64_t z = m1 + M1 * u;
-    k[b] = z < N ? z : -1;
+    k[b] = tm_resolve(m1, m2, M1, M2, inv, N, wrap);
     if (residues_out) { residues_out[2 * b] = (int32_t)m1; residues_out[2 * b + 1] = (int32_t)m2; }
 }
 
@@ -576,7 +572,7 @@ int tm_crt_impl(const tm_plan_s *p, const int32_t *resid, int64_t batch, int32_t
                 cudaStream_t s) {
     if (batch == 0) return TM_OK;
     crt_kernel<<<(unsigned)((batch + 255) / 256), 256, 0, s>>>(resid, batch, p->M1, p->M2, p->crt_inv, p->N,
-                                                               residues_out, k);
+                                                               p->crt_wrap, residues_out, k);
     TM_CHECK_LAUNCH("tm_match: crt_kernel");
     return TM_OK;
 }

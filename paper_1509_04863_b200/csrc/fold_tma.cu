@@ -50,6 +50,7 @@ struct TmaArgs {
     int32_t *residues_out;
     int64_t *k_out;
     uint32_t crt_inv;
+    int64_t crt_wrap;
     int xs_bytes;        // bytes reserved for the epilogue's x[0 .. K + q) stage
     int *work_counter;   // non-NULL: dynamic item assignment (atomic counter, zeroed per launch)
     // tensor-core fused mode: 8 warps correlate pair i (tc_core.cuh) while the fold streams pair i+1
@@ -254,13 +255,9 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 NBar::sync();
                 pair_modulus2<LOGL2, NBar>(nbuf, Ts2, nt, a.f, b);
                 pair_modulus1<LOGL2, NBar>(nbuf, Ts1, nt, a.f, b);
-                if (nt == 0) {  // Theorem 4: z = m1 + M1 ((m2 - m1) M1^{-1} mod M2); k = z < N ? z : -1
+                if (nt == 0) {  // steps 8-9 (tm_resolve)
                     const int64_t m1 = a.f.resid[b * 2], m2 = a.f.resid[b * 2 + 1];
-                    int64_t d = (m2 - m1) % a.M2;
-                    if (d < 0) d += a.M2;
-                    const int64_t u = (int64_t)(((unsigned __int128)d * a.crt_inv) % (uint64_t)a.M2);
-                    const int64_t z = m1 + a.M1 * u;
-                    a.k_out[b] = z < a.N ? z : -1;
+                    a.k_out[b] = tm_resolve(m1, m2, a.M1, a.M2, a.crt_inv, a.N, a.crt_wrap);
                     if (a.residues_out) { a.residues_out[2 * b] = (int32_t)m1; a.residues_out[2 * b + 1] = (int32_t)m2; }
                 }
                 __syncwarp();
@@ -712,6 +709,7 @@ int tm_fold_corr_fused(const tm_plan_s *p, const void *x, int64_t ldx, const voi
     a.residues_out = residues;
     a.k_out = k;
     a.crt_inv = p->crt_inv;
+    a.crt_wrap = p->crt_wrap;
     const int64_t grid = batch < p->num_sms ? batch : p->num_sms;
     switch (p->logL2) {
         case 10: { const size_t sm = smem_bytes(a, 3, 10); if (sm > 227 * 1024) return TM_EUNSUPPORTED; return launch<3, 10>(a, grid, sm, s); }

@@ -38,6 +38,7 @@ struct TcArgs {
     int64_t *k_out;         // [batch] (NULL: no CRT)
     int64_t N, M1, M2;
     uint32_t crt_inv;
+    int64_t crt_wrap;
     long long *dbg;  // optional per-CTA phase timestamps (tm_debug_tc_timestamps)
     int discard_y;   // 1: y rows (128-byte aligned, ldy multiple of 32) are scratch; drop
                      // their L2 lines without write-back once read (fused tm_run)
@@ -415,13 +416,7 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
         }
         if (a.resid) { a.resid[2 * b] = (int32_t)m[0]; a.resid[2 * b + 1] = (int32_t)m[1]; }
         if (a.residues_out) { a.residues_out[2 * b] = (int32_t)m[0]; a.residues_out[2 * b + 1] = (int32_t)m[1]; }
-        if (a.k_out) {  // Theorem 4: z = m1 + M1 ((m2 - m1) M1^{-1} mod M2); k = z < N ? z : -1 (C9)
-            int64_t d = m[1] - m[0];  // |m2 - m1| < M2
-            if (d < 0) d += a.M2;
-            const int64_t u = (int64_t)(((uint64_t)d * a.crt_inv) % (uint64_t)a.M2);  // d, inv < M2 <= 2^32
-            const int64_t z = m[0] + a.M1 * u;
-            a.k_out[b] = z < a.N ? z : -1;
-        }
+        if (a.k_out) a.k_out[b] = tm_resolve(m[0], m[1], a.M1, a.M2, a.crt_inv, a.N, a.crt_wrap);  // steps 8-9
         if (a.dbg) {
             tstamp[5] = gtime();
             int smid;

@@ -29,12 +29,30 @@ struct tm_plan_s {
     cudaEvent_t aux_ev[2][16];  // fold-done / ntt-done events per chunk
     int64_t tf_bytes;
     uint32_t crt_inv;    // M1^{-1} mod M2
+    int64_t crt_wrap;    // TM_ALIAS_REPAIR with M1 | N: s2 (reading C10), else 0
     // tensor-core correlation engine (corr_tc.cu)
     int use_tc;          // tm_run / tm_correlate use corr_tc_kernel
     int tc_ok;           // plan shape eligible for it
     int tc_NA[2], tc_NMC, tc_R, tc_NC, tc_JA, tc_CCH, tc_lmax;
     uint32_t tc_ncols, tc_offB, tc_offTp, tc_offMisc, tc_smem;
 };
+
+// Alg. 1 steps 8-9 by Theorem 4:
+//   z = m1 + M1 ((m2 - m1) M1^{-1} mod M2),  k = z if z < N;
+// with the alias repair (reading C10: the candidate sets taken mod N),
+// k = z - N if N <= z < N + wrap (wrap = s2 then, 0 otherwise); else NO_MATCH
+// (k = -1, reading C9).  Residues are in range, so |m2 - m1| < M2 and
+// d * inv < M2^2 <= 2^64.
+__host__ __device__ __forceinline__ int64_t tm_resolve(int64_t m1, int64_t m2, int64_t M1, int64_t M2, uint32_t inv,
+                                                      int64_t N, int64_t wrap) {
+    int64_t d = m2 - m1;
+    if (d < 0) d += M2;
+    const int64_t u = (int64_t)(((uint64_t)d * inv) % (uint64_t)M2);
+    const int64_t z = m1 + M1 * u;
+    if (z < N) return z;
+    if (z < N + wrap) return z - N;
+    return -1;
+}
 
 // ---- error plumbing (plan.cu) ----
 void tm_set_error(const char *fmt, ...);

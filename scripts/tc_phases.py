@@ -6,7 +6,7 @@ N, K, B = 2**20, 4096, 1024
 plan = tm.Plan(N, K, seed=9)
 x, t, _ = plan.generate(0, B, 0.1)
 y1, y2 = plan.fold(x)
-dbg = torch.zeros(B * 8 + 256, dtype=torch.int64, device='cuda')
+dbg = torch.zeros(B * 8 + 512, dtype=torch.int64, device='cuda')
 L.tm_debug_tc_timestamps.argtypes = [ctypes.c_void_p]
 for it in range(3):
     L.tm_debug_tc_timestamps(dbg.data_ptr() if it == 2 else None)
@@ -33,3 +33,8 @@ print('(ns stamps) first TC start per SM us: min %.1f p50 %.1f max %.1f' % (firs
 print('last TC end per SM us: min %.1f p50 %.1f max %.1f' % (last.min(), np.median(last), last.max()))
 cnt = np.array([(d[:, 6] == s).sum() for s in sms])
 print('pairs per SM', np.bincount(cnt))
+if len(sys.argv) > 1 and sys.argv[1] == 'run':
+    ex = dd[B * 8: B * 8 + 296].reshape(148, 2)
+    k0 = ex[:, 0].min()
+    print('CTA entry us: max %.1f; TC exit us: min %.1f p50 %.1f max %.1f' % ((ex[:, 0].max() - k0) / 1e3, (ex[:, 1].min() - k0) / 1e3, np.median(ex[:, 1] - k0) / 1e3, (ex[:, 1].max() - k0) / 1e3))
+    print('first TC start after kernel entry us: min %.1f p50 %.1f max %.1f' % ((first.min()*1e3 + t0 - k0) / 1e3, (np.median(first)*1e3 + t0 - k0) / 1e3, (first.max()*1e3 + t0 - k0) / 1e3))

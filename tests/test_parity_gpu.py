@@ -40,7 +40,7 @@ def crt_closed(m1, M1, m2, M2, N):
     return z if z < N else -1
 
 
-def check_int_pairs(tm, plan, x_h, t_h, pairs, staged=True, run=True):
+def check_int_pairs(tm, plan, x_h, t_h, pairs, staged=True, run=True, alias_repair=False):
     """Full staged + fused comparison for the given pair indices."""
     x = up(x_h)
     t = up(t_h)
@@ -53,7 +53,7 @@ def check_int_pairs(tm, plan, x_h, t_h, pairs, staged=True, run=True):
     y1h, y2h, r1h, r2h = (v.cpu().numpy() for v in (y1, y2, r1, r2))
     resh, kh, res_runh, k_runh = res.cpu().numpy(), k.cpu().numpy(), res_run.cpu().numpy(), k_run.cpu().numpy()
     for b in pairs:
-        o = oracle.ftm(x_h[b], t_h[b], M=plan.M1 if plan.M1 != plan.K else 0)
+        o = oracle.ftm(x_h[b], t_h[b], M=plan.M1 if plan.M1 != plan.K else 0, alias_repair=alias_repair)
         np.testing.assert_array_equal(y1h[b], o["y1"], err_msg=f"y1 pair {b}")
         np.testing.assert_array_equal(y2h[b], o["y2"], err_msg=f"y2 pair {b}")
         np.testing.assert_array_equal(r1h[b], o["r1"], err_msg=f"r1 pair {b}")
@@ -101,6 +101,26 @@ def test_cfg1_exact(tm, engine):
     x_h, t_h, k0 = tmgen.batch(1, 0, 64, N, K, 0.0)
     kh, _ = check_int_pairs(tm, plan, x_h, t_h, range(64))
     assert np.mean(kh == k0) > 0.5  # SURVEY measured 0.758 for this configuration
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_alias_repair_flag(tm, engine):
+    """TM_ALIAS_REPAIR (reading C10): cfg1 shape with the planted
+    shift k0 < s2 = 16, where the literal reading loses the wrapped peaks; the
+    GPU's k (staged tm_match and fused tm_run) equals the oracle's mod-N
+    reading for every pair, and recovers more shifts than the literal one."""
+    N, K, B = 4096, 256, 64
+    rng = np.random.default_rng(77)
+    x_h = (1 - 2 * rng.integers(0, 2, (B, N))).astype(np.int8)
+    k0 = np.arange(B) % 16
+    t_h = np.stack([x_h[b][(k0[b] + np.arange(K)) % N] for b in range(B)]).astype(np.int8)
+    plan = tm.Plan(N, K, seed=0, engine=engine, alias_repair=True)
+    kh, kr = check_int_pairs(tm, plan, x_h, t_h, range(B), alias_repair=True)
+    plain = tm.Plan(N, K, seed=0, engine=engine)
+    _, k_lit = plain.run(up(x_h), up(t_h))
+    k_lit = k_lit.cpu().numpy()
+    assert np.sum(kh == k0) > np.sum(k_lit == k0)
+    assert np.all(kh[k_lit >= 0] == k_lit[k_lit >= 0])
 
 
 @pytest.mark.parametrize("engine", ENGINES)
