@@ -175,3 +175,13 @@ int tm_tc_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf, c
     TM_CHECK_LAUNCH("tc_template_copy");
     return TM_OK;
 }
+
+int tm_tc_any(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt, int64_t batch,
+              void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s) {
+    const char *env = getenv("TM_TC_TILED");  // tests / A-B: "0" never, "1" whenever eligible
+    const bool force = env && env[0] == '1', never = env && env[0] == '0';
+    if (p->tct_ok && ws && !never && (force || !p->tc_ok || batch < p->num_sms))
+        return tm_tc_tiled_correlate(p, y1, y2, t, ldt, batch, r1, r2, resid, residues_out, k,
+                                     (char *)ws + tm_ws(p, batch).tiled, s);
+    return tm_tc_correlate(p, y1, y2, t, ldt, batch, r1, r2, resid, residues_out, k, s);
+}

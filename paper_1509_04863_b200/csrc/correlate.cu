@@ -505,7 +505,8 @@ extern "C" __attribute__((visibility("default"))) int tm_fold_template(tm_plan p
 }
 
 int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const void *tf, int64_t batch,
-                      void *r1, void *r2, int32_t *resid, void *tile_scratch, void *gntt_scratch, cudaStream_t s) {
+                      void *r1, void *r2, int32_t *resid, void *tile_scratch, void *gntt_scratch, cudaStream_t s,
+                      void *tc_ws) {
     if (batch == 0) return TM_OK;
     if (p->dtype == TM_F32 && tm_fft_f32_ok(p))
         return tm_fft_f32_correlate(p, y1, y2, tf, batch, r1, r2, resid, s);
@@ -528,7 +529,7 @@ int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const 
         }
         return TM_OK;
     }
-    if (p->use_tc) return tm_tc_correlate(p, y1, y2, tf, p->tf_bytes, batch, r1, r2, resid, nullptr, nullptr, s);
+    if (p->use_tc) return tm_tc_any(p, y1, y2, tf, p->tf_bytes, batch, r1, r2, resid, nullptr, nullptr, tc_ws, s);
     if (p->fast_corr) return tm_fast_correlate(p, y1, y2, nullptr, tf, batch, r1, r2, resid, s);
     if (p->big_corr) return tm_gntt_correlate(p, y1, y2, nullptr, tf, batch, r1, r2, resid, gntt_scratch, s);
     if (!corr_in_smem(p)) {
@@ -565,7 +566,7 @@ extern "C" __attribute__((visibility("default"))) int tm_correlate(tm_plan p, co
     if (batch > 0 && (!y1 || !y2 || !tf || !r1 || !r2)) { tm_set_error("tm_correlate: NULL pointer"); return TM_EINVAL; }
     if (p->big_corr && !ws) { tm_set_error("tm_correlate: workspace required for this plan"); return TM_EINVAL; }
     void *g = ws ? (char *)ws + tm_ws(p, batch).gntt : nullptr;
-    return tm_correlate_impl(p, y1, y2, tf, batch, r1, r2, nullptr, nullptr, g, (cudaStream_t)stream);
+    return tm_correlate_impl(p, y1, y2, tf, batch, r1, r2, nullptr, nullptr, g, (cudaStream_t)stream, ws);
 }
 
 int tm_crt_impl(const tm_plan_s *p, const int32_t *resid, int64_t batch, int32_t *residues_out, int64_t *k,

@@ -649,7 +649,7 @@ bool tm_overlap_tc_ok(const tm_plan_s *p, int64_t batch) {
     static const char *env = getenv("TM_OVERLAP");
     static const bool on = env && env[0] == '1';
     if (!on) return false;
-    return p->use_tc && p->fast_fold && p->M1 <= TCOLS && p->q1 <= 1024 && batch >= 2 * 64 &&
+    return p->use_tc && p->tc_ok && p->fast_fold && p->M1 <= TCOLS && p->q1 <= 1024 && batch >= 2 * 64 &&
            p->N % 16 == 0 && p->N == p->M1 * p->q1;
 }
 
@@ -729,7 +729,8 @@ bool tm_fused_tc_ok(const tm_plan_s *p, int64_t batch) {
     static const char *env = getenv("TM_FUSED_TC");
     static const bool off = env && env[0] == '0';
     if (off) return false;
-    return p->use_tc && p->fast_fold && p->M1 <= TCOLS && p->q1 <= 1024 && p->N == p->M1 * p->q1 && batch >= 1;
+    return p->use_tc && p->tc_ok && p->fast_fold && p->M1 <= TCOLS && p->q1 <= 1024 && p->N == p->M1 * p->q1 &&
+           batch >= 1;
 }
 
 int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,

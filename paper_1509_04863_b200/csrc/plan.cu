@@ -159,17 +159,18 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
         // correlation engine: tensor cores when eligible (TM_CORR=ntt in the
         // environment forces the NTT for A/B measurements of the default)
         tm_tc_plan(p);
+        tm_tc_tiled_plan(p);
         static const char *env = getenv("TM_CORR");
         const bool env_ntt = env && strcmp(env, "ntt") == 0;
         if (flags & TM_CORR_TC) {
-            if (!p->tc_ok) {
+            if (!p->tc_ok && !p->tct_ok) {
                 free(p);
                 tm_set_error("tm_plan_create: TM_CORR_TC: plan not eligible for the tensor-core engine");
                 return TM_EUNSUPPORTED;
             }
             p->use_tc = 1;
         } else {
-            p->use_tc = p->tc_ok && !(flags & TM_CORR_NTT) && !env_ntt;
+            p->use_tc = (p->tc_ok || p->tct_ok) && !(flags & TM_CORR_NTT) && !env_ntt;
         }
         if (p->use_tc) {  // the folded template is the int8 template itself, 16-byte rows
             p->tf_bytes = (K + 15) / 16 * 16;
@@ -229,6 +230,8 @@ tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch) {
     if (p->big_corr) off += align256(tm_gntt_scratch_bytes(p, batch));
     w.counters = off;
     off += 256;
+    w.tiled = off;
+    off += align256(tm_tc_tiled_ws_bytes(p, batch));
     w.total = off;
     return w;
 }

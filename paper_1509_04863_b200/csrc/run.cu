@@ -160,7 +160,7 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
         if (rc) return rc;
         tm_prof_mark(1, s);
         tm_prof_mark(2, s);
-        rc = tm_tc_correlate(p, W.y1, W.y2, t, p->K, batch, nullptr, nullptr, nullptr, residues, k, s);
+        rc = tm_tc_any(p, W.y1, W.y2, t, p->K, batch, nullptr, nullptr, nullptr, residues, k, ws, s);
         tm_prof_mark(3, s);
         tm_prof_mark(4, s);
         return rc;
@@ -228,7 +228,7 @@ extern "C" __attribute__((visibility("default"))) int tm_correlate_match(tm_plan
     cudaStream_t s = (cudaStream_t)stream;
     RunWs W = run_ws(p, batch, ws);
     int rc;
-    if (p->use_tc) return tm_tc_correlate(p, y1, y2, t, p->K, batch, nullptr, nullptr, nullptr, residues, k, s);
+    if (p->use_tc) return tm_tc_any(p, y1, y2, t, p->K, batch, nullptr, nullptr, nullptr, residues, k, ws, s);
     if (p->fast_corr) {
         rc = tm_fast_correlate(p, y1, y2, t, nullptr, batch, nullptr, nullptr, W.resid, s);
     } else if (p->big_corr) {

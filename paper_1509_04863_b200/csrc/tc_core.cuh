@@ -127,13 +127,14 @@ __device__ __forceinline__ int32_t limb(int32_t v, int l, int nl) {
     return (l == nl - 1) ? (v >> (4 * l)) : ((v >> (4 * l)) & 15);
 }
 
-// Stage limb l (of nl) of y_1, y_2 (blocks s < R of P entries, zero beyond
-// len_j) into the interleaved B layout: row 2 s + j.  One warp per block row:
-// lane i holds entries 4i .. 4i+3 (chunk h = i / 4).  Returns this thread's
-// range flags (bit 0: some |y| needs 2 limbs, bit 1: 3 limbs).
-__device__ __forceinline__ int stage_y(const TcArgs &a, uint8_t *B, int64_t b, int l, int nl, int warp, int lane) {
+// Stage limb l (of nl) of y_1, y_2 blocks s_begin + [0, nrows) (P entries each,
+// zero outside [0, len_j)) into the interleaved B layout: row 2 s + j.  One warp
+// per block row: lane i holds entries 4i .. 4i+3 (chunk h = i / 4).  Returns
+// this thread's range flags (bit 0: some |y| needs 2 limbs, bit 1: 3, bit 2: 4).
+__device__ __forceinline__ int stage_yw(const TcArgs &a, uint8_t *B, int64_t b, int l, int nl, int64_t s_begin,
+                                        int nrows, int warp, int lane) {
     int flags = 0;
-    const uint32_t lbo = 32u * a.R;  // bytes per chunk column h: 2 R rows of 16 B
+    const uint32_t lbo = 32u * nrows;  // bytes per chunk column h: 2 nrows rows of 16 B
     const int h = lane >> 2, wq = lane & 3;
     constexpr int RB = 4;                 // block rows in flight per warp
     constexpr int NW = NTHR / 32;
@@ -142,13 +143,13 @@ __device__ __forceinline__ int stage_y(const TcArgs &a, uint8_t *B, int64_t b, i
         const int32_t *yr = a.y[j] + b * a.ldy[j];
         const int64_t len = a.len[j];
         const bool al = ((((uintptr_t)yr) & 15) == 0);
-        for (int s0 = warp; s0 < a.R; s0 += RB * NW) {
+        for (int s0 = warp; s0 < nrows; s0 += RB * NW) {
             int32_t v[RB][4];
 #pragma unroll
             for (int u = 0; u < RB; ++u) {
-                const int64_t i0 = (int64_t)P * (s0 + u * NW) + 4 * lane;
+                const int64_t i0 = (int64_t)P * (s_begin + s0 + u * NW) + 4 * lane;
                 v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0;
-                if (s0 + u * NW < a.R) {
+                if (s0 + u * NW < nrows && i0 >= 0) {
                     if (al && i0 + 4 <= len) {
                         const int4 q = *reinterpret_cast<const int4 *>(yr + i0);
                         v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
@@ -162,11 +163,12 @@ __device__ __forceinline__ int stage_y(const TcArgs &a, uint8_t *B, int64_t b, i
 #pragma unroll
             for (int u = 0; u < RB; ++u) {
                 const int s = s0 + u * NW;
-                if (s >= a.R) break;
+                if (s >= nrows) break;
                 const int32_t v0 = v[u][0], v1 = v[u][1], v2 = v[u][2], v3 = v[u][3];
                 const uint32_t o1 = (uint32_t)(v0 + 128) | (uint32_t)(v1 + 128) | (uint32_t)(v2 + 128) | (uint32_t)(v3 + 128);
                 const uint32_t o2 = (uint32_t)(v0 + 2048) | (uint32_t)(v1 + 2048) | (uint32_t)(v2 + 2048) | (uint32_t)(v3 + 2048);
-                flags |= (o1 > 255u ? 1 : 0) | (o2 > 4095u ? 2 : 0);
+                const uint32_t o3 = (uint32_t)(v0 + 32768) | (uint32_t)(v1 + 32768) | (uint32_t)(v2 + 32768) | (uint32_t)(v3 + 32768);
+                flags |= (o1 > 255u ? 1 : 0) | (o2 > 4095u ? 2 : 0) | (o3 > 65535u ? 4 : 0);
                 *reinterpret_cast<uint32_t *>(B + lbo * h + 16 * (2 * s + j) + 4 * wq) =
                     nl == 1 ? pack4(v0, v1, v2, v3)
                             : pack4(limb(v0, l, nl), limb(v1, l, nl), limb(v2, l, nl), limb(v3, l, nl));
@@ -174,6 +176,10 @@ __device__ __forceinline__ int stage_y(const TcArgs &a, uint8_t *B, int64_t b, i
         }
     }
     return flags;
+}
+
+__device__ __forceinline__ int stage_y(const TcArgs &a, uint8_t *B, int64_t b, int l, int nl, int warp, int lane) {
+    return stage_yw(a, B, b, l, nl, 0, a.R, warp, lane);
 }
 
 // TMEM -> registers for 8 output blocks [a0, a0 + 8) of both moduli (limb l

@@ -34,6 +34,7 @@ struct tm_plan_s {
     int use_tc;          // tm_run / tm_correlate use corr_tc_kernel
     int tc_ok;           // plan shape eligible for it
     int tc_NA[2], tc_NMC, tc_R, tc_NC, tc_JA, tc_CCH, tc_lmax;
+    int tct_ok, tct_lmax;  // tiled tensor-core correlation (corr_tc_tiled.cu) eligible
     uint32_t tc_ncols, tc_offB, tc_offTp, tc_offMisc, tc_smem;
 };
 
@@ -92,6 +93,7 @@ struct tm_ws_layout {
     size_t f32_tiles;     // fp32 per-tile argmax partials (tm_run, TM_F32)
     size_t gntt;          // grid-pass NTT scratch (big_corr plans)
     size_t counters;      // int32 work counters (tm_run overlap mode, one per chunk)
+    size_t tiled;         // tiled tensor-core correlation: packed keys + partial sums
     size_t total;
 };
 tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch);
@@ -129,10 +131,19 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
                  int64_t len, void *y1, void *y2, int accumulate, void *ws, cudaStream_t s);
 int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const void *tf,
                       int64_t batch, void *r1, void *r2, int32_t *resid, void *tile_scratch,
-                      void *gntt_scratch, cudaStream_t s);
+                      void *gntt_scratch, cudaStream_t s, void *tc_ws = nullptr);
 void tm_tc_plan(tm_plan_s *p);
 int tm_tc_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt, int64_t batch,
                     void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k, cudaStream_t s);
 int tm_tc_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf, cudaStream_t s);
+void tm_tc_tiled_plan(tm_plan_s *p);
+size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch);
+int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt,
+                          int64_t batch, void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k,
+                          void *ws, cudaStream_t s);
+// the tensor-core engine for a batch: one CTA per pair (corr_tc.cu) or tiled
+// over CTAs (few pairs / long templates); ws = the whole tm_workspace_bytes area
+int tm_tc_any(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt, int64_t batch,
+              void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s);
 int tm_crt_impl(const tm_plan_s *p, const int32_t *resid, int64_t batch, int32_t *residues_out,
                 int64_t *k, cudaStream_t s);

@@ -288,6 +288,27 @@ def test_tc_engine_limbs_and_ragged_shapes(tm, N, K, M, B):
     check_int_pairs(tm, plan, x_h, t_h, range(B))
 
 
+@pytest.mark.parametrize("tiled", ["0", "1"])
+@pytest.mark.parametrize("N,K,M,B,binary", [(2 ** 14, 200, 0, 3, False), (4096, 256, 0, 8, True),
+                                            (2 ** 18, 4096, 0, 3, True), (2 ** 20, 8192, 0, 2, True),
+                                            (30000, 300, 333, 3, False)])
+def test_tc_one_cta_and_tiled_kernels(tm, N, K, M, B, binary, tiled, monkeypatch):
+    """Both tensor-core kernels on the same shapes: one CTA per pair
+    (corr_tc_kernel) and the tiled split over output tiles and template ranges
+    with partial-sum atomics or packed-key argmax (corr_tc_tiled); bit-exact vs
+    the oracle (general int8 data exercises 3-4 limbs)."""
+    monkeypatch.setenv("TM_TC_TILED", tiled)
+    plan = tm.Plan(N, K, M=M, seed=6, binary=binary, engine="tc")
+    rng = np.random.default_rng(N + K + B)
+    if binary:
+        x_h, t_h, _ = tmgen.batch(6, 0, B, N, K, 0.1)
+    else:
+        x_h = rng.integers(-128, 128, (B, N)).astype(np.int8)
+        x_h[0] = 127
+        t_h = rng.integers(-128, 128, (B, K)).astype(np.int8)
+    check_int_pairs(tm, plan, x_h, t_h, range(B))
+
+
 def test_tc_and_ntt_engines_agree_on_cfg2(tm):
     """Every pair of a full cfg2 batch: residues and k from the two exact engines
     are identical (both are pinned to the oracle on sampled pairs above)."""
