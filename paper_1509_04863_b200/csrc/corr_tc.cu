@@ -180,7 +180,9 @@ int tm_tc_any(const tm_plan_s *p, const void *y1, const void *y2, const void *t,
               void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s) {
     const char *env = getenv("TM_TC_TILED");  // tests / A-B: "0" never, "1" whenever eligible
     const bool force = env && env[0] == '1', never = env && env[0] == '0';
-    if (p->tct_ok && ws && !never && (force || !p->tc_ok || batch < p->num_sms))
+    // one CTA per pair whenever it fits (measured faster even at 64 pairs, cfg4);
+    // the tiled kernel for plans the one-CTA kernel cannot take (cfg5: K = 65536)
+    if (p->tct_ok && ws && !never && (force || !p->tc_ok))
         return tm_tc_tiled_correlate(p, y1, y2, t, ldt, batch, r1, r2, resid, residues_out, k,
                                      (char *)ws + tm_ws(p, batch).tiled, s);
     return tm_tc_correlate(p, y1, y2, t, ldt, batch, r1, r2, resid, residues_out, k, s);

@@ -13,9 +13,13 @@
 // Epilogue: with one template range per pair, the tile's lowest-index maximum
 // per modulus goes to an atomicMax on a packed key (r + 2^42) << 21 | (2^21 -
 // 1 - k) (max r, ties to the lowest k); with several ranges the tile's partial
-// r are added (int64 atomics, exact) into r.  tc_tiled_finish then does, per
-// pair, the leftover outputs k in [128 NA_j, M_j) (dot products), the argmax
-// (from the keys or from r) and steps 8-9 (tm_resolve).
+// r are added (int64 atomics, exact) into r, and the CTA that completes a
+// tile's last range reduces the tile's final r to the same packed key.
+// tc_tiled_leftover computes the <= 8 outputs k in [128 NA_j, M_j) per
+// modulus (dot products split over K-slices), and tc_tiled_final combines keys
+// and leftovers per pair and does steps 8-9 (tm_resolve).
+#include <algorithm>
+
 #include "tc_core.cuh"
 
 namespace {
@@ -33,6 +37,8 @@ struct TiledArgs {
     unsigned long long *keys;  // [batch][2] (n_cr == 1), zeroed
     int64_t *racc[2];          // [batch][Mj] partial sums (n_cr > 1), zeroed; or r outputs
     int write_r;               // n_cr == 1: store r values (staged tm_correlate)
+    unsigned *tile_cnt;        // [batch][n_at] template ranges finished per tile (n_cr > 1), zeroed
+    int64_t *lsum;             // [batch][2 MAXLEFT] leftover dot products, zeroed
 };
 
 __device__ __forceinline__ unsigned long long pack_key(int64_t r, int64_t k) {
@@ -181,7 +187,25 @@ __global__ void __launch_bounds__(NTHR, 2) corr_tc_tiled(const TiledArgs T) {
                 }
             }
         }
-        if (T.n_cr == 1) {
+        if (T.n_cr > 1) {
+            // the CTA that completes a tile's last template range reduces its final r
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) *nlflag = (atomicAdd(T.tile_cnt + b * T.n_at + at, 1u) == (unsigned)(T.n_cr - 1));
+            __syncthreads();
+            if (*nlflag) {
+                __threadfence();
+                for (int ar0 = 16 * hw; ar0 < 16 * hw + 16; ++ar0) {
+                    const int64_t ab = a0 + ar0;
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int64_t k = P * ab + brow;
+                        if (ab < a.NA[j] && k < a.M[j]) amax(bv[j], bk[j], __ldcg(T.racc[j] + b * a.M[j] + k), k);
+                    }
+                }
+            }
+        }
+        if (T.n_cr == 1 || *nlflag) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
 #pragma unroll
@@ -199,66 +223,67 @@ __global__ void __launch_bounds__(NTHR, 2) corr_tc_tiled(const TiledArgs T) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(a.ncols));
 }
 
-// per pair: leftovers k in [128 NA_j, M_j), argmax, steps 8-9
-__global__ void __launch_bounds__(256) tc_tiled_finish(const TiledArgs T, int32_t *resid, int32_t *residues_out,
-                                                       int64_t *k_out, int64_t *r_out0, int64_t *r_out1) {
+// leftover outputs k in [128 NA_j, M_j) (at most MAXLEFT per modulus): CTA
+// (K-slice, pair) adds its partial dot products into lsum (exact int64)
+constexpr int LSLICE = 4096;
+__global__ void __launch_bounds__(256) tc_tiled_leftover(const TiledArgs T) {
     const TcArgs &a = T.a;
-    const int64_t b = blockIdx.x;
+    const int64_t b = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    __shared__ int64_t sv[8][2], sk[8][2];
-    __shared__ int64_t lsum[8];
+    const int64_t i0 = (int64_t)blockIdx.x * LSLICE, i1 = min(a.K, i0 + LSLICE);
+    __shared__ int64_t part[8];
+    const int nleft0 = (int)max((int64_t)0, a.M[0] - (int64_t)P * a.NA[0]);
+    const int nleft1 = (int)max((int64_t)0, a.M[1] - (int64_t)P * a.NA[1]);
+    const int8_t *tr = a.t + b * a.ldt;
+    for (int q = 0; q < nleft0 + nleft1; ++q) {
+        const int j = q < nleft0 ? 0 : 1;
+        const int64_t k = (int64_t)P * a.NA[j] + (j ? q - nleft0 : q);
+        const int32_t *yr = a.y[j] + b * a.ldy[j] + k;
+        int64_t sum = 0;
+#pragma unroll 4
+        for (int64_t i = i0 + tid; i < i1; i += 256) sum += (int64_t)tr[i] * yr[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) part[warp] = sum;
+        __syncthreads();
+        if (tid == 0) {
+            int64_t tot = 0;
+            for (int w = 0; w < 8; ++w) tot += part[w];
+            atomicAdd(reinterpret_cast<unsigned long long *>(T.lsum + b * 2 * MAXLEFT + q), (unsigned long long)tot);
+        }
+        __syncthreads();
+    }
+}
+
+// per pair: tile keys + leftovers -> residues; steps 8-9 (tm_resolve)
+__global__ void tc_tiled_final(const TiledArgs T, int64_t batch, int32_t *resid, int32_t *residues_out,
+                               int64_t *k_out, int64_t *r_out0, int64_t *r_out1) {
+    const TcArgs &a = T.a;
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    const int nleft0 = (int)max((int64_t)0, a.M[0] - (int64_t)P * a.NA[0]);
+    const int nleft1 = (int)max((int64_t)0, a.M[1] - (int64_t)P * a.NA[1]);
     int64_t m[2];
     for (int j = 0; j < 2; ++j) {
         int64_t bv = INT64_MIN, bk = INT64_MAX;
-        if (T.n_cr > 1) {  // argmax over the accumulated r
-            const int64_t *r = T.racc[j] + b * a.M[j];
-            const int64_t lim = min(a.M[j], (int64_t)P * a.NA[j]);
-            for (int64_t k = tid; k < lim; k += 256) amax(bv, bk, r[k], k);
-        } else if (tid == 0) {
-            const unsigned long long key = T.keys[2 * b + j];
-            if (key) {
-                bk = ((int64_t)1 << KEY_SHIFT) - 1 - (int64_t)(key & (((unsigned long long)1 << KEY_SHIFT) - 1));
-                bv = (int64_t)(key >> KEY_SHIFT) - KEY_BIAS;
-            }
+        const unsigned long long key = T.keys[2 * b + j];
+        if (key) {
+            bk = ((int64_t)1 << KEY_SHIFT) - 1 - (int64_t)(key & (((unsigned long long)1 << KEY_SHIFT) - 1));
+            bv = (int64_t)(key >> KEY_SHIFT) - KEY_BIAS;
         }
-        // leftovers (dot products over all threads)
-        const int64_t k0 = (int64_t)P * a.NA[j];
-        for (int64_t k = k0; k < a.M[j]; ++k) {
-            const int32_t *yr = a.y[j] + b * a.ldy[j] + k;
-            const int8_t *tr = a.t + b * a.ldt;
-            int64_t s = 0;
-            for (int64_t i = tid; i < a.K; i += 256) s += (int64_t)tr[i] * yr[i];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) lsum[warp] = s;
-            __syncthreads();
-            if (tid == 0) {
-                int64_t tot = 0;
-                for (int w = 0; w < 8; ++w) tot += lsum[w];
-                amax(bv, bk, tot, k);
-                int64_t *ro = j ? r_out1 : r_out0;
-                if (ro) ro[b * a.M[j] + k] = tot;
-            }
-            __syncthreads();
+        const int nleft = j ? nleft1 : nleft0;
+        for (int q = 0; q < nleft; ++q) {
+            const int64_t r = T.lsum[b * 2 * MAXLEFT + (j ? nleft0 : 0) + q];
+            const int64_t k = (int64_t)P * a.NA[j] + q;
+            int64_t *ro = j ? r_out1 : r_out0;
+            if (ro) ro[b * a.M[j] + k] = r;
+            amax(bv, bk, r, k);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
-            amax(bv, bk, ov, ok);
-        }
-        if (lane == 0) { sv[warp][j] = bv; sk[warp][j] = bk; }
-        __syncthreads();
-        int64_t v = INT64_MIN, kk = INT64_MAX;
-        for (int w = 0; w < 8; ++w) amax(v, kk, sv[w][j], sk[w][j]);
-        m[j] = kk;
-        __syncthreads();
+        m[j] = bk;
     }
-    if (tid == 0) {
-        if (resid) { resid[2 * b] = (int32_t)m[0]; resid[2 * b + 1] = (int32_t)m[1]; }
-        if (residues_out) { residues_out[2 * b] = (int32_t)m[0]; residues_out[2 * b + 1] = (int32_t)m[1]; }
-        if (k_out) k_out[b] = tm_resolve(m[0], m[1], a.M1, a.M2, a.crt_inv, a.N, a.crt_wrap);  // steps 8-9
-    }
+    if (resid) { resid[2 * b] = (int32_t)m[0]; resid[2 * b + 1] = (int32_t)m[1]; }
+    if (residues_out) { residues_out[2 * b] = (int32_t)m[0]; residues_out[2 * b + 1] = (int32_t)m[1]; }
+    if (k_out) k_out[b] = tm_resolve(m[0], m[1], a.M1, a.M2, a.crt_inv, a.N, a.crt_wrap);  // steps 8-9
 }
 
 }  // namespace
@@ -281,7 +306,9 @@ void tm_tc_tiled_plan(tm_plan_s *p) {
 
 size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch) {
     if (!p->tct_ok) return 0;
-    return (size_t)batch * 2 * 8 + (size_t)batch * (p->M1 + p->M2) * 8 + 512;
+    // keys [batch][2] | lsum [batch][2 MAXLEFT] | tile counters [batch][<= 2^KEY_SHIFT / (128 NT)] | racc
+    return 256 + (size_t)batch * (16 + 16 * MAXLEFT + 4 * (((int64_t)1 << KEY_SHIFT) / (P * NT) + 1)) +
+           (size_t)batch * (p->M1 + p->M2) * 8 + 1024;
 }
 
 // r1/r2 (int64, may be NULL), residues_out/resid (may be NULL), k (may be NULL).
@@ -316,17 +343,19 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, co
     T.CR = (NC + n_cr - 1) / n_cr;
     T.n_cr = (NC + T.CR - 1) / T.CR;
     char *w = (char *)ws;
-    T.keys = (unsigned long long *)w;
-    int64_t *racc = (int64_t *)(w + ((size_t)batch * 16 + 255) / 256 * 256);
+    auto carve = [&](size_t bytes) { char *q = w; w += (bytes + 255) / 256 * 256; return q; };
+    T.keys = (unsigned long long *)carve((size_t)batch * 16);
+    T.lsum = (int64_t *)carve((size_t)batch * 16 * MAXLEFT);
+    T.tile_cnt = (unsigned *)carve((size_t)batch * T.n_at * 4);
+    const size_t zero_bytes = (size_t)(w - (char *)ws);  // keys, lsum, counters: one memset
+    int64_t *racc = (int64_t *)carve((size_t)batch * (p->M1 + p->M2) * 8);
     T.racc[0] = r1 ? (int64_t *)r1 : racc;
     T.racc[1] = r2 ? (int64_t *)r2 : racc + batch * p->M1;
     T.write_r = (r1 != nullptr);
-    cudaError_t e = cudaSuccess;
-    if (T.n_cr > 1) {
+    cudaError_t e = cudaMemsetAsync(ws, 0, zero_bytes, s);
+    if (e == cudaSuccess && T.n_cr > 1) {
         e = cudaMemsetAsync(T.racc[0], 0, (size_t)batch * p->M1 * 8, s);
         if (e == cudaSuccess) e = cudaMemsetAsync(T.racc[1], 0, (size_t)batch * p->M2 * 8, s);
-    } else {
-        e = cudaMemsetAsync(T.keys, 0, (size_t)batch * 16, s);
     }
     if (e != cudaSuccess) return tm_cuda_status(e, "tm_correlate: tiled reset");
     static bool attr = false;
@@ -336,7 +365,14 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, co
     }
     corr_tc_tiled<<<dim3((unsigned)(T.n_at * T.n_cr), (unsigned)batch), NTHR, SMEM_BYTES, s>>>(T);
     TM_CHECK_LAUNCH("corr_tc_tiled");
-    tc_tiled_finish<<<(unsigned)batch, 256, 0, s>>>(T, resid, residues_out, k, (int64_t *)r1, (int64_t *)r2);
-    TM_CHECK_LAUNCH("tc_tiled_finish");
+    const int nleft = (int)(std::max<int64_t>(0, p->M1 - (int64_t)P * T.a.NA[0]) +
+                            std::max<int64_t>(0, p->M2 - (int64_t)P * T.a.NA[1]));
+    if (nleft > 0) {
+        tc_tiled_leftover<<<dim3((unsigned)((p->K + LSLICE - 1) / LSLICE), (unsigned)batch), 256, 0, s>>>(T);
+        TM_CHECK_LAUNCH("tc_tiled_leftover");
+    }
+    tc_tiled_final<<<(unsigned)((batch + 127) / 128), 128, 0, s>>>(T, batch, resid, residues_out, k, (int64_t *)r1,
+                                                                     (int64_t *)r2);
+    TM_CHECK_LAUNCH("tc_tiled_final");
     return TM_OK;
 }
