@@ -47,17 +47,21 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _LIB_PATH
+    # TM_LIB_VARIANT=<name> loads paper_1509_04863_b200/libtm_<name>.so instead
+    # (same-box A/B measurements of build variants; scripts/build_variant.py)
+    v = os.environ.get("TM_LIB_VARIANT")
+    return os.path.join(_HERE, f"libtm_{v}.so") if v else _LIB_PATH
 
 
 def lib():
     """Load libtm.so; raise loudly if it has not been built (no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            raise ImportError(f"{_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+        path = lib_path()
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                               "(there is no CPU fallback for the CUDA path)")
-        L = ctypes.CDLL(_LIB_PATH)
+        L = ctypes.CDLL(path)
         L.tm_plan_create.restype = ctypes.c_int
         L.tm_plan_create.argtypes = [ctypes.POINTER(_p), _i64, _i64, _i64, _u64, ctypes.c_int, _u32]
         L.tm_plan_query.restype = ctypes.c_int

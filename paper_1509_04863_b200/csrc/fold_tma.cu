@@ -310,6 +310,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
         uint32_t pph = 0;
         for (;;) {
             mbar_wait(&pfull[pb], pph);
+            long long te0 = 0;
+            if constexpr (TCM) te0 = tc::gtime();
             const int64_t item = pitem[pb];
             if (item < 0) {
                 if constexpr (FUSED) {
@@ -338,6 +340,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 int32_t *o2 = a.y2 + it.b * a.ldy2;
                 const int M2 = (int)a.M2, M1 = (int)a.M1, K = (int)a.K;
                 const int dlo = -16 * ntile;
+                // (a straight-line / unrolled variant of this loop measured slower in the
+                // fused kernel: it competes harder with the fold warps for issue slots)
                 for (int k = et; k < M2; k += NE * 32) {
                     // bin k collects the unwrapped diagonals d = k and d = k - M2 (d >= dlo)
                     int32_t C = comb_at(pv, a.priv_stride, k, ntile, width);
@@ -374,6 +378,9 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             if (lane == 0) {
                 mbar_arrive(&pempty[pb]);
                 if constexpr (FUSED) mbar_arrive(&yready[pb]);
+            }
+            if constexpr (TCM) {  // instrumentation: duration of this CTA's latest epilogue
+                if (a.tca.dbg && et == 0) a.tca.dbg[8 * a.n_items + 3 * gridDim.x + blockIdx.x] = tc::gtime() - te0;
             }
             if (++pb == 2) { pb = 0; pph ^= 1; }
         }
@@ -558,6 +565,9 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
         if (lane == 0) {
             mbar_arrive(&pfull[pb]);
             if constexpr (FUSED) mbar_arrive(&yready[pb]);
+        }
+        if constexpr (TCM) {  // instrumentation: end of this CTA's latest fold item
+            if (a.tca.dbg && warp == 0 && lane == 0) a.tca.dbg[8 * a.n_items + 2 * gridDim.x + blockIdx.x] = tc::gtime();
         }
         if (++pb == 2) { pb = 0; pph ^= 1; }
     }

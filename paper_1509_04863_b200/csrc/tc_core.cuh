@@ -14,6 +14,9 @@ namespace tc {
 constexpr int P = 128;
 constexpr int NTHR = 256;
 constexpr int MAXLEFT = 8;  // outputs k in [P*NA, M) done by warp dot products
+#ifndef TC_RB
+#define TC_RB 8
+#endif
 // misc area (offMisc): mbarrier | TMEM slot | sv[16] | sk[16] | pbegin[2] (fused kernel) |
 // leftover partial sums [8 warps][2 MAXLEFT]
 constexpr int MISC_PBEGIN = 16 + 2 * 16 * 8;
@@ -136,7 +139,7 @@ __device__ __forceinline__ int stage_yw(const TcArgs &a, uint8_t *B, int64_t b, 
     int flags = 0;
     const uint32_t lbo = 32u * nrows;  // bytes per chunk column h: 2 nrows rows of 16 B
     const int h = lane >> 2, wq = lane & 3;
-    constexpr int RB = 4;                 // block rows in flight per warp
+    constexpr int RB = TC_RB;             // block rows in flight per warp
     constexpr int NW = NTHR / 32;
 #pragma unroll 1
     for (int j = 0; j < 2; ++j) {

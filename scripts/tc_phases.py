@@ -37,4 +37,9 @@ if len(sys.argv) > 1 and sys.argv[1] == 'run':
     ex = dd[B * 8: B * 8 + 296].reshape(148, 2)
     k0 = ex[:, 0].min()
     print('CTA entry us: max %.1f; TC exit us: min %.1f p50 %.1f max %.1f' % ((ex[:, 0].max() - k0) / 1e3, (ex[:, 1].min() - k0) / 1e3, np.median(ex[:, 1] - k0) / 1e3, (ex[:, 1].max() - k0) / 1e3))
+    fe = dd[B * 8 + 296: B * 8 + 296 + 148]
+    tail = ex[:, 1] - fe
+    print('last fold item end us: min %.1f p50 %.1f max %.1f; TC tail after it us: min %.1f p50 %.1f max %.1f' % ((fe.min() - k0) / 1e3, (np.median(fe) - k0) / 1e3, (fe.max() - k0) / 1e3, tail.min() / 1e3, np.median(tail) / 1e3, tail.max() / 1e3))
+    ep = dd[B * 8 + 444: B * 8 + 444 + 148]
+    print('fold epilogue (last item) us: min %.1f p50 %.1f max %.1f' % (ep.min() / 1e3, np.median(ep) / 1e3, ep.max() / 1e3))
     print('first TC start after kernel entry us: min %.1f p50 %.1f max %.1f' % ((first.min()*1e3 + t0 - k0) / 1e3, (np.median(first)*1e3 + t0 - k0) / 1e3, (first.max()*1e3 + t0 - k0) / 1e3))
