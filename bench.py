@@ -300,7 +300,7 @@ def main():
     if path == 2:
         # fused kernel = the whole step: algorithmic bytes = x and t read once, k and
         # residues written once (y never needs to leave the chip)
-        kernel = "fold_pm1_tma<3,0,1,TC> (fused fold + tensor-core correlation + argmax + CRT)"
+        kernel = "fold_pm1_tma<4,0,1,TC> (fused fold + tensor-core correlation + argmax + CRT)"
         fold_bytes = B * (N + K) * bx + B * (8 + 8)
         tkey = args.workload + ":fused_tc"
     else:

@@ -55,6 +55,12 @@ __host__ __device__ __forceinline__ int64_t tm_resolve(int64_t m1, int64_t m2, i
     return -1;
 }
 
+// mbarrier.try_wait suspend-time hint (ns): a waiting thread sleeps until the
+// phase completes (or this bound elapses) instead of re-issuing the test
+#ifndef MBAR_SUSPEND_NS
+#define MBAR_SUSPEND_NS 0
+#endif
+
 // ---- error plumbing (plan.cu) ----
 void tm_set_error(const char *fmt, ...);
 int tm_cuda_status(cudaError_t e, const char *what);
