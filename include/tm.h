@@ -201,6 +201,19 @@ int tm_correlate_match(tm_plan plan, const void *y1, const void *y2, const void 
                        int32_t *residues, int64_t *k, void *ws, void *stream);
 
 /*
+ * tm_correlate_many -- steps 4-9 for ONE folded signal against many templates
+ * (the GPS / CDMA acquisition shape of section 3.5: one received
+ * code, one template per satellite / user): template i's
+ * k[i] is what tm_correlate_match would return for the pair (x, t_i).  Fold
+ * once (tm_fold), then call this.  y1 [len_y1], y2 [len_y2] of the one
+ * signal; t [n_templates][K]; residues [n][2] (may be NULL), k [n].  ws of
+ * tm_workspace_bytes(plan, n_templates).  The tensor-core engine reads y with
+ * stride 0 (no copies); the other engines broadcast y into the workspace.
+ */
+int tm_correlate_many(tm_plan plan, const void *y1, const void *y2, const void *t, int64_t n_templates,
+                      int32_t *residues, int64_t *k, void *ws, void *stream);
+
+/*
  * tm_run_host -- tm_run on HOST buffers: copies x_host/t_host (pinned memory
  * recommended) to the caller's device staging buffers in chunks of
  * `chunk` pairs, overlapping the copy of chunk i+1 with the compute of chunk

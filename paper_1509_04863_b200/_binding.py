@@ -16,7 +16,7 @@ TM_OK, TM_EINVAL, TM_EUNSUPPORTED, TM_ECUDA = 0, 1, 2, 3
 
 EXPORTED_SYMBOLS = (
     "tm_plan_create", "tm_plan_query", "tm_workspace_bytes", "tm_plan_destroy", "tm_generate",
-    "tm_fold", "tm_fold_template", "tm_correlate", "tm_match", "tm_run", "tm_run_host", "tm_correlate_match",
+    "tm_fold", "tm_fold_template", "tm_correlate", "tm_match", "tm_run", "tm_run_host", "tm_correlate_match", "tm_correlate_many",
     "tm_status_string", "tm_last_error", "tm_launch_count", "tm_profile_events", "tm_run_path",
 )
 RUN_PATHS = {0: "staged (fold -> NTT/fp32 correlation -> CRT)", 1: "staged (fold -> tensor-core correlation)",
@@ -84,6 +84,8 @@ def lib():
         L.tm_run.argtypes = [_p, _p, _i64, _p, _i64, _p, _p, _p, _p]
         L.tm_correlate_match.restype = ctypes.c_int
         L.tm_correlate_match.argtypes = [_p, _p, _p, _p, _i64, _p, _p, _p, _p]
+        L.tm_correlate_many.restype = ctypes.c_int
+        L.tm_correlate_many.argtypes = [_p, _p, _p, _p, _i64, _p, _p, _p, _p]
         L.tm_run_host.restype = ctypes.c_int
         L.tm_run_host.argtypes = [_p, _p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p]
         L.tm_launch_count.restype = _u64
@@ -131,6 +133,11 @@ def _stream(stream):
 
 def _ptr(t):
     return None if t is None else t.data_ptr()
+
+
+def _ld(x):
+    """Row stride of a [batch][n] tensor (a single row may carry any stride in torch)."""
+    return x.stride(0) if x.shape[0] > 1 else x.shape[1]
 
 
 class Plan:
@@ -186,7 +193,7 @@ class Plan:
             t = torch.empty((batch, self.K), dtype=self.x_dtype, device=device)
         if k0 is None:
             k0 = torch.empty(batch, dtype=torch.int64, device=device)
-        ldx = x.stride(0) if x is not None and x.dim() == 2 else length
+        ldx = _ld(x) if x is not None and x.dim() == 2 else length
         _check(lib().tm_generate(self._h, pair0, batch, float(noise), offset, length, _ptr(x), ldx, _ptr(t),
                                  _ptr(k0), _stream(stream)), "tm_generate")
         return x, t, k0
@@ -202,7 +209,7 @@ class Plan:
             y2 = torch.zeros((batch, self.len_y2), dtype=self.y_dtype, device=x.device)
         if ws is None:
             ws = self.workspace(batch, x.device)
-        _check(lib().tm_fold(self._h, _ptr(x), x.stride(0), batch, offset, length, _ptr(y1), _ptr(y2),
+        _check(lib().tm_fold(self._h, _ptr(x), _ld(x), batch, offset, length, _ptr(y1), _ptr(y2),
                              int(accumulate), _ptr(ws), _stream(stream)), "tm_fold")
         return y1, y2
 
@@ -246,7 +253,7 @@ class Plan:
             k = torch.empty(batch, dtype=torch.int64, device=x.device)
         if ws is None:
             ws = self.workspace(batch, x.device)
-        _check(lib().tm_run(self._h, _ptr(x), x.stride(0), _ptr(t), batch, _ptr(residues), _ptr(k), _ptr(ws),
+        _check(lib().tm_run(self._h, _ptr(x), _ld(x), _ptr(t), batch, _ptr(residues), _ptr(k), _ptr(ws),
                             _stream(stream)), "tm_run")
         return residues, k
 
@@ -268,10 +275,25 @@ class Plan:
         """tm_run_path: which kernel sequence tm_run launches for this batch (instrumentation)."""
         return int(lib().tm_run_path(self._h, batch))
 
+    def correlate_many(self, y1, y2, t, residues=None, k=None, ws=None, stream=None):
+        """tm_correlate_many: one folded signal (y1 [len_y1], y2 [len_y2]) against
+        templates t [n][K] -> residues [n][2], k [n]."""
+        import torch
+        n = t.shape[0]
+        if residues is None:
+            residues = torch.empty((n, 2), dtype=torch.int32, device=t.device)
+        if k is None:
+            k = torch.empty(n, dtype=torch.int64, device=t.device)
+        if ws is None:
+            ws = self.workspace(n, t.device)
+        _check(lib().tm_correlate_many(self._h, _ptr(y1), _ptr(y2), _ptr(t), n, _ptr(residues), _ptr(k), _ptr(ws),
+                                       _stream(stream)), "tm_correlate_many")
+        return residues, k
+
     def run_host(self, x_host, t_host, chunk: int, residues_host, k_host, dev_x, dev_t, dev_out, ws, stream=None):
         """tm_run_host: x_host/t_host/residues_host/k_host are (pinned) CPU tensors."""
         batch = x_host.shape[0]
-        _check(lib().tm_run_host(self._h, _ptr(x_host), x_host.stride(0), _ptr(t_host), batch, chunk,
+        _check(lib().tm_run_host(self._h, _ptr(x_host), _ld(x_host), _ptr(t_host), batch, chunk,
                                  _ptr(residues_host), _ptr(k_host), _ptr(dev_x), _ptr(dev_t), _ptr(dev_out),
                                  _ptr(ws), _stream(stream)), "tm_run_host")
 

@@ -139,13 +139,15 @@ void tm_tc_fill_args(const tm_plan_s *p, const void *y1, const void *y2, const v
 }
 
 // r1/r2 (may be NULL), resid (may be NULL), k (NULL: no CRT).  t is int8 [batch][ldt].
-int tm_tc_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt, int64_t batch,
-                    void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k, cudaStream_t s) {
+int tm_tc_correlate(const tm_plan_s *p, const void *y1, const void *y2, int64_t ldy1, int64_t ldy2, const void *t,
+                    int64_t ldt, int64_t batch, void *r1, void *r2, int32_t *resid, int32_t *residues_out,
+                    int64_t *k, cudaStream_t s) {
     if (!p->tc_ok) return TM_EUNSUPPORTED;
     if (batch == 0) return TM_OK;
     if (batch > 0x7FFFFFFF) { tm_set_error("tm_correlate: batch too large"); return TM_EUNSUPPORTED; }
     TcArgs a{};
     tm_tc_fill_args(p, y1, y2, t, ldt, r1, r2, resid, residues_out, k, a);
+    a.ldy[0] = ldy1; a.ldy[1] = ldy2;  // 0: one folded signal shared by every template
     a.dbg = g_tc_dbg;
     static bool attr = false;
     if (!attr) {
@@ -178,12 +180,18 @@ int tm_tc_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf, c
 
 int tm_tc_any(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt, int64_t batch,
               void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s) {
+    return tm_tc_any_ld(p, y1, y2, p->len_y1, p->len_y2, t, ldt, batch, r1, r2, resid, residues_out, k, ws, s);
+}
+
+int tm_tc_any_ld(const tm_plan_s *p, const void *y1, const void *y2, int64_t ldy1, int64_t ldy2, const void *t,
+                 int64_t ldt, int64_t batch, void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k,
+                 void *ws, cudaStream_t s) {
     const char *env = getenv("TM_TC_TILED");  // tests / A-B: "0" never, "1" whenever eligible
     const bool force = env && env[0] == '1', never = env && env[0] == '0';
     // one CTA per pair whenever it fits (measured faster even at 64 pairs, cfg4);
     // the tiled kernel for plans the one-CTA kernel cannot take (cfg5: K = 65536)
     if (p->tct_ok && ws && !never && (force || !p->tc_ok))
-        return tm_tc_tiled_correlate(p, y1, y2, t, ldt, batch, r1, r2, resid, residues_out, k,
+        return tm_tc_tiled_correlate(p, y1, y2, ldy1, ldy2, t, ldt, batch, r1, r2, resid, residues_out, k,
                                      (char *)ws + tm_ws(p, batch).tiled, s);
-    return tm_tc_correlate(p, y1, y2, t, ldt, batch, r1, r2, resid, residues_out, k, s);
+    return tm_tc_correlate(p, y1, y2, ldy1, ldy2, t, ldt, batch, r1, r2, resid, residues_out, k, s);
 }

@@ -312,14 +312,15 @@ size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch) {
 }
 
 // r1/r2 (int64, may be NULL), residues_out/resid (may be NULL), k (may be NULL).
-int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt,
-                          int64_t batch, void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k,
-                          void *ws, cudaStream_t s) {
+int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, int64_t ldy1, int64_t ldy2,
+                          const void *t, int64_t ldt, int64_t batch, void *r1, void *r2, int32_t *resid,
+                          int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s) {
     if (!p->tct_ok) return TM_EUNSUPPORTED;
     if (batch == 0) return TM_OK;
     if (batch > 65535) return TM_EUNSUPPORTED;
     TiledArgs T{};
     tm_tc_fill_args(p, y1, y2, t, ldt, nullptr, nullptr, nullptr, nullptr, nullptr, T.a);
+    T.a.ldy[0] = ldy1; T.a.ldy[1] = ldy2;
     // the tiles cover NA_j = the plan's block counts (computed here: tc_ok may be false)
     const int NC = (int)((p->K + P - 2) / P) + 1;
     T.a.NC = NC;

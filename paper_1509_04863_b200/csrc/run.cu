@@ -1,6 +1,7 @@
 // run.cu -- tm_run (the whole of Algorithm 1 FTM(), on
 // device buffers) and tm_run_host (the same on host buffers, with the
 // host->device copies of chunk i+1 overlapped with the compute of chunk i).
+#include <algorithm>
 #include <cstdlib>
 
 #include "tm_internal.cuh"
@@ -123,7 +124,7 @@ static int run_overlap_tc(const tm_plan_s *pc, const void *x, int64_t ldx, const
         if (rc) return rc;
         cudaEventRecord(p->aux_ev[0][c], s);
         cudaStreamWaitEvent(s2, p->aux_ev[0][c], 0);
-        rc = tm_tc_correlate(p, y1c, y2c, (const int8_t *)t + b0 * p->K, p->K, nb, nullptr, nullptr, nullptr,
+        rc = tm_tc_correlate(p, y1c, y2c, p->len_y1, p->len_y2, (const int8_t *)t + b0 * p->K, p->K, nb, nullptr, nullptr, nullptr,
                              residues ? residues + 2 * b0 : nullptr, k + b0, s2);
         if (rc) return rc;
     }
@@ -295,4 +296,32 @@ extern "C" __attribute__((visibility("default"))) int tm_run_host(tm_plan p, con
     for (int i = 0; i < 2; ++i) { cudaEventDestroy(copied[i]); cudaEventDestroy(freed[i]); }
     cudaStreamDestroy(sc);
     return rc;
+}
+
+// copy one folded signal into every row of a batch (the non-tensor-core engines
+// of tm_correlate_many read y with a per-pair stride)
+__global__ void broadcast_rows(const uint32_t *__restrict__ src, int64_t n, int64_t ld, int64_t rows,
+                               uint32_t *__restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * rows; i += (int64_t)gridDim.x * blockDim.x)
+        dst[(i / n) * ld + i % n] = src[i % n];
+}
+
+extern "C" __attribute__((visibility("default"))) int tm_correlate_many(tm_plan p, const void *y1, const void *y2,
+                                                                        const void *t, int64_t n_templates,
+                                                                        int32_t *residues, int64_t *k, void *ws,
+                                                                        void *stream) {
+    if (!p) { tm_set_error("tm_correlate_many: NULL plan"); return TM_EINVAL; }
+    if (n_templates < 0) { tm_set_error("tm_correlate_many: n_templates < 0"); return TM_EINVAL; }
+    if (n_templates == 0) return TM_OK;
+    if (!y1 || !y2 || !t || !k || !ws) { tm_set_error("tm_correlate_many: NULL pointer"); return TM_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p->use_tc)  // y read with stride 0: every template's CTAs stage the same folded signal
+        return tm_tc_any_ld(p, y1, y2, 0, 0, t, p->K, n_templates, nullptr, nullptr, nullptr, residues, k, ws, s);
+    RunWs W = run_ws(p, n_templates, ws);
+    const unsigned g = (unsigned)std::min<int64_t>((n_templates * (p->len_y1 + p->len_y2) + 255) / 256, 65535 * 4);
+    broadcast_rows<<<g, 256, 0, s>>>((const uint32_t *)y1, p->len_y1, p->len_y1, n_templates, (uint32_t *)W.y1);
+    TM_CHECK_LAUNCH("tm_correlate_many: broadcast");
+    broadcast_rows<<<g, 256, 0, s>>>((const uint32_t *)y2, p->len_y2, p->len_y2, n_templates, (uint32_t *)W.y2);
+    TM_CHECK_LAUNCH("tm_correlate_many: broadcast");
+    return tm_correlate_match(p, W.y1, W.y2, t, n_templates, residues, k, ws, stream);
 }

@@ -139,17 +139,21 @@ int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const 
                       int64_t batch, void *r1, void *r2, int32_t *resid, void *tile_scratch,
                       void *gntt_scratch, cudaStream_t s, void *tc_ws = nullptr);
 void tm_tc_plan(tm_plan_s *p);
-int tm_tc_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt, int64_t batch,
-                    void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k, cudaStream_t s);
+int tm_tc_correlate(const tm_plan_s *p, const void *y1, const void *y2, int64_t ldy1, int64_t ldy2, const void *t,
+                    int64_t ldt, int64_t batch, void *r1, void *r2, int32_t *resid, int32_t *residues_out,
+                    int64_t *k, cudaStream_t s);
 int tm_tc_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf, cudaStream_t s);
 void tm_tc_tiled_plan(tm_plan_s *p);
 size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch);
-int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt,
-                          int64_t batch, void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k,
-                          void *ws, cudaStream_t s);
+int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, int64_t ldy1, int64_t ldy2,
+                          const void *t, int64_t ldt, int64_t batch, void *r1, void *r2, int32_t *resid,
+                          int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s);
 // the tensor-core engine for a batch: one CTA per pair (corr_tc.cu) or tiled
 // over CTAs (few pairs / long templates); ws = the whole tm_workspace_bytes area
 int tm_tc_any(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt, int64_t batch,
               void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s);
+int tm_tc_any_ld(const tm_plan_s *p, const void *y1, const void *y2, int64_t ldy1, int64_t ldy2, const void *t,
+                 int64_t ldt, int64_t batch, void *r1, void *r2, int32_t *resid, int32_t *residues_out, int64_t *k,
+                 void *ws, cudaStream_t s);
 int tm_crt_impl(const tm_plan_s *p, const int32_t *resid, int64_t batch, int32_t *residues_out,
                 int64_t *k, cudaStream_t s);

@@ -480,3 +480,37 @@ def test_table2_noise_trend_on_gpu(tm):
     assert rates[20] >= 0.95
     assert rates[20] >= rates[1] >= rates[-6]
     assert rates[-6] <= 0.3
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_correlate_many_templates(tm, engine):
+    """tm_correlate_many (the section 3.5 shape P:228-244): one folded
+    signal against 24 templates (16 windows of it at spread shifts with 10%
+    flips, 8 unrelated codes); every template's residues and k equal the
+    oracle's steps 4-9 on the oracle's fold of that signal."""
+    N, K, T = 2 ** 20, 4096, 24
+    plan = tm.Plan(N, K, seed=8, engine=engine)
+    rng = np.random.default_rng(808)
+    x_h = (1 - 2 * rng.integers(0, 2, N)).astype(np.int8)
+    shifts = rng.integers(0, N, 16)
+    t_h = np.empty((T, K), np.int8)
+    for i in range(16):
+        w = x_h[(shifts[i] + np.arange(K)) % N].copy()
+        flip = rng.random(K) < 0.1
+        w[flip] = -w[flip]
+        t_h[i] = w
+    t_h[16:] = (1 - 2 * rng.integers(0, 2, (T - 16, K))).astype(np.int8)
+    x = up(x_h[None, :])
+    y1, y2 = plan.fold(x)
+    res, k = plan.correlate_many(y1[0], y2[0], up(t_h))
+    torch.cuda.synchronize()
+    res, k = res.cpu().numpy(), k.cpu().numpy()
+    y1o, y2o = oracle.fold(x_h, plan.M1, K), oracle.fold(x_h, plan.M2, K)
+    hits = 0
+    for i in range(T):
+        m1 = oracle.argmax(oracle.correlate(y1o, plan.M1, t_h[i]))
+        m2 = oracle.argmax(oracle.correlate(y2o, plan.M2, t_h[i]))
+        assert tuple(res[i]) == (m1, m2), i
+        assert k[i] == oracle.resolve(m1, plan.M1, m2, plan.M2, N), i
+        hits += i < 16 and k[i] == shifts[i]
+    print(f"correlate_many: {hits}/16 planted shifts recovered")
