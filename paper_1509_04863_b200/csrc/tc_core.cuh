@@ -195,6 +195,24 @@ __device__ __forceinline__ void epi_chunk(const TcArgs &a, uint32_t taddr, int a
 #pragma unroll
     for (int l = 0; l < NL; ++l) tmem_ld16(taddr + 2 * a.NMC * l + 2 * a0, v + 16 * l);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if constexpr (NL == 1) {
+        // common case (one limb, no r output, whole chunk inside both moduli): the
+        // thread's outputs of a modulus rise in k with i, so a strict int32 > keeps
+        // the lowest index; one merge per chunk
+        if (!a.r[0] && !a.r[1] && a0 + 8 <= a.NA[0] && a0 + 8 <= a.NA[1] &&
+            (int64_t)P * (a0 + 8) <= a.M[0] && (int64_t)P * (a0 + 8) <= a.M[1]) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                int32_t best = v[j];
+                int bi = 0;
+#pragma unroll
+                for (int i = 1; i < 8; ++i)
+                    if (v[2 * i + j] > best) { best = v[2 * i + j]; bi = i; }
+                amax(bv[j], bk[j], (int64_t)best, (int64_t)P * (a0 + bi) + brow);
+            }
+            return;
+        }
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
 #pragma unroll
