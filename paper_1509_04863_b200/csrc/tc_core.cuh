@@ -136,7 +136,7 @@ __device__ __forceinline__ int32_t limb(int32_t v, int l, int nl) {
 // this thread's range flags (bit 0: some |y| needs 2 limbs, bit 1: 3, bit 2: 4).
 __device__ __forceinline__ int stage_yw(const TcArgs &a, uint8_t *B, int64_t b, int l, int nl, int64_t s_begin,
                                         int nrows, int warp, int lane) {
-    int flags = 0;
+    uint32_t mag = 0;
     const uint32_t lbo = 32u * nrows;  // bytes per chunk column h: 2 nrows rows of 16 B
     const int h = lane >> 2, wq = lane & 3;
     constexpr int RB = TC_RB;             // block rows in flight per warp
@@ -168,17 +168,18 @@ __device__ __forceinline__ int stage_yw(const TcArgs &a, uint8_t *B, int64_t b, 
                 const int s = s0 + u * NW;
                 if (s >= nrows) break;
                 const int32_t v0 = v[u][0], v1 = v[u][1], v2 = v[u][2], v3 = v[u][3];
-                const uint32_t o1 = (uint32_t)(v0 + 128) | (uint32_t)(v1 + 128) | (uint32_t)(v2 + 128) | (uint32_t)(v3 + 128);
-                const uint32_t o2 = (uint32_t)(v0 + 2048) | (uint32_t)(v1 + 2048) | (uint32_t)(v2 + 2048) | (uint32_t)(v3 + 2048);
-                const uint32_t o3 = (uint32_t)(v0 + 32768) | (uint32_t)(v1 + 32768) | (uint32_t)(v2 + 32768) | (uint32_t)(v3 + 32768);
-                flags |= (o1 > 255u ? 1 : 0) | (o2 > 4095u ? 2 : 0) | (o3 > 65535u ? 4 : 0);
+                // v ^ (v >> 31) is v (v >= 0) or -v - 1: below 2^b iff v fits b+1 signed
+                // bits, and an OR of values below 2^b stays below 2^b (thresholds 2^7,
+                // 2^11, 2^15 are the 1-, 2-, 3-limb limits)
+                mag |= (uint32_t)(v0 ^ (v0 >> 31)) | (uint32_t)(v1 ^ (v1 >> 31)) | (uint32_t)(v2 ^ (v2 >> 31)) |
+                       (uint32_t)(v3 ^ (v3 >> 31));
                 *reinterpret_cast<uint32_t *>(B + lbo * h + 16 * (2 * s + j) + 4 * wq) =
                     nl == 1 ? pack4(v0, v1, v2, v3)
                             : pack4(limb(v0, l, nl), limb(v1, l, nl), limb(v2, l, nl), limb(v3, l, nl));
             }
         }
     }
-    return flags;
+    return (mag > 127u ? 1 : 0) | (mag > 2047u ? 2 : 0) | (mag > 32767u ? 4 : 0);
 }
 
 __device__ __forceinline__ int stage_y(const TcArgs &a, uint8_t *B, int64_t b, int l, int nl, int warp, int lane) {
