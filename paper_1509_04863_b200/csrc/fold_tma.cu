@@ -766,9 +766,15 @@ int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void 
     a.tc_off = (uint32_t)base;
     const size_t sm = base + p->tc_smem;
     if (sm > 227 * 1024) return TM_EUNSUPPORTED;
+    // whole pairs are equal-sized items: the static round-robin schedule balances
+    // them as well as a dynamic counter and needs no per-launch reset
+#ifdef TM_FUSED_DYNAMIC
     cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
     if (e != cudaSuccess) return tm_cuda_status(e, "tm_run: counter reset");
     a.work_counter = counter;
+#else
+    (void)counter;
+#endif
     const int64_t grid = batch < p->num_sms ? batch : p->num_sms;
     if (nst == 4) return launch<4, 0, 1, true>(a, grid, sm, s);
     return launch<3, 0, 1, true>(a, grid, sm, s);
