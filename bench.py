@@ -43,6 +43,7 @@ WORKLOADS = {
                  desc="cfg5: one signal N=2^31 (+-1 int8, 2 GiB), K=65536, 5% flips, split over the GPUs; "
                       "partial folds summed by one NCCL all-reduce"),
 }
+EV_EVERY = 10  # timed steps between two stage-event samples
 METRIC = "signal Gsamples/s matched (1/2/4/8 B200) and % of HBM roofline; match success rate"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
@@ -57,6 +58,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle cpu_baseline budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stage-events", action="store_true", help="A/B only: no per-step stage events")
     return ap.parse_args()
 
 
@@ -222,9 +224,13 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, stage events per step (tm_profile_events)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    for e5 in ev:          # torch creates the CUDA event lazily on first record
+    # ---- timed region: K steps.  Stage events (tm_profile_events) on every
+    # EV_EVERY-th step only: each event record costs ~2.7 us of GPU time.
+    path = plan.run_path(B)
+    nev = 2 if path == 2 else 5   # fused: before / after the one kernel
+    ev_steps = [i for i in range(args.steps) if i % EV_EVERY == 0] if not args.no_stage_events else []
+    ev = {i: [torch.cuda.Event(enable_timing=True) for _ in range(nev)] for i in ev_steps}
+    for e5 in ev.values():  # torch creates the CUDA event lazily on first record
         for e in e5:
             e.record(stream)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -232,12 +238,18 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = tm.launch_count()
+    keep = None
     with ClockSampler(local) as clocks:
         start.record(stream)
+        h0 = time.perf_counter()
         for i in range(args.steps):
-            keep = tm.profile_events(ev[i])
-            step()
-        tm.profile_events(None)
+            if i in ev:
+                keep = tm.profile_events(ev[i])
+                step()
+                tm.profile_events(None)
+            else:
+                step()
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
         stop.record(stream)
         torch.cuda.synchronize()
     launches = tm.launch_count() - launches0
@@ -245,9 +257,9 @@ def main():
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(stop)
-    stage_ms = [[e[i].elapsed_time(e[i + 1]) for i in range(4)] for e in ev]
+    stage_ms = [[e[i].elapsed_time(e[i + 1]) for i in range(nev - 1)] for e in ev.values()] or [[0.0] * (nev - 1)]
     fold_ms = statistics.mean(s[0] for s in stage_ms)
-    stage_mean = [statistics.mean(s[i] for s in stage_ms) for i in range(4)]
+    stage_mean = [statistics.mean(s[i] for s in stage_ms) for i in range(nev - 1)]
     t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
@@ -296,7 +308,6 @@ def main():
 
     bx = x.element_size()
     peak, peak_src = measured_peaks()
-    path = plan.run_path(B)
     if path == 2:
         # fused kernel = the whole step: algorithmic bytes = x and t read once, k and
         # residues written once (y never needs to leave the chip)
@@ -335,8 +346,11 @@ def main():
                      "algorithmic_bytes_per_launch": fold_bytes, "peak_source": peak_src,
                      "kernel_ms": fold_ms},
         "run_path": tm.RUN_PATHS.get(path, str(path)),
-        "stage_ms": {"fold": stage_mean[0], "fold_template": stage_mean[1], "correlate_argmax": stage_mean[2],
-                     "crt": stage_mean[3]},
+        "stage_ms": ({"fused_kernel": stage_mean[0]} if nev == 2 else
+                     {"fold": stage_mean[0], "fold_template": stage_mean[1], "correlate_argmax": stage_mean[2],
+                      "crt": stage_mean[3]}),
+        "stage_events": f"on {len(ev)} of {args.steps} timed steps (every {EV_EVERY}th)",
+        "host_enqueue_ms_per_step": host_ms,
         "step_hbm_frac": (B * N * bx / (ms_max / args.steps * 1e-3) / 1e9) / peak,
         "success_rate": success,
         "cpu_baseline": cpu,

@@ -21,7 +21,7 @@ extern "C" __attribute__((visibility("default"))) uint64_t tm_launch_count(void)
 }
 
 extern "C" __attribute__((visibility("default"))) int tm_profile_events(void **events, int n) {
-    if (events && n < 5) { tm_set_error("tm_profile_events: need >= 5 events"); return TM_EINVAL; }
+    if (events && n < 2) { tm_set_error("tm_profile_events: need >= 2 events"); return TM_EINVAL; }
     g_prof_ev = events;
     g_prof_n = events ? n : 0;
     return TM_OK;
