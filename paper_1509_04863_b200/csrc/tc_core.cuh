@@ -381,10 +381,27 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
     for (int q = 0; q < nleft0 + nleft1; ++q) {
         const int j = q < nleft0 ? 0 : 1;
         const int64_t k = (int64_t)P * a.NA[j] + (j ? q - nleft0 : q);
-        const int32_t *yr = a.y[j] + b * a.ldy[j] + k;
         int64_t s = 0;
+        if (nl == 1 && (k & 15) == 0 && k + a.K <= (int64_t)P * a.R) {
+            // y_j is in B as int8 (one limb): 16-byte chunks of y_j[k + 16c ..] and of
+            // the template, 4 dp4a per chunk, no global loads
+            const uint32_t lbo = 32u * a.R;
+            int32_t s32 = 0;
+            for (int c = tid; c < (a.K + 15) / 16; c += NTHR) {
+                const int64_t m0 = k + 16 * c;
+                const uint4 yv = *reinterpret_cast<const uint4 *>(B + lbo * ((m0 >> 4) & 7) + 16 * (2 * (m0 >> 7) + j));
+                const uint4 tv = *reinterpret_cast<const uint4 *>(tp + 128 + 16 * c);
+                s32 = __dp4a((int)yv.x, (int)tv.x, s32);
+                s32 = __dp4a((int)yv.y, (int)tv.y, s32);
+                s32 = __dp4a((int)yv.z, (int)tv.z, s32);
+                s32 = __dp4a((int)yv.w, (int)tv.w, s32);
+            }
+            s = s32;
+        } else {
+            const int32_t *yr = a.y[j] + b * a.ldy[j] + k;
 #pragma unroll 8
-        for (int i = tid; i < a.K; i += NTHR) s += (int64_t)(int8_t)tp[128 + i] * yr[i];
+            for (int i = tid; i < a.K; i += NTHR) s += (int64_t)(int8_t)tp[128 + i] * yr[i];
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) lp[warp * 2 * MAXLEFT + q] = s;
