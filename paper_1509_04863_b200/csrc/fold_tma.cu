@@ -126,7 +126,10 @@ __device__ __forceinline__ Item decode(const TmaArgs &a, int64_t item) {
     return it;
 }
 
-constexpr int NE = 4;  // epilogue warps
+#ifndef TM_NE
+#define TM_NE 8
+#endif
+constexpr int NE = TM_NE;  // epilogue warps
 
 // comb(d): total count of unwrapped diagonal d (relative to the CTA's first column)
 // from the warp-private arrays of one buffer: only the <= 3 warps whose strip
