@@ -636,10 +636,13 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
         cudaError_t e = cudaMemsetAsync(a.counts, 0, (size_t)batch * (p->M1 + p->M2) * 4, s);
         if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: memset");
     }
-    const size_t smem = smem_bytes(a, 4, 0);
+#ifndef TM_FOLD_NST
+#define TM_FOLD_NST 4
+#endif
+    const size_t smem = smem_bytes(a, TM_FOLD_NST, 0);
     if (smem > 227 * 1024) return TM_EUNSUPPORTED;
     const int64_t grid = a.n_items < p->num_sms ? a.n_items : p->num_sms;
-    return launch<4, 0>(a, grid, smem, s);
+    return launch<TM_FOLD_NST, 0>(a, grid, smem, s);
 }
 
 // Overlap mode of tm_run: the owner-mode fold of a chunk of pairs with dynamic item
