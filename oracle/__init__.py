@@ -77,6 +77,14 @@ def lib():
         L.or_phi_dense.argtypes = [_i64, _i64, _i64, _p]
         L.or_thm1_That_y_i64.restype = None
         L.or_thm1_That_y_i64.argtypes = [_p, _i64, _p, _i64, _p]
+        for n in ("or_block_fold_i8", "or_block_fold_f32"):
+            getattr(L, n).restype = None
+            getattr(L, n).argtypes = [_p, _i64, _i64, _p, _p]
+        L.or_block_correlate_f64.restype = None
+        L.or_block_correlate_f64.argtypes = [_p, _i64, _p, _i64, _p]
+        for n in ("or_ftm_block_i8", "or_ftm_block_f32"):
+            getattr(L, n).restype = _i64
+            getattr(L, n).argtypes = [_p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p]
         _lib = L
     return _lib
 
@@ -258,3 +266,56 @@ def thm1_That_y(y: np.ndarray, M: int, t: np.ndarray) -> np.ndarray:
     out = np.zeros(M, np.int64)
     lib().or_thm1_That_y_i64(_ptr(y), M, _ptr(t), t.shape[0], _ptr(out))
     return out
+
+
+# --------------------------------------------------------------------------
+# Strategy 2: the Block sampling matrix of Theorem 2
+# --------------------------------------------------------------------------
+def block_fold(x: np.ndarray, M: int, phi: np.ndarray | None = None) -> np.ndarray:
+    """y = [Phi_M ... Phi_M] x_pad (x zero-padded to a multiple of M),
+    Phi_M = circ(phi); phi None = Eq. (3)'s r on one block (Phi_M = I)."""
+    x = _as_input(x)
+    N = x.shape[0]
+    if _is_int(x):
+        y = np.zeros(M, np.int64)
+        ph = None if phi is None else np.ascontiguousarray(phi, np.int8)
+        lib().or_block_fold_i8(_ptr(x), N, M, None if ph is None else _ptr(ph), _ptr(y))
+    else:
+        y = np.zeros(M, np.float64)
+        ph = None if phi is None else np.ascontiguousarray(phi, np.float32)
+        lib().or_block_fold_f32(_ptr(x), N, M, None if ph is None else _ptr(ph), _ptr(y))
+    return y
+
+
+def block_correlate(y: np.ndarray, M: int, t: np.ndarray) -> np.ndarray:
+    """(T^ y)_i, T^ = circ([t 0_{M-K}]) (Theorem 2): cyclic correlation."""
+    t = _as_input(t)
+    if _is_int(t):
+        return thm1_That_y(np.ascontiguousarray(y, np.int64), M, t)
+    y = np.ascontiguousarray(y[:M], np.float64)
+    out = np.zeros(M, np.float64)
+    lib().or_block_correlate_f64(_ptr(y), M, _ptr(t), t.shape[0], _ptr(out))
+    return out
+
+
+def ftm_block(x: np.ndarray, t: np.ndarray, M: int = 0, want_vectors: bool = True) -> dict:
+    """FTM() with strategy 2 (Block Phi, Phi_M = I): y_j has M_j entries and
+    the correlation is cyclic (T^ = circ(t)); steps 7-9 as in ftm()."""
+    x = _as_input(x)
+    t = _as_input(t)
+    N, K = x.shape[0], t.shape[0]
+    M1, M2 = moduli(N, K, M)
+    res = np.zeros(2, np.int64)
+    if _is_int(x):
+        assert _is_int(t)
+        dt, fn = np.int64, lib().or_ftm_block_i8
+    else:
+        assert t.dtype == np.float32
+        dt, fn = np.float64, lib().or_ftm_block_f32
+    if not want_vectors:
+        k = fn(_ptr(x), N, _ptr(t), K, M, _ptr(res), None, None, None, None)
+        return dict(k=k, residues=(int(res[0]), int(res[1])), M1=M1, M2=M2)
+    y1 = np.zeros(M1, dt); y2 = np.zeros(M2, dt)
+    r1 = np.zeros(M1, dt); r2 = np.zeros(M2, dt)
+    k = fn(_ptr(x), N, _ptr(t), K, M, _ptr(res), _ptr(y1), _ptr(y2), _ptr(r1), _ptr(r2))
+    return dict(k=k, residues=(int(res[0]), int(res[1])), M1=M1, M2=M2, y1=y1, y2=y2, r1=r1, r2=r2)

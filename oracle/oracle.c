@@ -22,6 +22,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+void or_thm1_That_y_i64(const int64_t *y, int64_t M, const int8_t *t, int64_t K, int64_t *out);
+
 /* ------------------------------------------------------------------ */
 /* helpers                                                              */
 /* ------------------------------------------------------------------ */
@@ -289,6 +291,98 @@ int64_t or_ftm_f32(const float *x, int64_t N, const float *t, int64_t K, int64_t
     if (residues) { residues[0] = m1; residues[1] = m2; }
     if (y1o) memcpy(y1o, y1, sizeof(double) * (M1 + K));
     if (y2o) memcpy(y2o, y2, sizeof(double) * (M2 + K));
+    if (r1o) memcpy(r1o, r1, sizeof(double) * M1);
+    if (r2o) memcpy(r2o, r2, sizeof(double) * M2);
+    free(y1); free(y2); free(r1); free(r2);
+    return k;
+}
+
+/* ------------------------------------------------------------------ */
+/* Strategy 2 (Theorem 2): the Block sampling       */
+/* matrix Phi = [Phi_M Phi_M ... Phi_M] (ceil(N/M) blocks), Phi_M an M x M */
+/* circulant, applied to x zero-padded to ceil(N/M)*M samples ("we can    */
+/* pad zeros into the tail of x until M divides N"):               */
+/*     y_j = sum_{c < N} Phi_M[j][c mod M] x_c,   j = 0 .. M-1,            */
+/*     Phi_M = circ(phi): Phi_M[j][l] = phi[(l - j) mod M].      */
+/* phi == NULL is Eq. (3)'s sampling vector r restricted to one block      */
+/* (r_k = 1 iff k mod M == 0), i.e. Phi_M = I, and the literal      */
+/* sum becomes y_j = sum_{i : j + iM < N} x_{j + iM} (i ascending).        */
+/* A non-null phi (a seeded circulant) is the general Theorem 2 operator;  */
+/* it serves the dense Theorem 2 pin only (it scrambles the peak of Eq. 5, */
+/* which needs Phi_M = I -- reading C21).                                  */
+/* ------------------------------------------------------------------ */
+void or_block_fold_i8(const int8_t *x, int64_t N, int64_t M, const int8_t *phi, int64_t *y) {
+    for (int64_t j = 0; j < M; ++j) {
+        int64_t s = 0;
+        if (!phi) {
+            for (int64_t p = j; p < N; p += M) s += (int64_t)x[p];
+        } else {
+            for (int64_t c = 0; c < N; ++c) s += (int64_t)phi[or_mod(c % M - j, M)] * (int64_t)x[c];
+        }
+        y[j] = s;
+    }
+}
+
+void or_block_fold_f32(const float *x, int64_t N, int64_t M, const float *phi, double *y) {
+    for (int64_t j = 0; j < M; ++j) {
+        double s = 0.0;
+        if (!phi) {
+            for (int64_t p = j; p < N; p += M) s += (double)x[p];
+        } else {
+            for (int64_t c = 0; c < N; ++c) s += (double)phi[or_mod(c % M - j, M)] * (double)x[c];
+        }
+        y[j] = s;
+    }
+}
+
+/* Theorem 2's T^ = circ(t) with t zero-padded to M:        */
+/*     (T^ y)_i = sum_{u=0}^{K-1} t_u y_{(i+u) mod M},  i = 0 .. M-1.       */
+void or_block_correlate_f64(const double *y, int64_t M, const float *t, int64_t K, double *out) {
+    for (int64_t i = 0; i < M; ++i) {
+        double acc = 0.0;
+        for (int64_t u = 0; u < K; ++u) acc += (double)t[u] * y[or_mod(i + u, M)];
+        out[i] = acc;
+    }
+}
+
+/* FTM() with strategy 2 (Phi_M = I): steps 2, 3 (Block fold), 4-6 (T^ y,  */
+/* cyclic), 7, 8-9 (or_resolve).  Outputs as or_ftm_*; y has M entries.    */
+int64_t or_ftm_block_i8(const int8_t *x, int64_t N, const int8_t *t, int64_t K, int64_t M,
+                        int64_t *residues, int64_t *y1o, int64_t *y2o, int64_t *r1o, int64_t *r2o) {
+    int64_t M1, M2;
+    if (or_moduli(N, K, M, &M1, &M2) != 0) return -3;
+    int64_t *y1 = (int64_t *)malloc(sizeof(int64_t) * M1), *y2 = (int64_t *)malloc(sizeof(int64_t) * M2);
+    int64_t *r1 = (int64_t *)malloc(sizeof(int64_t) * M1), *r2 = (int64_t *)malloc(sizeof(int64_t) * M2);
+    or_block_fold_i8(x, N, M1, NULL, y1);
+    or_block_fold_i8(x, N, M2, NULL, y2);
+    or_thm1_That_y_i64(y1, M1, t, K, r1);
+    or_thm1_That_y_i64(y2, M2, t, K, r2);
+    int64_t m1 = or_argmax_i64(r1, M1), m2 = or_argmax_i64(r2, M2);
+    int64_t k = or_resolve(m1, M1, m2, M2, N, 0);
+    if (residues) { residues[0] = m1; residues[1] = m2; }
+    if (y1o) memcpy(y1o, y1, sizeof(int64_t) * M1);
+    if (y2o) memcpy(y2o, y2, sizeof(int64_t) * M2);
+    if (r1o) memcpy(r1o, r1, sizeof(int64_t) * M1);
+    if (r2o) memcpy(r2o, r2, sizeof(int64_t) * M2);
+    free(y1); free(y2); free(r1); free(r2);
+    return k;
+}
+
+int64_t or_ftm_block_f32(const float *x, int64_t N, const float *t, int64_t K, int64_t M,
+                         int64_t *residues, double *y1o, double *y2o, double *r1o, double *r2o) {
+    int64_t M1, M2;
+    if (or_moduli(N, K, M, &M1, &M2) != 0) return -3;
+    double *y1 = (double *)malloc(sizeof(double) * M1), *y2 = (double *)malloc(sizeof(double) * M2);
+    double *r1 = (double *)malloc(sizeof(double) * M1), *r2 = (double *)malloc(sizeof(double) * M2);
+    or_block_fold_f32(x, N, M1, NULL, y1);
+    or_block_fold_f32(x, N, M2, NULL, y2);
+    or_block_correlate_f64(y1, M1, t, K, r1);
+    or_block_correlate_f64(y2, M2, t, K, r2);
+    int64_t m1 = or_argmax_f64(r1, M1), m2 = or_argmax_f64(r2, M2);
+    int64_t k = or_resolve(m1, M1, m2, M2, N, 0);
+    if (residues) { residues[0] = m1; residues[1] = m2; }
+    if (y1o) memcpy(y1o, y1, sizeof(double) * M1);
+    if (y2o) memcpy(y2o, y2, sizeof(double) * M2);
     if (r1o) memcpy(r1o, r1, sizeof(double) * M1);
     if (r2o) memcpy(r2o, r2, sizeof(double) * M2);
     free(y1); free(y2); free(r1); free(r2);

@@ -409,3 +409,83 @@ def test_alias_repair_recovers_wrapped_peaks():
         lit_ok += a["k"] == k0
         rep_ok += b["k"] == k0
     assert alias > 10 and rep_ok == lit_ok + alias
+
+
+# ------------------------------------------------- strategy 2: Block Phi (Thm 2)
+def block_phi_dense(phi, N):
+    """Phi = [Phi_M ... Phi_M] with Phi_M = circ(phi), on x zero-padded
+    to a multiple of M: returns the M x N block of columns actually read."""
+    M = phi.shape[0]
+    nb = -(-N // M)
+    return np.hstack([circ(phi)] * nb)[:, :N]
+
+
+@pytest.mark.parametrize("N,M", [(64, 8), (60, 8), (96, 12), (50, 7)])
+def test_block_fold_equals_dense_theorem2_phi(N, M):
+    """y = Phi x for the Block Phi of Theorem 2 (seeded circulant Phi_M and the
+    paper's Phi_M = I), M | N and M not dividing N (zero padding)."""
+    rng = np.random.default_rng(N * 100 + M)
+    x = rand_pm1(rng, N)
+    phi = rng.integers(-3, 4, M).astype(np.int8)
+    np.testing.assert_array_equal(oracle.block_fold(x, M, phi), block_phi_dense(phi.astype(np.int64), N) @ x.astype(np.int64))
+    e0 = np.zeros(M, np.int64); e0[0] = 1
+    np.testing.assert_array_equal(oracle.block_fold(x, M), block_phi_dense(e0, N) @ x.astype(np.int64))
+    xf = rng.standard_normal(N).astype(np.float32)
+    phif = rng.standard_normal(M).astype(np.float32)
+    np.testing.assert_allclose(oracle.block_fold(xf, M, phif),
+                               block_phi_dense(phif.astype(np.float64), N) @ xf.astype(np.float64), rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("N,M,K", [(64, 8, 3), (96, 12, 5), (120, 10, 10)])
+def test_theorem2_identity(N, M, K):
+    """Theorem 2: T^ y = Phi T_bar x, T^ = circ([t 0_{M-K}]),
+    T_bar = blockdiag(T^, ..., T^), for a seeded circulant Phi_M (M | N).  The
+    oracle's cyclic correlation equals the dense T^ y."""
+    rng = np.random.default_rng(7 * N + K)
+    x = rand_pm1(rng, N)
+    t = rand_pm1(rng, K)
+    phi = rng.integers(-2, 3, M).astype(np.int8)
+    tp = np.zeros(M, np.int64); tp[:K] = t
+    That = circ(tp)
+    Tbar = np.kron(np.eye(N // M, dtype=np.int64), That)
+    Phi = block_phi_dense(phi.astype(np.int64), N)
+    y = oracle.block_fold(x, M, phi)
+    lhs = oracle.block_correlate(y, M, t)
+    np.testing.assert_array_equal(lhs, That @ y)
+    np.testing.assert_array_equal(lhs, Phi @ (Tbar @ x.astype(np.int64)))
+    tf = rng.standard_normal(K).astype(np.float32)
+    yf = rng.standard_normal(M)
+    tpf = np.zeros(M); tpf[:K] = tf
+    np.testing.assert_allclose(oracle.block_correlate(yf, M, tf), circ(tpf) @ yf, rtol=1e-12, atol=1e-12)
+
+
+def test_block_equals_strategy1_when_M_divides_N():
+    """With Phi_M = I and M | N the Block fold is y[0..M) of Eq. 2 (no sample is
+    counted twice: s = 0) and Eq. 2's extension is the cyclic copy, so the two
+    strategies give the same correlation for the first modulus."""
+    rng = np.random.default_rng(99)
+    N, K = 1024, 32
+    x = rand_pm1(rng, N)
+    t = rand_pm1(rng, K)
+    y = oracle.fold(x, K, K)
+    np.testing.assert_array_equal(oracle.block_fold(x, K), y[:K])
+    np.testing.assert_array_equal(oracle.block_correlate(oracle.block_fold(x, K), K, t), oracle.correlate(y, K, t))
+    b = oracle.ftm_block(x, t)
+    a = oracle.ftm(x, t)
+    assert b["residues"][0] == a["residues"][0]
+
+
+def test_block_strategy_recovers_every_isolated_window():
+    """x = 0 except a +-1 window equal to t at k0 (so (Tx)_k0 = K is the unique
+    maximum of the brute-force scores): the Block strategy returns k0 for every
+    k0 in [0, N - K], including the windows that cross a block boundary of
+    either modulus (the cyclic T^ of Theorem 2 reads them whole)."""
+    N, K = 256, 16
+    rng = np.random.default_rng(5)
+    t = rand_pm1(rng, K)
+    for k0 in range(0, N - K + 1):
+        x = np.zeros(N, np.int8)
+        x[k0:k0 + K] = t
+        s = brute_scores(x, t)
+        assert s[k0] == K and (s < K).sum() == N - 1
+        assert oracle.ftm_block(x, t, want_vectors=False)["k"] == k0
