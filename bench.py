@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle cpu_baseline budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strategy", type=int, default=1, choices=[1, 2],
+                    help="1: D_{M+K} (P:152, default); 2: Block Phi of Theorem 2 (P:159-177, TM_BLOCK)")
     ap.add_argument("--no-stage-events", action="store_true", help="A/B only: no per-step stage events")
     return ap.parse_args()
 
@@ -144,7 +146,7 @@ def cpu_info():
     return os.cpu_count(), model
 
 
-def oracle_rate(wl, budget_s: float, max_pairs: int | None = None):
+def oracle_rate(wl, budget_s: float, max_pairs: int | None = None, strategy: int = 1):
     """Time the CPU oracle (single thread, as it stands) on pairs of the same
     workload until the budget is spent.  Returns (Gsamples/s, pairs, seconds)."""
     import numpy as np
@@ -157,7 +159,7 @@ def oracle_rate(wl, budget_s: float, max_pairs: int | None = None):
     while spent < budget_s and (max_pairs is None or done < max_pairs):
         x, t, _ = tmgen.batch(wl["seed"], done, 1, N, K, wl["noise"], dtype=dt)
         t0 = time.perf_counter()
-        oracle.ftm(x[0], t[0], want_vectors=False)
+        (oracle.ftm_block if strategy == 2 else oracle.ftm)(x[0], t[0], want_vectors=False)
         spent += time.perf_counter() - t0
         done += 1
     return done * N / spent / 1e9, done, spent
@@ -172,8 +174,8 @@ def run_reference(args, wl):
     cores, model = cpu_info()
     # each step: one pair of the workload through the oracle (a bounded sample)
     if args.warmup:
-        oracle_rate(wl, float("inf"), max_pairs=min(args.warmup, 3))
-    rate, pairs, spent = oracle_rate(wl, float("inf"), max_pairs=max(args.steps, 1))
+        oracle_rate(wl, float("inf"), max_pairs=min(args.warmup, 3), strategy=args.strategy)
+    rate, pairs, spent = oracle_rate(wl, float("inf"), max_pairs=max(args.steps, 1), strategy=args.strategy)
     sample = f"{pairs} pair(s) of {wl['desc']} (one pair per step), host-generated by tmgen"
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "Gsamples/s", "n_gpus": args.gpus,
@@ -181,7 +183,7 @@ def run_reference(args, wl):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "i8" if wl["dtype"] == "int8" else "f64", "data": "synthetic",
         "config": {"workload": wl["desc"], "N": wl["N"], "K": wl["K"], "batch": wl["B"],
-                   "parallelism": "single CPU thread (oracle)"},
+                   "parallelism": "single CPU thread (oracle)", "strategy": args.strategy},
         "cpu_baseline": {"value": rate, "unit": "Gsamples/s", "cores": 1, "kind": "oracle", "sample": sample,
                          "host_cpus": cores, "cpu_model": model},
         "e2e": {"value": rate, "unit": "Gsamples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -208,7 +210,7 @@ def main():
     if wl.get("single"):
         return run_single_signal(args, wl, rank, world, local, dev)
     N, K, B = wl["N"], wl["K"], wl["B"]
-    plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"])
+    plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"], block=args.strategy == 2)
     stream = torch.cuda.current_stream()
     # inputs resident in HBM: this rank's pairs [rank*B, rank*B + B)
     x, t, k0 = plan.generate(rank * B, B, wl["noise"], device=dev)
@@ -328,7 +330,7 @@ def main():
     cpu = None
     if not args.no_cpu_baseline:
         cores, model = cpu_info()
-        rate, pairs, spent = oracle_rate(wl, args.cpu_seconds)
+        rate, pairs, spent = oracle_rate(wl, args.cpu_seconds, strategy=args.strategy)
         cpu = {"value": rate, "unit": "Gsamples/s", "cores": 1, "kind": "oracle",
                "sample": f"{pairs} pair(s) of {wl['desc']}, {spent:.1f} s single-threaded",
                "host_cpus": cores, "cpu_model": model}
@@ -340,6 +342,7 @@ def main():
         "data": "synthetic (seeded counter-based generator, inputs generated on device)",
         "config": {"workload": wl["desc"], "N": N, "K": K, "batch_per_gpu": B, "M1": plan.M1, "M2": plan.M2,
                    "parallelism": f"dp{world} (independent pairs)",
+                   "strategy": "2 (Block Phi, Theorem 2)" if args.strategy == 2 else "1 (D_{M+K}, P:152)",
                    "l2": f"no flush: per-step input {B * N * bx / 2**30:.2f} GiB > 126 MB L2"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": kernel,
@@ -373,7 +376,7 @@ def run_single_signal(args, wl, rank, world, local, dev):
     from paper_1509_04863_b200 import dist as tmdist
 
     N, K = wl["N"], wl["K"]
-    plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"])
+    plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"], block=args.strategy == 2)
     stream = torch.cuda.current_stream()
     off, ln = tmdist.signal_chunks(N, plan.M1, world)[rank]
     x, t, k0 = plan.generate(0, 1, wl["noise"], offset=off, length=ln, device=dev)

@@ -64,6 +64,16 @@ enum {
                                (a true peak m < s2 that the mod-N wrap of Eq. 2
                                moved into bin m + M2 - s2).  Default: off, the
                                literal unreduced sets of P:104-105 (C9). */
+#define TM_BLOCK 16u    /* strategy 2 of P:150-151: the Block sampling matrix
+                           Phi = [Phi_M ... Phi_M] of Theorem 2 with
+                           Eq. 3's Phi_M = I, on x zero-padded to a multiple of
+                           M_j: y_j[k] = sum_{p < N, p = k mod M_j} x[p]
+                           (no sample counted twice), and the correlation is
+                           cyclic, (T^ y)_k = sum_i t_i y[(k+i) mod M_j].  The
+                           y buffers keep their M_j + K entries; the tail is the
+                           cyclic copy y[M_j + c] = y[c].  Exclusive with
+                           TM_ALIAS_REPAIR (no wrap alias exists).  Default:
+                           strategy 1 (D_{M+K}). */
 #define TM_CORR_TC 4u   /* TM_I8 correlation engine: int8 tensor cores
                            (tcgen05.mma kind::i8, exact int32 accumulation of
                            4-bit limbs of y); TM_EUNSUPPORTED if the plan is not

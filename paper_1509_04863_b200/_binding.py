@@ -11,6 +11,7 @@ TM_I8, TM_F32 = 0, 1
 TM_BINARY = 1
 TM_CORR_NTT, TM_CORR_TC = 2, 4
 TM_ALIAS_REPAIR = 8
+TM_BLOCK = 16
 _ENGINES = {None: 0, "auto": 0, "ntt": TM_CORR_NTT, "tc": TM_CORR_TC}
 TM_OK, TM_EINVAL, TM_EUNSUPPORTED, TM_ECUDA = 0, 1, 2, 3
 
@@ -142,10 +143,11 @@ def _ld(x):
 
 class Plan:
     """tm_plan: Alg. 1 step 2 (M1 = M or K, M2 = M1 + 1).  dtype is "int8" or "float32".
-    engine (int8 only): None/"auto" (tensor cores when eligible), "ntt" or "tc"."""
+    engine (int8 only): None/"auto" (tensor cores when eligible), "ntt" or "tc".
+    block: strategy 2 (Theorem 2's Block Phi, TM_BLOCK) instead of strategy 1."""
 
     def __init__(self, N: int, K: int, M: int = 0, seed: int = 0, dtype: str = "int8", binary: bool = True,
-                 engine: str | None = None, alias_repair: bool = False):
+                 engine: str | None = None, alias_repair: bool = False, block: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1509_04863_b200.Plan needs a CUDA device (no CPU fallback)")
@@ -155,6 +157,8 @@ class Plan:
             flags |= _ENGINES[engine]
         if alias_repair:
             flags |= TM_ALIAS_REPAIR
+        if block:
+            flags |= TM_BLOCK
         h = _p()
         _check(lib().tm_plan_create(ctypes.byref(h), N, K, M, seed, self.dtype, flags), "tm_plan_create")
         self._h = h

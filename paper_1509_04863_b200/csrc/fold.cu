@@ -38,7 +38,7 @@ namespace {
 template <typename T, typename Acc>
 __global__ void fold_general(const T *__restrict__ x, int64_t ldx, int64_t N, int64_t offset,
                              int64_t len, int64_t M1, int64_t M2, int64_t K, int64_t q1, int64_t q2,
-                             Acc *__restrict__ y1, Acc *__restrict__ y2, int accumulate) {
+                             Acc *__restrict__ y1, Acc *__restrict__ y2, int accumulate, int block) {
     const int j = blockIdx.z;  // 0: modulus M1, 1: modulus M2
     const int64_t M = j ? M2 : M1, q = j ? q2 : q1;
     Acc *y = (j ? y2 : y1) + (int64_t)blockIdx.y * (M + K);
@@ -46,6 +46,14 @@ __global__ void fold_general(const T *__restrict__ x, int64_t ldx, int64_t N, in
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M + K;
          k += (int64_t)gridDim.x * blockDim.x) {
         Acc acc = 0;
+        if (block) {  // strategy 2: x zero-padded, no wrap; y[M + c] = y[c] (K <= M)
+            for (int64_t p = k < M ? k : k - M; p < N; p += M) {
+                const int64_t rel = p - offset;
+                if (rel >= 0 && rel < len) acc += (Acc)xb[rel];
+            }
+            if (accumulate) y[k] += acc; else y[k] = acc;
+            continue;
+        }
         int64_t p = k % N;
         for (int64_t i = 0; i < q; ++i) {
             int64_t rel = p - offset;
@@ -245,7 +253,7 @@ __global__ void __launch_bounds__(PM_WARPS * 32, 2) fold_pm1(PmArgs a) {
 __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t N, int64_t offset,
                               int64_t len, int64_t M1, int64_t M2, int64_t K, int64_t q2,
                               int64_t row0, int64_t rows, const int32_t *__restrict__ counts,
-                              int32_t *__restrict__ y1, int32_t *__restrict__ y2, int accumulate) {
+                              int32_t *__restrict__ y1, int32_t *__restrict__ y2, int accumulate, int block) {
     const int64_t b = blockIdx.y;
     const int8_t *xb = x + b * ldx;
     const int32_t *c1 = counts + b * (M1 + M2), *c2 = c1 + M1;
@@ -263,7 +271,7 @@ __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t
         int32_t n = (int32_t)rows - ((gs >= row0 && gs < row0 + rows) ? 1 : 0);
         int32_t v = n - c2[k];
         int64_t j = k - (M2 - q2);               // the mod-N wrap: bin M2 - q + j gets x[j]
-        if (j >= 0 && j < q2) v += xat(j);
+        if (!block && j >= 0 && j < q2) v += xat(j);
         return v;
     };
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M2 + K;
@@ -280,7 +288,7 @@ __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t
             int64_t c = k - M2;                  // extension: y2[M2+c] = y2[c] - x[c] + x[c+s2]
             int64_t e = c + s2;
             if (e >= N) e -= N;
-            v = base2(c) - xat(c) + xat(e);
+            v = block ? base2(c) : base2(c) - xat(c) + xat(e);  // strategy 2: cyclic copy
         }
         if (accumulate) o2[k] += v; else o2[k] = v;
     }
@@ -354,7 +362,7 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
             int64_t gx = (p->M2 + p->K + 255) / 256;
             fold_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(
                 (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, offset / p->M1, rows,
-                (const int32_t *)((char *)ws + L.fold_counts), (int32_t *)y1, (int32_t *)y2, accumulate);
+                (const int32_t *)((char *)ws + L.fold_counts), (int32_t *)y1, (int32_t *)y2, accumulate, p->block);
             TM_CHECK_LAUNCH("tm_fold: fold_finalize");
             return TM_OK;
         }
@@ -386,7 +394,7 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
         int64_t gx = (p->M2 + p->K + 255) / 256;
         fold_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(
             (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, a.row0, a.rows,
-            counts, (int32_t *)y1, (int32_t *)y2, accumulate);
+            counts, (int32_t *)y1, (int32_t *)y2, accumulate, p->block);
         TM_CHECK_LAUNCH("tm_fold: fold_finalize");
         return TM_OK;
     }
@@ -402,11 +410,11 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
     if (p->dtype == TM_I8) {
         fold_general<int8_t, int32_t><<<grid, 256, 0, s>>>((const int8_t *)x, ldx, p->N, offset, len,
                                                            p->M1, p->M2, p->K, p->q1, p->q2,
-                                                           (int32_t *)y1, (int32_t *)y2, accumulate);
+                                                           (int32_t *)y1, (int32_t *)y2, accumulate, p->block);
     } else {
         fold_general<float, float><<<grid, 256, 0, s>>>((const float *)x, ldx, p->N, offset, len,
                                                         p->M1, p->M2, p->K, p->q1, p->q2,
-                                                        (float *)y1, (float *)y2, accumulate);
+                                                        (float *)y1, (float *)y2, accumulate, p->block);
     }
     TM_CHECK_LAUNCH("tm_fold: fold_general");
     return TM_OK;

@@ -33,6 +33,7 @@ struct F32Args {
     int64_t M1, M2, K, N, q2;
     int64_t rows, row0;        // rows of the chunk [offset, offset + len) and its first global row
     int64_t R, nrc;            // rows per item, row chunks
+    int block;                 // TM_BLOCK: no wrap, cyclic extension
     int64_t n_strips, n_groups;
     float *parts;              // [batch][nrc][M1 + n_strips (R + 127)]
 };
@@ -118,7 +119,7 @@ __global__ void fold_f32_finalize(F32Args a, int64_t offset, int64_t len, float 
             }
         }
         const int64_t j = k - (a.M2 - a.q2);  // the mod-N wrap: bin M2 - q + j gets x[j]
-        if (j >= 0 && j < a.q2) acc += xat(j);
+        if (!a.block && j >= 0 && j < a.q2) acc += xat(j);
         return acc;
     };
     const int64_t s2 = a.q2 * a.M2 - a.N;
@@ -137,7 +138,7 @@ __global__ void fold_f32_finalize(F32Args a, int64_t offset, int64_t len, float 
             const int64_t c = k - a.M2;                  // extension: y2[M2+c] = y2[c] - x[c] + x[c+s2]
             int64_t e = c + s2;
             if (e >= a.N) e -= a.N;
-            v = base2(c) - xat(c) + xat(e);
+            v = a.block ? base2(c) : base2(c) - xat(c) + xat(e);
         }
         if (accumulate) o2[k] += v; else o2[k] = v;
     }
@@ -172,6 +173,7 @@ int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     a.x = (const float *)x; a.ldx = ldx;
     a.M1 = p->M1; a.M2 = p->M2; a.K = p->K; a.N = p->N; a.q2 = p->q2;
     a.rows = len / p->M1; a.row0 = offset / p->M1;
+    a.block = p->block;
     geometry(p, a.rows, &a.R, &a.nrc);
     a.n_strips = p->M1 / 128;
     a.n_groups = (a.n_strips + FW - 1) / FW;

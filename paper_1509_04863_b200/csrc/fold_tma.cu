@@ -51,6 +51,7 @@ struct TmaArgs {
     int64_t *k_out;
     uint32_t crt_inv;
     int64_t crt_wrap;
+    int block;            // TM_BLOCK: no wrap term, cyclic extension
     int xs_bytes;        // bytes reserved for the epilogue's x[0 .. K + q) stage
     int *work_counter;   // non-NULL: dynamic item assignment (atomic counter, zeroed per launch)
     // tensor-core fused mode: 8 warps correlate pair i (tc_core.cuh) while the fold streams pair i+1
@@ -332,7 +333,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 const int q = (int)it.nrow;  // = q1 = q2 (M1 | N)
                 // stage x[0 .. K + q) (all the wrap/extension terms read) with coalesced
                 // 16-byte loads: one memory latency per pair instead of one per bin
-                {
+                // (TM_BLOCK reads neither term)
+                if (!a.block) {
                     const int nx = (int)((a.K + q + 15) / 16);
                     const uint4 *src = reinterpret_cast<const uint4 *>(a.x + it.b * a.ldx);
                     uint4 *dst = reinterpret_cast<uint4 *>(xs);
@@ -353,10 +355,10 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                     if (gs < 0) gs += M2;
                     int32_t v = q - (gs < q ? 1 : 0) - C;
                     const int j = k - (M2 - q);  // mod-N wrap: bin M2 - q + j gets x[j]
-                    if (j >= 0) v += xb[j];
+                    if (j >= 0 && !a.block) v += xb[j];
                     if (a.accumulate) o2[k] += v; else o2[k] = v;
                     if (k < K) {                 // y2[M2 + k] = y2[k] - x[k] + x[k + q]  (s2 = q)
-                        const int32_t e = v - xb[k] + xb[k + q];
+                        const int32_t e = a.block ? v : v - xb[k] + xb[k + q];
                         if (a.accumulate) o2[M2 + k] += e; else o2[M2 + k] = e;
                     }
                 }
@@ -586,6 +588,7 @@ int setup_args(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, in
                void *y2, int accumulate, void *ws, int64_t R, int64_t n_rc, TmaArgs &a) {
     a.x = (const int8_t *)x; a.ldx = ldx;
     a.N = p->N; a.M1 = p->M1; a.M2 = p->M2; a.K = p->K; a.q2 = p->q2;
+    a.block = p->block;
     a.rows = len / p->M1; a.row0 = offset / p->M1;
     a.n_groups = (p->M1 + TCOLS - 1) / TCOLS;
     a.R = R; a.n_rc = n_rc;

@@ -84,7 +84,8 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
     if (N < 1 || N >= (int64_t(1) << 62)) { tm_set_error("tm_plan_create: N=%lld out of range", (long long)N); return TM_EINVAL; }
     if (K < 1) { tm_set_error("tm_plan_create: K=%lld < 1", (long long)K); return TM_EINVAL; }
     if (dtype != TM_I8 && dtype != TM_F32) { tm_set_error("tm_plan_create: bad dtype %d", dtype); return TM_EINVAL; }
-    if (flags & ~(TM_BINARY | TM_CORR_NTT | TM_CORR_TC | TM_ALIAS_REPAIR)) { tm_set_error("tm_plan_create: unknown flags 0x%x", flags); return TM_EINVAL; }
+    if ((flags & TM_BLOCK) && (flags & TM_ALIAS_REPAIR)) { tm_set_error("tm_plan_create: TM_BLOCK and TM_ALIAS_REPAIR are exclusive"); return TM_EINVAL; }
+    if (flags & ~(TM_BINARY | TM_CORR_NTT | TM_CORR_TC | TM_ALIAS_REPAIR | TM_BLOCK)) { tm_set_error("tm_plan_create: unknown flags 0x%x", flags); return TM_EINVAL; }
     if ((flags & TM_CORR_NTT) && (flags & TM_CORR_TC)) { tm_set_error("tm_plan_create: TM_CORR_NTT and TM_CORR_TC are exclusive"); return TM_EINVAL; }
     if ((flags & (TM_CORR_NTT | TM_CORR_TC)) && dtype != TM_I8) { tm_set_error("tm_plan_create: TM_CORR_* needs TM_I8"); return TM_EINVAL; }
     if ((flags & TM_BINARY) && dtype != TM_I8) { tm_set_error("tm_plan_create: TM_BINARY needs TM_I8"); return TM_EINVAL; }
@@ -131,6 +132,7 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
     p->device = dev; p->num_sms = sms;
     p->crt_inv = inv_mod(M1, M2);
     // reading C10's repair applies when M1 | N (then S_M1 needs no reduction mod N)
+    p->block = (flags & TM_BLOCK) ? 1 : 0;
     p->crt_wrap = ((flags & TM_ALIAS_REPAIR) && N % M1 == 0) ? p->s2 : 0;
     // fast packed +-1 fold: rows of M1 int8 columns, 512-column warp strips
     p->fast_fold = (dtype == TM_I8) && (flags & TM_BINARY) && (N % M1 == 0) && (M1 % 512 == 0) &&

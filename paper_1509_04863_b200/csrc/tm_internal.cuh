@@ -29,6 +29,7 @@ struct tm_plan_s {
     cudaEvent_t aux_ev[2][16];  // fold-done / ntt-done events per chunk
     int64_t tf_bytes;
     uint32_t crt_inv;    // M1^{-1} mod M2
+    int block;           // TM_BLOCK: strategy 2 (Theorem 2), no wrap, cyclic extension
     int64_t crt_wrap;    // TM_ALIAS_REPAIR with M1 | N: s2 (reading C10), else 0
     // tensor-core correlation engine (corr_tc.cu)
     int use_tc;          // tm_run / tm_correlate use corr_tc_kernel

@@ -62,6 +62,8 @@ def test_plan_create_rejects_invalid_without_gpu(libtm):
     assert L.tm_plan_create(ctypes.byref(h), 1024, 40, 32, 0, 0, 1) == 1  # M1 < K
     assert L.tm_plan_create(ctypes.byref(h), 0, 4, 0, 0, 0, 0) == 1
     assert L.tm_plan_create(ctypes.byref(h), 1024, 64, 0, 0, 1, 1) == 1   # TM_BINARY needs int8
+    assert L.tm_plan_create(ctypes.byref(h), 1024, 64, 0, 0, 0, 16 | 8) == 1  # TM_BLOCK excludes TM_ALIAS_REPAIR
+    assert L.tm_plan_create(ctypes.byref(h), 1024, 64, 0, 0, 0, 32) == 1   # unknown flag
 
 
 def test_ntt_constants():

@@ -514,3 +514,88 @@ def test_correlate_many_templates(tm, engine):
         assert k[i] == oracle.resolve(m1, plan.M1, m2, plan.M2, N), i
         hits += i < 16 and k[i] == shifts[i]
     print(f"correlate_many: {hits}/16 planted shifts recovered")
+
+
+# ------------------------------------------------------------- strategy 2 (TM_BLOCK)
+def check_block_pairs(plan, x_h, t_h, pairs, f32=False):
+    """TM_BLOCK against oracle.ftm_block: y_j[0..M_j) and the cyclic tail
+    y_j[M_j + c] = y_j[c], r_j, residues and k (staged and tm_run)."""
+    x, t = up(x_h), up(t_h)
+    y1, y2 = plan.fold(x)
+    r1, r2 = plan.correlate(y1, y2, plan.fold_template(t))
+    res, k = plan.match(r1, r2)
+    res_run, k_run = plan.run(x, t)
+    torch.cuda.synchronize()
+    K = plan.K
+    for b in pairs:
+        o = oracle.ftm_block(x_h[b], t_h[b], M=plan.M1 if plan.M1 != plan.K else 0)
+        exp = {"y1": np.concatenate([o["y1"], o["y1"][:K]]), "y2": np.concatenate([o["y2"], o["y2"][:K]]),
+               "r1": o["r1"], "r2": o["r2"]}
+        for name, g in (("y1", y1), ("y2", y2), ("r1", r1), ("r2", r2)):
+            gv = g[b].cpu().numpy()
+            if f32:
+                assert np.max(np.abs(gv.astype(np.float64) - exp[name])) <= 1e-5 * np.max(np.abs(exp[name])), (name, b)
+            else:
+                np.testing.assert_array_equal(gv, exp[name], err_msg=f"{name} pair {b}")
+        if f32:
+            for j, name in enumerate(("r1", "r2")):
+                s = np.sort(o[name])
+                if s[-1] - s[-2] > 1e-5 * np.max(np.abs(o[name])):
+                    assert int(res[b, j]) == o["residues"][j] == int(res_run[b, j]), (b, j)
+            if tuple(int(v) for v in res[b]) == o["residues"]:
+                assert int(k[b]) == o["k"]
+        else:
+            assert tuple(res[b].tolist()) == o["residues"] == tuple(res_run[b].tolist()), b
+            assert int(k[b]) == o["k"] == int(k_run[b]), b
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("N,K,M,B,binary", [(4096, 256, 0, 8, True), (2 ** 16, 1024, 0, 4, True),
+                                            (4096 * 37, 4096, 0, 3, True), (1000, 37, 0, 4, False),
+                                            (997, 40, 45, 4, False), (2 ** 14, 200, 0, 3, False)])
+def test_block_strategy_int(tm, N, K, M, B, binary, engine):
+    """TM_BLOCK (Theorem 2 with Eq. 3's Phi_M = I, x zero-padded)
+    bit-exact against the oracle on the packed +-1, general and tensor-core paths."""
+    plan = tm.Plan(N, K, M=M, seed=3, binary=binary, engine=engine, block=True)
+    if binary:
+        x_h, t_h, _ = tmgen.batch(3, 0, B, N, K, 0.1)
+    else:
+        rng = np.random.default_rng(N + K + M)
+        x_h = rng.integers(-128, 128, (B, N)).astype(np.int8)
+        t_h = np.stack([x_h[b][(np.arange(K) + 11 * b) % N] for b in range(B)]).astype(np.int8)
+    check_block_pairs(plan, x_h, t_h, range(B))
+
+
+@pytest.mark.parametrize("N,K,M", [(2 ** 16, 512, 0), (30011, 250, 260)])
+def test_block_strategy_f32(tm, N, K, M):
+    plan = tm.Plan(N, K, M=M, seed=33, dtype="float32", block=True)
+    x_h, t_h, _ = tmgen.batch(33, 0, 3, N, K, 0.5, dtype=np.float32)
+    check_block_pairs(plan, x_h, t_h, range(3), f32=True)
+
+
+def test_block_strategy_fused_batch(tm):
+    """tm_run's persistent fused path (batch >= #SMs) under TM_BLOCK: every
+    pair's residues and k equal the oracle's Block FTM."""
+    N, K, B = 2 ** 18, 2048, 300
+    plan = tm.Plan(N, K, seed=62, block=True)
+    x_h, t_h, _ = tmgen.batch(62, 0, B, N, K, 0.05)
+    res, k = plan.run(up(x_h), up(t_h))
+    torch.cuda.synchronize()
+    rr, kk = res.cpu().numpy(), k.cpu().numpy()
+    for b in range(B):
+        o = oracle.ftm_block(x_h[b], t_h[b], want_vectors=False)
+        assert tuple(rr[b]) == o["residues"] and kk[b] == o["k"], b
+
+
+def test_block_strategy_has_no_wrap_alias(tm):
+    """cfg1 shape with k0 < s2 = 16: strategy 1 loses the peaks its mod-N wrap
+    moves (reading C10); strategy 2 counts no sample twice and does not."""
+    N, K, B = 4096, 256, 64
+    rng = np.random.default_rng(78)
+    x_h = (1 - 2 * rng.integers(0, 2, (B, N))).astype(np.int8)
+    k0 = np.arange(B) % 16
+    t_h = np.stack([x_h[b][(k0[b] + np.arange(K)) % N] for b in range(B)]).astype(np.int8)
+    _, kb = tm.Plan(N, K, block=True).run(up(x_h), up(t_h))
+    _, kl = tm.Plan(N, K).run(up(x_h), up(t_h))
+    kb, kl = kb.cpu().numpy(), kl.cpu().numpy()
+    assert np.sum(kb == k0) > np.sum(kl == k0)
