@@ -25,7 +25,7 @@
 namespace {
 using namespace tc;
 
-constexpr int NT = 32;    // output blocks per tile (MMA N = 2 NT = 64)
+constexpr int NT_MIN = 32;  // output blocks per tile: NT in {32, 64} (MMA N = 2 NT)
 constexpr int TCCH = 16;  // template blocks per A chunk
 constexpr int KEY_SHIFT = 21;
 constexpr int64_t KEY_BIAS = (int64_t)1 << 42;
@@ -45,13 +45,75 @@ __device__ __forceinline__ unsigned long long pack_key(int64_t r, int64_t k) {
     return ((unsigned long long)(r + KEY_BIAS) << KEY_SHIFT) | (unsigned long long)(((int64_t)1 << KEY_SHIFT) - 1 - k);
 }
 
-// smem: A [256 * (8 (TCCH-1) + 15)] | B [8 * 2 (NT + TCCH - 1) * 16] | tp slice | misc
-constexpr int A_BYTES = 256 * (8 * (TCCH - 1) + 15);
-constexpr int B_BYTES = 8 * 2 * (NT + TCCH - 1) * 16;
+// smem: A [2][256 * (8 (TCCH-1) + 15)] | B [2][8 * 2 (NT + TCCH - 1) * 16] | tp slice | misc.
+// Passes (chunk, limb) alternate between the two A and B buffers, so the
+// staging of pass p + 1 overlaps the MMAs of pass p (mbarrier mdone[p & 1]).
+// An SS MMA costs ~(4096 + 32 N) / 128 cycles (shared-memory operand reads), so
+// N = 128 (NT = 64) does twice the work of N = 64 in 1.33x the time.
+constexpr int A_BYTES = (256 * (8 * (TCCH - 1) + 15) + 127) / 128 * 128;
+template <int NT>
+constexpr int b_bytes() { return (8 * (2 * (NT + TCCH - 1) * 16 + 16) + 127) / 128 * 128; }
+// B chunk-column stride: 32 nrows + 16 bytes, an odd multiple of 16 modulo 128, so
+// the 8 chunk columns a warp's store touches fall in distinct bank quads
+__device__ __forceinline__ uint32_t b_lbo(int nrows) { return 32u * nrows + 16u; }
 constexpr int TP_BYTES = 128 * TCCH + 256;
-constexpr int SMEM_BYTES = A_BYTES + B_BYTES + TP_BYTES + 64;
+template <int NT>
+constexpr int smem_bytes() { return 2 * A_BYTES + 2 * b_bytes<NT>() + TP_BYTES + 64; }
 
-__global__ void __launch_bounds__(NTHR, 2) corr_tc_tiled(const TiledArgs T) {
+// Warp roles: warps 0-7 stage (limb scan, template slices, A copies, B windows,
+// epilogue); warp 8 only issues the MMAs, so that staging pass p + 1 overlaps
+// the tensor core working on pass p (with one warp doing both, the issue loop
+// blocks on the tensor core's queue and staging and MMAs serialise).
+// Named barriers: 1 + (p & 1) "pass p staged" (256 arrive, issuer syncs), 3 the
+// 256 staging threads.
+constexpr int TNTHR = NTHR + 32;
+__device__ __forceinline__ void stagers_sync() { asm volatile("bar.sync 3, %0;" ::"n"(NTHR) : "memory"); }
+
+// Stage limb l of the B window (y_1 and y_2 blocks s_begin + [0, nrows)) with
+// both moduli's rows in one batch of loads: row r = 2 s + j, warp w takes rows
+// w + 8 u, RB rows in flight per warp (one L2 round trip per pass at NT = 32;
+// the one-CTA kernel's stage_yw walks the moduli one after the other).
+template <int RB>
+__device__ __forceinline__ void stage_window(const TcArgs &a, uint8_t *B, int64_t b, int l, int nl, int64_t s_begin,
+                                             int nrows, int warp, int lane) {
+    const uint32_t lbo = b_lbo(nrows);
+    const int h = lane >> 2, wq = lane & 3;
+    const int32_t *yr0 = a.y[0] + b * a.ldy[0], *yr1 = a.y[1] + b * a.ldy[1];
+    const bool al0 = ((((uintptr_t)yr0) & 15) == 0), al1 = ((((uintptr_t)yr1) & 15) == 0);
+    for (int r0 = warp; r0 < 2 * nrows; r0 += RB * (NTHR / 32)) {
+        int32_t v[RB][4];
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const int r = r0 + u * (NTHR / 32), j = r & 1;
+            const int64_t i0 = (int64_t)P * (s_begin + (r >> 1)) + 4 * lane;
+            const int32_t *yr = j ? yr1 : yr0;
+            const int64_t len = a.len[j];
+            v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0;
+            if (r < 2 * nrows && i0 >= 0) {
+                if ((j ? al1 : al0) && i0 + 4 <= len) {
+                    const int4 q = *reinterpret_cast<const int4 *>(yr + i0);
+                    v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (i0 + e < len) v[u][e] = yr[i0 + e];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const int r = r0 + u * (NTHR / 32);
+            if (r >= 2 * nrows) break;
+            *reinterpret_cast<uint32_t *>(B + lbo * h + 16 * r + 4 * wq) =
+                nl == 1 ? pack4(v[u][0], v[u][1], v[u][2], v[u][3])
+                        : pack4(limb(v[u][0], l, nl), limb(v[u][1], l, nl), limb(v[u][2], l, nl), limb(v[u][3], l, nl));
+        }
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
+    constexpr int B_BYTES = b_bytes<NT>();
     extern __shared__ __align__(1024) uint8_t sm[];
     const TcArgs &a = T.a;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -59,76 +121,79 @@ __global__ void __launch_bounds__(NTHR, 2) corr_tc_tiled(const TiledArgs T) {
     const int at = blockIdx.x % T.n_at, cr = blockIdx.x / T.n_at;
     const int a0 = at * NT;
     const int cb = cr * T.CR, ce = min(a.NC, cb + T.CR);
-    uint8_t *A = sm, *B = sm + A_BYTES, *tp = B + B_BYTES;
-    uint64_t *mdone = reinterpret_cast<uint64_t *>(tp + TP_BYTES);
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(mdone + 1);
-    int *nlflag = reinterpret_cast<int *>(mdone + 2);
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                     "r"(a.ncols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
+    uint8_t *Abuf = sm, *Bbuf = sm + 2 * A_BYTES, *tp = Bbuf + 2 * B_BYTES;
+    uint64_t *mdone = reinterpret_cast<uint64_t *>(tp + TP_BYTES);  // [2]
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(mdone + 2);
+    int *nlflag = reinterpret_cast<int *>(mdone + 3);
+    long long ts[8] = {gtime(), 0, 0, 0, 0, 0, 0, 0};  // instrumentation (a.dbg): phase stamps
     if (tid == 32) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mdone)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mdone + 1)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // ---- limb count: scan this CTA's whole y window (blocks [a0 + cb, a0 + NT + ce - 1)) ----
+    // ---- limb count: scan this CTA's whole y window (blocks [a0 + cb, a0 + NT + ce - 1)),
+    // 16-byte loads with several in flight (a latency-bound scalar scan cost ~30% of the kernel)
     int fl = 0;
     {
         const int64_t s0 = a0 + cb, n = NT + (ce - cb) - 1;
-        for (int j = 0; j < 2; ++j) {
+        uint32_t mag = 0;  // OR of v ^ (v >> 31): below 2^b iff every v fits b + 1 signed bits
+        for (int j = 0; j < 2 && tid < NTHR; ++j) {
             const int32_t *yr = a.y[j] + b * a.ldy[j];
-            for (int64_t i = P * s0 + tid; i < P * (s0 + n) && i < a.len[j]; i += NTHR) {
-                const int32_t v = yr[i];
-                fl |= ((uint32_t)(v + 128) > 255u ? 1 : 0) | ((uint32_t)(v + 2048) > 4095u ? 2 : 0) |
-                      ((uint32_t)(v + 32768) > 65535u ? 4 : 0);
+            const int64_t lo = P * s0, hi = min(P * (s0 + n), a.len[j]);
+            if (hi <= lo) continue;
+            if ((((uintptr_t)(yr + lo)) & 15) == 0) {
+                const int64_t n4 = (hi - lo) >> 2;
+                const int4 *q = reinterpret_cast<const int4 *>(yr + lo);
+#pragma unroll 4
+                for (int64_t i = tid; i < n4; i += NTHR) {
+                    const int4 v = q[i];
+                    mag |= (uint32_t)(v.x ^ (v.x >> 31)) | (uint32_t)(v.y ^ (v.y >> 31)) |
+                           (uint32_t)(v.z ^ (v.z >> 31)) | (uint32_t)(v.w ^ (v.w >> 31));
+                }
+                for (int64_t i = lo + 4 * n4 + tid; i < hi; i += NTHR) mag |= (uint32_t)(yr[i] ^ (yr[i] >> 31));
+            } else {
+#pragma unroll 4
+                for (int64_t i = lo + tid; i < hi; i += NTHR) mag |= (uint32_t)(yr[i] ^ (yr[i] >> 31));
             }
         }
+        fl = (mag > 127u ? 1 : 0) | (mag > 2047u ? 2 : 0) | (mag > 32767u ? 4 : 0);
     }
     fl = __syncthreads_or(fl & 1) | (__syncthreads_or(fl & 2) << 1) | (__syncthreads_or(fl & 4) << 2);
     int nl = (fl & 4) ? 4 : (fl & 2) ? 3 : (fl & 1) ? 2 : 1;
     if (nl > T.lmax) nl = T.lmax;
+    // TMEM: 2 NT columns per limb, allocated after the scan so that two CTAs fit
+    // per SM whenever 2 NT nl <= 256
+    uint32_t ncols = 32;
+    while (ncols < (uint32_t)(2 * NT * nl)) ncols *= 2;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(ncols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
     (void)nlflag;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tbase = *tslot;
+    ts[1] = gtime();
 
+    // pass q = (chunk, limb) uses A[chunk & 1], B[q & 1] and commits to mdone[q & 1]
+    // (its (q >> 1)-th phase).  Before staging pass q the stagers wait for pass q - 2,
+    // which (commits being cumulative) also frees the A buffer of chunk - 2.
     uint32_t pass = 0;
-    for (int c0 = cb; c0 < ce; c0 += TCCH) {
-        const int c1 = min(ce, c0 + TCCH);
-        const int nrows = NT + (c1 - c0) - 1;  // B window: blocks [a0 + c0, a0 + c0 + nrows)
-        for (int l = 0; l < nl; ++l) {
-            if (pass > 0) group_wait<CtaSync>(mdone, (pass - 1) & 1u, warp);  // previous pass done with A, B
-            if (l == 0) {
-                // template slice: tp'[j] = t[128 c0 + j - 128] (zero outside [0, K))
-                const int8_t *tr = a.t + b * a.ldt;
-                for (int i = tid; i < TP_BYTES; i += NTHR) {
-                    const int64_t j = 128 * (int64_t)c0 + i - 128;
-                    tp[i] = (j >= 0 && j < a.K) ? (uint8_t)tr[j] : 0;
-                }
-                __syncthreads();
-                const int n = (8 * (c1 - c0 - 1) + 15) * 16;
-                for (int c = tid; c < n; c += NTHR) {
-                    const int J = c >> 4, sg = c & 15;
-                    const int sh = sg + 1, m = sh >> 2, r = 8 * (sh & 3);
-                    const uint32_t *w = reinterpret_cast<const uint32_t *>(tp + 16 * J) + m;
-                    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
-                    uint4 o;
-                    o.x = __funnelshift_r(w0, w1, r);
-                    o.y = __funnelshift_r(w1, w2, r);
-                    o.z = __funnelshift_r(w2, w3, r);
-                    o.w = __funnelshift_r(w3, w4, r);
-                    reinterpret_cast<uint4 *>(A)[c] = o;
-                }
-            }
-            stage_yw(a, B, b, l, nl, (int64_t)a0 + c0, nrows, warp, lane);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncthreads();
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (warp == 0) {
-                const uint32_t lbo = 32u * nrows;
+    if (warp == NTHR / 32) {
+        // ---- MMA issuer
+        int ch = 0;
+        for (int c0 = cb; c0 < ce; c0 += TCCH, ++ch) {
+            const int c1 = min(ce, c0 + TCCH);
+            const int nrows = NT + (c1 - c0) - 1;
+            const uint8_t *A = Abuf + (ch & 1) * A_BYTES;
+            for (int l = 0; l < nl; ++l) {
+                const uint8_t *B = Bbuf + (pass & 1) * B_BYTES;
+                if (pass & 1) asm volatile("bar.sync 2, %0;" ::"n"(TNTHR) : "memory");
+                else asm volatile("bar.sync 1, %0;" ::"n"(TNTHR) : "memory");
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t lbo = b_lbo(nrows);
                 const uint64_t ad0 = sdesc(smem_u32(A), 256, 128);
                 const uint64_t bd0 = sdesc(smem_u32(B), lbo, 128);
                 const uint32_t id = idesc_i8(2 * NT);
@@ -141,21 +206,92 @@ __global__ void __launch_bounds__(NTHR, 2) corr_tc_tiled(const TiledArgs T) {
                         mma_i8(dcol, ad, bd, id, (c != cb || ks) ? 1u : 0u);
                     }
                 }
-                umma_commit(mdone);
+                umma_commit(mdone + (pass & 1));
+                ++pass;
             }
-            ++pass;
+        }
+    } else {
+        // ---- stagers.  The template slice of the next chunk is prefetched into
+        // registers (tw_) while the current chunk is staged.
+        constexpr int TPW = TP_BYTES / 4;
+        uint32_t tw_[(TPW + NTHR - 1) / NTHR];
+        auto load_slice = [&](int c0v) {  // tp'[j] = t[128 c0v + j - 128] (zero outside [0, K))
+            const int8_t *tr = a.t + b * a.ldt;
+            const int64_t base = 128 * (int64_t)c0v - 128;
+            const bool fast = base >= 0 && base + TP_BYTES <= a.K && ((((uintptr_t)(tr + base)) & 3) == 0);
+#pragma unroll
+            for (int u = 0; u < (TPW + NTHR - 1) / NTHR; ++u) {
+                const int i = tid + u * NTHR;
+                if (i >= TPW) break;
+                if (fast) {
+                    tw_[u] = __ldg(reinterpret_cast<const uint32_t *>(tr + base) + i);
+                } else {
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int64_t j = base + 4 * i + e;
+                        if (j >= 0 && j < a.K) w |= (uint32_t)(uint8_t)tr[j] << (8 * e);
+                    }
+                    tw_[u] = w;
+                }
+            }
+        };
+        load_slice(cb);
+        int ch = 0;
+        for (int c0 = cb; c0 < ce; c0 += TCCH, ++ch) {
+            const int c1 = min(ce, c0 + TCCH);
+            const int nrows = NT + (c1 - c0) - 1;  // B window: blocks [a0 + c0, a0 + c0 + nrows)
+            uint8_t *A = Abuf + (ch & 1) * A_BYTES;
+            for (int l = 0; l < nl; ++l) {
+                uint8_t *B = Bbuf + (pass & 1) * B_BYTES;
+                long long tw = gtime();
+                if (pass >= 2) mbar_wait(mdone + (pass & 1), ((pass - 2) >> 1) & 1u);
+                long long tw2 = gtime();
+                ts[4] += tw2 - tw;
+                if (l == 0) {
+                    stagers_sync();  // every stager is done reading the previous slice
+#pragma unroll
+                    for (int u = 0; u < (TPW + NTHR - 1) / NTHR; ++u)
+                        if (tid + u * NTHR < TPW) reinterpret_cast<uint32_t *>(tp)[tid + u * NTHR] = tw_[u];
+                    stagers_sync();
+                    if (c1 < ce) load_slice(c1);
+                    const int n = (8 * (c1 - c0 - 1) + 15) * 16;
+                    for (int c = tid; c < n; c += NTHR) {
+                        const int J = c >> 4, sg = c & 15;
+                        const int sh = sg + 1, m = sh >> 2, r = 8 * (sh & 3);
+                        const uint32_t *w = reinterpret_cast<const uint32_t *>(tp + 16 * J) + m;
+                        const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
+                        uint4 o;
+                        o.x = __funnelshift_r(w0, w1, r);
+                        o.y = __funnelshift_r(w1, w2, r);
+                        o.z = __funnelshift_r(w2, w3, r);
+                        o.w = __funnelshift_r(w3, w4, r);
+                        reinterpret_cast<uint4 *>(A)[c] = o;
+                    }
+                }
+                ts[5] += gtime() - tw2;  // template slice + A build
+                tw2 = gtime();
+                stage_window<12>(a, B, b, l, nl, (int64_t)a0 + c0, nrows, warp, lane);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                if (pass & 1) asm volatile("bar.arrive 2, %0;" ::"n"(TNTHR) : "memory");
+                else asm volatile("bar.arrive 1, %0;" ::"n"(TNTHR) : "memory");
+                ts[6] += gtime() - tw2;  // B staging
+                ++pass;
+            }
         }
     }
-    group_wait<CtaSync>(mdone, (pass - 1) & 1u, warp);
+    mbar_wait(mdone + ((pass - 1) & 1), ((pass - 1) >> 1) & 1u);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    ts[2] = gtime();
 
-    // ---- epilogue: warp w: TMEM lanes 32 (w & 3) (rows b'), blocks a0 + 16 (w >> 2) + [0, 16)
-    {
+    // ---- epilogue (warps 0-7): warp w: TMEM lanes 32 (w & 3) (rows b'), blocks a0 + (NT / 2) (w >> 2) + [0, NT / 2)
+    if (warp < NTHR / 32) {
         const int qw = warp & 3, hw = warp >> 2;
         const int brow = P - 1 - (32 * qw + lane);
         const uint32_t taddr = tbase + ((uint32_t)(32 * qw) << 16);
         int64_t bv[2] = {INT64_MIN, INT64_MIN}, bk[2] = {INT64_MAX, INT64_MAX};
-        for (int ar0 = 16 * hw; ar0 < 16 * hw + 16; ar0 += 8) {
+        for (int ar0 = (NT / 2) * hw; ar0 < (NT / 2) * hw + NT / 2; ar0 += 8) {
             int64_t r[8][2];
 #pragma unroll
             for (int i = 0; i < 8; ++i) r[i][0] = r[i][1] = 0;
@@ -190,12 +326,12 @@ __global__ void __launch_bounds__(NTHR, 2) corr_tc_tiled(const TiledArgs T) {
         if (T.n_cr > 1) {
             // the CTA that completes a tile's last template range reduces its final r
             __threadfence();
-            __syncthreads();
+            stagers_sync();
             if (tid == 0) *nlflag = (atomicAdd(T.tile_cnt + b * T.n_at + at, 1u) == (unsigned)(T.n_cr - 1));
-            __syncthreads();
+            stagers_sync();
             if (*nlflag) {
                 __threadfence();
-                for (int ar0 = 16 * hw; ar0 < 16 * hw + 16; ++ar0) {
+                for (int ar0 = (NT / 2) * hw; ar0 < (NT / 2) * hw + NT / 2; ++ar0) {
                     const int64_t ab = a0 + ar0;
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
@@ -220,7 +356,15 @@ __global__ void __launch_bounds__(NTHR, 2) corr_tc_tiled(const TiledArgs T) {
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(a.ncols));
+    if (a.dbg && tid == 0) {
+        ts[3] = gtime();
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        ts[7] = ((long long)smid << 32) | ((long long)pass << 8) | nl;
+        long long *d = a.dbg + 8 * ((int64_t)blockIdx.y * gridDim.x + blockIdx.x);
+        for (int i = 0; i < 8; ++i) d[i] = ts[i];
+    }
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols));
 }
 
 // leftover outputs k in [128 NA_j, M_j) (at most MAXLEFT per modulus): CTA
@@ -307,7 +451,7 @@ void tm_tc_tiled_plan(tm_plan_s *p) {
 size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch) {
     if (!p->tct_ok) return 0;
     // keys [batch][2] | lsum [batch][2 MAXLEFT] | tile counters [batch][<= 2^KEY_SHIFT / (128 NT)] | racc
-    return 256 + (size_t)batch * (16 + 16 * MAXLEFT + 4 * (((int64_t)1 << KEY_SHIFT) / (P * NT) + 1)) +
+    return 256 + (size_t)batch * (16 + 16 * MAXLEFT + 4 * (((int64_t)1 << KEY_SHIFT) / (P * NT_MIN) + 1)) +
            (size_t)batch * (p->M1 + p->M2) * 8 + 1024;
 }
 
@@ -321,6 +465,7 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     TiledArgs T{};
     tm_tc_fill_args(p, y1, y2, t, ldt, nullptr, nullptr, nullptr, nullptr, nullptr, T.a);
     T.a.ldy[0] = ldy1; T.a.ldy[1] = ldy2;
+    T.a.dbg = tm_tc_dbg_buffer();
     // the tiles cover NA_j = the plan's block counts (computed here: tc_ok may be false)
     const int NC = (int)((p->K + P - 2) / P) + 1;
     T.a.NC = NC;
@@ -332,15 +477,22 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         T.a.NA[j] = (int)na;
     }
     T.lmax = p->tct_lmax;
-    uint32_t ncols = 32;
-    while (ncols < (uint32_t)(2 * NT * T.lmax)) ncols *= 2;
-    T.a.ncols = ncols;
+    const char *env_nt = getenv("TM_TILED_NT");  // A/B: "32" or "64"
+    const int NT = (env_nt && atoi(env_nt) == 32) ? 32 : 64;
     const int namax = T.a.NA[0] > T.a.NA[1] ? T.a.NA[0] : T.a.NA[1];
     T.n_at = (namax + NT - 1) / NT;
-    // template ranges: enough CTAs for two per SM, ranges of >= 2 chunks
+    // template ranges: minimise waves x blocks per CTA over 2 resident CTAs per SM
+    // (a grid just over one wave doubles the time), fewer ranges on near-ties
+    // (each extra range adds one int64 atomic per output)
+    const int max_cr = std::max(1, (NC + 2 * TCCH - 1) / (2 * TCCH));
+    const int64_t slots = 2 * (int64_t)p->num_sms;
     int n_cr = 1;
-    const int max_cr = (NC + 2 * TCCH - 1) / (2 * TCCH);
-    while (n_cr < max_cr && batch * T.n_at * n_cr < 2 * p->num_sms) ++n_cr;
+    double best = 1e300;
+    for (int c = 1; c <= max_cr; ++c) {
+        const int64_t ctas = batch * T.n_at * c;
+        const double cost = (double)((ctas + slots - 1) / slots) * (double)((NC + c - 1) / c);
+        if (cost < best * 0.95) { best = cost; n_cr = c; }
+    }
     T.CR = (NC + n_cr - 1) / n_cr;
     T.n_cr = (NC + T.CR - 1) / T.CR;
     char *w = (char *)ws;
@@ -361,10 +513,15 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     if (e != cudaSuccess) return tm_cuda_status(e, "tm_correlate: tiled reset");
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(corr_tc_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(corr_tc_tiled<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<32>());
+        cudaFuncSetAttribute(corr_tc_tiled<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<64>());
         attr = true;
     }
-    corr_tc_tiled<<<dim3((unsigned)(T.n_at * T.n_cr), (unsigned)batch), NTHR, SMEM_BYTES, s>>>(T);
+    const dim3 grid((unsigned)(T.n_at * T.n_cr), (unsigned)batch);
+    if (NT == 32)
+        corr_tc_tiled<32><<<grid, TNTHR, smem_bytes<32>(), s>>>(T);
+    else
+        corr_tc_tiled<64><<<grid, TNTHR, smem_bytes<64>(), s>>>(T);
     TM_CHECK_LAUNCH("corr_tc_tiled");
     const int nleft = (int)(std::max<int64_t>(0, p->M1 - (int64_t)P * T.a.NA[0]) +
                             std::max<int64_t>(0, p->M2 - (int64_t)P * T.a.NA[1]));

@@ -38,10 +38,11 @@ namespace {
 template <typename T, typename Acc>
 __global__ void fold_general(const T *__restrict__ x, int64_t ldx, int64_t N, int64_t offset,
                              int64_t len, int64_t M1, int64_t M2, int64_t K, int64_t q1, int64_t q2,
-                             Acc *__restrict__ y1, Acc *__restrict__ y2, int accumulate, int block) {
+                             Acc *__restrict__ y1, int64_t ldy1, Acc *__restrict__ y2, int64_t ldy2, int accumulate,
+                             int block) {
     const int j = blockIdx.z;  // 0: modulus M1, 1: modulus M2
     const int64_t M = j ? M2 : M1, q = j ? q2 : q1;
-    Acc *y = (j ? y2 : y1) + (int64_t)blockIdx.y * (M + K);
+    Acc *y = (j ? y2 : y1) + (int64_t)blockIdx.y * (j ? ldy2 : ldy1);
     const T *xb = x + (int64_t)blockIdx.y * ldx;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M + K;
          k += (int64_t)gridDim.x * blockDim.x) {
@@ -253,11 +254,12 @@ __global__ void __launch_bounds__(PM_WARPS * 32, 2) fold_pm1(PmArgs a) {
 __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t N, int64_t offset,
                               int64_t len, int64_t M1, int64_t M2, int64_t K, int64_t q2,
                               int64_t row0, int64_t rows, const int32_t *__restrict__ counts,
-                              int32_t *__restrict__ y1, int32_t *__restrict__ y2, int accumulate, int block) {
+                              int32_t *__restrict__ y1, int64_t ldy1, int32_t *__restrict__ y2, int64_t ldy2,
+                              int accumulate, int block) {
     const int64_t b = blockIdx.y;
     const int8_t *xb = x + b * ldx;
     const int32_t *c1 = counts + b * (M1 + M2), *c2 = c1 + M1;
-    int32_t *o1 = y1 + b * (M1 + K), *o2 = y2 + b * (M2 + K);
+    int32_t *o1 = y1 + b * ldy1, *o2 = y2 + b * ldy2;
     auto xat = [&](int64_t pos) -> int32_t {  // x at a global position, 0 outside the chunk
         int64_t rel = pos - offset;
         return (rel >= 0 && rel < len) ? (int32_t)xb[rel] : 0;
@@ -340,11 +342,11 @@ void pick_rows_tma(const tm_plan_s *p, int64_t batch, int64_t rows, int64_t n_gr
 }  // namespace
 
 int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
-                void *y1, void *y2, int accumulate, void *ws, int64_t R, int64_t n_rc, cudaStream_t s,
-                bool *used_counts);
+                void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, int64_t R, int64_t n_rc,
+                cudaStream_t s, bool *used_counts);
 
-int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset,
-                 int64_t len, void *y1, void *y2, int accumulate, void *ws, cudaStream_t s) {
+int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
+                    void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, cudaStream_t s) {
     if (batch == 0) return TM_OK;
     const bool aligned = ((uintptr_t)x % 16 == 0) && (ldx % 16 == 0);
     const bool fast = p->fast_fold && aligned && (offset % p->M1 == 0) && (len % p->M1 == 0) &&
@@ -355,14 +357,16 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
         const int64_t rows = len / p->M1, n_groups = (p->M1 + PM_COLS - 1) / PM_COLS;
         pick_rows_tma(p, batch, rows, n_groups, &R, &nrc);
         bool used_counts = false;
-        int rc = tm_fold_tma(p, x, ldx, batch, offset, len, y1, y2, accumulate, ws, R, nrc, s, &used_counts);
+        int rc = tm_fold_tma(p, x, ldx, batch, offset, len, y1, ldy1, y2, ldy2, accumulate, ws, R, nrc, s,
+                             &used_counts);
         if (rc != TM_EUNSUPPORTED) {
             if (rc != TM_OK || !used_counts) return rc;
             tm_ws_layout L = tm_ws(p, batch);
             int64_t gx = (p->M2 + p->K + 255) / 256;
             fold_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(
                 (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, offset / p->M1, rows,
-                (const int32_t *)((char *)ws + L.fold_counts), (int32_t *)y1, (int32_t *)y2, accumulate, p->block);
+                (const int32_t *)((char *)ws + L.fold_counts), (int32_t *)y1, ldy1, (int32_t *)y2, ldy2, accumulate,
+                p->block);
             TM_CHECK_LAUNCH("tm_fold: fold_finalize");
             return TM_OK;
         }
@@ -394,13 +398,14 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
         int64_t gx = (p->M2 + p->K + 255) / 256;
         fold_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(
             (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, a.row0, a.rows,
-            counts, (int32_t *)y1, (int32_t *)y2, accumulate, p->block);
+            counts, (int32_t *)y1, ldy1, (int32_t *)y2, ldy2, accumulate, p->block);
         TM_CHECK_LAUNCH("tm_fold: fold_finalize");
         return TM_OK;
     }
     if (p->dtype == TM_F32 && ws && len > 0) {  // strip kernel + fixed-order finalize
         tm_ws_layout L = tm_ws(p, batch);
-        int rc = tm_fold_f32(p, x, ldx, batch, offset, len, y1, y2, accumulate, (char *)ws + L.fold_counts, s);
+        int rc = tm_fold_f32(p, x, ldx, batch, offset, len, y1, ldy1, y2, ldy2, accumulate,
+                             (char *)ws + L.fold_counts, s);
         if (rc != TM_EUNSUPPORTED) return rc;
     }
     if (batch > 65535) { tm_set_error("tm_fold: general kernel supports batch <= 65535"); return TM_EUNSUPPORTED; }
@@ -410,11 +415,13 @@ int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, 
     if (p->dtype == TM_I8) {
         fold_general<int8_t, int32_t><<<grid, 256, 0, s>>>((const int8_t *)x, ldx, p->N, offset, len,
                                                            p->M1, p->M2, p->K, p->q1, p->q2,
-                                                           (int32_t *)y1, (int32_t *)y2, accumulate, p->block);
+                                                           (int32_t *)y1, ldy1, (int32_t *)y2, ldy2, accumulate,
+                                                           p->block);
     } else {
         fold_general<float, float><<<grid, 256, 0, s>>>((const float *)x, ldx, p->N, offset, len,
                                                         p->M1, p->M2, p->K, p->q1, p->q2,
-                                                        (float *)y1, (float *)y2, accumulate, p->block);
+                                                        (float *)y1, ldy1, (float *)y2, ldy2, accumulate,
+                                                        p->block);
     }
     TM_CHECK_LAUNCH("tm_fold: fold_general");
     return TM_OK;

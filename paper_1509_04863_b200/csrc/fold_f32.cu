@@ -89,12 +89,12 @@ __global__ void __launch_bounds__(FW * 32) fold_f32_strips(F32Args a) {
 }
 
 // bin sums, wrap and extension; x read only for the wrap/extension terms
-__global__ void fold_f32_finalize(F32Args a, int64_t offset, int64_t len, float *__restrict__ y1,
-                                  float *__restrict__ y2, int accumulate) {
+__global__ void fold_f32_finalize(F32Args a, int64_t offset, int64_t len, float *__restrict__ y1, int64_t ldy1,
+                                  float *__restrict__ y2, int64_t ldy2, int accumulate) {
     const int64_t b = blockIdx.y;
     const float *xb = a.x + b * a.ldx;
     const float *pb = a.parts + b * a.nrc * part_stride(a);
-    float *o1 = y1 + b * (a.M1 + a.K), *o2 = y2 + b * (a.M2 + a.K);
+    float *o1 = y1 + b * ldy1, *o2 = y2 + b * ldy2;
     auto xat = [&](int64_t pos) -> float {  // x at a global position, 0 outside the chunk
         const int64_t rel = pos - offset;
         return (rel >= 0 && rel < len) ? xb[rel] : 0.f;
@@ -166,7 +166,7 @@ size_t tm_fold_f32_ws_bytes(const tm_plan_s *p, int64_t batch) {
 
 // TM_EUNSUPPORTED (nothing enqueued) when the chunk or alignment does not qualify.
 int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
-                void *y1, void *y2, int accumulate, void *parts, cudaStream_t s) {
+                void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *parts, cudaStream_t s) {
     if (!tm_fold_f32_ok(p) || !parts) return TM_EUNSUPPORTED;
     if (((uintptr_t)x % 16) || (ldx % 4) || (offset % p->M1) || (len % p->M1) || len == 0) return TM_EUNSUPPORTED;
     F32Args a{};
@@ -190,8 +190,8 @@ int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     TM_CHECK_LAUNCH("tm_fold: fold_f32_strips");
     int64_t gx = (p->M2 + p->K + 255) / 256;
     if (gx > 65535) gx = 65535;
-    fold_f32_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(a, offset, len, (float *)y1, (float *)y2,
-                                                                           accumulate);
+    fold_f32_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(a, offset, len, (float *)y1, ldy1,
+                                                                           (float *)y2, ldy2, accumulate);
     TM_CHECK_LAUNCH("tm_fold: fold_f32_finalize");
     return TM_OK;
 }

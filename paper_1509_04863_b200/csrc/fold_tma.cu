@@ -629,11 +629,12 @@ int launch(const TmaArgs &a, int64_t grid, size_t smem, cudaStream_t s) {
 }  // namespace
 
 int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
-                void *y1, void *y2, int accumulate, void *ws, int64_t R, int64_t n_rc, cudaStream_t s,
-                bool *used_counts) {
+                void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, int64_t R, int64_t n_rc,
+                cudaStream_t s, bool *used_counts) {
     TmaArgs a{};
     int rc = setup_args(p, x, ldx, batch, offset, len, y1, y2, accumulate, ws, R, n_rc, a);
     if (rc) return rc;
+    a.ldy1 = ldy1; a.ldy2 = ldy2;
     *used_counts = !a.owner;
     if (!a.owner) {
         cudaError_t e = cudaMemsetAsync(a.counts, 0, (size_t)batch * (p->M1 + p->M2) * 4, s);

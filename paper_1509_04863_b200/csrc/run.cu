@@ -157,11 +157,13 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
             if (rc != TM_EUNSUPPORTED) return rc;
         }
         // step 3, then steps 4-9 in one tensor-core kernel (argmax + CRT in its epilogue)
-        int rc = tm_fold_impl(p, x, ldx, batch, 0, p->N, W.y1, W.y2, 0, W.fold_ws, s);
+        // (y rows at the 16-byte aligned strides ldy*_run: vector loads in the correlation)
+        int rc = tm_fold_impl_ld(p, x, ldx, batch, 0, p->N, W.y1, p->ldy1_run, W.y2, p->ldy2_run, 0, W.fold_ws, s);
         if (rc) return rc;
         tm_prof_mark(1, s);
         tm_prof_mark(2, s);
-        rc = tm_tc_any(p, W.y1, W.y2, t, p->K, batch, nullptr, nullptr, nullptr, residues, k, ws, s);
+        rc = tm_tc_any_ld(p, W.y1, W.y2, p->ldy1_run, p->ldy2_run, t, p->K, batch, nullptr, nullptr, nullptr,
+                          residues, k, ws, s);
         tm_prof_mark(3, s);
         tm_prof_mark(4, s);
         return rc;

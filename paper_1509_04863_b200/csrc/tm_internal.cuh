@@ -133,9 +133,15 @@ int tm_fft_f32_correlate(const tm_plan_s *p, const void *y1, const void *y2, con
 bool tm_fold_f32_ok(const tm_plan_s *p);
 size_t tm_fold_f32_ws_bytes(const tm_plan_s *p, int64_t batch);
 int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
-                void *y1, void *y2, int accumulate, void *parts, cudaStream_t s);
-int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset,
-                 int64_t len, void *y1, void *y2, int accumulate, void *ws, cudaStream_t s);
+                void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *parts, cudaStream_t s);
+// tm_fold with explicit row strides of y1, y2 (>= len_y1, len_y2; the public
+// tm_fold uses len_y*, tm_run's staged paths the 16-byte aligned ldy*_run)
+int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
+                    void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, cudaStream_t s);
+inline int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset,
+                        int64_t len, void *y1, void *y2, int accumulate, void *ws, cudaStream_t s) {
+    return tm_fold_impl_ld(p, x, ldx, batch, offset, len, y1, p->len_y1, y2, p->len_y2, accumulate, ws, s);
+}
 int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const void *tf,
                       int64_t batch, void *r1, void *r2, int32_t *resid, void *tile_scratch,
                       void *gntt_scratch, cudaStream_t s, void *tc_ws = nullptr);
