@@ -405,12 +405,23 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
     int pb = 0;
     uint32_t pph = 0;
     const uint32_t ring_u32 = smem_u32(ring);
+#ifdef TM_CONS_PROF
+    long long cp_wait = 0, cp_busy = 0, cp_t = clock64();
+#endif
     for (int64_t seq = 0;; ++seq) {
         mbar_wait(&full[s], ph);  // first stage of the next item (or the end marker)
         const int64_t item = item_q[seq & 7];
         mbar_wait(&pempty[pb], pph ^ 1);
         if constexpr (FUSED) mbar_wait(&ydone[pb], pph ^ 1);  // bounds the fold's lead over the NTT
         if (item < 0) {  // tell the epilogue (and the NTT / tensor-core warps) to stop
+#ifdef TM_CONS_PROF
+            if constexpr (TCM) {
+                if (a.tca.dbg && lane == 0 && warp < 8) {
+                    long long *d = a.tca.dbg + 8 * a.n_items + 4 * gridDim.x + 16 * blockIdx.x + 2 * warp;
+                    d[0] = cp_wait; d[1] = cp_busy;
+                }
+            }
+#endif
             if (lane == 0 && warp == 0) {
                 pitem[pb] = -1;
                 if constexpr (TCM) mbar_arrive(reinterpret_cast<uint64_t *>(smem + a.tc_off + a.tca.offMisc + tc::MISC_PBEGIN) + pb);
@@ -446,8 +457,15 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             for (int half = 0; half < 2; ++half) {
                 const int rbase = t * 16 + half * 8;
                 if (rbase >= nrow) break;
+#ifdef TM_CONS_PROF
+                { long long t1 = clock64(); cp_busy += t1 - cp_t; cp_t = t1; }
+#endif
                 mbar_wait(&full[s], ph);
+#ifdef TM_CONS_PROF
+                { long long t1 = clock64(); cp_wait += t1 - cp_t; cp_t = t1; }
+#endif
                 const uint32_t st = ring_u32 + s * STAGE_BYTES + colb;
+                const uint32_t rstride = full_tile ? TCOLS : width;
 #pragma unroll
                 for (int g = 0; g < 2; ++g) {
                     // 4 rows r = 8 half + 4 g + rho, rho = 0..3 (alpha = r >> 2 = 2 half + g)
@@ -455,13 +473,24 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
 #pragma unroll
                     for (int rho = 0; rho < 4; ++rho) {
                         const int rr = g * 4 + rho;
-                        uint4 v = make_uint4(0, 0, 0, 0);
+                        uint4 v;
+#ifndef TM_FOLD_BRANCHY
+                        // branch-free: every lane loads inside the stage (rows past the
+                        // item's end hold stale bytes) and a row mask zeroes what is not data
+                        const uint32_t msk = (full_tile || (active && rbase + rr < nrow)) ? 0x02020202u : 0u;
+                        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                     : "r"(st + rr * rstride));
+#else
+                        const uint32_t msk = 0x02020202u;
+                        v = make_uint4(0, 0, 0, 0);
                         if (full_tile || (active && rbase + rr < nrow))
                             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                                          : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                                         : "r"(st + rr * (full_tile ? TCOLS : width)));
-                        m[rho][0] = v.x & 0x02020202u; m[rho][1] = v.y & 0x02020202u;
-                        m[rho][2] = v.z & 0x02020202u; m[rho][3] = v.w & 0x02020202u;
+                                         : "r"(st + rr * rstride));
+#endif
+                        m[rho][0] = v.x & msk; m[rho][1] = v.y & msk;
+                        m[rho][2] = v.z & msk; m[rho][3] = v.w & msk;
                     }
                     if (!active) continue;
                     // M1: column sums in byte lanes
