@@ -20,6 +20,7 @@
 //    the finished y1/y2 directly (counts -> values, the mod-N wrap and the
 //    strategy-1 extension), so no workspace, memset or second kernel is needed.
 #include <cstdlib>
+#include <type_traits>
 
 #include "ntt_core.cuh"
 #include "tc_core.cuh"
@@ -468,49 +469,46 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 const uint32_t rstride = full_tile ? TCOLS : width;
 #pragma unroll
                 for (int g = 0; g < 2; ++g) {
-                    // 4 rows r = 8 half + 4 g + rho, rho = 0..3 (alpha = r >> 2 = 2 half + g)
-                    uint32_t m[4][4];
+                    // 4 rows r = 8 half + 4 g + rho, rho = 0..3 (alpha = r >> 2 = 2 half + g).
+                    // FULL (the tile is 16 whole rows of TCOLS columns): no row masks.
+                    auto group = [&](auto fullc) {
+                        constexpr bool FULL = decltype(fullc)::value;
+                        uint32_t m[4][4];
 #pragma unroll
-                    for (int rho = 0; rho < 4; ++rho) {
-                        const int rr = g * 4 + rho;
-                        uint4 v;
-#ifndef TM_FOLD_BRANCHY
-                        // branch-free: every lane loads inside the stage (rows past the
-                        // item's end hold stale bytes) and a row mask zeroes what is not data
-                        const uint32_t msk = (full_tile || (active && rbase + rr < nrow)) ? 0x02020202u : 0u;
-                        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                                     : "r"(st + rr * rstride));
-#else
-                        const uint32_t msk = 0x02020202u;
-                        v = make_uint4(0, 0, 0, 0);
-                        if (full_tile || (active && rbase + rr < nrow))
+                        for (int rho = 0; rho < 4; ++rho) {
+                            const int rr = g * 4 + rho;
+                            uint4 v;
+                            // branch-free: every lane loads inside the stage (rows past the
+                            // item's end hold stale bytes) and a row mask zeroes what is not data
+                            const uint32_t msk = (FULL || (active && rbase + rr < nrow)) ? 0x02020202u : 0u;
                             asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                                          : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                                         : "r"(st + rr * rstride));
-#endif
-                        m[rho][0] = v.x & msk; m[rho][1] = v.y & msk;
-                        m[rho][2] = v.z & msk; m[rho][3] = v.w & msk;
-                    }
-                    if (!active) continue;
-                    // M1: column sums in byte lanes
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) a1[w] = a1[w] + (m[0][w] + m[1][w]) + (m[2][w] + m[3][w]);
-                    // M2: row r, byte j -> window byte 16 - r + j.  With alpha = r >> 2 and
-                    // rho = r & 3, window word 4 - alpha + k' (k' = -1..3) receives
-                    // funnelshift_r(m[k'], m[k'+1], 8 rho) (m[-1] = m[4] = 0).
-                    const int alpha = half * 2 + g;
-#pragma unroll
-                    for (int kk = -1; kk < 4; ++kk) {
-                        uint32_t add = (kk >= 0) ? m[0][kk] : 0u;
-#pragma unroll
-                        for (int rho = 1; rho < 4; ++rho) {
-                            const uint32_t lo = (kk >= 0) ? m[rho][kk] : 0u;
-                            const uint32_t hi = (kk + 1 < 4) ? m[rho][kk + 1] : 0u;
-                            add += fsr(lo, hi, 8 * rho);
+                                         : "r"(st + rr * (FULL ? (uint32_t)TCOLS : rstride)));
+                            m[rho][0] = v.x & msk; m[rho][1] = v.y & msk;
+                            m[rho][2] = v.z & msk; m[rho][3] = v.w & msk;
                         }
-                        W[4 - alpha + kk] += add;
-                    }
+                        if (!FULL && !active) return;
+                        // M1: column sums in byte lanes
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) a1[w] = a1[w] + (m[0][w] + m[1][w]) + (m[2][w] + m[3][w]);
+                        // M2: row r, byte j -> window byte 16 - r + j.  With alpha = r >> 2 and
+                        // rho = r & 3, window word 4 - alpha + k' (k' = -1..3) receives
+                        // funnelshift_r(m[k'], m[k'+1], 8 rho) (m[-1] = m[4] = 0).
+                        const int alpha = half * 2 + g;
+#pragma unroll
+                        for (int kk = -1; kk < 4; ++kk) {
+                            uint32_t add = (kk >= 0) ? m[0][kk] : 0u;
+#pragma unroll
+                            for (int rho = 1; rho < 4; ++rho) {
+                                const uint32_t lo = (kk >= 0) ? m[rho][kk] : 0u;
+                                const uint32_t hi = (kk + 1 < 4) ? m[rho][kk + 1] : 0u;
+                                add += fsr(lo, hi, 8 * rho);
+                            }
+                            W[4 - alpha + kk] += add;
+                        }
+                    };
+                    if (full_tile) group(std::true_type{});
+                    else group(std::false_type{});
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
