@@ -314,6 +314,18 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
         int pb = 0;
         uint32_t pph = 0;
         for (;;) {
+            if constexpr (TCM) {
+                // the pair of this buffer is known as soon as its fold starts: stage
+                // x[0 .. K + q) (the wrap / extension terms) while it is being folded
+                mbar_wait(reinterpret_cast<uint64_t *>(smem + a.tc_off + a.tca.offMisc + tc::MISC_PBEGIN) + pb, pph);
+                const int64_t item0 = pitem[pb];
+                if (item0 >= 0 && a.owner && !a.block) {
+                    const int nx = (int)((a.K + decode(a, item0).nrow + 15) / 16);
+                    const uint4 *src = reinterpret_cast<const uint4 *>(a.x + decode(a, item0).b * a.ldx);
+                    uint4 *dst = reinterpret_cast<uint4 *>(xs);
+                    for (int i = et; i < nx; i += NE * 32) dst[i] = src[i];
+                }
+            }
             mbar_wait(&pfull[pb], pph);
             long long te0 = 0;
             if constexpr (TCM) te0 = tc::gtime();
@@ -336,10 +348,12 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 // 16-byte loads: one memory latency per pair instead of one per bin
                 // (TM_BLOCK reads neither term)
                 if (!a.block) {
-                    const int nx = (int)((a.K + q + 15) / 16);
-                    const uint4 *src = reinterpret_cast<const uint4 *>(a.x + it.b * a.ldx);
-                    uint4 *dst = reinterpret_cast<uint4 *>(xs);
-                    for (int i = et; i < nx; i += NE * 32) dst[i] = src[i];
+                    if constexpr (!TCM) {  // (TCM: staged above, before the fold finished)
+                        const int nx = (int)((a.K + q + 15) / 16);
+                        const uint4 *src = reinterpret_cast<const uint4 *>(a.x + it.b * a.ldx);
+                        uint4 *dst = reinterpret_cast<uint4 *>(xs);
+                        for (int i = et; i < nx; i += NE * 32) dst[i] = src[i];
+                    }
                     asm volatile("bar.sync 2, %0;" ::"n"(NE * 32) : "memory");
                 }
                 const int8_t *xb = reinterpret_cast<const int8_t *>(xs);
