@@ -151,6 +151,19 @@ __device__ __forceinline__ int32_t comb_at(const uint16_t *pv, int stride, int d
     return v;
 }
 
+// comb_at for pad = 16 ntile <= 1024 (at most three strips hold a diagonal): the
+// strips are w1 = max(d, 0) >> 9 and the next two, with no loop
+__device__ __forceinline__ int32_t comb3(const uint16_t *pv, int stride, int d, int pad, int nw) {
+    const int w1 = d < 0 ? 0 : (d >> 9);
+    int32_t v = 0;
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        const int w = w1 + e, j = d - 512 * w + pad;
+        if (w < nw && j >= 0 && j < 512 + pad) v += (int32_t)pv[w * stride + j];
+    }
+    return v;
+}
+
 constexpr int ntt_threads(int logl2) { return logl2 > 0 ? (1 << (logl2 - 4)) : 0; }
 
 // NST: ring stages.  LOGL2 > 0 selects the fused kernel: NT = L2/16 extra threads
@@ -362,10 +375,14 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 const int dlo = -16 * ntile;
                 // (a straight-line / unrolled variant of this loop measured slower in the
                 // fused kernel: it competes harder with the fold warps for issue slots)
+                const int pad = 16 * ntile, nw = width >> 9;
+                const bool c3 = pad <= 1024;
                 for (int k = et; k < M2; k += NE * 32) {
                     // bin k collects the unwrapped diagonals d = k and d = k - M2 (d >= dlo)
-                    int32_t C = comb_at(pv, a.priv_stride, k, ntile, width);
-                    if (k - M2 >= dlo) C += comb_at(pv, a.priv_stride, k - M2, ntile, width);
+                    int32_t C = c3 ? comb3(pv, a.priv_stride, k, pad, nw) : comb_at(pv, a.priv_stride, k, ntile, width);
+                    if (k - M2 >= dlo)
+                        C += c3 ? comb3(pv, a.priv_stride, k - M2, pad, nw)
+                                : comb_at(pv, a.priv_stride, k - M2, ntile, width);
                     int gs = M1 - k;
                     if (gs < 0) gs += M2;
                     int32_t v = q - (gs < q ? 1 : 0) - C;
