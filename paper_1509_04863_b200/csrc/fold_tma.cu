@@ -377,6 +377,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 // fused kernel: it competes harder with the fold warps for issue slots)
                 const int pad = 16 * ntile, nw = width >> 9;
                 const bool c3 = pad <= 1024;
+#pragma unroll 2
                 for (int k = et; k < M2; k += NE * 32) {
                     // bin k collects the unwrapped diagonals d = k and d = k - M2 (d >= dlo)
                     int32_t C = c3 ? comb3(pv, a.priv_stride, k, pad, nw) : comb_at(pv, a.priv_stride, k, ntile, width);
