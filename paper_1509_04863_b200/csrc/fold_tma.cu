@@ -241,8 +241,12 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 const int64_t b = pitem[pb];  // fused mode: items are whole pairs
                 if (b < 0) break;
                 tc::tc_pre<GS>(a.tca, tsm, b, gt);  // template side while the pair is being folded
+                // y_1 is complete when the consumers finish the pair (pfull): stage it
+                // while the epilogue warps finish y_2
+                tc::group_wait<GS>(&pfull[pb], pph, gt >> 5);
+                const int fl1 = tc::stage_y(a.tca, tsm + a.tca.offB, b, 0, 1, gt >> 5, lane, 0, 1);
                 tc::group_wait<GS>(&yready[pb], pph, gt >> 5);
-                tc::tc_main<GS>(a.tca, tsm, b, gt, warp & 3, tbase, mph);
+                tc::tc_main<GS>(a.tca, tsm, b, gt, warp & 3, tbase, mph, fl1);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&ydone[pb]);
                 if (++pb == 2) { pb = 0; pph ^= 1; }

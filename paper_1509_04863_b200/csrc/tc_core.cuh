@@ -135,14 +135,14 @@ __device__ __forceinline__ int32_t limb(int32_t v, int l, int nl) {
 // per block row: lane i holds entries 4i .. 4i+3 (chunk h = i / 4).  Returns
 // this thread's range flags (bit 0: some |y| needs 2 limbs, bit 1: 3, bit 2: 4).
 __device__ __forceinline__ int stage_yw(const TcArgs &a, uint8_t *B, int64_t b, int l, int nl, int64_t s_begin,
-                                        int nrows, int warp, int lane) {
+                                        int nrows, int warp, int lane, int jlo = 0, int jhi = 2) {
     uint32_t mag = 0;
     const uint32_t lbo = 32u * nrows;  // bytes per chunk column h: 2 nrows rows of 16 B
     const int h = lane >> 2, wq = lane & 3;
     constexpr int RB = TC_RB;             // block rows in flight per warp
     constexpr int NW = NTHR / 32;
 #pragma unroll 1
-    for (int j = 0; j < 2; ++j) {
+    for (int j = jlo; j < jhi; ++j) {
         const int32_t *yr = a.y[j] + b * a.ldy[j];
         const int64_t len = a.len[j];
         const bool al = ((((uintptr_t)yr) & 15) == 0);
@@ -182,8 +182,9 @@ __device__ __forceinline__ int stage_yw(const TcArgs &a, uint8_t *B, int64_t b, 
     return (mag > 127u ? 1 : 0) | (mag > 2047u ? 2 : 0) | (mag > 32767u ? 4 : 0);
 }
 
-__device__ __forceinline__ int stage_y(const TcArgs &a, uint8_t *B, int64_t b, int l, int nl, int warp, int lane) {
-    return stage_yw(a, B, b, l, nl, 0, a.R, warp, lane);
+__device__ __forceinline__ int stage_y(const TcArgs &a, uint8_t *B, int64_t b, int l, int nl, int warp, int lane,
+                                       int jlo = 0, int jhi = 2) {
+    return stage_yw(a, B, b, l, nl, 0, a.R, warp, lane, jlo, jhi);
 }
 
 // TMEM -> registers for 8 output blocks [a0, a0 + 8) of both moduli (limb l
@@ -303,8 +304,11 @@ __device__ __forceinline__ void tc_pre(const TcArgs &a, uint8_t *sm, int64_t b, 
 // (a.ncols allocated by the caller), mph = commits already completed on the
 // group's mbarrier (sm + offMisc, count 1), updated.
 template <class Sync>
+// fl1 >= 0: y_1 was already staged as limb 0 of a one-limb pass (stage_y with
+// jlo = 0, jhi = 1, while y_2 was being finished) and fl1 is this thread's
+// range flags of it; only y_2 is staged here.
 __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b, int tid, int qw, uint32_t tbase,
-                                        uint32_t &mph) {
+                                        uint32_t &mph, int fl1 = -1) {
     const int warp = tid >> 5, lane = tid & 31;
     long long tstamp[6];
     tstamp[0] = gtime();
@@ -317,7 +321,7 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
     uint8_t *tp = sm + a.offTp;
 
     // ---- y -> B: limb 0 (= y itself when |y| <= 127, the common case) ----
-    const int fl = stage_y(a, B, b, 0, 1, warp, lane);
+    const int fl = fl1 >= 0 ? (fl1 | stage_y(a, B, b, 0, 1, warp, lane, 1, 2)) : stage_y(a, B, b, 0, 1, warp, lane);
     const int need2 = Sync::sync_or(fl & 1);
     const int need3 = Sync::sync_or(fl & 2);
     int nl = need3 ? 3 : (need2 ? 2 : 1);
