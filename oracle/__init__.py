@@ -82,6 +82,12 @@ def lib():
             getattr(L, n).argtypes = [_p, _i64, _i64, _p, _p]
         L.or_block_correlate_f64.restype = None
         L.or_block_correlate_f64.argtypes = [_p, _i64, _p, _i64, _p]
+        L.or_crt_multi.restype = _i64
+        L.or_crt_multi.argtypes = [_p, _p, ctypes.c_int]
+        L.or_crt_sets_multi.restype = _i64
+        L.or_crt_sets_multi.argtypes = [_p, _p, ctypes.c_int, _i64]
+        L.or_ftm_multi_i8.restype = _i64
+        L.or_ftm_multi_i8.argtypes = [_p, _i64, _p, _i64, _p, ctypes.c_int, _p]
         for n in ("or_ftm_block_i8", "or_ftm_block_f32"):
             getattr(L, n).restype = _i64
             getattr(L, n).argtypes = [_p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p]
@@ -319,3 +325,30 @@ def ftm_block(x: np.ndarray, t: np.ndarray, M: int = 0, want_vectors: bool = Tru
     r1 = np.zeros(M1, dt); r2 = np.zeros(M2, dt)
     k = fn(_ptr(x), N, _ptr(t), K, M, _ptr(res), _ptr(y1), _ptr(y2), _ptr(r1), _ptr(r2))
     return dict(k=k, residues=(int(res[0]), int(res[1])), M1=M1, M2=M2, y1=y1, y2=y2, r1=r1, r2=r2)
+
+
+# --------------------------------------------------------------------------
+# Theorem 4 with alpha moduli
+# --------------------------------------------------------------------------
+def crt_multi(m, M) -> int:
+    """The unique z in [0, prod M) with z = m_j (mod M_j); -1 if not co-prime."""
+    m = np.ascontiguousarray(m, np.int64); M = np.ascontiguousarray(M, np.int64)
+    return lib().or_crt_multi(_ptr(m), _ptr(M), len(M))
+
+
+def crt_sets_multi(m, M, N: int) -> int:
+    """Steps 8-9 literally: the common element of the alpha candidate sets."""
+    m = np.ascontiguousarray(m, np.int64); M = np.ascontiguousarray(M, np.int64)
+    return lib().or_crt_sets_multi(_ptr(m), _ptr(M), len(M), N)
+
+
+def ftm_multi(x: np.ndarray, t: np.ndarray, moduli) -> dict:
+    """FTM() over alpha pairwise co-prime moduli (int8 data): k and residues."""
+    x = _as_input(x); t = _as_input(t)
+    assert _is_int(x) and _is_int(t)
+    M = np.ascontiguousarray(moduli, np.int64)
+    res = np.zeros(len(M), np.int64)
+    k = lib().or_ftm_multi_i8(_ptr(x), x.shape[0], _ptr(t), t.shape[0], _ptr(M), len(M), _ptr(res))
+    if k == -3:
+        raise ValueError("moduli must be >= K, pairwise co-prime, with product > N")
+    return dict(k=k, residues=tuple(int(v) for v in res))

@@ -298,6 +298,88 @@ int64_t or_ftm_f32(const float *x, int64_t N, const float *t, int64_t K, int64_t
 }
 
 /* ------------------------------------------------------------------ */
+/* Theorem 4 with alpha moduli: "any integer m is uniquely     */
+/* specified mod N by its remainders modulo alpha relatively prime         */
+/* integers M_1 .. M_alpha as long as prod M_i >= N" (Alg. 1 uses alpha =  */
+/* 2).  The unique z in [0, prod M_i) with       */
+/* z = m_i (mod M_i), by folding the congruences in one at a time with the */
+/* two-modulus rule of or_crt (extended Euclid).  Returns -1 if two moduli */
+/* share a factor, INT64_MAX if z does not fit (prod M_i beyond 2^63).     */
+/* ------------------------------------------------------------------ */
+int64_t or_crt_multi(const int64_t *m, const int64_t *M, int alpha) {
+    __int128 z = m[0], P = M[0];
+    for (int j = 1; j < alpha; ++j) {
+        /* extended Euclid on (P mod M_j, M_j) -> inverse of P modulo M_j */
+        __int128 old_r = P % M[j], r = M[j], old_s = 1, s = 0;
+        while (r != 0) {
+            __int128 qq = old_r / r, tmp;
+            tmp = r;  r = old_r - qq * r;  old_r = tmp;
+            tmp = s;  s = old_s - qq * s;  old_s = tmp;
+        }
+        if (old_r != 1) return -1;
+        __int128 inv = old_s % M[j];
+        if (inv < 0) inv += M[j];
+        __int128 d = ((__int128)m[j] - z) % M[j];
+        if (d < 0) d += M[j];
+        z += P * ((d * inv) % M[j]);   /* z = m_i (mod M_i) for every i <= j */
+        P *= M[j];
+        if (P > ((__int128)1 << 100)) return INT64_MAX;
+    }
+    return z > (__int128)INT64_MAX ? INT64_MAX : (int64_t)z;
+}
+
+/* Steps 8-9 literally for alpha sets: the elements common to   */
+/* every S_Mj = { m_j + i M_j : i < ceil(N / M_j) }.  Returns the single     */
+/* common element, -1 if none, -2 if several.  Small N only (tests).        */
+int64_t or_crt_sets_multi(const int64_t *m, const int64_t *M, int alpha, int64_t N) {
+    int64_t found = -1, count = 0;
+    for (int64_t i = 0; i < or_ceil_div(N, M[0]); ++i) {
+        int64_t a = m[0] + i * M[0];
+        int in_all = 1;
+        for (int j = 1; j < alpha && in_all; ++j) {
+            in_all = 0;
+            for (int64_t u = 0; u < or_ceil_div(N, M[j]); ++u)
+                if (m[j] + u * M[j] == a) { in_all = 1; break; }
+        }
+        if (in_all) { if (count == 0) found = a; ++count; }
+    }
+    return count > 1 ? -2 : found;
+}
+
+/* FTM() with alpha moduli: for each M_j the Eq. 2 fold (strategy 1, M_j + K */
+/* entries), the correlation and the argmax of Alg. 1 steps 3-7; then z =    */
+/* or_crt_multi and k = z if z < N else -1 (reading C9).  Requires K <= M_j, */
+/* pairwise co-prime moduli and prod M_j > N (else returns -3).  Outputs:    */
+/* residues[alpha] (may be NULL).                                            */
+int64_t or_ftm_multi_i8(const int8_t *x, int64_t N, const int8_t *t, int64_t K, const int64_t *M, int alpha,
+                        int64_t *residues) {
+    __int128 P = 1;
+    for (int j = 0; j < alpha; ++j) {
+        if (M[j] < K) return -3;
+        for (int i = 0; i < j; ++i) {
+            int64_t a = M[i], b = M[j];
+            while (b) { int64_t r = a % b; a = b; b = r; }
+            if (a != 1) return -3;
+        }
+        P *= M[j];
+        if (P > ((__int128)1 << 100)) P = ((__int128)1 << 100);
+    }
+    if (P <= N) return -3;
+    int64_t m[16];
+    for (int j = 0; j < alpha; ++j) {
+        int64_t *y = (int64_t *)malloc(sizeof(int64_t) * (M[j] + K));
+        int64_t *r = (int64_t *)malloc(sizeof(int64_t) * M[j]);
+        or_fold_i8(x, N, M[j], K, 0, N, y);                          /* step 3 */
+        or_correlate_i64(y, M[j], K, t, r);                          /* steps 4-6 */
+        m[j] = or_argmax_i64(r, M[j]);                               /* step 7 */
+        free(y); free(r);
+    }
+    if (residues) for (int j = 0; j < alpha; ++j) residues[j] = m[j];
+    int64_t z = or_crt_multi(m, M, alpha);                           /* steps 8-9 */
+    return (z >= 0 && z < N) ? z : -1;
+}
+
+/* ------------------------------------------------------------------ */
 /* Strategy 2 (Theorem 2): the Block sampling       */
 /* matrix Phi = [Phi_M Phi_M ... Phi_M] (ceil(N/M) blocks), Phi_M an M x M */
 /* circulant, applied to x zero-padded to ceil(N/M)*M samples ("we can    */

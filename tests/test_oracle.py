@@ -489,3 +489,57 @@ def test_block_strategy_recovers_every_isolated_window():
         s = brute_scores(x, t)
         assert s[k0] == K and (s < K).sum() == N - 1
         assert oracle.ftm_block(x, t, want_vectors=False)["k"] == k0
+
+
+# ------------------------------------------------- Theorem 4 with alpha moduli (f4(ii))
+@pytest.mark.parametrize("M", [(3, 5, 7), (4, 5, 9, 7), (11, 12, 13), (2, 3, 5, 7, 11)])
+def test_crt_multi_exhaustive_against_literal_sets(M):
+    """Every residue tuple of pairwise co-prime moduli: the CRT value is the one
+    common element of the alpha candidate sets (Thm 4),
+    and it reproduces the residues."""
+    P = int(np.prod(M))
+    for z in range(P):
+        m = [z % Mj for Mj in M]
+        assert oracle.crt_multi(m, M) == z
+    rng = np.random.default_rng(len(M))
+    for _ in range(40):
+        m = [int(rng.integers(0, Mj)) for Mj in M]
+        z = oracle.crt_multi(m, M)
+        assert oracle.crt_sets_multi(m, M, P) == z
+
+
+def test_crt_multi_special_cases():
+    assert oracle.crt_multi([5], [7]) == 5
+    assert oracle.crt_multi([1, 2], [4, 6]) == -1          # not co-prime
+    for m1, m2 in ((0, 0), (3, 4), (255, 0), (17, 200)):
+        assert oracle.crt_multi([m1, m2], [256, 257]) == oracle.crt(m1, 256, m2, 257)
+
+
+def test_ftm_multi_two_moduli_equals_algorithm1():
+    """alpha = 2 with (M, M + 1) is Algorithm 1 itself."""
+    rng = np.random.default_rng(41)
+    N, K = 4096, 64
+    for trial in range(5):
+        x = rand_pm1(rng, N)
+        k0 = int(rng.integers(0, N))
+        t = x[(k0 + np.arange(K)) % N].copy()
+        a = oracle.ftm(x, t, want_vectors=False)
+        b = oracle.ftm_multi(x, t, (K, K + 1))
+        assert (a["k"], a["residues"]) == (b["k"], b["residues"])
+
+
+def test_ftm_multi_three_small_moduli_recovers_isolated_windows():
+    """alpha = 3 lets M be far below sqrt(N) (17 * 18 * 19 > 4096 while 17 * 18
+    < 4096): with x zero outside a +-1 window equal to t, every shift whose
+    window avoids the doubly counted head (k0 >= max s_j) is recovered."""
+    N, K, M = 4096, 16, (17, 18, 19)
+    with pytest.raises(ValueError):
+        oracle.ftm_multi(np.zeros(N, np.int8), np.ones(K, np.int8), (17, 18))   # 306 <= N
+    smax = max(-(-N // Mj) * Mj - N for Mj in M)
+    rng = np.random.default_rng(8)
+    t = rand_pm1(rng, K)
+    for k0 in range(smax, N - K + 1, 7):
+        x = np.zeros(N, np.int8)
+        x[k0:k0 + K] = t
+        o = oracle.ftm_multi(x, t, M)
+        assert o["k"] == k0 and o["residues"] == tuple(k0 % Mj for Mj in M)
