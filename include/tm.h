@@ -261,6 +261,41 @@ enum { TM_PATH_STAGED = 0, TM_PATH_STAGED_TC = 1, TM_PATH_FUSED_TC = 2, TM_PATH_
        TM_PATH_OVERLAP = 4 };
 int tm_run_path(tm_plan plan, int64_t batch);
 
+/*
+ * ---- More than two moduli: Theorem 4 with alpha moduli ----
+ * "Any integer m is uniquely specified mod N by its remainders modulo alpha
+ * relatively prime integers M_1 .. M_alpha as long as prod M_i >= N" (read as
+ * > N, reading C8); Algorithm 1 is the case alpha = 2, M_2 = M_1 + 1.
+ * More moduli allow M_j far below sqrt(N) (each M_j >= K still), at the
+ * price of one fold + correlation per pair of moduli.
+ *
+ * tm_mplan_create -- moduli: host array of alpha (2 <= alpha <= 8) pairwise
+ *   co-prime integers, K <= M_j < 2^31, prod M_j > N.  Each M_j is folded,
+ *   correlated and argmax-ed exactly as in Algorithm 1 (strategy 1, Eq. 2,
+ *   reading C5's mod-N wrap), by sub-plans of moduli (M, M + 1): when both M
+ *   and M + 1 are in the set one sub-plan serves both, otherwise the M + 1
+ *   residue is computed and discarded.  dtype / flags as tm_plan_create
+ *   (TM_ALIAS_REPAIR is rejected).  Errors: TM_EINVAL for bad arguments (the
+ *   reason in tm_last_error), TM_EUNSUPPORTED / TM_ECUDA from a sub-plan.
+ * tm_mplan_workspace_bytes -- device workspace tm_mplan_run needs for batch.
+ * tm_mplan_run -- x int8 [batch][ldx] (ldx >= N), t int8 [batch][K], device;
+ *   residues int32 [batch][alpha] (may be NULL): m~_j of modulus moduli[j];
+ *   k int64 [batch]: the CRT value z in [0, prod M_j) if z < N, else -1
+ *   (reading C9).  Enqueued on stream; ws as sized above.
+ * tm_crt_multi -- steps 8-9 alone (Garner's mixed-radix CRT, one thread per
+ *   pair): residues int32 [batch][alpha] (device), moduli host [alpha] as
+ *   above, k int64 [batch] (device).
+ */
+typedef struct tm_mplan_s *tm_mplan;
+int tm_mplan_create(tm_mplan *out, int64_t N, int64_t K, const int64_t *moduli, int alpha, uint64_t seed,
+                    int dtype, uint32_t flags);
+size_t tm_mplan_workspace_bytes(tm_mplan plan, int64_t batch);
+int tm_mplan_run(tm_mplan plan, const void *x, int64_t ldx, const void *t, int64_t batch, int32_t *residues,
+                 int64_t *k, void *ws, void *stream);
+int tm_crt_multi(const int32_t *residues, int64_t batch, int alpha, const int64_t *moduli, int64_t N, int64_t *k,
+                 void *stream);
+void tm_mplan_destroy(tm_mplan plan);
+
 const char *tm_status_string(int status);
 const char *tm_last_error(void);
 

@@ -19,6 +19,7 @@ EXPORTED_SYMBOLS = (
     "tm_plan_create", "tm_plan_query", "tm_workspace_bytes", "tm_plan_destroy", "tm_generate",
     "tm_fold", "tm_fold_template", "tm_correlate", "tm_match", "tm_run", "tm_run_host", "tm_correlate_match", "tm_correlate_many",
     "tm_status_string", "tm_last_error", "tm_launch_count", "tm_profile_events", "tm_run_path",
+    "tm_mplan_create", "tm_mplan_workspace_bytes", "tm_mplan_run", "tm_crt_multi", "tm_mplan_destroy",
 )
 RUN_PATHS = {0: "staged (fold -> NTT/fp32 correlation -> CRT)", 1: "staged (fold -> tensor-core correlation)",
              2: "fused (fold + tensor-core correlation in one kernel)", 3: "fused (fold + NTT)", 4: "overlap"}
@@ -95,6 +96,16 @@ def lib():
         L.tm_profile_events.argtypes = [ctypes.POINTER(_p), ctypes.c_int]
         L.tm_run_path.restype = ctypes.c_int
         L.tm_run_path.argtypes = [_p, _i64]
+        L.tm_mplan_create.restype = ctypes.c_int
+        L.tm_mplan_create.argtypes = [ctypes.POINTER(_p), _i64, _i64, _p, ctypes.c_int, _u64, ctypes.c_int, _u32]
+        L.tm_mplan_workspace_bytes.restype = ctypes.c_size_t
+        L.tm_mplan_workspace_bytes.argtypes = [_p, _i64]
+        L.tm_mplan_run.restype = ctypes.c_int
+        L.tm_mplan_run.argtypes = [_p, _p, _i64, _p, _i64, _p, _p, _p, _p]
+        L.tm_crt_multi.restype = ctypes.c_int
+        L.tm_crt_multi.argtypes = [_p, _i64, ctypes.c_int, _p, _i64, _p, _p]
+        L.tm_mplan_destroy.restype = None
+        L.tm_mplan_destroy.argtypes = [_p]
         L.tm_status_string.restype = ctypes.c_char_p
         L.tm_status_string.argtypes = [ctypes.c_int]
         L.tm_last_error.restype = ctypes.c_char_p
@@ -308,3 +319,65 @@ class Plan:
         dev_t = torch.empty((2 * chunk, self.K), dtype=self.x_dtype, device=device)
         dev_out = torch.empty(((batch * 8 + 255) // 256 * 256) + batch * 8, dtype=torch.uint8, device=device)
         return dev_x, dev_t, dev_out, self.workspace(chunk, device)
+
+
+class MultiPlan:
+    """tm_mplan: Theorem 4 with alpha pairwise co-prime moduli.
+    moduli: alpha integers, K <= M_j < 2^31, product > N."""
+
+    def __init__(self, N: int, K: int, moduli, seed: int = 0, dtype: str = "int8", binary: bool = True,
+                 engine: str | None = None, block: bool = False):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1509_04863_b200.MultiPlan needs a CUDA device (no CPU fallback)")
+        self.N, self.K = N, K
+        self.moduli = [int(m) for m in moduli]
+        self.alpha = len(self.moduli)
+        dt = {"int8": TM_I8, "float32": TM_F32}[str(dtype).replace("torch.", "")]
+        flags = TM_BINARY if (binary and dt == TM_I8) else 0
+        if dt == TM_I8:
+            flags |= _ENGINES[engine]
+        if block:
+            flags |= TM_BLOCK
+        self._M = (ctypes.c_int64 * self.alpha)(*self.moduli)
+        h = _p()
+        _check(lib().tm_mplan_create(ctypes.byref(h), N, K, ctypes.cast(self._M, _p), self.alpha, seed, dt, flags),
+               "tm_mplan_create")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.tm_mplan_destroy(h)
+            self._h = None
+
+    def workspace(self, batch: int, device="cuda"):
+        import torch
+        n = lib().tm_mplan_workspace_bytes(self._h, batch)
+        return torch.empty(max(int(n), 1), dtype=torch.uint8, device=device)
+
+    def run(self, x, t, residues=None, k=None, ws=None, stream=None):
+        """Steps 3-7 per modulus, then Garner's CRT: (residues [batch][alpha], k [batch])."""
+        import torch
+        batch = x.shape[0]
+        if residues is None:
+            residues = torch.empty((batch, self.alpha), dtype=torch.int32, device=x.device)
+        if k is None:
+            k = torch.empty(batch, dtype=torch.int64, device=x.device)
+        if ws is None:
+            ws = self.workspace(batch, x.device)
+        _check(lib().tm_mplan_run(self._h, _ptr(x), _ld(x), _ptr(t), batch, _ptr(residues), _ptr(k), _ptr(ws),
+                                  _stream(stream)), "tm_mplan_run")
+        return residues, k
+
+
+def crt_multi(residues, moduli, N: int, k=None, stream=None):
+    """tm_crt_multi: steps 8-9 alone for residues int32 [batch][alpha] (device)."""
+    import torch
+    batch, alpha = residues.shape
+    if k is None:
+        k = torch.empty(batch, dtype=torch.int64, device=residues.device)
+    M = (ctypes.c_int64 * alpha)(*[int(m) for m in moduli])
+    _check(lib().tm_crt_multi(_ptr(residues), batch, alpha, ctypes.cast(M, _p), N, _ptr(k), _stream(stream)),
+           "tm_crt_multi")
+    return k

@@ -77,8 +77,10 @@ static uint32_t inv_mod(int64_t a, int64_t m) {
     return (uint32_t)v;
 }
 
-extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t seed,
-                              int dtype, uint32_t flags) {
+// need_product = 0: a sub-plan of a multi-modulus plan (tm_mplan_create), whose
+// own pair of moduli need not cover N (Theorem 4 is applied to all alpha moduli)
+int tm_plan_create_impl(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t seed, int dtype, uint32_t flags,
+                        int need_product) {
     if (!out) { tm_set_error("tm_plan_create: out is NULL"); return TM_EINVAL; }
     *out = nullptr;
     if (N < 1 || N >= (int64_t(1) << 62)) { tm_set_error("tm_plan_create: N=%lld out of range", (long long)N); return TM_EINVAL; }
@@ -91,7 +93,7 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
     if ((flags & TM_BINARY) && dtype != TM_I8) { tm_set_error("tm_plan_create: TM_BINARY needs TM_I8"); return TM_EINVAL; }
     int64_t M1 = M ? M : K, M2 = M1 + 1;
     if (M1 < K) { tm_set_error("tm_plan_create: M1=%lld < K=%lld (Alg. 1 step 2 needs M1 >= K)", (long long)M1, (long long)K); return TM_EINVAL; }
-    if ((__int128)M1 * (__int128)M2 <= (__int128)N) {
+    if (need_product && (__int128)M1 * (__int128)M2 <= (__int128)N) {
         int64_t kmin = 1;
         while ((__int128)kmin * (kmin + 1) <= (__int128)N) kmin *= 2;
         int64_t lo = kmin / 2;
@@ -190,6 +192,11 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *ou
     }
     *out = p;
     return TM_OK;
+}
+
+extern "C" __attribute__((visibility("default"))) int tm_plan_create(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t seed,
+                              int dtype, uint32_t flags) {
+    return tm_plan_create_impl(out, N, K, M, seed, dtype, flags, 1);
 }
 
 extern "C" __attribute__((visibility("default"))) int tm_plan_query(tm_plan plan, tm_plan_info *info) {

@@ -136,6 +136,8 @@ int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
                 void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *parts, cudaStream_t s);
 // tm_fold with explicit row strides of y1, y2 (>= len_y1, len_y2; the public
 // tm_fold uses len_y*, tm_run's staged paths the 16-byte aligned ldy*_run)
+int tm_plan_create_impl(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t seed, int dtype, uint32_t flags,
+                        int need_product);
 int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
                     void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, cudaStream_t s);
 inline int tm_fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset,

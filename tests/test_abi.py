@@ -64,6 +64,16 @@ def test_plan_create_rejects_invalid_without_gpu(libtm):
     assert L.tm_plan_create(ctypes.byref(h), 1024, 64, 0, 0, 1, 1) == 1   # TM_BINARY needs int8
     assert L.tm_plan_create(ctypes.byref(h), 1024, 64, 0, 0, 0, 16 | 8) == 1  # TM_BLOCK excludes TM_ALIAS_REPAIR
     assert L.tm_plan_create(ctypes.byref(h), 1024, 64, 0, 0, 0, 32) == 1   # unknown flag
+    M = (ctypes.c_int64 * 3)(17, 18, 20)                                      # 18, 20 not co-prime
+    L.tm_mplan_create.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                  ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32]
+    assert L.tm_mplan_create(ctypes.byref(h), 4096, 16, M, 3, 0, 0, 1) == 1
+    assert b"co-prime" in L.tm_last_error()
+    M = (ctypes.c_int64 * 2)(17, 18)                                          # 306 <= N
+    assert L.tm_mplan_create(ctypes.byref(h), 4096, 16, M, 2, 0, 0, 1) == 1
+    M = (ctypes.c_int64 * 3)(15, 17, 19)                                      # 15 < K
+    assert L.tm_mplan_create(ctypes.byref(h), 4096, 16, M, 3, 0, 0, 1) == 1
+    assert L.tm_mplan_create(ctypes.byref(h), 4096, 16, M, 1, 0, 0, 1) == 1   # alpha < 2
 
 
 def test_ntt_constants():

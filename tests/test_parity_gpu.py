@@ -599,3 +599,62 @@ def test_block_strategy_has_no_wrap_alias(tm):
     _, kl = tm.Plan(N, K).run(up(x_h), up(t_h))
     kb, kl = kb.cpu().numpy(), kl.cpu().numpy()
     assert np.sum(kb == k0) > np.sum(kl == k0)
+
+
+# ------------------------------------------------------------- alpha > 2 moduli (Theorem 4)
+@pytest.mark.parametrize("N,K,moduli,B,binary", [
+    (2 ** 16, 64, (65, 66, 67), 4, True),               # generic folds, M far below sqrt(N)
+    (2 ** 20, 1024, (1024, 1025, 1027), 3, True),       # packed (1024, 1025) sub-plan + a generic one
+    (2 ** 24, 256, (257, 258, 259, 263), 2, True),      # K = 256 at N = 2^24: impossible with alpha = 2
+    (30000, 40, (41, 43, 47), 3, False),                # general int8 data, N not a multiple of any M
+])
+def test_multi_moduli_against_oracle(tm, N, K, moduli, B, binary):
+    """tm_mplan_run: every residue and k equal the oracle's alpha-modulus FTM."""
+    plan = tm.MultiPlan(N, K, moduli, seed=4, binary=binary)
+    rng = np.random.default_rng(N + K)
+    if binary:
+        x_h, t_h, _ = tmgen.batch(4, 0, B, N, K, 0.05)
+    else:
+        x_h = rng.integers(-128, 128, (B, N)).astype(np.int8)
+        t_h = np.stack([x_h[b][(np.arange(K) + 97 * b) % N] for b in range(B)]).astype(np.int8)
+    res, k = plan.run(up(x_h), up(t_h))
+    torch.cuda.synchronize()
+    res, k = res.cpu().numpy(), k.cpu().numpy()
+    for b in range(B):
+        o = oracle.ftm_multi(x_h[b], t_h[b], moduli)
+        assert tuple(int(v) for v in res[b]) == o["residues"] and int(k[b]) == o["k"], b
+
+
+def test_multi_moduli_recovers_planted_shifts(tm):
+    """alpha = 3 at N = 2^24 with M = 257.. (two moduli would need M >= 4096):
+    x zero outside a +-1 window equal to t, so (Tx)_k0 = K is the unique peak
+    and every shift past the doubly counted head is recovered exactly (at
+    random +-1 x this K would be far below the paper's K^2 / log K ~ N regime)."""
+    N, K, B, M = 2 ** 24, 256, 8, (257, 258, 259)
+    plan = tm.MultiPlan(N, K, M, binary=False)
+    rng = np.random.default_rng(21)
+    smax = max(-(-N // Mj) * Mj - N for Mj in M)
+    k0 = rng.integers(smax, N - K, B)
+    x_h = np.zeros((B, N), np.int8)
+    t_h = (1 - 2 * rng.integers(0, 2, (B, K))).astype(np.int8)
+    for b in range(B):
+        x_h[b, k0[b]:k0[b] + K] = t_h[b]
+    res, k = plan.run(up(x_h), up(t_h))
+    k = k.cpu().numpy()
+    np.testing.assert_array_equal(k, k0)
+    for b in range(2):
+        assert int(k[b]) == oracle.ftm_multi(x_h[b], t_h[b], M)["k"]
+
+
+def test_crt_multi_kernel(tm):
+    """tm_crt_multi (Garner) equals the oracle's CRT on random residues, k = -1 beyond N."""
+    rng = np.random.default_rng(3)
+    for M in ((3, 5, 7), (257, 258, 259, 263), (65521, 65519, 65497), (1 << 30, 3, 5, 7, 11, 13, 17, 19)):
+        B = 4000
+        res = np.stack([rng.integers(0, Mj, B) for Mj in M], axis=1).astype(np.int32)
+        P = int(np.prod([int(v) for v in M]))
+        N = min(P - 1, (1 << 62) - 1) // 2 + 1
+        k = tm.crt_multi(up(res), M, N).cpu().numpy()
+        for b in range(0, B, 37):
+            z = oracle.crt_multi(res[b].astype(np.int64), M)
+            assert int(k[b]) == (z if z < N else -1), (M, b)
