@@ -13,7 +13,9 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum",
         "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active",
-        "lts__t_bytes.sum", "launch__shared_mem_per_block_dynamic"]
+        "lts__t_bytes.sum", "launch__shared_mem_per_block_dynamic",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 rows = list(csv.reader(open(sys.argv[1])))
 hdr, units = rows[0], rows[1]
 out = {}
