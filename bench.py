@@ -385,6 +385,7 @@ def run_single_signal(args, wl, rank, world, local, dev):
     y2 = torch.empty((1, plan.len_y2), dtype=torch.int32, device=dev)
     res = torch.empty((1, 2), dtype=torch.int32, device=dev)
     k = torch.empty(1, dtype=torch.int64, device=dev)
+    keys = torch.empty((1, 2), dtype=torch.int64, device=dev)
     torch.cuda.synchronize()
 
     def step(ev=None):
@@ -394,7 +395,12 @@ def run_single_signal(args, wl, rank, world, local, dev):
         if world > 1:
             tmdist.allreduce_folds(y1, y2)
         if ev: ev[2].record(stream)
-        plan.correlate_match(y1, y2, t, residues=res, k=k, ws=ws, stream=stream)
+        if world > 1:  # split the correlation by outputs, MAX-reduce the keys
+            plan.correlate_match_part(y1, y2, t, rank, world, keys=keys, ws=ws, stream=stream)
+            tmdist.allreduce_max_keys(keys)
+            plan.match_keys(keys, residues=res, k=k, stream=stream)
+        else:
+            plan.correlate_match(y1, y2, t, residues=res, k=k, ws=ws, stream=stream)
         if ev: ev[3].record(stream)
 
     for _ in range(max(args.warmup, 3)):
@@ -435,7 +441,11 @@ def run_single_signal(args, wl, rank, world, local, dev):
             plan.fold(xd, offset=off, length=ln, y1=y1, y2=y2, ws=ws, stream=stream)
             if world > 1:
                 tmdist.allreduce_folds(y1, y2)
-            plan.correlate_match(y1, y2, t, residues=res, k=k, ws=ws, stream=stream)
+                plan.correlate_match_part(y1, y2, t, rank, world, keys=keys, ws=ws, stream=stream)
+                tmdist.allreduce_max_keys(keys)
+                plan.match_keys(keys, residues=res, k=k, stream=stream)
+            else:
+                plan.correlate_match(y1, y2, t, residues=res, k=k, ws=ws, stream=stream)
             kh.copy_(k, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -473,7 +483,9 @@ def run_single_signal(args, wl, rank, world, local, dev):
             "data": "synthetic (seeded counter-based generator, chunks generated on each rank's device)",
             "config": {"workload": wl["desc"], "N": N, "K": K, "M1": plan.M1, "M2": plan.M2, "chunk_samples": ln,
                        "parallelism": f"sequence split over {world} rank(s) + NCCL all-reduce of y1||y2 "
-                                      f"({(plan.len_y1 + plan.len_y2) * 4} B)",
+                                      f"({(plan.len_y1 + plan.len_y2) * 4} B)"
+                                      + (f"; correlation split by output blocks + all-reduce MAX of 16 B keys"
+                                         if world > 1 else ""),
                        "l2": "no flush: per-rank input > 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "kernel": "tm_fold (fold_pm1_tma + fold_finalize)",

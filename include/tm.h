@@ -262,6 +262,26 @@ enum { TM_PATH_STAGED = 0, TM_PATH_STAGED_TC = 1, TM_PATH_FUSED_TC = 2, TM_PATH_
 int tm_run_path(tm_plan plan, int64_t batch);
 
 /*
+ * ---- One huge signal over several GPUs: the correlation split by outputs ----
+ * SURVEY 8(e)(ii).  After the all-reduce of the partial folds every rank holds
+ * the whole y1, y2; tm_correlate_match_part computes steps 5-7 (Eq. 4 and the
+ * argmax) for part `part` of `nparts` contiguous ranges of output blocks only,
+ * on the tiled tensor-core engine, and writes per pair and modulus the best
+ * (r, k) of its range (max r, lowest k on ties, reading C7) as an
+ * order-preserving int64 key: keys int64 [batch][2] (device), key =
+ * (((r + 2^42) << 21) | (2^21 - 1 - k)) XOR 2^63 read as int64 (|r| < 2^41,
+ * k < 2^21), INT64_MIN for an empty range.  The element-wise MAX of the keys over all parts (one
+ * all-reduce MAX of 16 bytes per pair) is the key of the whole correlation;
+ * tm_match_keys turns it into residues int32 [batch][2] (may be NULL) and k
+ * int64 [batch] (steps 8-9, as tm_match).  ws: tm_workspace_bytes.
+ * TM_EUNSUPPORTED if the plan is not eligible for the tiled engine (int8 data,
+ * K <= 2^17, M2 < 2^21, |r| < 2^41).
+ */
+int tm_correlate_match_part(tm_plan plan, const void *y1, const void *y2, const void *t, int64_t batch, int part,
+                            int nparts, int64_t *keys, void *ws, void *stream);
+int tm_match_keys(tm_plan plan, const int64_t *keys, int64_t batch, int32_t *residues, int64_t *k, void *stream);
+
+/*
  * ---- More than two moduli: Theorem 4 with alpha moduli ----
  * "Any integer m is uniquely specified mod N by its remainders modulo alpha
  * relatively prime integers M_1 .. M_alpha as long as prod M_i >= N" (read as

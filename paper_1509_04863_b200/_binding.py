@@ -19,6 +19,7 @@ EXPORTED_SYMBOLS = (
     "tm_plan_create", "tm_plan_query", "tm_workspace_bytes", "tm_plan_destroy", "tm_generate",
     "tm_fold", "tm_fold_template", "tm_correlate", "tm_match", "tm_run", "tm_run_host", "tm_correlate_match", "tm_correlate_many",
     "tm_status_string", "tm_last_error", "tm_launch_count", "tm_profile_events", "tm_run_path",
+    "tm_correlate_match_part", "tm_match_keys",
     "tm_mplan_create", "tm_mplan_workspace_bytes", "tm_mplan_run", "tm_crt_multi", "tm_mplan_destroy",
 )
 RUN_PATHS = {0: "staged (fold -> NTT/fp32 correlation -> CRT)", 1: "staged (fold -> tensor-core correlation)",
@@ -96,6 +97,10 @@ def lib():
         L.tm_profile_events.argtypes = [ctypes.POINTER(_p), ctypes.c_int]
         L.tm_run_path.restype = ctypes.c_int
         L.tm_run_path.argtypes = [_p, _i64]
+        L.tm_correlate_match_part.restype = ctypes.c_int
+        L.tm_correlate_match_part.argtypes = [_p, _p, _p, _p, _i64, ctypes.c_int, ctypes.c_int, _p, _p, _p]
+        L.tm_match_keys.restype = ctypes.c_int
+        L.tm_match_keys.argtypes = [_p, _p, _i64, _p, _p, _p]
         L.tm_mplan_create.restype = ctypes.c_int
         L.tm_mplan_create.argtypes = [ctypes.POINTER(_p), _i64, _i64, _p, ctypes.c_int, _u64, ctypes.c_int, _u32]
         L.tm_mplan_workspace_bytes.restype = ctypes.c_size_t
@@ -284,6 +289,30 @@ class Plan:
             ws = self.workspace(batch, y1.device)
         _check(lib().tm_correlate_match(self._h, _ptr(y1), _ptr(y2), _ptr(t), batch, _ptr(residues), _ptr(k),
                                         _ptr(ws), _stream(stream)), "tm_correlate_match")
+        return residues, k
+
+    def correlate_match_part(self, y1, y2, t, part: int, nparts: int, keys=None, ws=None, stream=None):
+        """tm_correlate_match_part: this part's best (r, k) per modulus as int64 keys [batch][2]."""
+        import torch
+        batch = y1.shape[0]
+        if keys is None:
+            keys = torch.empty((batch, 2), dtype=torch.int64, device=y1.device)
+        if ws is None:
+            ws = self.workspace(batch, y1.device)
+        _check(lib().tm_correlate_match_part(self._h, _ptr(y1), _ptr(y2), _ptr(t), batch, part, nparts, _ptr(keys),
+                                             _ptr(ws), _stream(stream)), "tm_correlate_match_part")
+        return keys
+
+    def match_keys(self, keys, residues=None, k=None, stream=None):
+        """tm_match_keys: (MAX-reduced) keys -> residues, k (steps 8-9)."""
+        import torch
+        batch = keys.shape[0]
+        if residues is None:
+            residues = torch.empty((batch, 2), dtype=torch.int32, device=keys.device)
+        if k is None:
+            k = torch.empty(batch, dtype=torch.int64, device=keys.device)
+        _check(lib().tm_match_keys(self._h, _ptr(keys), batch, _ptr(residues), _ptr(k), _stream(stream)),
+               "tm_match_keys")
         return residues, k
 
     def run_path(self, batch: int) -> int:

@@ -33,6 +33,7 @@ constexpr int64_t KEY_BIAS = (int64_t)1 << 42;
 struct TiledArgs {
     TcArgs a;              // y, t, K, M, NA, crt constants (NMC, R, NC unused except NC)
     int n_at, n_cr, CR;    // tiles over output blocks, template ranges, blocks per range
+    int at0, n_atp;        // this launch's tiles [at0, at0 + n_atp) (a part of a split correlation)
     int lmax;
     unsigned long long *keys;  // [batch][2] (n_cr == 1), zeroed
     int64_t *racc[2];          // [batch][Mj] partial sums (n_cr > 1), zeroed; or r outputs
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
     const TcArgs &a = T.a;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t b = blockIdx.y;
-    const int at = blockIdx.x % T.n_at, cr = blockIdx.x / T.n_at;
+    const int at = T.at0 + blockIdx.x % T.n_atp, cr = blockIdx.x / T.n_atp;
     const int a0 = at * NT;
     const int cb = cr * T.CR, ce = min(a.NC, cb + T.CR);
     uint8_t *Abuf = sm, *Bbuf = sm + 2 * A_BYTES, *tp = Bbuf + 2 * B_BYTES;
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(256) tc_tiled_leftover(const TiledArgs T) {
 
 // per pair: tile keys + leftovers -> residues; steps 8-9 (tm_resolve)
 __global__ void tc_tiled_final(const TiledArgs T, int64_t batch, int32_t *resid, int32_t *residues_out,
-                               int64_t *k_out, int64_t *r_out0, int64_t *r_out1) {
+                               int64_t *k_out, int64_t *r_out0, int64_t *r_out1, int64_t *keys_out, int with_left) {
     const TcArgs &a = T.a;
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= batch) return;
@@ -415,7 +416,7 @@ __global__ void tc_tiled_final(const TiledArgs T, int64_t batch, int32_t *resid,
             bk = ((int64_t)1 << KEY_SHIFT) - 1 - (int64_t)(key & (((unsigned long long)1 << KEY_SHIFT) - 1));
             bv = (int64_t)(key >> KEY_SHIFT) - KEY_BIAS;
         }
-        const int nleft = j ? nleft1 : nleft0;
+        const int nleft = with_left ? (j ? nleft1 : nleft0) : 0;
         for (int q = 0; q < nleft; ++q) {
             const int64_t r = T.lsum[b * 2 * MAXLEFT + (j ? nleft0 : 0) + q];
             const int64_t k = (int64_t)P * a.NA[j] + q;
@@ -424,13 +425,39 @@ __global__ void tc_tiled_final(const TiledArgs T, int64_t batch, int32_t *resid,
             amax(bv, bk, r, k);
         }
         m[j] = bk;
+        if (keys_out)  // split correlation: this part's (max r, lowest k) as an order-preserving int64
+            keys_out[2 * b + j] = bk == INT64_MAX ? INT64_MIN : (int64_t)(pack_key(bv, bk) ^ (1ull << 63));
     }
+    if (keys_out) return;
     if (resid) { resid[2 * b] = (int32_t)m[0]; resid[2 * b + 1] = (int32_t)m[1]; }
     if (residues_out) { residues_out[2 * b] = (int32_t)m[0]; residues_out[2 * b + 1] = (int32_t)m[1]; }
     if (k_out) k_out[b] = tm_resolve(m[0], m[1], a.M1, a.M2, a.crt_inv, a.N, a.crt_wrap);  // steps 8-9
 }
 
+// split correlation: all-reduced (MAX) keys -> residues -> steps 8-9
+__global__ void match_keys_kernel(const int64_t *keys, int64_t batch, int64_t M1, int64_t M2, uint32_t inv,
+                                  int64_t N, int64_t wrap, int32_t *residues, int64_t *k) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    int64_t m[2];
+    for (int j = 0; j < 2; ++j) {
+        const unsigned long long key = (unsigned long long)keys[2 * b + j] ^ (1ull << 63);
+        m[j] = ((int64_t)1 << KEY_SHIFT) - 1 - (int64_t)(key & (((unsigned long long)1 << KEY_SHIFT) - 1));
+    }
+    if (residues) { residues[2 * b] = (int32_t)m[0]; residues[2 * b + 1] = (int32_t)m[1]; }
+    if (k) k[b] = tm_resolve(m[0], m[1], M1, M2, inv, N, wrap);
+}
+
 }  // namespace
+
+int tm_tc_match_keys(const tm_plan_s *p, const int64_t *keys, int64_t batch, int32_t *residues, int64_t *k,
+                     cudaStream_t s) {
+    if (batch == 0) return TM_OK;
+    match_keys_kernel<<<(unsigned)((batch + 127) / 128), 128, 0, s>>>(keys, batch, p->M1, p->M2, p->crt_inv, p->N,
+                                                                       p->crt_wrap, residues, k);
+    TM_CHECK_LAUNCH("tm_match_keys");
+    return TM_OK;
+}
 
 // Plan-time eligibility (int8 data whose |y| fits 4 four-bit limbs and whose
 // |r| fits the packed key) and geometry.
@@ -458,7 +485,8 @@ size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch) {
 // r1/r2 (int64, may be NULL), residues_out/resid (may be NULL), k (may be NULL).
 int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, int64_t ldy1, int64_t ldy2,
                           const void *t, int64_t ldt, int64_t batch, void *r1, void *r2, int32_t *resid,
-                          int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s) {
+                          int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s, int part, int nparts,
+                          int64_t *keys_out) {
     if (!p->tct_ok) return TM_EUNSUPPORTED;
     if (batch == 0) return TM_OK;
     if (batch > 65535) return TM_EUNSUPPORTED;
@@ -477,10 +505,14 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         T.a.NA[j] = (int)na;
     }
     T.lmax = p->tct_lmax;
-    const char *env_nt = getenv("TM_TILED_NT");  // A/B: "32" or "64"
-    const int NT = (env_nt && atoi(env_nt) == 32) ? 32 : 64;
+    const char *env_nt = getenv("TM_TILED_NT");  // A/B: "32" (default, measured faster) or "64"
+    const int NT = (env_nt && atoi(env_nt) == 64) ? 64 : 32;
     const int namax = T.a.NA[0] > T.a.NA[1] ? T.a.NA[0] : T.a.NA[1];
     T.n_at = (namax + NT - 1) / NT;
+    // split correlation: part `part` of `nparts` takes a contiguous
+    // range of output tiles
+    T.at0 = (int)((int64_t)T.n_at * part / nparts);
+    T.n_atp = (int)((int64_t)T.n_at * (part + 1) / nparts) - T.at0;
     // template ranges: minimise waves x blocks per CTA over 2 resident CTAs per SM
     // (a grid just over one wave doubles the time), fewer ranges on near-ties
     // (each extra range adds one int64 atomic per output)
@@ -489,7 +521,7 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     int n_cr = 1;
     double best = 1e300;
     for (int c = 1; c <= max_cr; ++c) {
-        const int64_t ctas = batch * T.n_at * c;
+        const int64_t ctas = batch * std::max(T.n_atp, 1) * c;
         const double cost = (double)((ctas + slots - 1) / slots) * (double)((NC + c - 1) / c);
         if (cost < best * 0.95) { best = cost; n_cr = c; }
     }
@@ -517,20 +549,23 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         cudaFuncSetAttribute(corr_tc_tiled<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<64>());
         attr = true;
     }
-    const dim3 grid((unsigned)(T.n_at * T.n_cr), (unsigned)batch);
-    if (NT == 32)
-        corr_tc_tiled<32><<<grid, TNTHR, smem_bytes<32>(), s>>>(T);
-    else
-        corr_tc_tiled<64><<<grid, TNTHR, smem_bytes<64>(), s>>>(T);
-    TM_CHECK_LAUNCH("corr_tc_tiled");
+    const dim3 grid((unsigned)(T.n_atp * T.n_cr), (unsigned)batch);
+    if (T.n_atp > 0) {
+        if (NT == 32)
+            corr_tc_tiled<32><<<grid, TNTHR, smem_bytes<32>(), s>>>(T);
+        else
+            corr_tc_tiled<64><<<grid, TNTHR, smem_bytes<64>(), s>>>(T);
+        TM_CHECK_LAUNCH("corr_tc_tiled");
+    }
     const int nleft = (int)(std::max<int64_t>(0, p->M1 - (int64_t)P * T.a.NA[0]) +
                             std::max<int64_t>(0, p->M2 - (int64_t)P * T.a.NA[1]));
-    if (nleft > 0) {
+    const int with_left = part == 0;  // the leftover outputs belong to part 0
+    if (nleft > 0 && with_left) {
         tc_tiled_leftover<<<dim3((unsigned)((p->K + LSLICE - 1) / LSLICE), (unsigned)batch), 256, 0, s>>>(T);
         TM_CHECK_LAUNCH("tc_tiled_leftover");
     }
     tc_tiled_final<<<(unsigned)((batch + 127) / 128), 128, 0, s>>>(T, batch, resid, residues_out, k, (int64_t *)r1,
-                                                                     (int64_t *)r2);
+                                                                     (int64_t *)r2, keys_out, with_left);
     TM_CHECK_LAUNCH("tc_tiled_final");
     return TM_OK;
 }

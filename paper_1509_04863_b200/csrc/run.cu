@@ -219,6 +219,35 @@ extern "C" __attribute__((visibility("default"))) int tm_run_path(tm_plan p, int
     return TM_PATH_STAGED;
 }
 
+// the correlation of one huge signal split over ranks by output
+// tiles; each rank's best (r, k) per modulus as order-preserving int64 keys
+extern "C" __attribute__((visibility("default"))) int tm_correlate_match_part(tm_plan p, const void *y1,
+                                                                              const void *y2, const void *t,
+                                                                              int64_t batch, int part, int nparts,
+                                                                              int64_t *keys, void *ws, void *stream) {
+    if (!p) { tm_set_error("tm_correlate_match_part: NULL plan"); return TM_EINVAL; }
+    if (batch < 0 || nparts < 1 || part < 0 || part >= nparts) {
+        tm_set_error("tm_correlate_match_part: bad batch / part / nparts");
+        return TM_EINVAL;
+    }
+    if (batch == 0) return TM_OK;
+    if (!y1 || !y2 || !t || !keys || !ws) { tm_set_error("tm_correlate_match_part: NULL pointer"); return TM_EINVAL; }
+    if (!p->tct_ok) {
+        tm_set_error("tm_correlate_match_part: plan not eligible for the tiled tensor-core engine");
+        return TM_EUNSUPPORTED;
+    }
+    return tm_tc_tiled_correlate(p, y1, y2, p->len_y1, p->len_y2, t, p->K, batch, nullptr, nullptr, nullptr, nullptr,
+                                 nullptr, (char *)ws + tm_ws(p, batch).tiled, (cudaStream_t)stream, part, nparts,
+                                 keys);
+}
+
+extern "C" __attribute__((visibility("default"))) int tm_match_keys(tm_plan p, const int64_t *keys, int64_t batch,
+                                                                    int32_t *residues, int64_t *k, void *stream) {
+    if (!p || batch < 0) { tm_set_error("tm_match_keys: bad arguments"); return TM_EINVAL; }
+    if (batch > 0 && (!keys || !k)) { tm_set_error("tm_match_keys: NULL pointer"); return TM_EINVAL; }
+    return tm_tc_match_keys(p, keys, batch, residues, k, (cudaStream_t)stream);
+}
+
 // steps 4-9 on already-folded vectors (e.g. after an all-reduce of partial folds)
 extern "C" __attribute__((visibility("default"))) int tm_correlate_match(tm_plan p, const void *y1, const void *y2,
                                                                          const void *t, int64_t batch,

@@ -156,7 +156,10 @@ void tm_tc_tiled_plan(tm_plan_s *p);
 size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch);
 int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, int64_t ldy1, int64_t ldy2,
                           const void *t, int64_t ldt, int64_t batch, void *r1, void *r2, int32_t *resid,
-                          int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s);
+                          int32_t *residues_out, int64_t *k, void *ws, cudaStream_t s, int part = 0,
+                          int nparts = 1, int64_t *keys_out = nullptr);
+int tm_tc_match_keys(const tm_plan_s *p, const int64_t *keys, int64_t batch, int32_t *residues, int64_t *k,
+                     cudaStream_t s);
 // the tensor-core engine for a batch: one CTA per pair (corr_tc.cu) or tiled
 // over CTAs (few pairs / long templates); ws = the whole tm_workspace_bytes area
 int tm_tc_any(const tm_plan_s *p, const void *y1, const void *y2, const void *t, int64_t ldt, int64_t batch,

@@ -9,6 +9,11 @@
   concatenated y1 || y2 vector -- `allreduce_folds`.  The fold of Eq. 2 is
   additive over any partition of the positions (pinned in tests), so the sum
   is exactly the full fold.
+* The correlation of that one signal can then be split by output blocks
+  (SURVEY 8(e)(ii)): each rank runs tm_correlate_match_part for its part and the
+  per-pair keys (order-preserving int64 of (max r, lowest k), include/tm.h) are
+  combined with ONE all-reduce MAX -- `allreduce_max_keys`; tm_match_keys then
+  gives identical residues and k on every rank.
 No arithmetic of the method lives here.
 """
 from __future__ import annotations
@@ -43,6 +48,13 @@ def allreduce_folds(y1, y2, group=None):
     flat = torch.cat([y1.reshape(-1), y2.reshape(-1)])
     dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
     return flat[:n1].view_as(y1), flat[n1:].view_as(y2)
+
+
+def allreduce_max_keys(keys, group=None):
+    """Element-wise MAX of the split-correlation keys (int64 [batch][2]) over ranks."""
+    import torch.distributed as dist
+    dist.all_reduce(keys, op=dist.ReduceOp.MAX, group=group)
+    return keys
 
 
 def max_over_ranks(value: float, device=None, group=None) -> float:

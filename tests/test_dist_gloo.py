@@ -66,7 +66,21 @@ def _worker(rank, world, port, q):
         ks = [None] * world
         dist.all_gather_object(ks, k)
         tmax = tmdist.max_over_ranks(1.0 + rank)
-        q.put((rank, ok_fold, ks, k == oracle.ftm(x, t)["k"], tmax))
+        # split correlation (8(e)(ii)): each rank's best (r, k) over its half of the
+        # outputs as the documented int64 key, one all-reduce MAX, decode
+        def key(r, kk):
+            v = (((int(r) + (1 << 42)) << 21) | ((1 << 21) - 1 - int(kk))) ^ (1 << 63)
+            return v - (1 << 64) if v >= (1 << 63) else v
+        keys = []
+        for r in (r1, r2):
+            lo, hi = len(r) * rank // world, len(r) * (rank + 1) // world
+            kk = lo + int(np.argmax(r[lo:hi]))
+            keys.append(key(r[kk], kk))
+        keys = torch.tensor([keys], dtype=torch.int64)
+        tmdist.allreduce_max_keys(keys)
+        dec = [((1 << 21) - 1 - ((int(v) + (1 << 64)) % (1 << 64) & ((1 << 21) - 1))) for v in keys[0]]
+        ok_keys = dec == [oracle.argmax(r1), oracle.argmax(r2)]
+        q.put((rank, ok_fold and ok_keys, ks, k == oracle.ftm(x, t)["k"], tmax))
     finally:
         dist.destroy_process_group()
 

@@ -658,3 +658,28 @@ def test_crt_multi_kernel(tm):
         for b in range(0, B, 37):
             z = oracle.crt_multi(res[b].astype(np.int64), M)
             assert int(k[b]) == (z if z < N else -1), (M, b)
+
+
+# ------------------------------------------------------------- split correlation
+@pytest.mark.parametrize("nparts", [1, 2, 3, 8])
+def test_split_correlation_parts_max_equals_whole(tm, nparts):
+    """tm_correlate_match_part over every part, element-wise MAX of the keys (what
+    the all-reduce computes), tm_match_keys: identical residues and k to the
+    whole correlation and to the oracle; parts beyond the tile count are empty."""
+    N, K, B = 2 ** 22, 16384, 2
+    plan = tm.Plan(N, K, seed=14)
+    x_h, t_h, _ = tmgen.batch(14, 0, B, N, K, 0.05)
+    x, t = up(x_h), up(t_h)
+    y1, y2 = plan.fold(x)
+    keys = None
+    for part in range(nparts):
+        kp = plan.correlate_match_part(y1, y2, t, part, nparts)
+        keys = kp.clone() if keys is None else torch.maximum(keys, kp)
+    res, k = plan.match_keys(keys)
+    res_w, k_w = plan.correlate_match(y1, y2, t)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res.cpu().numpy(), res_w.cpu().numpy())
+    np.testing.assert_array_equal(k.cpu().numpy(), k_w.cpu().numpy())
+    for b in range(B):
+        o = oracle.ftm(x_h[b], t_h[b], want_vectors=False)
+        assert tuple(res[b].tolist()) == o["residues"] and int(k[b]) == o["k"]
