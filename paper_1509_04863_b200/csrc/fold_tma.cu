@@ -406,8 +406,11 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 const int dlo = -16 * ntile;
                 int64_t bin0 = ((int64_t)dlo + it.cs_cta - g0) % a.M2;
                 if (bin0 < 0) bin0 += a.M2;
+                const int pad = 16 * ntile, nw = width >> 9;
+                const bool c3 = pad <= 1024;
                 for (int i = et; i < width - dlo; i += NE * 32) {
-                    const int v = comb_at(pv, a.priv_stride, dlo + i, ntile, width);
+                    const int v = c3 ? comb3(pv, a.priv_stride, dlo + i, pad, nw)
+                                     : comb_at(pv, a.priv_stride, dlo + i, ntile, width);
                     if (v) {
                         int64_t bin = bin0 + i;
                         while (bin >= a.M2) bin -= a.M2;
