@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
 
 // leftover outputs k in [128 NA_j, M_j) (at most MAXLEFT per modulus): CTA
 // (K-slice, pair) adds its partial dot products into lsum (exact int64)
-constexpr int LSLICE = 4096;
+constexpr int LSLICE = 1024;  // K-slice per CTA (4 terms per thread: latency-bound loop)
 __global__ void __launch_bounds__(256) tc_tiled_leftover(const TiledArgs T) {
     const TcArgs &a = T.a;
     const int64_t b = blockIdx.y;

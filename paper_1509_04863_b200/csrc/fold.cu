@@ -276,6 +276,8 @@ __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t
         if (!block && j >= 0 && j < q2) v += xat(j);
         return v;
     };
+    // (launched with ~4 bins per thread: the unrolled iterations' loads are independent)
+#pragma unroll 4
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M2 + K;
          k += (int64_t)gridDim.x * blockDim.x) {
         if (k < M1 + K) {
@@ -362,7 +364,7 @@ int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batc
         if (rc != TM_EUNSUPPORTED) {
             if (rc != TM_OK || !used_counts) return rc;
             tm_ws_layout L = tm_ws(p, batch);
-            int64_t gx = (p->M2 + p->K + 255) / 256;
+            int64_t gx = (p->M2 + p->K + 1023) / 1024;
             fold_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(
                 (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, offset / p->M1, rows,
                 (const int32_t *)((char *)ws + L.fold_counts), (int32_t *)y1, ldy1, (int32_t *)y2, ldy2, accumulate,
@@ -395,7 +397,7 @@ int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batc
         if (items > 0x7FFFFFFF) { tm_set_error("tm_fold: too many work items"); return TM_EUNSUPPORTED; }
         fold_pm1<<<(unsigned)items, PM_WARPS * 32, smem, s>>>(a);
         TM_CHECK_LAUNCH("tm_fold: fold_pm1");
-        int64_t gx = (p->M2 + p->K + 255) / 256;
+        int64_t gx = (p->M2 + p->K + 1023) / 1024;
         fold_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(
             (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, a.row0, a.rows,
             counts, (int32_t *)y1, ldy1, (int32_t *)y2, ldy2, accumulate, p->block);
