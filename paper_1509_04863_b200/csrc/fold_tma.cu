@@ -245,8 +245,20 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 // while the epilogue warps finish y_2
                 tc::group_wait<GS>(&pfull[pb], pph, gt >> 5);
                 const int fl1 = tc::stage_y(a.tca, tsm + a.tca.offB, b, 0, 1, gt >> 5, lane, 0, 1);
+                // the CTA's last pair (static schedule): the TMA ring is idle from here on,
+                // so the A operand of the second template chunk is built into it now and
+                // the MMAs of both chunks run back to back on the kernel's tail
+                uint8_t *a_alt = nullptr;
+#ifndef TM_NO_RING_A
+                if (a.work_counter == nullptr && b + (int64_t)gridDim.x >= a.n_items && a.tca.NC > a.tca.CCH &&
+                    2 * a.tca.CCH >= a.tca.NC &&
+                    (uint32_t)(256 * (8 * (a.tca.NC - a.tca.CCH - 1) + 15)) <= (uint32_t)(NST * STAGE_BYTES)) {
+                    tc::build_a(a.tca, tsm, a.tca.CCH, a.tca.NC, gt, smem);
+                    a_alt = smem;
+                }
+#endif
                 tc::group_wait<GS>(&yready[pb], pph, gt >> 5);
-                tc::tc_main<GS>(a.tca, tsm, b, gt, warp & 3, tbase, mph, fl1);
+                tc::tc_main<GS>(a.tca, tsm, b, gt, warp & 3, tbase, mph, fl1, a_alt);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&ydone[pb]);
                 if (++pb == 2) { pb = 0; pph ^= 1; }

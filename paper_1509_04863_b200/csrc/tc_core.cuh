@@ -254,7 +254,8 @@ struct GroupSync {
 
 // A operand for the template blocks c in [c0, c1): chunk (J, s) of the buffer =
 // tp[16 (J + 8 c0) + s + 1 + e], J < 8 (c1 - c0 - 1) + 15.
-__device__ __forceinline__ void build_a(const TcArgs &a, uint8_t *sm, int c0, int c1, int tid) {
+__device__ __forceinline__ void build_a(const TcArgs &a, uint8_t *sm, int c0, int c1, int tid,
+                                        uint8_t *dst = nullptr) {
     const uint8_t *tp = sm + a.offTp + 128 * c0;
     const int n = (8 * (c1 - c0 - 1) + 15) * 16;
     for (int c = tid; c < n; c += NTHR) {
@@ -267,7 +268,7 @@ __device__ __forceinline__ void build_a(const TcArgs &a, uint8_t *sm, int c0, in
         o.y = __funnelshift_r(w1, w2, r);
         o.z = __funnelshift_r(w2, w3, r);
         o.w = __funnelshift_r(w3, w4, r);
-        reinterpret_cast<uint4 *>(sm)[c] = o;
+        reinterpret_cast<uint4 *>(dst ? dst : sm)[c] = o;
     }
 }
 
@@ -308,7 +309,7 @@ template <class Sync>
 // jlo = 0, jhi = 1, while y_2 was being finished) and fl1 is this thread's
 // range flags of it; only y_2 is staged here.
 __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b, int tid, int qw, uint32_t tbase,
-                                        uint32_t &mph, int fl1 = -1) {
+                                        uint32_t &mph, int fl1 = -1, uint8_t *a_alt = nullptr) {
     const int warp = tid >> 5, lane = tid & 31;
     long long tstamp[6];
     tstamp[0] = gtime();
@@ -342,12 +343,17 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
     const int nsplit = 2 * a.NMC / nsp;
     uint32_t pass = 0;
     int staged = 0;  // limb in B
-    for (int c0 = 0; c0 < a.NC; c0 += a.CCH) {
+    int ch = 0;
+    for (int c0 = 0; c0 < a.NC; c0 += a.CCH, ++ch) {
         const int c1 = min(a.NC, c0 + a.CCH);
+        // a_alt: the A operand of chunk 1 was built elsewhere in advance (the fused
+        // kernel's free TMA ring, for a CTA's last pair): no wait, no rebuild
+        const bool alt = a_alt != nullptr && ch == 1;
+        uint8_t *abuf = alt ? a_alt : sm;
         for (int l = 0; l < nl; ++l) {
-            if (pass > 0) {
+            if (pass > 0 && !(alt && nl == 1)) {
                 group_wait<Sync>(mdone, (mph + pass - 1) & 1u, warp);
-                if (l == 0) build_a(a, sm, c0, c1, tid);
+                if (l == 0 && !alt) build_a(a, sm, c0, c1, tid);
                 if (l != staged) { stage_y(a, B, b, l, nl, warp, lane); staged = l; }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core
@@ -356,7 +362,7 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (warp == 0) {
                 const uint32_t lbo = 32u * a.R;
-                const uint64_t ad0 = sdesc(smem_u32(sm), 256, 128);
+                const uint64_t ad0 = sdesc(smem_u32(abuf), 256, 128);
                 const uint64_t bd0 = sdesc(smem_u32(B), lbo, 128);
                 const uint32_t id = idesc_i8(nsp);
                 for (int sp = 0; sp < nsplit; ++sp) {
