@@ -124,7 +124,8 @@ def test_alias_repair_flag(tm, engine):
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-@pytest.mark.parametrize("N,K,M", [(1000, 37, 0), (997, 40, 45), (64, 8, 0), (12, 3, 4), (5000, 71, 80)])
+@pytest.mark.parametrize("N,K,M", [(1000, 37, 0), (997, 40, 45), (64, 8, 0), (12, 3, 4), (5000, 71, 80),
+                                   (1000, 1, 40)])  # K = 1: r = y[0..M) (SURVEY 8(c.2) special case)
 def test_general_fold_wrap_cases(tm, N, K, M, engine):
     """M not dividing N (mod-N wrap, reading C5), M > K, tiny sizes: general kernels."""
     rng = np.random.default_rng(N + K)
