@@ -63,7 +63,10 @@ enum {
                                N <= z < N + s2, k = z - N instead of NO_MATCH
                                (a true peak m < s2 that the mod-N wrap of Eq. 2
                                moved into bin m + M2 - s2).  Default: off, the
-                               literal unreduced sets of P:104-105 (C9). */
+                               literal unreduced sets of P:104-105 (C9).
+                               TM_EUNSUPPORTED unless M1 | N (the closed form;
+                               the oracle's literal mod-N sets also cover
+                               M1 not dividing N). */
 #define TM_BLOCK 16u    /* strategy 2 of P:150-151: the Block sampling matrix
                            Phi = [Phi_M ... Phi_M] of Theorem 2 with
                            Eq. 3's Phi_M = I, on x zero-padded to a multiple of

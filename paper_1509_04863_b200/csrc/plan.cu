@@ -92,6 +92,10 @@ int tm_plan_create_impl(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t 
     if ((flags & (TM_CORR_NTT | TM_CORR_TC)) && dtype != TM_I8) { tm_set_error("tm_plan_create: TM_CORR_* needs TM_I8"); return TM_EINVAL; }
     if ((flags & TM_BINARY) && dtype != TM_I8) { tm_set_error("tm_plan_create: TM_BINARY needs TM_I8"); return TM_EINVAL; }
     int64_t M1 = M ? M : K, M2 = M1 + 1;
+    if ((flags & TM_ALIAS_REPAIR) && N % (M1 ? M1 : 1) != 0) {
+        tm_set_error("tm_plan_create: TM_ALIAS_REPAIR is implemented for M1 | N only (reading C10's closed form)");
+        return TM_EUNSUPPORTED;
+    }
     if (M1 < K) { tm_set_error("tm_plan_create: M1=%lld < K=%lld (Alg. 1 step 2 needs M1 >= K)", (long long)M1, (long long)K); return TM_EINVAL; }
     if (need_product && (__int128)M1 * (__int128)M2 <= (__int128)N) {
         int64_t kmin = 1;

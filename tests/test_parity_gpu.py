@@ -684,3 +684,51 @@ def test_split_correlation_parts_max_equals_whole(tm, nparts):
     for b in range(B):
         o = oracle.ftm(x_h[b], t_h[b], want_vectors=False)
         assert tuple(res[b].tolist()) == o["residues"] and int(k[b]) == o["k"]
+
+
+# ------------------------------------------------------------- randomized sweep
+def _random_case(rng):
+    """A random small plan: N, K, M (M1 | N or not), dtype, data kind, flags."""
+    dtype = "float32" if rng.random() < 0.25 else "int8"
+    K = int(rng.integers(1, 300))
+    M = 0 if rng.random() < 0.5 else int(K + rng.integers(0, 200))
+    if max(M, K) < 2:
+        M = 2
+    M1 = M or K
+    Nmax = M1 * (M1 + 1) - 1
+    N = int(rng.integers(max(K, 2), min(Nmax, 200000) + 1))
+    if rng.random() < 0.4:               # M1 | N (the packed / fused paths' shape)
+        N = max(M1, (N // M1) * M1)
+    binary = dtype == "int8" and rng.random() < 0.6
+    block = rng.random() < 0.25
+    alias = (not block) and N % M1 == 0 and rng.random() < 0.3   # TM_ALIAS_REPAIR needs M1 | N
+    engine = rng.choice(["auto", "ntt"]) if dtype == "int8" else None
+    return N, K, M, dtype, binary, block, alias, engine
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_randomized_sweep_against_oracle(tm, seed):
+    """Random shapes and options through fold -> correlate -> match and tm_run:
+    int data bit-exact (y, r, residues, k), fp32 within reading C15."""
+    rng = np.random.default_rng(1000 + seed)
+    N, K, M, dtype, binary, block, alias, engine = _random_case(rng)
+    B = int(rng.integers(1, 4))
+    plan = tm.Plan(N, K, M=M, seed=seed, dtype=dtype, binary=binary, engine=engine, block=block,
+                   alias_repair=alias)
+    if dtype == "int8":
+        if binary:
+            x_h = (1 - 2 * rng.integers(0, 2, (B, N))).astype(np.int8)
+        else:
+            x_h = rng.integers(-128, 128, (B, N)).astype(np.int8)
+        k0 = rng.integers(0, N, B)
+        t_h = np.stack([x_h[b][(k0[b] + np.arange(K)) % N] for b in range(B)]).astype(np.int8)
+    else:
+        x_h = rng.standard_normal((B, N)).astype(np.float32)
+        k0 = rng.integers(0, N, B)
+        t_h = np.stack([x_h[b][(k0[b] + np.arange(K)) % N] for b in range(B)]).astype(np.float32)
+    if block:
+        check_block_pairs(plan, x_h, t_h, range(B), f32=(dtype == "float32"))
+    elif dtype == "int8":
+        check_int_pairs(tm, plan, x_h, t_h, range(B), alias_repair=alias)
+    else:
+        check_f32_pairs(tm, plan, x_h, t_h, range(B))
