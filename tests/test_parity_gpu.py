@@ -732,3 +732,31 @@ def test_randomized_sweep_against_oracle(tm, seed):
         check_int_pairs(tm, plan, x_h, t_h, range(B), alias_repair=alias)
     else:
         check_f32_pairs(tm, plan, x_h, t_h, range(B))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_randomized_large_shapes_sampled(tm, seed):
+    """Random packed-fold shapes (M1 a multiple of 512 dividing N, batches around
+    and above the SM count so the fused kernel runs): sampled pairs' residues and
+    k equal the oracle's, and tm_run equals the staged path on every pair."""
+    rng = np.random.default_rng(5000 + seed)
+    M1 = 512 * int(rng.integers(1, 9))
+    K = int(rng.integers(max(1, M1 // 4), M1 + 1))
+    q = int(rng.integers(16, min(M1, 1024) + 1))
+    N = M1 * q
+    B = int(rng.integers(100, 320))
+    block = rng.random() < 0.3
+    plan = tm.Plan(N, K, M=M1 if M1 != K else 0, seed=seed, block=block)
+    x_h, t_h, _ = tmgen.batch(seed + 77, 0, B, N, K, float(rng.random() * 0.2))
+    x, t = up(x_h), up(t_h)
+    res_run, k_run = plan.run(x, t)
+    y1, y2 = plan.fold(x)
+    res, k = plan.match(*plan.correlate(y1, y2, plan.fold_template(t)))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res_run.cpu().numpy(), res.cpu().numpy())
+    np.testing.assert_array_equal(k_run.cpu().numpy(), k.cpu().numpy())
+    rr, kk = res_run.cpu().numpy(), k_run.cpu().numpy()
+    f = oracle.ftm_block if block else oracle.ftm
+    for b in rng.choice(B, 3, replace=False):
+        o = f(x_h[b], t_h[b], M=M1 if M1 != K else 0, want_vectors=False)
+        assert tuple(rr[b]) == o["residues"] and kk[b] == o["k"], (b, N, K, M1, B)
