@@ -34,6 +34,8 @@
 // plan guarantees |y| <= 32767 (<= 3 limbs) and K*128*128 < 2^31 per limb.
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "tc_core.cuh"
 
 namespace {
@@ -58,7 +60,15 @@ __global__ void __launch_bounds__(NTHR, 2) corr_tc_kernel(const TcArgs a) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tbase = *tslot;
     uint32_t mph = 0;
-    tc_pair<CtaSync>(a, sm, blockIdx.x, tid, warp & 3, tbase, mph);
+    if (a.ldy[0] == 0 && a.ldy[1] == 0) {
+        // one folded signal against many templates (tm_correlate_many): persistent
+        // over templates, y staged into B once per CTA (when it needs one limb)
+        int y_pre = 0;
+        for (int64_t b = blockIdx.x; b < a.nbatch; b += gridDim.x)
+            tc_pair<CtaSync>(a, sm, b, tid, warp & 3, tbase, mph, &y_pre);
+    } else {
+        tc_pair<CtaSync>(a, sm, blockIdx.x, tid, warp & 3, tbase, mph);
+    }
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(a.ncols));
 }
 
@@ -158,7 +168,23 @@ int tm_tc_correlate(const tm_plan_s *p, const void *y1, const void *y2, int64_t 
                              cudaSharedmemCarveoutMaxShared);
         attr = true;
     }
-    corr_tc_kernel<<<(unsigned)batch, NTHR, p->tc_smem, s>>>(a);
+    a.nbatch = batch;
+    const bool shared_y = ldy1 == 0 && ldy2 == 0;
+    const int64_t grid = shared_y ? std::min<int64_t>(batch, 2 * (int64_t)p->num_sms) : batch;
+    size_t smem = p->tc_smem;
+    if (shared_y && p->tc_lmax > 1) {
+        // one folded signal, many templates: a B buffer per limb, staged once per CTA
+        // (tp and the misc area move up behind them), while two CTAs still fit per SM
+        const uint32_t bs = (uint32_t)(256 * p->tc_R + 127) / 128 * 128;
+        const size_t extra = (size_t)(p->tc_lmax - 1) * bs;
+        if (smem + extra <= 113 * 1024) {
+            a.bstride = bs;
+            a.offTp += (uint32_t)extra;
+            a.offMisc += (uint32_t)extra;
+            smem += extra;
+        }
+    }
+    corr_tc_kernel<<<(unsigned)grid, NTHR, smem, s>>>(a);
     TM_CHECK_LAUNCH("corr_tc_kernel");
     return TM_OK;
 }

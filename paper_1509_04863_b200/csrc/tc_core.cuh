@@ -43,6 +43,8 @@ struct TcArgs {
     uint32_t crt_inv;
     int64_t crt_wrap;
     long long *dbg;  // optional per-CTA phase timestamps (tm_debug_tc_timestamps)
+    int64_t nbatch;  // templates (one shared y, corr_tc_kernel's persistent loop)
+    uint32_t bstride;  // != 0: one B buffer per limb, this many bytes apart (staged once)
     int discard_y;   // 1: y rows (128-byte aligned, ldy multiple of 32) are scratch; drop
                      // their L2 lines without write-back once read (fused tm_run)
 };
@@ -309,7 +311,8 @@ template <class Sync>
 // jlo = 0, jhi = 1, while y_2 was being finished) and fl1 is this thread's
 // range flags of it; only y_2 is staged here.
 __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b, int tid, int qw, uint32_t tbase,
-                                        uint32_t &mph, int fl1 = -1, uint8_t *a_alt = nullptr) {
+                                        uint32_t &mph, int fl1 = -1, uint8_t *a_alt = nullptr,
+                                        int *y_pre = nullptr) {
     const int warp = tid >> 5, lane = tid & 31;
     long long tstamp[6];
     tstamp[0] = gtime();
@@ -322,14 +325,24 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
     uint8_t *tp = sm + a.offTp;
 
     // ---- y -> B: limb 0 (= y itself when |y| <= 127, the common case) ----
-    const int fl = fl1 >= 0 ? (fl1 | stage_y(a, B, b, 0, 1, warp, lane, 1, 2)) : stage_y(a, B, b, 0, 1, warp, lane);
-    const int need2 = Sync::sync_or(fl & 1);
-    const int need3 = Sync::sync_or(fl & 2);
-    int nl = need3 ? 3 : (need2 ? 2 : 1);
-    if (nl > a.LMAX) nl = a.LMAX;  // only reachable when the caller breaks TM_BINARY
-    if (nl > 1) {                  // re-stage limb 0 as the low 4 bits
-        Sync::sync();
-        stage_y(a, B, b, 0, nl, warp, lane);
+    // y_pre (one folded signal, many templates): *y_pre = 1 once B holds that y as
+    // one limb, which every later template of the CTA reuses without restaging
+    int nl;
+    if (y_pre && *y_pre > 0) {
+        nl = *y_pre;  // B (and, with bstride, the other limbs' buffers) already hold y
+    } else {
+        const int fl = fl1 >= 0 ? (fl1 | stage_y(a, B, b, 0, 1, warp, lane, 1, 2)) : stage_y(a, B, b, 0, 1, warp, lane);
+        const int need2 = Sync::sync_or(fl & 1);
+        const int need3 = Sync::sync_or(fl & 2);
+        nl = need3 ? 3 : (need2 ? 2 : 1);
+        if (nl > a.LMAX) nl = a.LMAX;  // only reachable when the caller breaks TM_BINARY
+        if (nl > 1) {                  // re-stage limb 0 as the low 4 bits
+            Sync::sync();
+            stage_y(a, B, b, 0, nl, warp, lane);
+            if (a.bstride)             // and every other limb into its own buffer, once
+                for (int l = 1; l < nl; ++l) stage_y(a, B + l * a.bstride, b, l, nl, warp, lane);
+        }
+        if (y_pre) *y_pre = (a.bstride || nl == 1) ? nl : 0;
     }
     tstamp[2] = gtime();
     tstamp[3] = tstamp[2];
@@ -351,7 +364,14 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
         const bool alt = a_alt != nullptr && ch == 1;
         uint8_t *abuf = alt ? a_alt : sm;
         for (int l = 0; l < nl; ++l) {
-            if (pass > 0 && !(alt && nl == 1)) {
+            uint8_t *Bl = a.bstride ? B + l * a.bstride : B;
+            if (a.bstride) {
+                // resident limb buffers: only a new A chunk waits for the MMAs
+                if (pass > 0 && l == 0 && !alt) {
+                    group_wait<Sync>(mdone, (mph + pass - 1) & 1u, warp);
+                    build_a(a, sm, c0, c1, tid);
+                }
+            } else if (pass > 0 && !(alt && nl == 1)) {
                 group_wait<Sync>(mdone, (mph + pass - 1) & 1u, warp);
                 if (l == 0 && !alt) build_a(a, sm, c0, c1, tid);
                 if (l != staged) { stage_y(a, B, b, l, nl, warp, lane); staged = l; }
@@ -363,7 +383,7 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
             if (warp == 0) {
                 const uint32_t lbo = 32u * a.R;
                 const uint64_t ad0 = sdesc(smem_u32(abuf), 256, 128);
-                const uint64_t bd0 = sdesc(smem_u32(B), lbo, 128);
+                const uint64_t bd0 = sdesc(smem_u32(Bl), lbo, 128);
                 const uint32_t id = idesc_i8(nsp);
                 for (int sp = 0; sp < nsplit; ++sp) {
                     const uint32_t dcol = tbase + 2 * a.NMC * l + sp * nsp;
@@ -485,9 +505,9 @@ __device__ __forceinline__ void tc_main(const TcArgs &a, uint8_t *sm, int64_t b,
 // Steps 4-9 for pair b (tc_pre then tc_main).
 template <class Sync>
 __device__ __forceinline__ void tc_pair(const TcArgs &a, uint8_t *sm, int64_t b, int tid, int qw, uint32_t tbase,
-                                        uint32_t &mph) {
+                                        uint32_t &mph, int *y_pre = nullptr) {
     tc_pre<Sync>(a, sm, b, tid);
-    tc_main<Sync>(a, sm, b, tid, qw, tbase, mph);
+    tc_main<Sync>(a, sm, b, tid, qw, tbase, mph, -1, nullptr, y_pre);
 }
 
 }  // namespace tc
