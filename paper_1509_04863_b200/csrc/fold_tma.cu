@@ -86,6 +86,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
+// Programmatic dependent launch (fused kernel, consecutive tm_run calls on a
+// stream): every CTA lets the next launch be scheduled at once (it can only take
+// an SM this grid has left), and each warp role waits for the previous grid
+// (griddepcontrol.wait: completed, memory visible) only before its first global
+// write -- so the next launch streams x while this one finishes its tail.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // x is streamed exactly once: its L2 lines are marked evict-first so that the
 // folded vectors (written, then read back by the correlation) stay in L2
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
@@ -177,6 +185,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
     fold_pm1_tma(TmaArgs a) {
     constexpr bool FUSED = LOGL2 > 0 || TCM;
     extern __shared__ __align__(1024) uint8_t smem[];
+    if constexpr (TCM) pdl_trigger();
     uint8_t *ring = smem;
     uint16_t *privb = reinterpret_cast<uint16_t *>(smem + NST * STAGE_BYTES);  // [2][TW][priv_stride]
     uint64_t *full = reinterpret_cast<uint64_t *>(privb + 2 * TW * a.priv_stride);
@@ -235,6 +244,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             int pb = 0;
             uint32_t pph = 0;
             uint64_t *pbegin = reinterpret_cast<uint64_t *>(tsm + a.tca.offMisc + tc::MISC_PBEGIN);
+            bool pdl_done = false;
             if (a.tca.dbg && gt == 0) a.tca.dbg[8 * a.n_items + 2 * blockIdx.x] = t_entry;
             for (;;) {
                 tc::group_wait<GS>(&pbegin[pb], pph, gt >> 5);
@@ -258,6 +268,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 }
 #endif
                 tc::group_wait<GS>(&yready[pb], pph, gt >> 5);
+                if (!pdl_done) { pdl_wait(); pdl_done = true; }  // before the first residues / k stores
                 tc::tc_main<GS>(a.tca, tsm, b, gt, warp & 3, tbase, mph, fl1, a_alt);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&ydone[pb]);
@@ -342,6 +353,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
         const int et = threadIdx.x - (TW + 1) * 32;  // 0 .. NE*32-1
         int pb = 0;
         uint32_t pph = 0;
+        bool pdl_done = false;
         for (;;) {
             if constexpr (TCM) {
                 // the pair of this buffer is known as soon as its fold starts: stage
@@ -356,6 +368,9 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 }
             }
             mbar_wait(&pfull[pb], pph);
+            if constexpr (TCM) {
+                if (!pdl_done) { pdl_wait(); pdl_done = true; }  // before this warp's first y2 store
+            }
             long long te0 = 0;
             if constexpr (TCM) te0 = tc::gtime();
             const int64_t item = pitem[pb];
@@ -588,6 +603,9 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             }
         }
         const int64_t c0 = it.cs_cta + warp * 512 + 16 * lane;
+        if constexpr (TCM) {
+            if (seq == 0) pdl_wait();  // first global write of this warp (y1) follows
+        }
         if (active) {
             // drain: lane l's low block (bins 16 l - 16 ntile + [0,16)) + lane l-1's pending carry
             uint32_t lo[8];
@@ -699,7 +717,27 @@ int launch(const TmaArgs &a, int64_t grid, size_t smem, cudaStream_t s) {
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         attr = true;
     }
-    k<<<(unsigned)grid, (TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM ? tc::NTHR : 0), smem, s>>>(a);
+    const unsigned nthr = (TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM ? tc::NTHR : 0);
+    static const bool no_pdl = getenv("TM_NO_PDL") != nullptr;  // A/B
+    if constexpr (TCM) {
+        if (!no_pdl) {  // programmatic dependent launch: see pdl_trigger / pdl_wait
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)grid);
+            cfg.blockDim = dim3(nthr);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            const cudaError_t e = cudaLaunchKernelEx(&cfg, k, a);
+            if (e != cudaSuccess) return tm_cuda_status(e, "fold_pm1_tma (PDL launch)");
+            TM_CHECK_LAUNCH("fold_pm1_tma");
+            return TM_OK;
+        }
+    }
+    k<<<(unsigned)grid, nthr, smem, s>>>(a);
     TM_CHECK_LAUNCH("fold_pm1_tma");
     return TM_OK;
 }

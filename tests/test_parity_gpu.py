@@ -760,3 +760,28 @@ def test_randomized_large_shapes_sampled(tm, seed):
     for b in rng.choice(B, 3, replace=False):
         o = f(x_h[b], t_h[b], M=M1 if M1 != K else 0, want_vectors=False)
         assert tuple(rr[b]) == o["residues"] and kk[b] == o["k"], (b, N, K, M1, B)
+
+
+def test_back_to_back_fused_runs(tm):
+    """Consecutive tm_run calls on one stream (the fused kernel overlaps the next
+    launch with its tail through programmatic dependent launch): several batches
+    and the same workspace, every pair's result equal to the staged path's."""
+    N, K, B = 2 ** 18, 2048, 300
+    plan = tm.Plan(N, K, seed=71)
+    ws = plan.workspace(B)
+    xs, ts, outs = [], [], []
+    for r in range(4):
+        x_h, t_h, _ = tmgen.batch(71, r * B, B, N, K, 0.05)
+        xs.append(up(x_h)); ts.append(up(t_h))
+    for r in range(4):
+        res = torch.empty((B, 2), dtype=torch.int32, device=DEV)
+        k = torch.empty(B, dtype=torch.int64, device=DEV)
+        plan.run(xs[r], ts[r], residues=res, k=k, ws=ws)
+        outs.append((res, k))
+    torch.cuda.synchronize()
+    for r in range(4):
+        y1, y2 = plan.fold(xs[r])
+        res_s, k_s = plan.match(*plan.correlate(y1, y2, plan.fold_template(ts[r])))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(outs[r][0].cpu().numpy(), res_s.cpu().numpy())
+        np.testing.assert_array_equal(outs[r][1].cpu().numpy(), k_s.cpu().numpy())
