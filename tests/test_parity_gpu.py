@@ -785,3 +785,27 @@ def test_back_to_back_fused_runs(tm):
         torch.cuda.synchronize()
         np.testing.assert_array_equal(outs[r][0].cpu().numpy(), res_s.cpu().numpy())
         np.testing.assert_array_equal(outs[r][1].cpu().numpy(), k_s.cpu().numpy())
+
+
+def test_back_to_back_fused_runs_two_plans(tm):
+    """Interleaved fused tm_run calls of two plans (different N, K, workspaces)
+    on one stream: each grid overlaps the previous one's tail (PDL); results
+    equal the oracle's."""
+    cfgs = [(2 ** 18, 2048, 200, 81), (2 ** 17, 1024, 160, 82)]
+    plans, data = [], []
+    for N, K, B, seed in cfgs:
+        plan = tm.Plan(N, K, seed=seed)
+        x_h, t_h, _ = tmgen.batch(seed, 0, B, N, K, 0.05)
+        plans.append(plan)
+        data.append((x_h, t_h, up(x_h), up(t_h), plan.workspace(B)))
+    outs = []
+    for i in (0, 1, 0, 1, 1, 0):
+        x_h, t_h, x, t, ws = data[i]
+        outs.append((i, *plans[i].run(x, t, ws=ws)))
+    torch.cuda.synchronize()
+    for i, res, k in outs:
+        x_h, t_h = data[i][0], data[i][1]
+        rr, kk = res.cpu().numpy(), k.cpu().numpy()
+        for b in (0, len(kk) // 2, len(kk) - 1):
+            o = oracle.ftm(x_h[b], t_h[b], want_vectors=False)
+            assert tuple(rr[b]) == o["residues"] and kk[b] == o["k"], (i, b)
