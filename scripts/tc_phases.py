@@ -23,6 +23,8 @@ ph = np.diff(d[:, :6], axis=1)
 names = ['tmpl', 'stage_y', 'buildA', 'mma', 'epi']
 for i, n in enumerate(names):
     print(f'{n:8s} mean {ph[:, i].mean():9.0f} p50 {np.median(ph[:, i]):9.0f} max {ph[:, i].max():9.0f}')
+last = ph[B - 148:]  # each CTA's last pair (static schedule)
+print('last pairs: ' + '  '.join(f'{n} {np.median(last[:, i]):.0f}' for i, n in enumerate(names)))
 tot = d[:, 5] - d[:, 0]
 print('pair lifetime mean', tot.mean(), 'span per SM', [(d[d[:,6]==s,5].max()-d[d[:,6]==s,0].min()) for s in range(3)])
 t0 = d[:, 0].min()
