@@ -408,8 +408,71 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 // fused kernel: it competes harder with the fold warps for issue slots)
                 const int pad = 16 * ntile, nw = width >> 9;
                 const bool c3 = pad <= 1024;
+                // the CTA's last pair (its epilogue is on the kernel's tail; mid-run the
+                // gentler per-bin loop below costs the concurrent fold less): runs of 16
+                // consecutive bins per thread with 16-byte loads and stores (pad <= 512:
+                // a diagonal then lies in at most two strips, or strip 0 when d < 0)
+                const bool runs = TCM && a.work_counter == nullptr && item + (int64_t)gridDim.x >= a.n_items &&
+                                  pad <= 512 && (q & 15) == 0 && (M1 & 15) == 0 && !a.accumulate &&
+                                  ((reinterpret_cast<uintptr_t>(o2) & 15) == 0);
+                if (runs) {
+                    const int stride = a.priv_stride;
+                    for (int r = et; r < (M1 >> 4); r += NE * 32) {
+                        const int k0 = r << 4;
+                        const int w1 = k0 >> 9, rel = (k0 & 511) + pad;
+                        int32_t C[16];
+                        {
+                            const uint4 *sp = reinterpret_cast<const uint4 *>(pv + w1 * stride + rel);
+                            const uint4 u0 = sp[0], u1 = sp[1];
+                            const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) { C[2 * i] = (int32_t)(w[i] & 0xFFFFu); C[2 * i + 1] = (int32_t)(w[i] >> 16); }
+                        }
+                        if (rel >= 512 && w1 + 1 < nw) {
+                            const uint4 *sp = reinterpret_cast<const uint4 *>(pv + (w1 + 1) * stride + rel - 512);
+                            const uint4 u0 = sp[0], u1 = sp[1];
+                            const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) { C[2 * i] += (int32_t)(w[i] & 0xFFFFu); C[2 * i + 1] += (int32_t)(w[i] >> 16); }
+                        }
+                        if (k0 + 15 >= M2 - pad) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (k0 + i >= M2 - pad) C[i] += (int32_t)pv[k0 + i - M2 + pad];
+                        }
+                        int32_t v[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] = q - (M1 - (k0 + i) < q ? 1 : 0) - C[i];
+                        if (!a.block && k0 + 15 >= M2 - q) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (k0 + i >= M2 - q) v[i] += xb[k0 + i - (M2 - q)];
+                        }
+                        int4 *dst = reinterpret_cast<int4 *>(o2 + k0);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) dst[i] = make_int4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                        if (k0 < K) {
+                            int32_t e[16];
+                            if (a.block) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) e[i] = v[i];
+                            } else {
+                                const uint4 xk = *reinterpret_cast<const uint4 *>(xb + k0);
+                                const uint4 xq = *reinterpret_cast<const uint4 *>(xb + k0 + q);
+                                const uint32_t wk[4] = {xk.x, xk.y, xk.z, xk.w}, wq[4] = {xq.x, xq.y, xq.z, xq.w};
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    e[i] = v[i] - (int32_t)(int8_t)(wk[i >> 2] >> (8 * (i & 3))) +
+                                           (int32_t)(int8_t)(wq[i >> 2] >> (8 * (i & 3)));
+                            }
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (k0 + i < K) o2[M2 + k0 + i] = e[i];
+                        }
+                    }
+                }
 #pragma unroll 2
-                for (int k = et; k < M2; k += NE * 32) {
+                for (int k = runs ? M1 + et : et; k < M2; k += NE * 32) {  // (runs: only bin M1 is left)
                     // bin k collects the unwrapped diagonals d = k and d = k - M2 (d >= dlo)
                     int32_t C = c3 ? comb3(pv, a.priv_stride, k, pad, nw) : comb_at(pv, a.priv_stride, k, ntile, width);
                     if (k - M2 >= dlo)
