@@ -38,7 +38,12 @@ struct F32Args {
     float *parts;              // [batch][nrc][M1 + n_strips (R + 127)]
 };
 
-__device__ __forceinline__ int64_t part_stride(const F32Args &a) { return a.M1 + a.n_strips * (a.R + 127); }
+// floats per (pair, row chunk) of partial sums, a multiple of 4 (the column sums
+// are stored as float4)
+__host__ __device__ __forceinline__ int64_t part_stride_of(int64_t M1, int64_t n_strips, int64_t R) {
+    return (M1 + n_strips * (R + 127) + 3) & ~int64_t(3);
+}
+__device__ __forceinline__ int64_t part_stride(const F32Args &a) { return part_stride_of(a.M1, a.n_strips, a.R); }
 
 __global__ void __launch_bounds__(FW * 32) fold_f32_strips(F32Args a) {
     extern __shared__ float emit[];  // [FW][RMAX + 127]
@@ -161,7 +166,7 @@ size_t tm_fold_f32_ws_bytes(const tm_plan_s *p, int64_t batch) {
     if (!tm_fold_f32_ok(p)) return 0;
     int64_t R, nrc;
     geometry(p, p->N / p->M1, &R, &nrc);
-    return (size_t)batch * nrc * (p->M1 + (p->M1 / 128) * (R + 127)) * 4;
+    return (size_t)batch * nrc * part_stride_of(p->M1, p->M1 / 128, R) * 4;
 }
 
 // TM_EUNSUPPORTED (nothing enqueued) when the chunk or alignment does not qualify.

@@ -244,6 +244,16 @@ def test_f32_small(tm):
     check_f32_pairs(tm, plan, x_h, t_h, range(4))
 
 
+def test_f32_partial_stride_alignment(tm):
+    """Regression (found by the randomized sweep): N = 12800, K = 256 gives a
+    partial-sum row of 256 + 2 * (50 + 127) = 610 floats; rows must be padded to
+    a multiple of 4 for the float4 column-sum stores."""
+    N, K = 12800, 256
+    plan = tm.Plan(N, K, seed=387, dtype="float32")
+    x_h, t_h, _ = tmgen.batch(387, 0, 3, N, K, 0.5, dtype=np.float32)
+    check_f32_pairs(tm, plan, x_h, t_h, range(3))
+
+
 def test_f32_ragged(tm):
     N, K = 30011, 250   # M1 does not divide N
     plan = tm.Plan(N, K, M=260, seed=32, dtype="float32")
