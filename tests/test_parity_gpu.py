@@ -210,7 +210,7 @@ def test_empty_batch_and_errors(tm):
 
 
 # ------------------------------------------------------------- fp32 (cfg3 shape)
-def check_f32_pairs(tm, plan, x_h, t_h, pairs):
+def check_f32_pairs(tm, plan, x_h, t_h, pairs, alias_repair=False):
     x, t = up(x_h), up(t_h)
     y1, y2 = plan.fold(x)
     tf = plan.fold_template(t)
@@ -220,7 +220,7 @@ def check_f32_pairs(tm, plan, x_h, t_h, pairs):
     torch.cuda.synchronize()
     tol = 1e-5
     for b in pairs:
-        o = oracle.ftm(x_h[b], t_h[b], M=plan.M1 if plan.M1 != plan.K else 0)
+        o = oracle.ftm(x_h[b], t_h[b], M=plan.M1 if plan.M1 != plan.K else 0, alias_repair=alias_repair)
         for name, g in (("y1", y1), ("y2", y2), ("r1", r1), ("r2", r2)):
             ov = o[name]
             gv = g[b].cpu().numpy().astype(np.float64)
@@ -232,7 +232,7 @@ def check_f32_pairs(tm, plan, x_h, t_h, pairs):
             if gap > tol * np.max(np.abs(ov)):
                 assert int(res[b, j]) == o["residues"][j] == int(res_run[b, j]), (b, j)
         m1, m2 = int(res[b, 0]), int(res[b, 1])
-        assert int(k[b]) == crt_closed(m1, plan.M1, m2, plan.M2, plan.N)
+        assert int(k[b]) == oracle.resolve(m1, plan.M1, m2, plan.M2, plan.N, alias_repair)
         if (m1, m2) == o["residues"]:
             assert int(k[b]) == o["k"]
 
@@ -741,7 +741,7 @@ def test_randomized_sweep_against_oracle(tm, seed):
     elif dtype == "int8":
         check_int_pairs(tm, plan, x_h, t_h, range(B), alias_repair=alias)
     else:
-        check_f32_pairs(tm, plan, x_h, t_h, range(B))
+        check_f32_pairs(tm, plan, x_h, t_h, range(B), alias_repair=alias)
 
 
 @pytest.mark.parametrize("seed", range(10))
