@@ -443,6 +443,8 @@ __global__ void argmax_kernel(const T *__restrict__ r1, const T *__restrict__ r2
 // steps 8-9 (tm_resolve)
 __global__ void crt_kernel(const int32_t *__restrict__ resid, int64_t batch, int64_t M1, int64_t M2,
                            uint32_t inv, int64_t N, int64_t wrap, int32_t *residues_out, int64_t *k) {
+    pdl_trigger();
+    pdl_wait();
     int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= batch) return;
     int64_t m1 = resid[2 * b], m2 = resid[2 * b + 1];
@@ -572,8 +574,9 @@ extern "C" __attribute__((visibility("default"))) int tm_correlate(tm_plan p, co
 int tm_crt_impl(const tm_plan_s *p, const int32_t *resid, int64_t batch, int32_t *residues_out, int64_t *k,
                 cudaStream_t s) {
     if (batch == 0) return TM_OK;
-    crt_kernel<<<(unsigned)((batch + 255) / 256), 256, 0, s>>>(resid, batch, p->M1, p->M2, p->crt_inv, p->N,
-                                                               p->crt_wrap, residues_out, k);
+    const cudaError_t e = launch_pdl(crt_kernel, dim3((unsigned)((batch + 255) / 256)), dim3(256), 0, s, resid, batch,
+                                     p->M1, p->M2, p->crt_inv, p->N, p->crt_wrap, residues_out, k);
+    if (e != cudaSuccess) return tm_cuda_status(e, "tm_match: crt_kernel");
     TM_CHECK_LAUNCH("tm_match: crt_kernel");
     return TM_OK;
 }

@@ -185,6 +185,8 @@ struct FftArgs {
 
 template <int LOGL>
 __global__ void __launch_bounds__(FGeo<LOGL>::NT, 1) fft_template_f32(FftArgs a) {
+    pdl_trigger();
+    pdl_wait();
     using G = FGeo<LOGL>;
     extern __shared__ float fsm[];
     float *br = fsm, *bi = fsm + G::L;
@@ -211,6 +213,8 @@ __device__ __forceinline__ void fmax_idx(float &bv, int &bi, float v, int i) {
 
 template <int LOGL>
 __global__ void __launch_bounds__(FGeo<LOGL>::NT, 1) fft_corr_f32(FftArgs a) {
+    pdl_trigger();
+    pdl_wait();
     using G = FGeo<LOGL>;
     extern __shared__ float fsm[];
     float *br = fsm, *bi = fsm + G::L;
@@ -309,12 +313,14 @@ int launch_pair(bool templ, const FftArgs &A, int64_t batch, cudaStream_t s) {
     if (templ) {
         auto k = fft_template_f32<LOGL>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<(unsigned)batch, G::NT, smem, s>>>(A);
+        const cudaError_t e = launch_pdl(k, dim3((unsigned)batch), dim3(G::NT), smem, s, A);
+        if (e != cudaSuccess) return tm_cuda_status(e, "fft_template_f32");
         TM_CHECK_LAUNCH("fft_template_f32");
     } else {
         auto k = fft_corr_f32<LOGL>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<(unsigned)batch, G::NT, smem, s>>>(A);
+        const cudaError_t e = launch_pdl(k, dim3((unsigned)batch), dim3(G::NT), smem, s, A);
+        if (e != cudaSuccess) return tm_cuda_status(e, "fft_corr_f32");
         TM_CHECK_LAUNCH("fft_corr_f32");
     }
     return TM_OK;

@@ -47,6 +47,7 @@ __device__ __forceinline__ int64_t part_stride(const F32Args &a) { return part_s
 
 __global__ void __launch_bounds__(FW * 32) fold_f32_strips(F32Args a) {
     extern __shared__ float emit[];  // [FW][RMAX + 127]
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t item = blockIdx.x;
     const int64_t rc = item % a.nrc;
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(FW * 32) fold_f32_strips(F32Args a) {
     for (int e = 0; e < 4; ++e) em[4 * lane + e - (nrow - 1) + R - 1] = s2[e];
     __syncwarp();
     float *pp = a.parts + (b * a.nrc + rc) * part_stride(a);
+    pdl_wait();  // the previous launch on the stream may still read the partial sums
     // column partial sums
     *reinterpret_cast<float4 *>(pp + c0) = make_float4(s1[0], s1[1], s1[2], s1[3]);
     // diagonal partials: indices [R - nrow, R + 127) were written (shorter chunks leave a zero head)
@@ -96,6 +98,8 @@ __global__ void __launch_bounds__(FW * 32) fold_f32_strips(F32Args a) {
 // bin sums, wrap and extension; x read only for the wrap/extension terms
 __global__ void fold_f32_finalize(F32Args a, int64_t offset, int64_t len, float *__restrict__ y1, int64_t ldy1,
                                   float *__restrict__ y2, int64_t ldy2, int accumulate) {
+    pdl_trigger();
+    pdl_wait();  // the strips of this fold
     const int64_t b = blockIdx.y;
     const float *xb = a.x + b * a.ldx;
     const float *pb = a.parts + b * a.nrc * part_stride(a);
@@ -191,12 +195,18 @@ int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
         cudaFuncSetAttribute(fold_f32_strips, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    fold_f32_strips<<<(unsigned)items, FW * 32, smem, s>>>(a);
+    {
+        const cudaError_t e = launch_pdl(fold_f32_strips, dim3((unsigned)items), dim3(FW * 32), smem, s, a);
+        if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: fold_f32_strips");
+    }
     TM_CHECK_LAUNCH("tm_fold: fold_f32_strips");
     int64_t gx = (p->M2 + p->K + 255) / 256;
     if (gx > 65535) gx = 65535;
-    fold_f32_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(a, offset, len, (float *)y1, ldy1,
-                                                                           (float *)y2, ldy2, accumulate);
+    {
+        const cudaError_t e = launch_pdl(fold_f32_finalize, dim3((unsigned)gx, (unsigned)batch), dim3(256), 0, s, a,
+                                         offset, len, (float *)y1, ldy1, (float *)y2, ldy2, accumulate);
+        if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: fold_f32_finalize");
+    }
     TM_CHECK_LAUNCH("tm_fold: fold_f32_finalize");
     return TM_OK;
 }

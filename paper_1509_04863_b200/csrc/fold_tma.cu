@@ -91,8 +91,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 // an SM this grid has left), and each warp role waits for the previous grid
 // (griddepcontrol.wait: completed, memory visible) only before its first global
 // write -- so the next launch streams x while this one finishes its tail.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // x is streamed exactly once: its L2 lines are marked evict-first so that the
 // folded vectors (written, then read back by the correlation) stay in L2
@@ -781,7 +779,7 @@ int launch(const TmaArgs &a, int64_t grid, size_t smem, cudaStream_t s) {
         attr = true;
     }
     const unsigned nthr = (TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM ? tc::NTHR : 0);
-    static const bool no_pdl = getenv("TM_NO_PDL") != nullptr;  // A/B
+    const bool no_pdl = !tm_pdl_enabled();  // A/B
     if constexpr (TCM) {
         if (!no_pdl) {  // programmatic dependent launch: see pdl_trigger / pdl_wait
             cudaLaunchConfig_t cfg{};

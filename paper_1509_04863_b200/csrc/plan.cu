@@ -227,6 +227,11 @@ extern "C" __attribute__((visibility("default"))) void tm_plan_destroy(tm_plan p
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
+bool tm_pdl_enabled() {
+    static const bool on = getenv("TM_NO_PDL") == nullptr;
+    return on;
+}
+
 tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch) {
     tm_ws_layout w{};
     size_t off = 0;

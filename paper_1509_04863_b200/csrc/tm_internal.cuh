@@ -72,6 +72,34 @@ void tm_count_launch();
         if (_e != cudaSuccess) return tm_cuda_status(_e, what);                \
         tm_count_launch();                                                     \
     } while (0)
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may be
+// scheduled while its predecessor on the stream runs, once that predecessor has
+// executed pdl_trigger(); pdl_wait() blocks until the predecessor has completed
+// and its memory is visible (a no-op without a PDL predecessor).  Kernels call
+// pdl_trigger() at entry and pdl_wait() before their first dependent global
+// access.  TM_NO_PDL in the environment launches them normally (A/B).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool tm_pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args &&...args) {
+    if (!tm_pdl_enabled()) {
+        k<<<grid, block, smem, s>>>(static_cast<KArgs>(args)...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // stage-boundary events of tm_run (tm_profile_events); NULL when disabled
 void tm_prof_mark(int stage, cudaStream_t s);
 
