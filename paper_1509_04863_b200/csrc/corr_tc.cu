@@ -43,6 +43,8 @@ using namespace tc;
 
 __global__ void __launch_bounds__(NTHR, 2) corr_tc_kernel(const TcArgs a) {
     extern __shared__ __align__(1024) uint8_t sm[];
+    pdl_trigger();
+    pdl_wait();  // y (and t) come from the preceding launches
     const int tid = threadIdx.x, warp = tid >> 5;
     uint64_t *mdone = reinterpret_cast<uint64_t *>(sm + a.offMisc);
     uint32_t *tslot = reinterpret_cast<uint32_t *>(sm + a.offMisc + 8);
@@ -184,7 +186,10 @@ int tm_tc_correlate(const tm_plan_s *p, const void *y1, const void *y2, int64_t 
             smem += extra;
         }
     }
-    corr_tc_kernel<<<(unsigned)grid, NTHR, smem, s>>>(a);
+    {
+        const cudaError_t e = launch_pdl(corr_tc_kernel, dim3((unsigned)grid), dim3(NTHR), smem, s, a);
+        if (e != cudaSuccess) return tm_cuda_status(e, "corr_tc_kernel");
+    }
     TM_CHECK_LAUNCH("corr_tc_kernel");
     return TM_OK;
 }

@@ -256,6 +256,8 @@ __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t
                               int64_t row0, int64_t rows, const int32_t *__restrict__ counts,
                               int32_t *__restrict__ y1, int64_t ldy1, int32_t *__restrict__ y2, int64_t ldy2,
                               int accumulate, int block) {
+    pdl_trigger();
+    pdl_wait();  // the counts of this fold
     const int64_t b = blockIdx.y;
     const int8_t *xb = x + b * ldx;
     const int32_t *c1 = counts + b * (M1 + M2), *c2 = c1 + M1;
@@ -365,10 +367,11 @@ int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batc
             if (rc != TM_OK || !used_counts) return rc;
             tm_ws_layout L = tm_ws(p, batch);
             int64_t gx = (p->M2 + p->K + 1023) / 1024;
-            fold_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(
+            { const cudaError_t e_ = launch_pdl(fold_finalize, dim3((unsigned)gx, (unsigned)batch), dim3(256), 0, s,
                 (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, offset / p->M1, rows,
                 (const int32_t *)((char *)ws + L.fold_counts), (int32_t *)y1, ldy1, (int32_t *)y2, ldy2, accumulate,
                 p->block);
+              if (e_ != cudaSuccess) return tm_cuda_status(e_, "tm_fold: fold_finalize"); }
             TM_CHECK_LAUNCH("tm_fold: fold_finalize");
             return TM_OK;
         }
@@ -398,9 +401,10 @@ int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batc
         fold_pm1<<<(unsigned)items, PM_WARPS * 32, smem, s>>>(a);
         TM_CHECK_LAUNCH("tm_fold: fold_pm1");
         int64_t gx = (p->M2 + p->K + 1023) / 1024;
-        fold_finalize<<<dim3((unsigned)gx, (unsigned)batch), 256, 0, s>>>(
-            (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, a.row0, a.rows,
+        { const cudaError_t e_ = launch_pdl(fold_finalize, dim3((unsigned)gx, (unsigned)batch), dim3(256), 0, s,
+                (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, a.row0, a.rows,
             counts, (int32_t *)y1, ldy1, (int32_t *)y2, ldy2, accumulate, p->block);
+              if (e_ != cudaSuccess) return tm_cuda_status(e_, "tm_fold: fold_finalize"); }
         TM_CHECK_LAUNCH("tm_fold: fold_finalize");
         return TM_OK;
     }

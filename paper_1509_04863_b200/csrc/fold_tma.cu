@@ -19,6 +19,7 @@
 //  * when an item is a whole pair (M1 <= 4096, full fold) the consumers write
 //    the finished y1/y2 directly (counts -> values, the mod-N wrap and the
 //    strategy-1 extension), so no workspace, memset or second kernel is needed.
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
     fold_pm1_tma(TmaArgs a) {
     constexpr bool FUSED = LOGL2 > 0 || TCM;
     extern __shared__ __align__(1024) uint8_t smem[];
-    if constexpr (TCM) pdl_trigger();
+    if constexpr (LOGL2 == 0) pdl_trigger();
     uint8_t *ring = smem;
     uint16_t *privb = reinterpret_cast<uint16_t *>(smem + NST * STAGE_BYTES);  // [2][TW][priv_stride]
     uint64_t *full = reinterpret_cast<uint64_t *>(privb + 2 * TW * a.priv_stride);
@@ -366,8 +367,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 }
             }
             mbar_wait(&pfull[pb], pph);
-            if constexpr (TCM) {
-                if (!pdl_done) { pdl_wait(); pdl_done = true; }  // before this warp's first y2 store
+            if constexpr (LOGL2 == 0) {  // before this warp's first y2 store / counts atomic
+                if (!pdl_done) { pdl_wait(); pdl_done = true; }
             }
             long long te0 = 0;
             if constexpr (TCM) te0 = tc::gtime();
@@ -664,8 +665,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             }
         }
         const int64_t c0 = it.cs_cta + warp * 512 + 16 * lane;
-        if constexpr (TCM) {
-            if (seq == 0) pdl_wait();  // first global write of this warp (y1) follows
+        if constexpr (LOGL2 == 0) {
+            if (seq == 0) pdl_wait();  // first global write of this warp (y1 / counts) follows
         }
         if (active) {
             // drain: lane l's low block (bins 16 l - 16 ntile + [0,16)) + lane l-1's pending carry
@@ -780,7 +781,7 @@ int launch(const TmaArgs &a, int64_t grid, size_t smem, cudaStream_t s) {
     }
     const unsigned nthr = (TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM ? tc::NTHR : 0);
     const bool no_pdl = !tm_pdl_enabled();  // A/B
-    if constexpr (TCM) {
+    if constexpr (LOGL2 == 0) {
         if (!no_pdl) {  // programmatic dependent launch: see pdl_trigger / pdl_wait
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3((unsigned)grid);
@@ -805,6 +806,15 @@ int launch(const TmaArgs &a, int64_t grid, size_t smem, cudaStream_t s) {
 
 }  // namespace
 
+// counts workspace reset as a PDL kernel (a memset between kernels would end the
+// overlap of consecutive steps): waits for the previous launch, then zeroes
+__global__ void zero_i32(int32_t *p, int64_t n) {
+    pdl_trigger();
+    pdl_wait();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = 0;
+}
+
 int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
                 void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, int64_t R, int64_t n_rc,
                 cudaStream_t s, bool *used_counts) {
@@ -814,8 +824,11 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     a.ldy1 = ldy1; a.ldy2 = ldy2;
     *used_counts = !a.owner;
     if (!a.owner) {
-        cudaError_t e = cudaMemsetAsync(a.counts, 0, (size_t)batch * (p->M1 + p->M2) * 4, s);
-        if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: memset");
+        const int64_t n = batch * (p->M1 + p->M2);
+        const int64_t blocks = std::min<int64_t>((n + 255) / 256, 4 * (int64_t)p->num_sms);
+        const cudaError_t e = launch_pdl(zero_i32, dim3((unsigned)blocks), dim3(256), 0, s, a.counts, n);
+        if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: counts reset");
+        TM_CHECK_LAUNCH("tm_fold: zero_i32");
     }
 #ifndef TM_FOLD_NST
 #define TM_FOLD_NST 4
