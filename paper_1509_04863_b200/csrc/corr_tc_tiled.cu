@@ -114,6 +114,8 @@ __device__ __forceinline__ void stage_window(const TcArgs &a, uint8_t *B, int64_
 
 template <int NT>
 __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int B_BYTES = b_bytes<NT>();
     extern __shared__ __align__(1024) uint8_t sm[];
     const TcArgs &a = T.a;
@@ -372,6 +374,8 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
 // (K-slice, pair) adds its partial dot products into lsum (exact int64)
 constexpr int LSLICE = 1024;  // K-slice per CTA (4 terms per thread: latency-bound loop)
 __global__ void __launch_bounds__(256) tc_tiled_leftover(const TiledArgs T) {
+    pdl_trigger();
+    pdl_wait();
     const TcArgs &a = T.a;
     const int64_t b = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -400,9 +404,23 @@ __global__ void __launch_bounds__(256) tc_tiled_leftover(const TiledArgs T) {
     }
 }
 
+// workspace reset as a PDL kernel (a memset would end the overlap of launches)
+__global__ void tiled_zero(int32_t *p0, int64_t n0, int32_t *p1, int64_t n1, int32_t *p2, int64_t n2) {
+    pdl_trigger();
+    pdl_wait();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1 + n2; i += stride) {
+        if (i < n0) p0[i] = 0;
+        else if (i < n0 + n1) p1[i - n0] = 0;
+        else p2[i - n0 - n1] = 0;
+    }
+}
+
 // per pair: tile keys + leftovers -> residues; steps 8-9 (tm_resolve)
 __global__ void tc_tiled_final(const TiledArgs T, int64_t batch, int32_t *resid, int32_t *residues_out,
                                int64_t *k_out, int64_t *r_out0, int64_t *r_out1, int64_t *keys_out, int with_left) {
+    pdl_trigger();
+    pdl_wait();
     const TcArgs &a = T.a;
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= batch) return;
@@ -537,12 +555,15 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     T.racc[0] = r1 ? (int64_t *)r1 : racc;
     T.racc[1] = r2 ? (int64_t *)r2 : racc + batch * p->M1;
     T.write_r = (r1 != nullptr);
-    cudaError_t e = cudaMemsetAsync(ws, 0, zero_bytes, s);
-    if (e == cudaSuccess && T.n_cr > 1) {
-        e = cudaMemsetAsync(T.racc[0], 0, (size_t)batch * p->M1 * 8, s);
-        if (e == cudaSuccess) e = cudaMemsetAsync(T.racc[1], 0, (size_t)batch * p->M2 * 8, s);
+    {
+        const int64_t n0 = (int64_t)(zero_bytes / 4);
+        const int64_t n1 = T.n_cr > 1 ? batch * p->M1 * 2 : 0, n2 = T.n_cr > 1 ? batch * p->M2 * 2 : 0;
+        const int64_t blocks = std::min<int64_t>((n0 + n1 + n2 + 255) / 256, 4 * (int64_t)p->num_sms);
+        const cudaError_t e = launch_pdl(tiled_zero, dim3((unsigned)blocks), dim3(256), 0, s, (int32_t *)ws, n0,
+                                         (int32_t *)T.racc[0], n1, (int32_t *)T.racc[1], n2);
+        if (e != cudaSuccess) return tm_cuda_status(e, "tm_correlate: tiled reset");
+        TM_CHECK_LAUNCH("tm_correlate: tiled reset");
     }
-    if (e != cudaSuccess) return tm_cuda_status(e, "tm_correlate: tiled reset");
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(corr_tc_tiled<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<32>());
@@ -551,21 +572,26 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     }
     const dim3 grid((unsigned)(T.n_atp * T.n_cr), (unsigned)batch);
     if (T.n_atp > 0) {
-        if (NT == 32)
-            corr_tc_tiled<32><<<grid, TNTHR, smem_bytes<32>(), s>>>(T);
-        else
-            corr_tc_tiled<64><<<grid, TNTHR, smem_bytes<64>(), s>>>(T);
+        const cudaError_t e = NT == 32 ? launch_pdl(corr_tc_tiled<32>, grid, dim3(TNTHR), smem_bytes<32>(), s, T)
+                                       : launch_pdl(corr_tc_tiled<64>, grid, dim3(TNTHR), smem_bytes<64>(), s, T);
+        if (e != cudaSuccess) return tm_cuda_status(e, "corr_tc_tiled");
         TM_CHECK_LAUNCH("corr_tc_tiled");
     }
     const int nleft = (int)(std::max<int64_t>(0, p->M1 - (int64_t)P * T.a.NA[0]) +
                             std::max<int64_t>(0, p->M2 - (int64_t)P * T.a.NA[1]));
     const int with_left = part == 0;  // the leftover outputs belong to part 0
     if (nleft > 0 && with_left) {
-        tc_tiled_leftover<<<dim3((unsigned)((p->K + LSLICE - 1) / LSLICE), (unsigned)batch), 256, 0, s>>>(T);
+        const cudaError_t e = launch_pdl(tc_tiled_leftover, dim3((unsigned)((p->K + LSLICE - 1) / LSLICE), (unsigned)batch),
+                                         dim3(256), 0, s, T);
+        if (e != cudaSuccess) return tm_cuda_status(e, "tc_tiled_leftover");
         TM_CHECK_LAUNCH("tc_tiled_leftover");
     }
-    tc_tiled_final<<<(unsigned)((batch + 127) / 128), 128, 0, s>>>(T, batch, resid, residues_out, k, (int64_t *)r1,
-                                                                     (int64_t *)r2, keys_out, with_left);
+    {
+        const cudaError_t e = launch_pdl(tc_tiled_final, dim3((unsigned)((batch + 127) / 128)), dim3(128), 0, s, T,
+                                         batch, resid, residues_out, k, (int64_t *)r1, (int64_t *)r2, keys_out,
+                                         with_left);
+        if (e != cudaSuccess) return tm_cuda_status(e, "tc_tiled_final");
+    }
     TM_CHECK_LAUNCH("tc_tiled_final");
     return TM_OK;
 }
