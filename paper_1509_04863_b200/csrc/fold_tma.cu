@@ -30,7 +30,12 @@ namespace {
 
 constexpr int TW = 8;                 // consumer warps, one 512-column strip each
 constexpr int TCOLS = TW * 512;       // columns per CTA group
-constexpr int SROWS = 8;              // rows per ring stage
+#ifndef TM_SROWS
+#define TM_SROWS 8
+#endif
+constexpr int SROWS = TM_SROWS;       // rows per ring stage (8, or 4 with twice the stages)
+constexpr int GPS = SROWS / 4;        // 4-row groups per stage
+static_assert(SROWS == 8 || SROWS == 4, "SROWS");
 constexpr int STAGE_BYTES = SROWS * TCOLS;
 
 struct TmaArgs {
@@ -583,8 +588,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             for (int i = 0; i < 4; ++i) { W[4 + i] = W[i]; W[i] = 0; }
             const bool full_tile = (t * 16 + 16 <= nrow) && width == TCOLS;
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const int rbase = t * 16 + half * 8;
+            for (int half = 0; half < 16 / SROWS; ++half) {
+                const int rbase = t * 16 + half * SROWS;
                 if (rbase >= nrow) break;
 #ifdef TM_CONS_PROF
                 { long long t1 = clock64(); cp_busy += t1 - cp_t; cp_t = t1; }
@@ -596,8 +601,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 const uint32_t st = ring_u32 + s * STAGE_BYTES + colb;
                 const uint32_t rstride = full_tile ? TCOLS : width;
 #pragma unroll
-                for (int g = 0; g < 2; ++g) {
-                    // 4 rows r = 8 half + 4 g + rho, rho = 0..3 (alpha = r >> 2 = 2 half + g).
+                for (int g = 0; g < GPS; ++g) {
+                    // 4 rows r = SROWS half + 4 g + rho, rho = 0..3 (alpha = r >> 2 = GPS half + g).
                     // FULL (the tile is 16 whole rows of TCOLS columns): no row masks.
                     auto group = [&](auto fullc) {
                         constexpr bool FULL = decltype(fullc)::value;
@@ -622,7 +627,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                         // M2: row r, byte j -> window byte 16 - r + j.  With alpha = r >> 2 and
                         // rho = r & 3, window word 4 - alpha + k' (k' = -1..3) receives
                         // funnelshift_r(m[k'], m[k'+1], 8 rho) (m[-1] = m[4] = 0).
-                        const int alpha = half * 2 + g;
+                        const int alpha = half * GPS + g;
 #pragma unroll
                         for (int kk = -1; kk < 4; ++kk) {
                             uint32_t add = (kk >= 0) ? m[0][kk] : 0u;
@@ -959,10 +964,12 @@ int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void 
     a.ldy2 = a.tca.ldy[1] = p->ldy2_run;
     a.tca.discard_y = 1;
     // 4-stage ring when the tensor-core region fits next to it, else 3 stages
-    const size_t base4 = (smem_bytes(a, 4, 0) + 1023) / 1024 * 1024;
-    const size_t base3 = (smem_bytes(a, 3, 0) + 1023) / 1024 * 1024;
-    const int nst = (base4 + p->tc_smem <= 227 * 1024) ? 4 : 3;
-    const size_t base = nst == 4 ? base4 : base3;
+    constexpr int K4 = 32 / SROWS;   // "4 stages" of 8 rows: the same 128 KB ring in SROWS-row stages
+    constexpr int K3 = 24 / SROWS;
+    const size_t base4 = (smem_bytes(a, K4, 0) + 1023) / 1024 * 1024;
+    const size_t base3 = (smem_bytes(a, K3, 0) + 1023) / 1024 * 1024;
+    const int nst = (base4 + p->tc_smem <= 227 * 1024) ? K4 : K3;
+    const size_t base = nst == K4 ? base4 : base3;
     a.tc_off = (uint32_t)base;
     const size_t sm = base + p->tc_smem;
     if (sm > 227 * 1024) return TM_EUNSUPPORTED;
@@ -976,6 +983,6 @@ int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void 
     (void)counter;
 #endif
     const int64_t grid = batch < p->num_sms ? batch : p->num_sms;
-    if (nst == 4) return launch<4, 0, 1, true>(a, grid, sm, s);
-    return launch<3, 0, 1, true>(a, grid, sm, s);
+    if (nst == K4) return launch<K4, 0, 1, true>(a, grid, sm, s);
+    return launch<K3, 0, 1, true>(a, grid, sm, s);
 }
