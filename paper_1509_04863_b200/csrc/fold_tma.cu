@@ -895,7 +895,7 @@ bool tm_fused_ok(const tm_plan_s *p, int64_t batch) {
     if (!on) return false;
     return p->fast_fold && p->fast_corr && p->n_primes == 1 && p->M1 <= TCOLS && p->q1 <= 1024 &&
            p->logL2 == p->logL1 + 1 && p->L1 == p->M1 && p->nload1 == p->M1 && p->logL2 >= 10 && p->logL2 <= 13 &&
-           batch >= p->num_sms;
+           batch >= p->num_sms && (TW + 1 + NE) * 32 + ntt_threads(p->logL2) <= 1024;  // one CTA's threads
 }
 
 int tm_fold_corr_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
