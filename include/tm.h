@@ -200,6 +200,13 @@ int tm_match(tm_plan plan, const void *r1, const void *r2, int64_t batch,
  * tm_run -- the whole hot path, == tm_fold(offset 0, len N) o tm_fold_template
  * o tm_correlate o tm_match, without materialising r (argmax fused into the
  * correlation epilogue).  x [batch][ldx], t [batch][K].
+ * Its kernels use programmatic dependent launch: consecutive tm_run calls on
+ * one stream may overlap on the device (the next call streams its inputs
+ * while the previous one finishes), but every write of a call happens after
+ * the previous call on the stream has completed, so results and the ordering
+ * against other stream operations are as for plain stream order.  (The
+ * inputs x, t of a call must not be written by the immediately preceding
+ * tm_run / tm_fold kernel on the stream -- they never are by this library.)
  */
 int tm_run(tm_plan plan, const void *x, int64_t ldx, const void *t, int64_t batch,
            int32_t *residues, int64_t *k, void *ws, void *stream);
