@@ -35,7 +35,7 @@ constexpr int TCOLS = TW * 512;       // columns per CTA group
 #endif
 constexpr int SROWS = TM_SROWS;       // rows per ring stage (8, or 4 with twice the stages)
 constexpr int GPS = SROWS / 4;        // 4-row groups per stage
-static_assert(SROWS == 8 || SROWS == 4, "SROWS");
+static_assert(SROWS == 8 || SROWS == 4 || SROWS == 16, "SROWS");
 constexpr int STAGE_BYTES = SROWS * TCOLS;
 
 struct TmaArgs {
