@@ -43,7 +43,7 @@ WORKLOADS = {
                  desc="cfg5: one signal N=2^31 (+-1 int8, 2 GiB), K=65536, 5% flips, split over the GPUs; "
                       "partial folds summed by one NCCL all-reduce"),
 }
-EV_EVERY = 10  # timed steps between two stage-event samples
+EV_EVERY = 20  # timed steps between two stage-event samples (an event between two launches also ends their PDL overlap)
 METRIC = "signal Gsamples/s matched (1/2/4/8 B200) and % of HBM roofline; match success rate"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
