@@ -819,3 +819,35 @@ def test_back_to_back_fused_runs_two_plans(tm):
         for b in (0, len(kk) // 2, len(kk) - 1):
             o = oracle.ftm(x_h[b], t_h[b], want_vectors=False)
             assert tuple(rr[b]) == o["residues"] and kk[b] == o["k"], (i, b)
+
+
+@pytest.mark.parametrize("kind", ["staged_tc", "tiled", "f32"])
+def test_back_to_back_staged_runs(tm, kind):
+    """Consecutive tm_run calls through the staged paths (PDL-launched chains:
+    counts reset, fold, finalize, correlation; or the fp32 chain) on one stream
+    with one workspace: every call's residues and k equal the oracle's."""
+    if kind == "staged_tc":
+        N, K, B, dt = 2 ** 18, 2048, 40, np.int8       # batch < SMs: fold -> one-CTA tensor-core kernel
+    elif kind == "tiled":
+        N, K, B, dt = 2 ** 22, 16384, 4, np.int8       # long template: tiled tensor-core kernel
+    else:
+        N, K, B, dt = 2 ** 16, 512, 6, np.float32
+    plan = tm.Plan(N, K, seed=91, dtype="float32" if dt == np.float32 else "int8")
+    ws = plan.workspace(B)
+    batches = [tmgen.batch(91, r * B, B, N, K, 0.05 if dt == np.int8 else 0.5, dtype=dt) for r in range(3)]
+    outs = []
+    for x_h, t_h, _ in batches:
+        res = torch.empty((B, 2), dtype=torch.int32, device=DEV)
+        k = torch.empty(B, dtype=torch.int64, device=DEV)
+        plan.run(up(x_h), up(t_h), residues=res, k=k, ws=ws)
+        outs.append((res, k))
+    torch.cuda.synchronize()
+    for (x_h, t_h, _), (res, k) in zip(batches, outs):
+        rr, kk = res.cpu().numpy(), k.cpu().numpy()
+        for b in (0, B - 1):
+            o = oracle.ftm(x_h[b], t_h[b], want_vectors=False)
+            if dt == np.int8:
+                assert tuple(rr[b]) == o["residues"] and kk[b] == o["k"], (kind, b)
+            else:
+                m1, m2 = int(rr[b, 0]), int(rr[b, 1])
+                assert int(kk[b]) == oracle.resolve(m1, plan.M1, m2, plan.M2, plan.N)
