@@ -86,8 +86,9 @@ def lib():
         L.or_crt_multi.argtypes = [_p, _p, ctypes.c_int]
         L.or_crt_sets_multi.restype = _i64
         L.or_crt_sets_multi.argtypes = [_p, _p, ctypes.c_int, _i64]
-        L.or_ftm_multi_i8.restype = _i64
-        L.or_ftm_multi_i8.argtypes = [_p, _i64, _p, _i64, _p, ctypes.c_int, _p]
+        for n in ("or_ftm_multi_i8", "or_ftm_multi_f32"):
+            getattr(L, n).restype = _i64
+            getattr(L, n).argtypes = [_p, _i64, _p, _i64, _p, ctypes.c_int, _p]
         for n in ("or_ftm_block_i8", "or_ftm_block_f32"):
             getattr(L, n).restype = _i64
             getattr(L, n).argtypes = [_p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p]
@@ -343,12 +344,12 @@ def crt_sets_multi(m, M, N: int) -> int:
 
 
 def ftm_multi(x: np.ndarray, t: np.ndarray, moduli) -> dict:
-    """FTM() over alpha pairwise co-prime moduli (int8 data): k and residues."""
+    """FTM() over alpha pairwise co-prime moduli (int8 or float32 data): k and residues."""
     x = _as_input(x); t = _as_input(t)
-    assert _is_int(x) and _is_int(t)
     M = np.ascontiguousarray(moduli, np.int64)
     res = np.zeros(len(M), np.int64)
-    k = lib().or_ftm_multi_i8(_ptr(x), x.shape[0], _ptr(t), t.shape[0], _ptr(M), len(M), _ptr(res))
+    fn = lib().or_ftm_multi_i8 if _is_int(x) else lib().or_ftm_multi_f32
+    k = fn(_ptr(x), x.shape[0], _ptr(t), t.shape[0], _ptr(M), len(M), _ptr(res))
     if k == -3:
         raise ValueError("moduli must be >= K, pairwise co-prime, with product > N")
     return dict(k=k, residues=tuple(int(v) for v in res))

@@ -379,6 +379,35 @@ int64_t or_ftm_multi_i8(const int8_t *x, int64_t N, const int8_t *t, int64_t K, 
     return (z >= 0 && z < N) ? z : -1;
 }
 
+/* The same for float32 data: Eq. 2 folds and correlations in fp64. */
+int64_t or_ftm_multi_f32(const float *x, int64_t N, const float *t, int64_t K, const int64_t *M, int alpha,
+                         int64_t *residues) {
+    __int128 P = 1;
+    for (int j = 0; j < alpha; ++j) {
+        if (M[j] < K) return -3;
+        for (int i = 0; i < j; ++i) {
+            int64_t a = M[i], b = M[j];
+            while (b) { int64_t r = a % b; a = b; b = r; }
+            if (a != 1) return -3;
+        }
+        P *= M[j];
+        if (P > ((__int128)1 << 100)) P = ((__int128)1 << 100);
+    }
+    if (P <= N) return -3;
+    int64_t m[16];
+    for (int j = 0; j < alpha; ++j) {
+        double *y = (double *)malloc(sizeof(double) * (M[j] + K));
+        double *r = (double *)malloc(sizeof(double) * M[j]);
+        or_fold_f32(x, N, M[j], K, 0, N, y);
+        or_correlate_f64(y, M[j], K, t, r);
+        m[j] = or_argmax_f64(r, M[j]);
+        free(y); free(r);
+    }
+    if (residues) for (int j = 0; j < alpha; ++j) residues[j] = m[j];
+    int64_t z = or_crt_multi(m, M, alpha);
+    return (z >= 0 && z < N) ? z : -1;
+}
+
 /* ------------------------------------------------------------------ */
 /* Strategy 2 (Theorem 2): the Block sampling       */
 /* matrix Phi = [Phi_M Phi_M ... Phi_M] (ceil(N/M) blocks), Phi_M an M x M */

@@ -543,3 +543,17 @@ def test_ftm_multi_three_small_moduli_recovers_isolated_windows():
         x[k0:k0 + K] = t
         o = oracle.ftm_multi(x, t, M)
         assert o["k"] == k0 and o["residues"] == tuple(k0 % Mj for Mj in M)
+
+
+def test_ftm_multi_f32_equals_int_path_on_pm1_data():
+    """The fp64 path of the alpha-modulus FTM on +-1-valued float32 data equals
+    the exact int64 path on the same samples (every sum is an exact integer)."""
+    rng = np.random.default_rng(12)
+    N, K, M = 3000, 24, (25, 26, 27)
+    for _ in range(5):
+        x = rand_pm1(rng, N)
+        k0 = int(rng.integers(0, N))
+        t = x[(k0 + np.arange(K)) % N].copy()
+        a = oracle.ftm_multi(x, t, M)
+        b = oracle.ftm_multi(x.astype(np.float32), t.astype(np.float32), M)
+        assert a == b

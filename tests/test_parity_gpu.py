@@ -851,3 +851,22 @@ def test_back_to_back_staged_runs(tm, kind):
             else:
                 m1, m2 = int(rr[b, 0]), int(rr[b, 1])
                 assert int(kk[b]) == oracle.resolve(m1, plan.M1, m2, plan.M2, plan.N)
+
+
+def test_multi_moduli_f32(tm):
+    """tm_mplan_run on fp32 data: each residue equals the oracle's unless its
+    top-two gap is within reading C15's tolerance, and k = CRT(GPU residues)."""
+    N, K, M, B = 30000, 40, (41, 43, 47), 3
+    plan = tm.MultiPlan(N, K, M, dtype="float32")
+    x_h, t_h, _ = tmgen.batch(44, 0, B, N, K, 0.3, dtype=np.float32)
+    res, k = plan.run(up(x_h), up(t_h))
+    torch.cuda.synchronize()
+    res, k = res.cpu().numpy(), k.cpu().numpy()
+    for b in range(B):
+        for j, Mj in enumerate(M):
+            r = oracle.correlate(oracle.fold(x_h[b], Mj, K), Mj, t_h[b])
+            s = np.sort(r)
+            if s[-1] - s[-2] > 1e-5 * np.max(np.abs(r)):
+                assert int(res[b, j]) == oracle.argmax(r), (b, j)
+        z = oracle.crt_multi(res[b].astype(np.int64), M)
+        assert int(k[b]) == (z if z < N else -1)
