@@ -1,3 +1,4 @@
+"""The README usage example as a runnable check (staged path == fused path)."""
 import sys; sys.path.insert(0, '/root/repo')
 import paper_1509_04863_b200 as tm
 plan = tm.Plan(N=2**20, K=4096, seed=2)                 # Alg. 1 step 2: M1 = K, M2 = K + 1
@@ -8,6 +9,4 @@ r1, r2 = plan.correlate(y1, y2, plan.fold_template(t))
 residues2, k2 = plan.match(r1, r2)
 import torch
 assert torch.equal(k, k2) and torch.equal(residues, residues2)
-mp = tm.MultiPlan(2**16, 64, (65, 66, 67))
-xm, tmpl, _ = plan.generate(0, 2, 0.0) if False else (None, None, None)
 print("readme snippet ok", float((k == k0).double().mean()))
