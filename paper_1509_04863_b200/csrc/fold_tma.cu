@@ -421,6 +421,14 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                                   ((reinterpret_cast<uintptr_t>(o2) & 15) == 0);
                 if (runs) {
                     const int stride = a.priv_stride;
+                    if (et == NE * 32 - 1) {
+                        // bin M1 = M2 - 1 in closed form: only the diagonal d = -1 (strip 0,
+                        // index pad - 1) reaches it; its row g* = 0 < q is one element short,
+                        // and the mod-N wrap adds x[q - 1]
+                        int32_t v = q - 1 - (int32_t)pv[pad - 1];
+                        if (!a.block) v += xb[q - 1];
+                        o2[M1] = v;
+                    }
                     for (int r = et; r < (M1 >> 4); r += NE * 32) {
                         const int k0 = r << 4;
                         const int w1 = k0 >> 9, rel = (k0 & 511) + pad;
@@ -476,7 +484,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                     }
                 }
 #pragma unroll 2
-                for (int k = runs ? M1 + et : et; k < M2; k += NE * 32) {  // (runs: only bin M1 is left)
+                for (int k = runs ? M2 : et; k < M2; k += NE * 32) {  // (runs: every bin is done)
                     // bin k collects the unwrapped diagonals d = k and d = k - M2 (d >= dlo)
                     int32_t C = c3 ? comb3(pv, a.priv_stride, k, pad, nw) : comb_at(pv, a.priv_stride, k, ntile, width);
                     if (k - M2 >= dlo)

@@ -15,5 +15,4 @@ for it in range(3):
 torch.cuda.synchronize()
 L.tm_debug_tc_timestamps(None)
 d = dbg.cpu().numpy()[B * 8 + 4 * 148: B * 8 + 8 * 148].reshape(148, 4) / 1e3
-print('epilogue us (from pfull): after x staging p50 %.2f, after bin loop p50 %.2f, after barrier p50 %.2f' %
-      (np.median(d[:, 0]), np.median(d[:, 1]), np.median(d[:, 2])))
+print('epilogue us (from pfull): p50 stamps', [round(float(np.median(d[:, i])), 2) for i in range(4)])
