@@ -318,7 +318,8 @@ def main():
         tkey = args.workload + ":fused_tc"
     else:
         # fold kernel algorithmic bytes per launch: read x once + write y1, y2 once
-        kernel = "fold_pm1_tma<4,0,1> (fold)"
+        kernel = ("fold_f32_strips + fold_f32_finalize (tm_fold, fp32)" if wl["dtype"] == "float32"
+                  else "fold_pm1_tma<4,0,1> (fold)")
         fold_bytes = B * N * bx + B * (plan.len_y1 + plan.len_y2) * 4
         tkey = args.workload
     achieved = fold_bytes / (fold_ms * 1e-3) / 1e9

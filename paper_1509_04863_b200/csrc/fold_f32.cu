@@ -33,6 +33,7 @@ struct F32Args {
     int64_t M1, M2, K, N, q2;
     int64_t rows, row0;        // rows of the chunk [offset, offset + len) and its first global row
     int64_t R, nrc;            // rows per item, row chunks
+    int64_t g0m, Rm;           // row0 mod M2, R mod M2 (the finalize's diagonal index of a chunk)
     int block;                 // TM_BLOCK: no wrap, cyclic extension
     int64_t n_strips, n_groups;
     float *parts;              // [batch][nrc][M1 + n_strips (R + 127)]
@@ -96,60 +97,101 @@ __global__ void __launch_bounds__(FW * 32) fold_f32_strips(F32Args a) {
 }
 
 // bin sums, wrap and extension; x read only for the wrap/extension terms
+// FS: strip slots per diagonal, >= (R - 1) / 128 + 2 (the most strips one diagonal spans)
+template <int FS>
 __global__ void fold_f32_finalize(F32Args a, int64_t offset, int64_t len, float *__restrict__ y1, int64_t ldy1,
                                   float *__restrict__ y2, int64_t ldy2, int accumulate) {
     pdl_trigger();
     pdl_wait();  // the strips of this fold
     const int64_t b = blockIdx.y;
-    const float *xb = a.x + b * a.ldx;
-    const float *pb = a.parts + b * a.nrc * part_stride(a);
+    const float *__restrict__ xb = a.x + b * a.ldx;
+    const float *__restrict__ pb = a.parts + b * a.nrc * part_stride(a);
     float *o1 = y1 + b * ldy1, *o2 = y2 + b * ldy2;
     auto xat = [&](int64_t pos) -> float {  // x at a global position, 0 outside the chunk
         const int64_t rel = pos - offset;
-        return (rel >= 0 && rel < len) ? xb[rel] : 0.f;
+        return (rel >= 0 && rel < len) ? __ldg(xb + rel) : 0.f;
     };
-    const int64_t R = a.R;
-    // sum of the anti-diagonal partials of bin k (over chunks, then strips, in order)
-    auto base2 = [&](int64_t k) -> float {
+    const int R = (int)a.R, M1 = (int)a.M1, M2 = (int)a.M2;
+    const int smax = (int)a.n_strips - 1;
+    const int64_t pst = part_stride(a);
+    // the strip partials of diagonal u (strips ascending) into t[0 .. n): strips s
+    // with 128 s - (R - 1) <= u <= 128 s + 127, partial index u - 128 s + R - 1, i.e.
+    // address pp + u + R - 1 + s (R - 1).  FS covers the most strips one diagonal
+    // spans (R <= RMAX), so all of them are loaded together and the thread waits one
+    // memory latency per diagonal.
+    auto dload = [&](const float *__restrict__ pp, int u, float (&t)[FS]) -> int {
+        const int slo = u < 0 ? 0 : (u >> 7);
+        const int shi = min((u + R - 1) >> 7, smax);
+        const int n = (u >= -(R - 1) && u <= M1 - 1) ? shi - slo + 1 : 0;
+        const float *__restrict__ q = pp + (u + R - 1 + slo * (R - 1));
+#pragma unroll
+        for (int i = 0; i < FS; ++i) t[i] = i < n ? __ldg(q + i * (R - 1)) : 0.f;
+        return n;
+    };
+    // sum of the anti-diagonal partials of bin k < M2: chunks in order, within a
+    // chunk the diagonals u = (k + G0) mod M2, u - M2, ... (u in [-(R - 1), M1 - 1],
+    // G0 = the chunk's first global row), strips ascending -- a fixed order
+    auto base2 = [&](int k) -> float {
         float acc = 0.f;
+        int g = (int)a.g0m;  // G0 mod M2
         for (int64_t rc = 0; rc < a.nrc; ++rc) {
-            const float *pp = pb + rc * part_stride(a) + a.M1;
-            const int64_t G0 = a.row0 + rc * R;          // global row of the chunk's row 0
-            // c - g_rel = u  with  (u - G0) mod M2 = k,  u in [-(R - 1), M1 - 1]
-            for (int64_t u = (k + G0) % a.M2; u >= -(R - 1); u -= a.M2) {
-                if (u > a.M1 - 1) continue;
-                // strips s with 128 s - (R - 1) <= u <= 128 s + 127, partial index u - 128 s + R - 1
-                int64_t slo = (u - 127 + 128 * 4096) / 128 - 4096;
-                if (128 * slo < u - 127) ++slo;
-                if (slo < 0) slo = 0;
-                int64_t shi = (u + R - 1) >= 0 ? (u + R - 1) / 128 : -1;
-                if (shi > a.n_strips - 1) shi = a.n_strips - 1;
-                for (int64_t s = slo; s <= shi; ++s) acc += pp[s * (R + 127) + (u - 128 * s + R - 1)];
+            const float *__restrict__ pp = pb + rc * pst + M1;
+            int u = k + g;
+            if (u >= M2) u -= M2;
+            if (R <= M2) {  // at most two diagonals: u and u - M2, loaded together
+                float t1[FS], t0[FS];
+                const int n1 = dload(pp, u, t1), n0 = dload(pp, u - M2, t0);
+#pragma unroll
+                for (int i = 0; i < FS; ++i)
+                    if (i < n1) acc += t1[i];
+#pragma unroll
+                for (int i = 0; i < FS; ++i)
+                    if (i < n0) acc += t0[i];
+            } else {
+                for (; u >= -(R - 1); u -= M2) {
+                    float t[FS];
+                    const int n = dload(pp, u, t);
+#pragma unroll
+                    for (int i = 0; i < FS; ++i)
+                        if (i < n) acc += t[i];
+                }
             }
+            g += (int)a.Rm;
+            if (g >= M2) g -= M2;
         }
         const int64_t j = k - (a.M2 - a.q2);  // the mod-N wrap: bin M2 - q + j gets x[j]
         if (!a.block && j >= 0 && j < a.q2) acc += xat(j);
         return acc;
     };
+    // bin k < M2 also writes its strategy-1 extension bin M2 + k (k < K):
+    // y2[M2 + c] = y2[c] - x[c] + x[c + s2] (strategy 2: y2[M2 + c] = y2[c])
     const int64_t s2 = a.q2 * a.M2 - a.N;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.M2 + a.K;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        if (k < a.M1 + a.K) {
+    const int64_t kend = a.M2 > a.M1 + a.K ? a.M2 : a.M1 + a.K;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kend; k += (int64_t)gridDim.x * blockDim.x) {
+        const bool has1 = k < a.M1 + a.K, has2 = k < a.M2;
+        float v1 = 0.f;
+        if (has1) {
             const int64_t c = k < a.M1 ? k : k - a.M1;   // M1 | N: y1[M1 + c] = y1[c]
-            float v = 0.f;
-            for (int64_t rc = 0; rc < a.nrc; ++rc) v += pb[rc * part_stride(a) + c];
-            if (accumulate) o1[k] += v; else o1[k] = v;
+            for (int64_t rc = 0; rc < a.nrc; ++rc) v1 += __ldg(pb + rc * pst + c);
         }
-        float v;
-        if (k < a.M2) {
-            v = base2(k);
-        } else {
-            const int64_t c = k - a.M2;                  // extension: y2[M2+c] = y2[c] - x[c] + x[c+s2]
-            int64_t e = c + s2;
-            if (e >= a.N) e -= a.N;
-            v = a.block ? base2(c) : base2(c) - xat(c) + xat(e);
+        float v = 0.f, ve = 0.f;
+        if (has2) {
+            v = base2((int)k);
+            if (k < a.K) {
+                int64_t e = k + s2;
+                if (e >= a.N) e -= a.N;
+                ve = a.block ? v : v - xat(k) + xat(e);
+            }
         }
-        if (accumulate) o2[k] += v; else o2[k] = v;
+        if (has1) {
+            if (accumulate) o1[k] += v1; else o1[k] = v1;
+        }
+        if (has2) {
+            if (accumulate) o2[k] += v; else o2[k] = v;
+            if (k < a.K) {
+                if (accumulate) o2[a.M2 + k] += ve; else o2[a.M2 + k] = ve;
+            }
+        }
     }
 }
 
@@ -163,7 +205,8 @@ void geometry(const tm_plan_s *p, int64_t rows, int64_t *R, int64_t *nrc) {
 }  // namespace
 
 bool tm_fold_f32_ok(const tm_plan_s *p) {
-    return p->dtype == TM_F32 && p->N % p->M1 == 0 && p->M1 % 128 == 0 && p->M1 + 1 == p->M2;
+    return p->dtype == TM_F32 && p->N % p->M1 == 0 && p->M1 % 128 == 0 && p->M1 + 1 == p->M2 &&
+           p->M2 + p->K < ((int64_t)1 << 30);  // int32 bin and partial indices in the finalize
 }
 
 size_t tm_fold_f32_ws_bytes(const tm_plan_s *p, int64_t batch) {
@@ -184,6 +227,8 @@ int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     a.rows = len / p->M1; a.row0 = offset / p->M1;
     a.block = p->block;
     geometry(p, a.rows, &a.R, &a.nrc);
+    a.g0m = a.row0 % a.M2;
+    a.Rm = a.R % a.M2;
     a.n_strips = p->M1 / 128;
     a.n_groups = (a.n_strips + FW - 1) / FW;
     a.parts = (float *)parts;
@@ -200,11 +245,14 @@ int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
         if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: fold_f32_strips");
     }
     TM_CHECK_LAUNCH("tm_fold: fold_f32_strips");
-    int64_t gx = (p->M2 + p->K + 255) / 256;
+    int64_t gx = ((p->M2 > p->M1 + p->K ? p->M2 : p->M1 + p->K) + 255) / 256;
     if (gx > 65535) gx = 65535;
     {
-        const cudaError_t e = launch_pdl(fold_f32_finalize, dim3((unsigned)gx, (unsigned)batch), dim3(256), 0, s, a,
-                                         offset, len, (float *)y1, ldy1, (float *)y2, ldy2, accumulate);
+        const int need = (int)((a.R - 1) / 128 + 2);
+        static_assert((RMAX - 1) / 128 + 2 <= 9, "strip slots");
+        auto fin = need <= 3 ? fold_f32_finalize<3> : need <= 5 ? fold_f32_finalize<5> : fold_f32_finalize<9>;
+        const cudaError_t e = launch_pdl(fin, dim3((unsigned)gx, (unsigned)batch), dim3(256), 0, s, a, offset, len,
+                                         (float *)y1, ldy1, (float *)y2, ldy2, accumulate);
         if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: fold_f32_finalize");
     }
     TM_CHECK_LAUNCH("tm_fold: fold_f32_finalize");
