@@ -138,15 +138,19 @@ __global__ void fold_f32_finalize(F32Args a, int64_t offset, int64_t len, float 
             const float *__restrict__ pp = pb + rc * pst + M1;
             int u = k + g;
             if (u >= M2) u -= M2;
-            if (R <= M2) {  // at most two diagonals: u and u - M2, loaded together
+            if (R <= M2) {  // at most two diagonals: u and (only for u >= M2 - R + 1) u - M2
                 float t1[FS], t0[FS];
-                const int n1 = dload(pp, u, t1), n0 = dload(pp, u - M2, t0);
+                const int n1 = dload(pp, u, t1);
+                const bool two = u - M2 >= -(R - 1);
+                const int n0 = two ? dload(pp, u - M2, t0) : 0;
 #pragma unroll
                 for (int i = 0; i < FS; ++i)
                     if (i < n1) acc += t1[i];
+                if (two) {
 #pragma unroll
-                for (int i = 0; i < FS; ++i)
-                    if (i < n0) acc += t0[i];
+                    for (int i = 0; i < FS; ++i)
+                        if (i < n0) acc += t0[i];
+                }
             } else {
                 for (; u >= -(R - 1); u -= M2) {
                     float t[FS];
@@ -245,7 +249,11 @@ int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
         if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: fold_f32_strips");
     }
     TM_CHECK_LAUNCH("tm_fold: fold_f32_strips");
-    int64_t gx = ((p->M2 > p->M1 + p->K ? p->M2 : p->M1 + p->K) + 255) / 256;
+    // 4 bins per thread when that still fills the GPU several times over (the
+    // per-thread setup is about as long as one bin's work)
+    const int64_t kend = p->M2 > p->M1 + p->K ? p->M2 : p->M1 + p->K;
+    int64_t gx = (kend + 255) / 256;
+    if (gx * batch >= 4 * 8 * (int64_t)p->num_sms) gx = (kend + 1023) / 1024;
     if (gx > 65535) gx = 65535;
     {
         const int need = (int)((a.R - 1) / 128 + 2);
