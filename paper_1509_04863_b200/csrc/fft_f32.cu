@@ -47,6 +47,16 @@ struct FGeo {
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
+
+// c_root[dir][j] = exp(-+2 pi i j / 128) (dir 0: forward, 1: inverse), uploaded by
+// ftables.  A twiddle w_n^(a 2^b + c) of an in-register layer is w_n^c (one table
+// load per layer) times w_n^(a 2^b), a root of order <= 128 whose index is a
+// compile-time constant after unrolling (a constant-bank operand, no load).
+__constant__ float2 c_root[2][128];
+template <int DIR>
+__device__ __forceinline__ float2 tw_mul(float2 base, int j128) {
+    return j128 == 0 ? base : cmul(base, c_root[DIR][j128]);
+}
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 
@@ -80,10 +90,11 @@ __device__ __forceinline__ void fdif(float2 (&v)[E], float *br, float *bi, int t
         for (int u = LOGE - 1; u >= 0; --u) {
             const int h = 1 << u;
             const float2 *tab = tw + ((1 << (blo + u)) - 1);
+            const float2 base = __ldg(tab + tlow);  // w_n^tlow, n = 2^(blo + u + 1)
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 if (m & h) continue;
-                const float2 w = __ldg(tab + (((m & (h - 1)) << blo) | tlow));
+                const float2 w = tw_mul<0>(base, (m & (h - 1)) * 64 / h);  // w_n^((m & (h-1)) 2^blo + tlow)
                 const float2 X = v[m], Y = v[m | h];
                 v[m] = cadd(X, Y);
                 v[m | h] = cmul(csub(X, Y), w);
@@ -96,26 +107,25 @@ __device__ __forceinline__ void fdif(float2 (&v)[E], float *br, float *bi, int t
         const float2 *tab = tw + ((1 << (LOGE + sb)) - 1);
         const bool upper = (t >> sb) & 1;
         const int tl = t & ((1 << sb) - 1);
+        const float2 base = __ldg(tab + (tl << LOGE));  // w_n^(16 tl), n = 2^(LOGE + sb + 1)
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const float ox = __shfl_xor_sync(0xffffffffu, v[m].x, 1 << sb);
             const float oy = __shfl_xor_sync(0xffffffffu, v[m].y, 1 << sb);
             const float2 o = make_float2(ox, oy);
-            if (upper) v[m] = cmul(csub(o, v[m]), __ldg(tab + ((tl << LOGE) | m)));
+            if (upper) v[m] = cmul(csub(o, v[m]), tw_mul<0>(base, m * (128 >> (LOGE + sb + 1))));
             else v[m] = cadd(v[m], o);
         }
     }
 #pragma unroll
     for (int u = LOGE - 1; u >= 0; --u) {
         const int h = 1 << u;
-        const float2 *tab = tw + (h - 1);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             if (m & h) continue;
-            const float2 w = __ldg(tab + (m & (h - 1)));
             const float2 X = v[m], Y = v[m | h];
             v[m] = cadd(X, Y);
-            v[m | h] = cmul(csub(X, Y), w);
+            v[m | h] = tw_mul<0>(csub(X, Y), (m & (h - 1)) * 64 / h);  // w_2h^(m & (h-1))
         }
     }
 }
@@ -127,11 +137,10 @@ __device__ __forceinline__ void fdit(float2 (&v)[E], float *br, float *bi, int t
 #pragma unroll
     for (int u = 0; u < LOGE; ++u) {
         const int h = 1 << u;
-        const float2 *tab = tw + (h - 1);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             if (m & h) continue;
-            const float2 Yw = cmul(v[m | h], __ldg(tab + (m & (h - 1))));
+            const float2 Yw = tw_mul<1>(v[m | h], (m & (h - 1)) * 64 / h);
             const float2 X = v[m];
             v[m] = cadd(X, Yw);
             v[m | h] = csub(X, Yw);
@@ -142,9 +151,10 @@ __device__ __forceinline__ void fdit(float2 (&v)[E], float *br, float *bi, int t
         const float2 *tab = tw + ((1 << (LOGE + sb)) - 1);
         const bool upper = (t >> sb) & 1;
         const int tl = t & ((1 << sb) - 1);
+        const float2 base = __ldg(tab + (tl << LOGE));
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const float2 send = upper ? cmul(v[m], __ldg(tab + ((tl << LOGE) | m))) : v[m];
+            const float2 send = upper ? cmul(v[m], tw_mul<1>(base, m * (128 >> (LOGE + sb + 1)))) : v[m];
             const float ox = __shfl_xor_sync(0xffffffffu, send.x, 1 << sb);
             const float oy = __shfl_xor_sync(0xffffffffu, send.y, 1 << sb);
             const float2 o = make_float2(ox, oy);
@@ -160,10 +170,11 @@ __device__ __forceinline__ void fdit(float2 (&v)[E], float *br, float *bi, int t
         for (int u = 0; u < LOGE; ++u) {
             const int h = 1 << u;
             const float2 *tab = tw + ((1 << (blo + u)) - 1);
+            const float2 base = __ldg(tab + tlow);
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 if (m & h) continue;
-                const float2 Yw = cmul(v[m | h], __ldg(tab + (((m & (h - 1)) << blo) | tlow)));
+                const float2 Yw = cmul(v[m | h], tw_mul<1>(base, (m & (h - 1)) * 64 / h));
                 const float2 X = v[m];
                 v[m] = cadd(X, Yw);
                 v[m | h] = csub(X, Yw);
@@ -299,6 +310,14 @@ int ftables(int device, const float2 **twf, const float2 **twi) {
         if (e != cudaSuccess) return tm_cuda_status(e, "tm: FFT table allocation");
         e = cudaMemcpy(F.d, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice);
         if (e != cudaSuccess) return tm_cuda_status(e, "tm: FFT table upload");
+        float2 roots[2][128];
+        for (int dir = 0; dir < 2; ++dir)
+            for (int j = 0; j < 128; ++j) {
+                const double ang = (dir ? 2.0 : -2.0) * M_PI * (double)j / 128.0;
+                roots[dir][j] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+            }
+        e = cudaMemcpyToSymbol(c_root, roots, sizeof(roots));
+        if (e != cudaSuccess) return tm_cuda_status(e, "tm: FFT root upload");
         F.ready = true;
     }
     *twf = F.d;
