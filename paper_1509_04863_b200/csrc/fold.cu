@@ -278,25 +278,30 @@ __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t
         if (!block && j >= 0 && j < q2) v += xat(j);
         return v;
     };
+    // bin k < M2 also writes its extension bin M2 + k (k < K) from its own base value:
+    // y2[M2 + c] = y2[c] - x[c] + x[c + s2] (strategy 2: y2[M2 + c] = y2[c]).
     // (launched with ~4 bins per thread: the unrolled iterations' loads are independent)
+    const int kend = (int)(M1 + K), m1 = (int)M1, m2 = (int)M2, kk = (int)K;  // M1 + K >= M2
 #pragma unroll 4
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M2 + K;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        if (k < M1 + K) {
-            int64_t c = k < M1 ? k : k - M1;     // M1 | N: y1[M1 + c] = y1[c]
-            int32_t v = (int32_t)rows - c1[c];
-            if (accumulate) o1[k] += v; else o1[k] = v;
-        }
-        int32_t v;
-        if (k < M2) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kend; k += gridDim.x * blockDim.x) {
+        const int c = k < m1 ? k : k - m1;       // M1 | N: y1[M1 + c] = y1[c]
+        const int32_t v1 = (int32_t)rows - c1[c];
+        int32_t v = 0, ve = 0;
+        if (k < m2) {
             v = base2(k);
-        } else {
-            int64_t c = k - M2;                  // extension: y2[M2+c] = y2[c] - x[c] + x[c+s2]
-            int64_t e = c + s2;
-            if (e >= N) e -= N;
-            v = block ? base2(c) : base2(c) - xat(c) + xat(e);  // strategy 2: cyclic copy
+            if (k < kk) {
+                int64_t e = k + s2;
+                if (e >= N) e -= N;
+                ve = block ? v : v - xat(k) + xat(e);
+            }
         }
-        if (accumulate) o2[k] += v; else o2[k] = v;
+        if (accumulate) o1[k] += v1; else o1[k] = v1;
+        if (k < m2) {
+            if (accumulate) o2[k] += v; else o2[k] = v;
+            if (k < kk) {
+                if (accumulate) o2[m2 + k] += ve; else o2[m2 + k] = ve;
+            }
+        }
     }
 }
 
