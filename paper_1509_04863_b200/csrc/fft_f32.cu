@@ -192,8 +192,14 @@ struct FftArgs {
     int64_t ldy1, ldy2, nload1, nload2, M1, M2;
     float *r1, *r2;          // [batch][Mj] or NULL
     int32_t *resid;          // [batch][2] or NULL
+    int64_t nb;              // templates (fft_template_f32: two per CTA)
 };
 
+// Two templates per transform (they are real): v = t_rev[b0] + i t_rev[b0 + 1],
+// V = FFT(v), and with V* the conjugate of V at frequency -f (mod L):
+//   T[b0](f) = (V(f) + V*(-f)) / 2,   T[b0 + 1](f) = (V(f) - V*(-f)) / (2i).
+// The DIF output holds frequency bitrev((t << LOGE) | m) in thread t, register m;
+// V(-f) comes from another thread, through shared memory in natural order.
 template <int LOGL>
 __global__ void __launch_bounds__(FGeo<LOGL>::NT, 1) fft_template_f32(FftArgs a) {
     pdl_trigger();
@@ -202,20 +208,38 @@ __global__ void __launch_bounds__(FGeo<LOGL>::NT, 1) fft_template_f32(FftArgs a)
     extern __shared__ float fsm[];
     float *br = fsm, *bi = fsm + G::L;
     const int t = threadIdx.x;
-    const int64_t b = blockIdx.x;
-    const float *tb = a.t + b * a.ldt;
+    const int64_t b0 = 2 * (int64_t)blockIdx.x;
+    const bool two = b0 + 1 < a.nb;
+    const float *tb0 = a.t + b0 * a.ldt, *tb1 = tb0 + a.ldt;
     float2 v[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) {
         const int i = G::idx(0, t, m);
         const int src = i == 0 ? 0 : G::L - i;  // t_rev[i] = t[(L - i) mod L] (reading C3)
-        v[m] = make_float2(src < a.K ? tb[src] : 0.f, 0.f);
+        v[m] = make_float2(src < a.K ? tb0[src] : 0.f, (two && src < a.K) ? tb1[src] : 0.f);
     }
     fdif<LOGL>(v, br, bi, t, a.twf);
-    const float s = 1.0f / (float)G::L;
-    float2 *o = a.tf + b * G::L;
+    // position p = (t << LOGE) | m holds frequency f = bitrev(p); -f (mod L) keeps f's
+    // lowest set bit and flips the bits above it, i.e. p' = p ^ (hb(p) - 1) (hb: the
+    // highest set bit): t' = t ^ (hb(t) - 1), m' = 15 - m for t > 0.  Stored as
+    // [m][t], both the writes and the partner reads are bank-conflict free.
+    __syncthreads();  // br / bi reuse
 #pragma unroll
-    for (int m = 0; m < E; ++m) o[m * G::NT + t] = make_float2(v[m].x * s, v[m].y * s);
+    for (int m = 0; m < E; ++m) {
+        br[m * G::NT + t] = v[m].x;
+        bi[m * G::NT + t] = v[m].y;
+    }
+    __syncthreads();
+    const float s = 0.5f / (float)G::L;
+    float2 *o0 = a.tf + b0 * G::L, *o1 = o0 + G::L;
+    const int tp = t ? t ^ ((1 << (31 - __clz(t))) - 1) : 0;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int mp = t ? (E - 1 - m) : (m ? m ^ ((1 << (31 - __clz(m))) - 1) : 0);
+        const float wx = br[mp * G::NT + tp], wy = -bi[mp * G::NT + tp];  // V*(-f)
+        o0[m * G::NT + t] = make_float2((v[m].x + wx) * s, (v[m].y + wy) * s);
+        if (two) o1[m * G::NT + t] = make_float2((v[m].y - wy) * s, (wx - v[m].x) * s);  // (V - V*) / 2i
+    }
 }
 
 __device__ __forceinline__ void fmax_idx(float &bv, int &bi, float v, int i) {
@@ -332,7 +356,7 @@ int launch_pair(bool templ, const FftArgs &A, int64_t batch, cudaStream_t s) {
     if (templ) {
         auto k = fft_template_f32<LOGL>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const cudaError_t e = launch_pdl(k, dim3((unsigned)batch), dim3(G::NT), smem, s, A);
+        const cudaError_t e = launch_pdl(k, dim3((unsigned)((batch + 1) / 2)), dim3(G::NT), smem, s, A);
         if (e != cudaSuccess) return tm_cuda_status(e, "fft_template_f32");
         TM_CHECK_LAUNCH("fft_template_f32");
     } else {
@@ -371,6 +395,7 @@ int tm_fft_f32_template(const tm_plan_s *p, const void *t, int64_t ldt, int64_t 
     if (rc) return rc;
     A.t = (const float *)t; A.ldt = ldt; A.K = p->K;
     A.tf = (float2 *)tf;
+    A.nb = batch;
     return dispatch(p->logL2, true, A, batch, s);
 }
 
