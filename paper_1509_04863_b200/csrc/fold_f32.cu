@@ -138,27 +138,19 @@ __global__ void fold_f32_finalize(F32Args a, int64_t offset, int64_t len, float 
             const float *__restrict__ pp = pb + rc * pst + M1;
             int u = k + g;
             if (u >= M2) u -= M2;
-            if (R <= M2) {  // at most two diagonals: u and (only for u >= M2 - R + 1) u - M2
-                float t1[FS], t0[FS];
-                const int n1 = dload(pp, u, t1);
-                const bool two = u - M2 >= -(R - 1);
-                const int n0 = two ? dload(pp, u - M2, t0) : 0;
+            // R <= rows < M2 (M1 M2 > N, Alg. 1 step 2): at most two diagonals, u and
+            // (only for u >= M2 - R + 1) u - M2, loaded together
+            float t1[FS], t0[FS];
+            const int n1 = dload(pp, u, t1);
+            const bool two = u - M2 >= -(R - 1);
+            const int n0 = two ? dload(pp, u - M2, t0) : 0;
+#pragma unroll
+            for (int i = 0; i < FS; ++i)
+                if (i < n1) acc += t1[i];
+            if (two) {
 #pragma unroll
                 for (int i = 0; i < FS; ++i)
-                    if (i < n1) acc += t1[i];
-                if (two) {
-#pragma unroll
-                    for (int i = 0; i < FS; ++i)
-                        if (i < n0) acc += t0[i];
-                }
-            } else {
-                for (; u >= -(R - 1); u -= M2) {
-                    float t[FS];
-                    const int n = dload(pp, u, t);
-#pragma unroll
-                    for (int i = 0; i < FS; ++i)
-                        if (i < n) acc += t[i];
-                }
+                    if (i < n0) acc += t0[i];
             }
             g += (int)a.Rm;
             if (g >= M2) g -= M2;
@@ -231,6 +223,7 @@ int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     a.rows = len / p->M1; a.row0 = offset / p->M1;
     a.block = p->block;
     geometry(p, a.rows, &a.R, &a.nrc);
+    if (a.R >= a.M2) return TM_EUNSUPPORTED;  // the finalize's two-diagonal bound (M1 M2 > N implies R < M2)
     a.g0m = a.row0 % a.M2;
     a.Rm = a.R % a.M2;
     a.n_strips = p->M1 / 128;

@@ -254,6 +254,26 @@ def test_f32_partial_stride_alignment(tm):
     check_f32_pairs(tm, plan, x_h, t_h, range(3))
 
 
+@pytest.mark.parametrize("N,K", [(2 ** 14, 128), (2 ** 18, 512), (2 ** 20, 1024), (2 ** 22, 2048)])
+def test_f32_finalize_geometries(tm, N, K):
+    """fold_f32_finalize strip-slot instantiations (R = rows per chunk: 128 -> 3 slots,
+    512 -> 5, 1024 -> 9) and two row chunks (2^22, 2048: rows 2048, the chunk residue
+    G0 mod M2 advanced per chunk); then the same fold as two accumulated half-chunks
+    (global-index bins) equals the full fold."""
+    plan = tm.Plan(N, K, seed=57, dtype="float32")
+    x_h, t_h, _ = tmgen.batch(57, 0, 3, N, K, 0.5, dtype=np.float32)
+    check_f32_pairs(tm, plan, x_h, t_h, range(3))
+    x = up(x_h)
+    y1, y2 = plan.fold(x)
+    h = (N // plan.M1 // 2) * plan.M1
+    a1, a2 = plan.fold(x[:, :h], 0, h)
+    plan.fold(x[:, h:], h, N - h, y1=a1, y2=a2, accumulate=True)
+    torch.cuda.synchronize()
+    for g, a in ((y1, a1), (y2, a2)):
+        g, a = g.cpu().numpy().astype(np.float64), a.cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(g - a)) <= 1e-5 * np.max(np.abs(g))
+
+
 def test_f32_ragged(tm):
     N, K = 30011, 250   # M1 does not divide N
     plan = tm.Plan(N, K, M=260, seed=32, dtype="float32")
