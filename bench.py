@@ -71,6 +71,16 @@ def dist_env():
     return rank, world, local
 
 
+def traffic_of(key):
+    """dram read + write bytes per launch of the roofline kernel(s) from one ncu --set
+    full capture (profiles/ncu_traffic.json), or None"""
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(tp):
+        return None
+    with open(tp) as f:
+        return json.load(f).get(key)
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -323,11 +333,7 @@ def main():
         fold_bytes = B * N * bx + B * (plan.len_y1 + plan.len_y2) * 4
         tkey = args.workload
     achieved = fold_bytes / (fold_ms * 1e-3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get(tkey)
+    traffic = traffic_of(tkey)
     cpu = None
     if not args.no_cpu_baseline:
         cores, model = cpu_info()
@@ -489,7 +495,8 @@ def run_single_signal(args, wl, rank, world, local, dev):
                                          if world > 1 else ""),
                        "l2": "no flush: per-rank input > 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": "tm_fold (fold_pm1_tma + fold_finalize)",
+                         "traffic": traffic_of(args.workload) if world == 1 else None,
+                         "kernel": "tm_fold (fold_pm1_tma + fold_finalize)",
                          "algorithmic_bytes_per_launch": fold_bytes, "peak_source": peak_src, "fold_ms": fold_ms},
             "stage_ms": {"fold": st[0], "allreduce": st[1], "correlate_match": st[2]},
             "success_rate": success, "k": int(k.item()), "k0": int(k0.item()),
