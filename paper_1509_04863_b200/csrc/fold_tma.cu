@@ -128,10 +128,12 @@ struct Item {
 };
 __device__ __forceinline__ Item decode(const TmaArgs &a, int64_t item) {
     Item it;
-    const int64_t rc = item % a.n_rc;
-    item /= a.n_rc;
+    // column groups fastest: CTAs running at the same time read adjacent 4 KB pieces
+    // of the same rows (cfg5, 16 groups: 0.412 -> 0.407 ms; row chunks fastest before)
     it.gi = item % a.n_groups;
-    it.b = item / a.n_groups;
+    item /= a.n_groups;
+    const int64_t rc = item % a.n_rc;
+    it.b = item / a.n_rc;
     it.ra = rc * a.R;
     const int64_t rb = (it.ra + a.R < a.rows) ? it.ra + a.R : a.rows;
     it.nrow = rb - it.ra;
