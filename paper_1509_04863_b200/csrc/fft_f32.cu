@@ -55,7 +55,9 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __constant__ float2 c_root[2][128];
 template <int DIR>
 __device__ __forceinline__ float2 tw_mul(float2 base, int j128) {
-    return j128 == 0 ? base : cmul(base, c_root[DIR][j128]);
+    if (j128 == 0) return base;
+    if (j128 == 32) return DIR ? make_float2(-base.y, base.x) : make_float2(base.y, -base.x);  // * (+-i)
+    return cmul(base, c_root[DIR][j128]);
 }
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
