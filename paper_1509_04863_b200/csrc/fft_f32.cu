@@ -65,19 +65,17 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(
 template <int LOGL>
 __device__ __forceinline__ void ftranspose(float2 (&v)[E], float *br, float *bi, int t, int kf, int kt) {
     using G = FGeo<LOGL>;
+    // one interleaved float2 plane over br .. br + 2L (bi = br + L): one 8-byte
+    // access per element; the swizzle keeps each half-warp's 16 indices distinct
+    // mod 16 (the 8-byte access's bank-conflict condition)
+    (void)bi;
+    float2 *buf = reinterpret_cast<float2 *>(br);
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int i = G::swz(G::idx(kf, t, m));
-        br[i] = v[m].x;
-        bi[i] = v[m].y;
-    }
+    for (int m = 0; m < E; ++m) buf[G::swz(G::idx(kf, t, m))] = v[m];
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int i = G::swz(G::idx(kt, t, m));
-        v[m] = make_float2(br[i], bi[i]);
-    }
+    for (int m = 0; m < E; ++m) v[m] = buf[G::swz(G::idx(kt, t, m))];
 }
 
 // forward DIF: natural (D0) -> bit-reversed (Df: index (t << LOGE) | m)
