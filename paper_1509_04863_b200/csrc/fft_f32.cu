@@ -15,7 +15,7 @@
 // Transform layout (the NTT kernels' scheme, corr_fast.cu): L = 2^LOGL, each of
 // NT = L / 16 threads holds 16 complex values in registers; index bits are
 // processed 4 at a time in registers with XOR-swizzled shared-memory
-// transposes (two float planes) between phases, leftover bits by warp
+// transposes (one interleaved float2 plane) between phases, leftover bits by warp
 // shuffles.  Forward = decimation in frequency (natural -> bit-reversed),
 // inverse = decimation in time (bit-reversed -> natural).  Twiddles: float2
 // tables built in double precision on the host, w_n^j at offset n/2 - 1.
