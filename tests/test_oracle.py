@@ -557,3 +557,124 @@ def test_ftm_multi_f32_equals_int_path_on_pm1_data():
         a = oracle.ftm_multi(x, t, M)
         b = oracle.ftm_multi(x.astype(np.float32), t.astype(np.float32), M)
         assert a == b
+
+
+# ------------------------------------------------- fp32 compositions (O6 on real data)
+def dense_strategy1(x, t, M1, M2):
+    """Algorithm 1 built from dense matrices with numpy, fp64: y_j = D_{M_j+K}(circ(r_j)) x
+    (Eq. 3), r_j[k] = sum_i t_i y_j[k+i] as a dense (M_j x (M_j+K)) Hankel-band
+    matrix (reading C3), lowest-index argmax (C7), z by brute-force search over
+    [0, M1 M2) (Theorem 4), k = z if z < N else -1 (C9)."""
+    N, K = x.shape[0], t.shape[0]
+    xs = x.astype(np.float64)
+    out = {}
+    res = []
+    for j, M in ((1, M1), (2, M2)):
+        r = np.array([1.0 if k % M == 0 else 0.0 for k in range(N)])
+        C = circ(r)
+        Phi = np.stack([C[i % N] for i in range(M + K)])
+        y = Phi @ xs
+        T = np.zeros((M, M + K))
+        for k in range(M):
+            T[k, k:k + K] = t.astype(np.float64)
+        rr = T @ y
+        out[f"y{j}"], out[f"r{j}"] = y, rr
+        res.append(int(np.flatnonzero(rr == rr.max())[0]))
+    z = next(z for z in range(M1 * M2) if z % M1 == res[0] and z % M2 == res[1])
+    out["residues"] = tuple(res)
+    out["k"] = z if z < N else -1
+    return out
+
+
+def test_ftm_f32_equals_dense_algorithm1():
+    """oracle.ftm on float32 data (or_ftm_f32) against the dense numpy
+    construction of every step, N <= 64, M dividing N and not, M > K."""
+    rng = np.random.default_rng(31)
+    for _ in range(60):
+        N = int(rng.integers(4, 65))
+        K = int(rng.integers(1, 9))
+        Mmin = max(K, int(math.isqrt(N)))
+        M = int(rng.integers(Mmin, Mmin + 4))
+        if M * (M + 1) <= N:
+            continue
+        x = rng.standard_normal(N).astype(np.float32)
+        k0 = int(rng.integers(0, N))
+        t = (x[(k0 + np.arange(K)) % N] + 0.1 * rng.standard_normal(K)).astype(np.float32)
+        o = oracle.ftm(x, t, M=M)
+        d = dense_strategy1(x, t, *oracle.moduli(N, K, M))
+        for key in ("y1", "y2", "r1", "r2"):
+            np.testing.assert_allclose(o[key], d[key], rtol=1e-12, atol=1e-12, err_msg=key)
+        assert o["residues"] == d["residues"] and o["k"] == d["k"]
+
+
+def test_ftm_f32_equals_int_path_on_pm1_data():
+    """On +-1-valued float32 data every sum of or_ftm_f32 is an exact integer,
+    so y1, y2, r1, r2, residues and k equal the exact int64 path (or_ftm_i8,
+    pinned above) -- including M not dividing N (the wrap, C5) and alias repair."""
+    rng = np.random.default_rng(32)
+    for N, K, M in ((4096, 256, 0), (3000, 60, 0), (1000, 37, 40), (5000, 71, 80), (997, 40, 45)):
+        for rep in range(3):
+            x = rand_pm1(rng, N)
+            k0 = int(rng.integers(0, N))
+            t = x[(k0 + np.arange(K)) % N].copy()
+            t[rng.random(K) < 0.1] *= -1
+            for repair in (False, True):
+                a = oracle.ftm(x, t, M=M, alias_repair=repair)
+                b = oracle.ftm(x.astype(np.float32), t.astype(np.float32), M=M, alias_repair=repair)
+                for key in ("y1", "y2", "r1", "r2"):
+                    np.testing.assert_array_equal(b[key], a[key].astype(np.float64), err_msg=key)
+                assert a["residues"] == b["residues"] and a["k"] == b["k"]
+
+
+def test_ftm_block_f32_equals_dense_theorem2():
+    """oracle.ftm_block on float32 data (or_ftm_block_f32): y_j = [I ... I] x_pad
+    (Theorem 2's Block Phi with Phi_M = I), r_j = circ([t 0]) y_j
+    (T^ of Theorem 2), lowest-index argmax, brute-force CRT."""
+    rng = np.random.default_rng(33)
+    for _ in range(40):
+        N = int(rng.integers(4, 65))
+        K = int(rng.integers(1, 9))
+        Mmin = max(K, int(math.isqrt(N)))
+        M = int(rng.integers(Mmin, Mmin + 4))
+        if M * (M + 1) <= N:
+            continue
+        x = rng.standard_normal(N).astype(np.float32)
+        t = rng.standard_normal(K).astype(np.float32)
+        o = oracle.ftm_block(x, t, M=M)
+        M1, M2 = oracle.moduli(N, K, M)
+        res = []
+        for j, Mj in ((1, M1), (2, M2)):
+            e0 = np.zeros(Mj); e0[0] = 1.0
+            y = block_phi_dense(e0, N) @ x.astype(np.float64)
+            tp = np.zeros(Mj); tp[:K] = t
+            r = circ(tp) @ y
+            np.testing.assert_allclose(o[f"y{j}"], y, rtol=1e-12, atol=1e-12)
+            np.testing.assert_allclose(o[f"r{j}"], r, rtol=1e-12, atol=1e-12)
+            res.append(int(np.flatnonzero(r == r.max())[0]))
+        assert o["residues"] == tuple(res)
+        z = next(z for z in range(M1 * M2) if z % M1 == res[0] and z % M2 == res[1])
+        assert o["k"] == (z if z < N else -1)
+
+
+def test_ftm_block_f32_equals_int_path_on_pm1_data():
+    rng = np.random.default_rng(34)
+    for N, K, M in ((4096, 256, 0), (30011, 250, 260), (1000, 37, 40)):
+        x = rand_pm1(rng, N)
+        k0 = int(rng.integers(0, N - K))
+        t = x[k0:k0 + K].copy()
+        a = oracle.ftm_block(x, t, M=M)
+        b = oracle.ftm_block(x.astype(np.float32), t.astype(np.float32), M=M)
+        for key in ("y1", "y2", "r1", "r2"):
+            np.testing.assert_array_equal(b[key], a[key].astype(np.float64), err_msg=key)
+        assert a["residues"] == b["residues"] and a["k"] == b["k"]
+
+
+def test_full_corr_f32_matches_dense_T():
+    """(Tx)_k = sum_i t_i x_{(k+i) mod N} on real data: or_full_corr_f32 against
+    T = circ([t 0]) built densely with numpy."""
+    rng = np.random.default_rng(35)
+    for N, K in ((16, 3), (40, 40), (97, 10)):
+        x = rng.standard_normal(N).astype(np.float32)
+        t = rng.standard_normal(K).astype(np.float32)
+        v = np.zeros(N); v[:K] = t
+        np.testing.assert_allclose(oracle.full_corr(x, t), circ(v) @ x.astype(np.float64), rtol=1e-12, atol=1e-12)
