@@ -2,12 +2,16 @@
 """bench.py -- throughput of the whole hot path of arXiv 1509.04863 Algorithm 1
 (fold -> template fold -> correlation -> argmax -> CRT) on B200s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5] [--impl reference]
 
-One process per GPU (torchrun for N > 1).  Independent (signal, template) pairs
-shard across ranks with no data-path collective (weak scaling: every rank
-folds its own batch of the configuration, global pair indices rank*B + b).
-A step = one tm_run over the rank's whole batch with inputs resident in HBM.
+One process per GPU (torchrun for N > 1).  Default workload cfg5: ONE signal of
+N = 2^31 samples split into contiguous chunks over the ranks (strong scaling);
+each rank folds its chunk, the partial folds are summed in place by one NCCL
+all-reduce, the correlation is split by output blocks (SingleSignal,
+paper_1509_04863_b200/single.py).  The batch workloads (cfg1-cfg4) shard
+independent (signal, template) pairs with no data-path collective (weak
+scaling, global pair indices rank*B + b); a step = one tm_run over the rank's
+whole batch with inputs resident in HBM.
 Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle
 (oracle/, the test-infrastructure checker) on a bounded sample instead.
 """
@@ -53,7 +57,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS),
+                    help="cfg5 (default): the largest configuration, one 2 GiB signal, split over the ranks")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle cpu_baseline budget")
@@ -61,6 +66,9 @@ def parse():
     ap.add_argument("--strategy", type=int, default=1, choices=[1, 2],
                     help="1: D_{M+K} (P:152, default); 2: Block Phi of Theorem 2 (P:159-177, TM_BLOCK)")
     ap.add_argument("--no-stage-events", action="store_true", help="A/B only: no per-step stage events")
+    ap.add_argument("--no-cfg1", action="store_true", help="skip the cfg1 latency sample")
+    ap.add_argument("--ref-seconds", type=float, default=150.0,
+                    help="--impl reference: CPU budget of the timed steps (each step is whole pairs)")
     return ap.parse_args()
 
 
@@ -88,6 +96,73 @@ def measured_peaks():
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy read+write)"
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+NOMINAL_HBM_GBS = 8000.0  # BASELINE.json north_star "~8 TB/s"
+
+
+def read_ceiling(tm, buf, stream, reps: int = 5):
+    """Live read-only streaming ceiling on this box (tm_probe_read_bw: a cp.async.bulk
+    ring over `buf`, one CTA per SM), best of `reps`, GB/s."""
+    import torch
+    nbytes = buf.numel() * buf.element_size()
+    best = None
+    for _ in range(reps + 1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        tm.probe_read_bw(buf, stream=stream)
+        b.record(stream)
+        b.synchronize()
+        ms = a.elapsed_time(b)
+        best = ms if best is None or ms < best else best
+    return (nbytes // (32 * 1024) * 32 * 1024) / (best * 1e-3) / 1e9
+
+
+def peak_denominators(ceiling):
+    peak, _ = measured_peaks()
+    d = {"nominal_8000": NOMINAL_HBM_GBS, "measured_copy": peak}
+    if ceiling:
+        d["read_ceiling_live"] = ceiling
+    return d
+
+
+def roofline_block(bound, achieved, kernel_ms, alg_bytes, kernel, traffic, ceiling):
+    peak, src = measured_peaks()
+    return {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": kernel, "algorithmic_bytes_per_launch": alg_bytes,
+            "peak_source": src, "kernel_ms": kernel_ms,
+            "frac_by_denominator": {k: achieved / v for k, v in peak_denominators(ceiling).items()},
+            "read_ceiling_gbs": ceiling}
+
+
+def step_stats(per_step, mean_ms):
+    xs = sorted(per_step)
+    return {"mean": mean_ms, "median": statistics.median(xs), "min": xs[0], "max": xs[-1], "n": len(xs)}
+
+
+def cfg1_latency(tm, dev, reps: int = 200):
+    """cfg1 (N=4096, K=256, one pair): tm_run latency, each call bracketed by its own
+    events (latency-bound); median / min / max in microseconds."""
+    import torch
+    wl = WORKLOADS["cfg1"]
+    plan = tm.Plan(wl["N"], wl["K"], seed=wl["seed"])
+    x, t, k0 = plan.generate(0, 1, wl["noise"], device=dev)
+    ws = plan.workspace(1, dev)
+    res = torch.empty((1, 2), dtype=torch.int32, device=dev)
+    k = torch.empty(1, dtype=torch.int64, device=dev)
+    s = torch.cuda.current_stream()
+    for _ in range(10):
+        plan.run(x, t, residues=res, k=k, ws=ws, stream=s)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record(s)
+        plan.run(x, t, residues=res, k=k, ws=ws, stream=s)
+        b.record(s)
+    torch.cuda.synchronize()
+    us = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
+    return {"workload": wl["desc"], "unit": "us", "median": statistics.median(us), "min": us[0], "max": us[-1],
+            "reps": reps, "path": tm.RUN_PATHS.get(plan.run_path(1)), "k_equals_k0": bool(int(k[0]) == int(k0[0]))}
 
 
 class ClockSampler:
@@ -176,23 +251,48 @@ def oracle_rate(wl, budget_s: float, max_pairs: int | None = None, strategy: int
 
 
 def run_reference(args, wl):
+    """The reference arm of this tier: the CPU oracle as it stands (single thread)
+    on the same workload; each step is whole pairs (cfg5: the whole 2^31-sample
+    pair), stopping early once --ref-seconds of timed CPU work is spent so the run
+    ends within minutes.  Rank 0 only; other ranks exit without work."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    import numpy as np
+
     import oracle
+    import tmgen
     oracle.build()
     cores, model = cpu_info()
-    # each step: one pair of the workload through the oracle (a bounded sample)
-    if args.warmup:
-        oracle_rate(wl, float("inf"), max_pairs=min(args.warmup, 3), strategy=args.strategy)
-    rate, pairs, spent = oracle_rate(wl, float("inf"), max_pairs=max(args.steps, 1), strategy=args.strategy)
-    sample = f"{pairs} pair(s) of {wl['desc']} (one pair per step), host-generated by tmgen"
+    N, K = wl["N"], wl["K"]
+    fn = oracle.ftm_block if args.strategy == 2 else oracle.ftm
+    dt = np.int8 if wl["dtype"] == "int8" else np.float32
+    warm = 0 if wl.get("single") else min(args.warmup, 3)   # a warm-up of a 40 s CPU pair buys nothing
+    times = []
+    pair = 0
+    for i in range(warm + max(args.steps, 1)):
+        x, t, _ = tmgen.batch(wl["seed"], 0 if wl.get("single") else pair, 1, N, K, wl["noise"], dtype=dt)
+        t0 = time.perf_counter()
+        fn(x[0], t[0], want_vectors=False)
+        el = time.perf_counter() - t0
+        del x
+        pair += 1
+        if i >= warm:
+            times.append(el)
+            if sum(times) >= args.ref_seconds:
+                break
+    spent = sum(times)
+    rate = len(times) * N / spent / 1e9
+    sample = (f"{len(times)} timed step(s) of {args.steps} requested, each one whole pair of {wl['desc']} "
+              f"(host-generated by tmgen), {spent:.1f} s single-threaded; stopped at the {args.ref_seconds:.0f} s "
+              f"budget" if len(times) < args.steps else
+              f"{len(times)} step(s), each one whole pair of {wl['desc']} (host-generated), {spent:.1f} s")
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "Gsamples/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": spent / max(pairs, 1) * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "steps": len(times), "steps_requested": args.steps, "warmup": warm, "ms_per_step": spent / len(times) * 1e3,
+        "higher_is_better": True, "scaling": "strong" if wl.get("single") else "weak", "vs_baseline": None,
         "dtype": "i8" if wl["dtype"] == "int8" else "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "N": wl["N"], "K": wl["K"], "batch": wl["B"],
+        "config": {"workload": wl["desc"], "N": N, "K": K, "batch": wl["B"],
                    "parallelism": "single CPU thread (oracle)", "strategy": args.strategy},
         "cpu_baseline": {"value": rate, "unit": "Gsamples/s", "cores": 1, "kind": "oracle", "sample": sample,
                          "host_cpus": cores, "cpu_model": model},
@@ -220,7 +320,9 @@ def main():
     if wl.get("single"):
         return run_single_signal(args, wl, rank, world, local, dev)
     N, K, B = wl["N"], wl["K"], wl["B"]
-    plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"], block=args.strategy == 2)
+    # inputs_stable: x and t are written before the timed region and never again, so
+    # consecutive launches may stream x before their predecessor completes (PDL)
+    plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"], block=args.strategy == 2, inputs_stable=True)
     stream = torch.cuda.current_stream()
     # inputs resident in HBM: this rank's pairs [rank*B, rank*B + B)
     x, t, k0 = plan.generate(rank * B, B, wl["noise"], device=dev)
@@ -281,6 +383,19 @@ def main():
         dist.all_reduce(succ)
         succ /= world
     success = float(succ.item())
+
+    # ---- per-step spread: a second pass with an event at every step boundary (the
+    # events end the PDL overlap of consecutive steps, so this pass is slightly
+    # slower than the headline pass above; it reports the spread, not the value)
+    bnd = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    torch.cuda.synchronize()
+    bnd[0].record(stream)
+    for i in range(args.steps):
+        step()
+        bnd[i + 1].record(stream)
+    torch.cuda.synchronize()
+    per_step = [bnd[i].elapsed_time(bnd[i + 1]) for i in range(args.steps)]
+    ceiling = read_ceiling(tm, x, stream)
 
     # ---- end to end through tm_run_host: pinned host inputs, H2D + compute + D2H per step
     e2e = None
@@ -351,10 +466,7 @@ def main():
                    "parallelism": f"dp{world} (independent pairs)",
                    "strategy": "2 (Block Phi, Theorem 2)" if args.strategy == 2 else "1 (D_{M+K}, P:152)",
                    "l2": f"no flush: per-step input {B * N * bx / 2**30:.2f} GiB > 126 MB L2"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": kernel,
-                     "algorithmic_bytes_per_launch": fold_bytes, "peak_source": peak_src,
-                     "kernel_ms": fold_ms},
+        "roofline": roofline_block("hbm", achieved, fold_ms, fold_bytes, kernel, traffic, ceiling),
         "run_path": tm.RUN_PATHS.get(path, str(path)),
         "stage_ms": ({"fused_kernel": stage_mean[0]} if nev == 2 else
                      {"fold": stage_mean[0], "fold_template": stage_mean[1], "correlate_argmax": stage_mean[2],
@@ -362,56 +474,44 @@ def main():
         "stage_events": f"on {len(ev)} of {args.steps} timed steps (every {EV_EVERY}th)",
         "host_enqueue_ms_per_step": host_ms,
         "step_hbm_frac": (B * N * bx / (ms_max / args.steps * 1e-3) / 1e9) / peak,
+        "step_hbm": {kk: B * N * bx / (ms_max / args.steps * 1e-3) / 1e9 / v
+                     for kk, v in peak_denominators(ceiling).items()},
+        "step_ms": step_stats(per_step, ms_max / args.steps),
         "success_rate": success,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
         "e2e": e2e,
         "gpu_launches": launches,
     }
+    if world == 1 and not args.no_cfg1 and args.workload != "cfg1":
+        line["cfg1_latency"] = cfg1_latency(tm, dev)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
 def run_single_signal(args, wl, rank, world, local, dev):
-    """cfg5: each rank folds its chunk of the one signal (global positions), the
-    partial folds are summed with one all-reduce, every rank correlates/matches."""
+    """cfg5: one signal split over the ranks through the library's
+    SingleSignal: each rank folds its chunk, the flat y1 || y2 buffer is summed in
+    place by one all-reduce, the correlation is split by output blocks and the
+    16-byte keys MAX-reduced (world > 1); every rank ends with the same k."""
     import torch
     import torch.distributed as dist
 
     import paper_1509_04863_b200 as tm
     from paper_1509_04863_b200 import dist as tmdist
+    from paper_1509_04863_b200.single import SingleSignal
 
     N, K = wl["N"], wl["K"]
-    plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"], block=args.strategy == 2)
+    plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"], block=args.strategy == 2, inputs_stable=True)
     stream = torch.cuda.current_stream()
-    off, ln = tmdist.signal_chunks(N, plan.M1, world)[rank]
+    ss = SingleSignal(plan, rank, world, device=dev)
+    off, ln = ss.offset, ss.length
     x, t, k0 = plan.generate(0, 1, wl["noise"], offset=off, length=ln, device=dev)
-    ws = plan.workspace(1, dev)
-    y1 = torch.empty((1, plan.len_y1), dtype=torch.int32, device=dev)
-    y2 = torch.empty((1, plan.len_y2), dtype=torch.int32, device=dev)
-    res = torch.empty((1, 2), dtype=torch.int32, device=dev)
-    k = torch.empty(1, dtype=torch.int64, device=dev)
-    keys = torch.empty((1, 2), dtype=torch.int64, device=dev)
     torch.cuda.synchronize()
 
-    def step(ev=None):
-        if ev: ev[0].record(stream)
-        plan.fold(x, offset=off, length=ln, y1=y1, y2=y2, accumulate=False, ws=ws, stream=stream)
-        if ev: ev[1].record(stream)
-        if world > 1:
-            tmdist.allreduce_folds(y1, y2)
-        if ev: ev[2].record(stream)
-        if world > 1:  # SURVEY 8(e)(ii): split the correlation by outputs, MAX-reduce the keys
-            plan.correlate_match_part(y1, y2, t, rank, world, keys=keys, ws=ws, stream=stream)
-            tmdist.allreduce_max_keys(keys)
-            plan.match_keys(keys, residues=res, k=k, stream=stream)
-        else:
-            plan.correlate_match(y1, y2, t, residues=res, k=k, ws=ws, stream=stream)
-        if ev: ev[3].record(stream)
-
     for _ in range(max(args.warmup, 3)):
-        step()
+        ss.step(x, t, stream=stream)
     torch.cuda.synchronize()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -422,7 +522,7 @@ def run_single_signal(args, wl, rank, world, local, dev):
     with ClockSampler(local) as clocks:
         start.record(stream)
         for i in range(args.steps):
-            step(ev[i])
+            ss.step(x, t, stream=stream, events=ev[i])
         stop.record(stream)
         torch.cuda.synchronize()
     launches = tm.launch_count() - l0
@@ -431,10 +531,16 @@ def run_single_signal(args, wl, rank, world, local, dev):
     ms_max = tmdist.max_over_ranks(start.elapsed_time(stop), device=dev)
     st = [statistics.mean(e[i].elapsed_time(e[i + 1]) for e in ev) for i in range(3)]
     fold_ms = tmdist.max_over_ranks(st[0], device=dev)
-    # e2e: the chunk copied from pinned host memory every step, k read back
+    # per-step spread (event at every step start; the last step ends at stop)
+    starts = [e[0] for e in ev] + [stop]
+    per_step = [starts[i].elapsed_time(starts[i + 1]) for i in range(args.steps)]
+    res_dev, k_dev = ss.residues.clone(), ss.k.clone()
+    ceiling = read_ceiling(tm, x, stream)
+    # e2e: every step copies this rank's chunk from pinned host memory, runs the
+    # same library step and reads k back
     e2e = None
     if args.e2e_steps > 0:
-        xh = torch.empty((1, ln), dtype=torch.int8, pin_memory=True)
+        xh = torch.empty((1, ln), dtype=x.dtype, pin_memory=True)
         xh.copy_(x.cpu())
         xd = torch.empty_like(x)
         kh = torch.empty(1, dtype=torch.int64, pin_memory=True)
@@ -445,66 +551,78 @@ def run_single_signal(args, wl, rank, world, local, dev):
         e0.record(stream)
         for _ in range(args.e2e_steps):
             xd.copy_(xh, non_blocking=True)
-            plan.fold(xd, offset=off, length=ln, y1=y1, y2=y2, ws=ws, stream=stream)
-            if world > 1:
-                tmdist.allreduce_folds(y1, y2)
-                plan.correlate_match_part(y1, y2, t, rank, world, keys=keys, ws=ws, stream=stream)
-                tmdist.allreduce_max_keys(keys)
-                plan.match_keys(keys, residues=res, k=k, stream=stream)
-            else:
-                plan.correlate_match(y1, y2, t, residues=res, k=k, ws=ws, stream=stream)
-            kh.copy_(k, non_blocking=True)
+            _, kk = ss.step(xd, t, stream=stream)
+            kh.copy_(kk, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = tmdist.max_over_ranks(e0.elapsed_time(e1), device=dev)
+        assert int(kh[0]) == int(k_dev[0]), "e2e k differs from the device-resident run"
         e2e = {"value": N * args.e2e_steps / (e_ms * 1e-3) / 1e9, "unit": "Gsamples/s",
-               "h2d_bytes_per_step": ln, "d2h_bytes_per_step": 8, "steps": args.e2e_steps}
+               "h2d_bytes_per_step": ln * x.element_size(), "d2h_bytes_per_step": 8, "steps": args.e2e_steps,
+               "path": "pinned host chunk -> device copy -> SingleSignal.step -> k to pinned host, per step"}
         del xh, xd
-    success = float((k == k0).double().item())
+    success = float((k_dev == k0).double().item())
     if rank == 0:
-        peak, peak_src = measured_peaks()
-        fold_bytes = ln + (plan.len_y1 + plan.len_y2) * 4
+        bx = x.element_size()
+        fold_bytes = ln * bx + (plan.len_y1 + plan.len_y2) * 4
         achieved = fold_bytes / (fold_ms * 1e-3) / 1e9
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            # the oracle's Eq. 2 fold of cfg5 alone is minutes of CPU: report the
-            # oracle on a bounded sample (the fold of 2^-6 of the signal's rows)
-            import numpy as np
-            import time as _t
-            import oracle
-            import tmgen
-            n_s = N // 64
-            xs = tmgen.signal(wl["seed"], 0, N, lo=0, length=n_s)
-            t0 = _t.perf_counter()
-            oracle.fold(xs, plan.M1, K)
-            oracle.fold(xs, plan.M2, K)
-            dt = _t.perf_counter() - t0
-            cpu = {"value": n_s / dt / 1e9, "unit": "Gsamples/s", "cores": 1, "kind": "oracle",
-                   "sample": f"oracle Eq. 2 folds (M1 and M2) of the first 2^25 samples of the cfg5 signal "
-                             f"taken as a signal of length 2^25 (correlation excluded: K=65536 is minutes of "
-                             f"CPU), {dt:.1f} s"}
+            cpu = cfg5_oracle_baseline(wl, plan, int(k_dev[0]), tuple(res_dev[0].tolist()))
+        value = N * args.steps / (ms_max * 1e-3) / 1e9
+        step_bytes = N * bx / world
         line = {
-            "metric": METRIC, "value": N * args.steps / (ms_max * 1e-3) / 1e9, "unit": "Gsamples/s",
+            "metric": METRIC, "value": value, "unit": "Gsamples/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i8",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "i8" if wl["dtype"] == "int8" else "f32",
             "data": "synthetic (seeded counter-based generator, chunks generated on each rank's device)",
             "config": {"workload": wl["desc"], "N": N, "K": K, "M1": plan.M1, "M2": plan.M2, "chunk_samples": ln,
-                       "parallelism": f"sequence split over {world} rank(s) + NCCL all-reduce of y1||y2 "
-                                      f"({(plan.len_y1 + plan.len_y2) * 4} B)"
-                                      + (f"; correlation split by output blocks + all-reduce MAX of 16 B keys"
-                                         if world > 1 else ""),
+                       "parallelism": f"sequence split over {world} rank(s)"
+                                      + (f" + in-place all-reduce of y1||y2 ({ss.reduce_bytes} B) + correlation "
+                                         f"split by output blocks + all-reduce MAX of 16 B keys" if world > 1 else ""),
                        "l2": "no flush: per-rank input > 126 MB L2"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic_of(args.workload) if world == 1 else None,
-                         "kernel": "tm_fold (fold_pm1_tma + fold_finalize)",
-                         "algorithmic_bytes_per_launch": fold_bytes, "peak_source": peak_src, "fold_ms": fold_ms},
+            "roofline": roofline_block("hbm", achieved, fold_ms, fold_bytes,
+                                       "tm_fold (zero_i32 + fold_pm1_tma + fold_finalize)",
+                                       traffic_of(args.workload) if world == 1 else None, ceiling),
             "stage_ms": {"fold": st[0], "allreduce": st[1], "correlate_match": st[2]},
-            "success_rate": success, "k": int(k.item()), "k0": int(k0.item()),
+            "step_ms": step_stats(per_step, ms_max / args.steps),
+            "step_hbm": {k: step_bytes / (ms_max / args.steps * 1e-3) / 1e9 / v
+                         for k, v in peak_denominators(ceiling).items()},
+            "success_rate": success, "k": int(k_dev[0]), "k0": int(k0.item()),
+            "residues": res_dev[0].tolist(),
             "cpu_baseline": cpu, "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
         }
+        if world == 1 and not args.no_cfg1:
+            line["cfg1_latency"] = cfg1_latency(tm, dev)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def cfg5_oracle_baseline(wl, plan, k_gpu, res_gpu):
+    """The oracle as it stands (single thread) on the whole cfg5 pair: host-generated
+    x (2 GiB) and t, Eq. 2 folds of both moduli, direct correlations, argmax, CRT.
+    Its k and residues are also checked against the GPU's (the full-size parity of
+    SURVEY 8(c.3))."""
+    import numpy as np
+
+    import oracle
+    import tmgen
+    N, K = wl["N"], wl["K"]
+    xs = tmgen.signal(wl["seed"], 0, N)
+    ts = tmgen.template(wl["seed"], 0, N, K, wl["noise"])
+    t0 = time.perf_counter()
+    o = oracle.ftm(xs, ts, want_vectors=False)
+    dt = time.perf_counter() - t0
+    cores, model = cpu_info()
+    del xs
+    return {"value": N / dt / 1e9, "unit": "Gsamples/s", "cores": 1, "kind": "oracle",
+            "sample": f"the whole cfg5 pair (N=2^31, K=65536): Eq. 2 folds of both moduli + direct correlations + "
+                      f"argmax + CRT, {dt:.1f} s single-threaded",
+            "seconds": dt, "host_cpus": cores, "cpu_model": model,
+            "oracle_k": int(o["k"]), "oracle_residues": list(o["residues"]),
+            "matches_gpu": bool(o["k"] == k_gpu and tuple(o["residues"]) == tuple(res_gpu))}
 
 
 if __name__ == "__main__":

@@ -83,6 +83,25 @@ enum {
                            eligible (|y| bound > 32767, K > 65536, shared
                            memory).  The two engines give identical results. */
 
+#define TM_INPUTS_STABLE 32u  /* caller asserts that x and t are not being written
+                                 when tm_run / tm_fold is enqueued: they were
+                                 written by work that has completed (e.g. before a
+                                 host synchronisation) and nothing writes them while
+                                 the call runs.  Lets back-to-back tm_run calls on a
+                                 stream overlap (programmatic dependent launch,
+                                 PDL): the next launch streams x while the previous
+                                 one finishes its tail, waiting for it
+                                 (griddepcontrol.wait) only before its first global
+                                 write.  Default (flag off): every thread of a
+                                 PDL-launched fold kernel waits for the previous
+                                 launch to complete before reading anything, so a
+                                 kernel that produces x right before tm_run is safe. */
+#define TM_KEEP_Y 64u   /* test hook: the fused tm_run kernel (TM_PATH_FUSED_TC)
+                           keeps the folded rows y1, y2 it writes into the
+                           workspace instead of dropping them from L2 without
+                           write-back once correlated; tm_run_fold_rows locates
+                           them.  Costs HBM write traffic; not for production. */
+
 typedef struct {
     int64_t N;          /* signal length */
     int64_t K;          /* template length */
@@ -265,11 +284,20 @@ int tm_profile_events(void **events, int n);
  * arguments.  TM_PATH_FUSED_TC: one persistent kernel (packed fold warps +
  * tensor-core correlation warps, argmax and CRT in its epilogue);
  * TM_PATH_STAGED_TC: fold kernel, then the tensor-core correlation kernel;
- * TM_PATH_STAGED: fold, then the NTT (or fp32) correlation and the CRT kernel;
- * TM_PATH_FUSED_NTT / TM_PATH_OVERLAP: opt-in experimental modes. */
-enum { TM_PATH_STAGED = 0, TM_PATH_STAGED_TC = 1, TM_PATH_FUSED_TC = 2, TM_PATH_FUSED_NTT = 3,
-       TM_PATH_OVERLAP = 4 };
+ * TM_PATH_STAGED: fold, then the NTT (or fp32) correlation and the CRT kernel. */
+enum { TM_PATH_STAGED = 0, TM_PATH_STAGED_TC = 1, TM_PATH_FUSED_TC = 2 };
 int tm_run_path(tm_plan plan, int64_t batch);
+/* tm_run_fold_rows: where tm_run(plan, batch, ws) writes the folded rows y1, y2
+ * inside ws: out[0] = byte offset of y1 [batch][out[1]] (int32/fp32 entries,
+ * row stride out[1] >= len_y1), out[2] = byte offset of y2 [batch][out[3]].
+ * With TM_KEEP_Y these rows hold Eq. 2's y_j after the call on every path; without
+ * it the fused path drops them (test instrumentation).  TM_EINVAL on bad args. */
+int tm_run_fold_rows(tm_plan plan, int64_t batch, int64_t *out);
+/* tm_probe_read_bw: enqueue one read-only HBM streaming pass over buf[0, bytes)
+ * (cp.async.bulk ring, one CTA per SM; bytes rounded down to 32 KiB; buf 16-byte
+ * aligned device memory) on stream, for timing a live read-only bandwidth
+ * ceiling with events (bench.py).  Not part of the method. */
+int tm_probe_read_bw(const void *buf, int64_t bytes, void *stream);
 
 /*
  * ---- One huge signal over several GPUs: the correlation split by outputs ----

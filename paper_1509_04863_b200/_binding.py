@@ -12,6 +12,8 @@ TM_BINARY = 1
 TM_CORR_NTT, TM_CORR_TC = 2, 4
 TM_ALIAS_REPAIR = 8
 TM_BLOCK = 16
+TM_INPUTS_STABLE = 32
+TM_KEEP_Y = 64
 _ENGINES = {None: 0, "auto": 0, "ntt": TM_CORR_NTT, "tc": TM_CORR_TC}
 TM_OK, TM_EINVAL, TM_EUNSUPPORTED, TM_ECUDA = 0, 1, 2, 3
 
@@ -21,9 +23,10 @@ EXPORTED_SYMBOLS = (
     "tm_status_string", "tm_last_error", "tm_launch_count", "tm_profile_events", "tm_run_path",
     "tm_correlate_match_part", "tm_match_keys",
     "tm_mplan_create", "tm_mplan_workspace_bytes", "tm_mplan_run", "tm_crt_multi", "tm_mplan_destroy",
+    "tm_run_fold_rows", "tm_probe_read_bw",
 )
 RUN_PATHS = {0: "staged (fold -> NTT/fp32 correlation -> CRT)", 1: "staged (fold -> tensor-core correlation)",
-             2: "fused (fold + tensor-core correlation in one kernel)", 3: "fused (fold + NTT)", 4: "overlap"}
+             2: "fused (fold + tensor-core correlation in one kernel)"}
 
 _i64, _u64, _i32, _u32, _p, _d = (ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32,
                                   ctypes.c_void_p, ctypes.c_double)
@@ -111,6 +114,10 @@ def lib():
         L.tm_crt_multi.argtypes = [_p, _i64, ctypes.c_int, _p, _i64, _p, _p]
         L.tm_mplan_destroy.restype = None
         L.tm_mplan_destroy.argtypes = [_p]
+        L.tm_run_fold_rows.restype = ctypes.c_int
+        L.tm_run_fold_rows.argtypes = [_p, _i64, ctypes.POINTER(_i64)]
+        L.tm_probe_read_bw.restype = ctypes.c_int
+        L.tm_probe_read_bw.argtypes = [_p, _i64, _p]
         L.tm_status_string.restype = ctypes.c_char_p
         L.tm_status_string.argtypes = [ctypes.c_int]
         L.tm_last_error.restype = ctypes.c_char_p
@@ -134,6 +141,12 @@ def profile_events(events):
     return arr  # keep alive while in use
 
 
+def probe_read_bw(buf, stream=None):
+    """tm_probe_read_bw: one read-only streaming pass over a device tensor (bench.py's
+    live read-only ceiling; instrumentation, not part of the method)."""
+    _check(lib().tm_probe_read_bw(_ptr(buf), buf.numel() * buf.element_size(), _stream(stream)), "tm_probe_read_bw")
+
+
 def _check(rc: int, where: str):
     if rc != TM_OK:
         raise TMError(rc, where)
@@ -152,6 +165,21 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
+def _scratch(nbytes: int, device, stream):
+    """A temporary device buffer used by a launch on `stream`: allocated while
+    `stream` is current and recorded on it, so the caching allocator does not hand
+    it to other work before the launch has finished with it."""
+    import torch
+    if stream is None or isinstance(stream, int):
+        st = torch.cuda.current_stream(device) if stream is None else torch.cuda.ExternalStream(stream, device=device)
+    else:
+        st = stream
+    with torch.cuda.stream(st):
+        buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    buf.record_stream(st)
+    return buf
+
+
 def _ld(x):
     """Row stride of a [batch][n] tensor (a single row may carry any stride in torch)."""
     return x.stride(0) if x.shape[0] > 1 else x.shape[1]
@@ -163,7 +191,8 @@ class Plan:
     block: strategy 2 (Theorem 2's Block Phi, TM_BLOCK) instead of strategy 1."""
 
     def __init__(self, N: int, K: int, M: int = 0, seed: int = 0, dtype: str = "int8", binary: bool = True,
-                 engine: str | None = None, alias_repair: bool = False, block: bool = False):
+                 engine: str | None = None, alias_repair: bool = False, block: bool = False,
+                 inputs_stable: bool = False, keep_y: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1509_04863_b200.Plan needs a CUDA device (no CPU fallback)")
@@ -175,6 +204,10 @@ class Plan:
             flags |= TM_ALIAS_REPAIR
         if block:
             flags |= TM_BLOCK
+        if inputs_stable:   # caller's x / t are not written while calls run (see tm.h)
+            flags |= TM_INPUTS_STABLE
+        if keep_y:          # test hook: the fused kernel keeps its y rows in ws
+            flags |= TM_KEEP_Y
         h = _p()
         _check(lib().tm_plan_create(ctypes.byref(h), N, K, M, seed, self.dtype, flags), "tm_plan_create")
         self._h = h
@@ -199,8 +232,20 @@ class Plan:
         n = lib().tm_workspace_bytes(self._h, batch)
         return torch.empty(max(int(n), 1), dtype=torch.uint8, device=device)
 
-    def _dev(self, t):
-        return t.device if t is not None else "cuda"
+    def _tmp_ws(self, batch: int, device, stream):
+        return _scratch(lib().tm_workspace_bytes(self._h, batch), device, stream)
+
+    def fold_rows(self, ws, batch: int):
+        """Views of the y1 / y2 rows tm_run writes into `ws` (tm_run_fold_rows; with
+        keep_y=True the fused kernel keeps them): (y1 [batch][len_y1], y2 [batch][len_y2])."""
+        import torch
+        out = (_i64 * 4)()
+        _check(lib().tm_run_fold_rows(self._h, batch, out), "tm_run_fold_rows")
+        o1, ld1, o2, ld2 = (int(v) for v in out)
+        es = 4
+        y1 = ws[o1:o1 + batch * ld1 * es].view(self.y_dtype).view(batch, ld1)[:, :self.len_y1]
+        y2 = ws[o2:o2 + batch * ld2 * es].view(self.y_dtype).view(batch, ld2)[:, :self.len_y2]
+        return y1, y2
 
     # ---- entry points --------------------------------------------------------------
     def generate(self, pair0: int, batch: int, noise: float, offset: int = 0, length: int | None = None,
@@ -228,7 +273,7 @@ class Plan:
         if y2 is None:
             y2 = torch.zeros((batch, self.len_y2), dtype=self.y_dtype, device=x.device)
         if ws is None:
-            ws = self.workspace(batch, x.device)
+            ws = self._tmp_ws(batch, x.device, stream)
         _check(lib().tm_fold(self._h, _ptr(x), _ld(x), batch, offset, length, _ptr(y1), _ptr(y2),
                              int(accumulate), _ptr(ws), _stream(stream)), "tm_fold")
         return y1, y2
@@ -241,14 +286,15 @@ class Plan:
         _check(lib().tm_fold_template(self._h, _ptr(t), batch, _ptr(tf), _stream(stream)), "tm_fold_template")
         return tf
 
-    def correlate(self, y1, y2, tf, r1=None, r2=None, stream=None):
+    def correlate(self, y1, y2, tf, r1=None, r2=None, ws=None, stream=None):
         import torch
         batch = y1.shape[0]
         if r1 is None:
             r1 = torch.empty((batch, self.M1), dtype=self.r_dtype, device=y1.device)
         if r2 is None:
             r2 = torch.empty((batch, self.M2), dtype=self.r_dtype, device=y1.device)
-        ws = self.workspace(batch, y1.device)
+        if ws is None:
+            ws = self._tmp_ws(batch, y1.device, stream)
         _check(lib().tm_correlate(self._h, _ptr(y1), _ptr(y2), _ptr(tf), batch, _ptr(r1), _ptr(r2), _ptr(ws),
                                   _stream(stream)), "tm_correlate")
         return r1, r2
@@ -272,7 +318,7 @@ class Plan:
         if k is None:
             k = torch.empty(batch, dtype=torch.int64, device=x.device)
         if ws is None:
-            ws = self.workspace(batch, x.device)
+            ws = self._tmp_ws(batch, x.device, stream)
         _check(lib().tm_run(self._h, _ptr(x), _ld(x), _ptr(t), batch, _ptr(residues), _ptr(k), _ptr(ws),
                             _stream(stream)), "tm_run")
         return residues, k
@@ -286,7 +332,7 @@ class Plan:
         if k is None:
             k = torch.empty(batch, dtype=torch.int64, device=y1.device)
         if ws is None:
-            ws = self.workspace(batch, y1.device)
+            ws = self._tmp_ws(batch, y1.device, stream)
         _check(lib().tm_correlate_match(self._h, _ptr(y1), _ptr(y2), _ptr(t), batch, _ptr(residues), _ptr(k),
                                         _ptr(ws), _stream(stream)), "tm_correlate_match")
         return residues, k
@@ -298,7 +344,7 @@ class Plan:
         if keys is None:
             keys = torch.empty((batch, 2), dtype=torch.int64, device=y1.device)
         if ws is None:
-            ws = self.workspace(batch, y1.device)
+            ws = self._tmp_ws(batch, y1.device, stream)
         _check(lib().tm_correlate_match_part(self._h, _ptr(y1), _ptr(y2), _ptr(t), batch, part, nparts, _ptr(keys),
                                              _ptr(ws), _stream(stream)), "tm_correlate_match_part")
         return keys
@@ -329,7 +375,7 @@ class Plan:
         if k is None:
             k = torch.empty(n, dtype=torch.int64, device=t.device)
         if ws is None:
-            ws = self.workspace(n, t.device)
+            ws = self._tmp_ws(n, t.device, stream)
         _check(lib().tm_correlate_many(self._h, _ptr(y1), _ptr(y2), _ptr(t), n, _ptr(residues), _ptr(k), _ptr(ws),
                                        _stream(stream)), "tm_correlate_many")
         return residues, k
@@ -394,7 +440,7 @@ class MultiPlan:
         if k is None:
             k = torch.empty(batch, dtype=torch.int64, device=x.device)
         if ws is None:
-            ws = self.workspace(batch, x.device)
+            ws = _scratch(lib().tm_mplan_workspace_bytes(self._h, batch), x.device, stream)
         _check(lib().tm_mplan_run(self._h, _ptr(x), _ld(x), _ptr(t), batch, _ptr(residues), _ptr(k), _ptr(ws),
                                   _stream(stream)), "tm_mplan_run")
         return residues, k

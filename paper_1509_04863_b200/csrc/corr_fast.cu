@@ -335,8 +335,7 @@ int tm_fast_template(const tm_plan_s *p, const void *t, int64_t batch, void *tf,
 
 int tm_fast_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, const void *tf,
                       int64_t batch, void *r1, void *r2, int32_t *resid, cudaStream_t s) {
-    static const bool no_pair = getenv("TM_NO_PAIR_KERNEL") != nullptr;
-    if (pair_ok(p) && !no_pair) {
+    if (pair_ok(p)) {
         FastArgs A{};
         fill_pair(p, A);
         A.y1 = (const int32_t *)y1; A.y2 = (const int32_t *)y2;

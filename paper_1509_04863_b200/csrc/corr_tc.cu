@@ -161,14 +161,9 @@ int tm_tc_correlate(const tm_plan_s *p, const void *y1, const void *y2, int64_t 
     tm_tc_fill_args(p, y1, y2, t, ldt, r1, r2, resid, residues_out, k, a);
     a.ldy[0] = ldy1; a.ldy[1] = ldy2;  // 0: one folded signal shared by every template
     a.dbg = g_tc_dbg;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(corr_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        // same (maximal) shared-memory carveout as the fold kernel, so CTAs of the two
-        // kernels can share an SM without a carveout reconfiguration (overlap mode)
-        cudaFuncSetAttribute(corr_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
-        attr = true;
+    {  // per device, once (same maximal carveout as the fold kernel: no reconfiguration between them)
+        const cudaError_t e = tm_smem_attr((const void *)corr_tc_kernel, 227 * 1024, true);
+        if (e != cudaSuccess) return tm_cuda_status(e, "corr_tc_kernel: shared-memory attribute");
     }
     a.nbatch = batch;
     const bool shared_y = ldy1 == 0 && ldy2 == 0;

@@ -564,11 +564,10 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         if (e != cudaSuccess) return tm_cuda_status(e, "tm_correlate: tiled reset");
         TM_CHECK_LAUNCH("tm_correlate: tiled reset");
     }
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(corr_tc_tiled<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<32>());
-        cudaFuncSetAttribute(corr_tc_tiled<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<64>());
-        attr = true;
+    {
+        cudaError_t e = tm_smem_attr((const void *)corr_tc_tiled<32>, (int)smem_bytes<32>());
+        if (e == cudaSuccess) e = tm_smem_attr((const void *)corr_tc_tiled<64>, (int)smem_bytes<64>());
+        if (e != cudaSuccess) return tm_cuda_status(e, "corr_tc_tiled: shared-memory attribute");
     }
     const dim3 grid((unsigned)(T.n_atp * T.n_cr), (unsigned)batch);
     if (T.n_atp > 0) {

@@ -2,11 +2,11 @@
 // (Eq. 2) for both co-prime moduli, restricted
 // to a chunk [offset, offset+len) of global positions (partial fold).
 //
-// Two kernels:
+// Kernels:
 //  * fold_general  -- any N, M, dtype, chunk: one thread per output entry k,
 //                     y[k] = sum_i x[(k + i M) mod N] over chunk positions.
-//  * fold_pm1      -- the packed +-1 kernel (TM_BINARY, M1 | N, M1 % 512 == 0,
-//                     row-aligned chunks): ONE pass over x feeds both moduli.
+//  * the packed +-1 kernel fold_pm1_tma (fold_tma.cu; TM_BINARY, M1 | N,
+//    M1 % 512 == 0, row-aligned chunks): ONE pass over x feeds both moduli.
 //    With x viewed as rows of M1 columns, x[g][c] = x[g*M1 + c]:
 //      - M1 bin of (g, c) is c           (column sums),
 //      - M2 bin of (g, c) is (c - g) mod M2, because M1 = -1 (mod M1+1): an
@@ -66,187 +66,7 @@ __global__ void fold_general(const T *__restrict__ x, int64_t ldx, int64_t N, in
     }
 }
 
-// ---------------------------------------------------------------------------
-// packed +-1 kernel
-// ---------------------------------------------------------------------------
-constexpr int PM_WARPS = 8;                 // warps per CTA, one 512-column strip each
-constexpr int PM_COLS = PM_WARPS * 512;     // columns per CTA (4096)
-
-struct PmArgs {
-    const int8_t *x;
-    int64_t ldx;
-    int64_t M1, M2;
-    int64_t rows;        // rows in the chunk (len / M1)
-    int64_t row0;        // global row of the chunk's first row (offset / M1)
-    int64_t R;           // rows per work item (multiple of 16)
-    int64_t n_rc;        // row chunks per (pair, group)
-    int64_t n_groups;    // column groups of PM_COLS per row
-    int32_t *counts;     // [batch][M1 + M2]: 2*negatives per base bin (y1 then y2)
-};
-
-__device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, int sh) {
-    return __funnelshift_r(lo, hi, sh);
-}
-
-__device__ __forceinline__ uint4 ld_stream(const int8_t *p) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-    return v;
-}
-
-__global__ void __launch_bounds__(PM_WARPS * 32, 2) fold_pm1(PmArgs a) {
-    extern __shared__ int32_t sm_y2[];  // unwrapped anti-diagonal counts of this item
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int64_t item = blockIdx.x;
-    const int64_t rc = item % a.n_rc; item /= a.n_rc;
-    const int64_t gi = item % a.n_groups;
-    const int64_t b = item / a.n_groups;
-    const int64_t ra = rc * a.R;
-    const int64_t rb = (ra + a.R < a.rows) ? ra + a.R : a.rows;
-    const int64_t nrow = rb - ra;
-    const int64_t cs_cta = gi * PM_COLS;
-    // unwrapped diagonal d = c - (g - ra) lies in [cs_cta - (nrow-1), cs_cta + PM_COLS - 1]
-    const int64_t d_min = cs_cta - (nrow - 1);
-    const int n_sm = (int)(PM_COLS + nrow - 1);
-    for (int i = threadIdx.x; i < n_sm; i += blockDim.x) sm_y2[i] = 0;
-    __syncthreads();
-
-    const int64_t cs = cs_cta + (int64_t)warp * 512;
-    const bool active = cs < a.M1;
-    const int64_t c0 = cs + 16 * lane;
-    uint32_t y1w[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) y1w[i] = 0;
-    uint32_t carry[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) carry[i] = 0;
-    uint32_t W[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) W[i] = 0;
-    uint32_t a1[4] = {0, 0, 0, 0};
-
-    const int64_t ntile = (nrow + 15) / 16;
-    if (active) {
-        const int8_t *base = a.x + b * a.ldx + ra * a.M1 + c0;
-        for (int64_t t = 0; t < ntile; ++t) {
-            uint32_t m[16][4];
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                if (t * 16 + r < nrow) {
-                    uint4 v = ld_stream(base + (t * 16 + r) * a.M1);
-                    m[r][0] = v.x & 0x02020202u; m[r][1] = v.y & 0x02020202u;
-                    m[r][2] = v.z & 0x02020202u; m[r][3] = v.w & 0x02020202u;
-                } else {
-                    m[r][0] = m[r][1] = m[r][2] = m[r][3] = 0u;
-                }
-            }
-            // ---- M1: column sums (per-byte counters)
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                uint32_t s = a1[w];
-#pragma unroll
-                for (int r = 0; r < 16; r += 2) s = s + m[r][w] + m[r + 1][w];
-                a1[w] = s;
-            }
-            if ((t & 3) == 3 || t == ntile - 1) {  // widen before byte counters can overflow
-#pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    y1w[2 * w] += __byte_perm(a1[w], 0, 0x4140);
-                    y1w[2 * w + 1] += __byte_perm(a1[w], 0, 0x4342);
-                    a1[w] = 0;
-                }
-            }
-            // ---- M2: anti-diagonals.  Row r = 4*al + rho, byte j -> window byte 16 - r + j.
-            uint32_t A[4][8];
-#pragma unroll
-            for (int rho = 0; rho < 4; ++rho)
-#pragma unroll
-                for (int i = 0; i < 8; ++i) A[rho][i] = 0;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const int al = r >> 2, rho = r & 3;
-#pragma unroll
-                for (int w = 0; w < 4; ++w) A[rho][4 - al + w] += m[r][w];
-            }
-            // carry the previous tile's low block into this tile's high block
-            uint32_t Wn[8];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { Wn[i] = 0; Wn[4 + i] = W[i]; }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                uint32_t v = Wn[i] + A[0][i];
-                v += fsr(A[1][i], i < 7 ? A[1][i + 1] : 0u, 8);
-                v += fsr(A[2][i], i < 7 ? A[2][i + 1] : 0u, 16);
-                v += fsr(A[3][i], i < 7 ? A[3][i + 1] : 0u, 24);
-                W[i] = v;
-            }
-            // ---- finished high block (bins c0 - 16t + [0,16)): widen, chain, flush
-            uint32_t cin[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                uint32_t v = __shfl_up_sync(0xffffffffu, carry[i], 1);
-                cin[i] = lane ? v : 0u;
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                carry[2 * i] = cin[2 * i] + __byte_perm(W[4 + i], 0, 0x4140);
-                carry[2 * i + 1] = cin[2 * i + 1] + __byte_perm(W[4 + i], 0, 0x4342);
-            }
-            if (lane == 31) {
-                const int idx = (int)(c0 - 16 * t - d_min);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    atomicAdd(&sm_y2[idx + 2 * i], (int)(carry[i] & 0xFFFFu));
-                    atomicAdd(&sm_y2[idx + 2 * i + 1], (int)(carry[i] >> 16));
-                }
-            }
-        }
-        // ---- drain: lanes 0..30 still hold their last finished block; every lane
-        //      holds an unfinished low block (bins c0 - 16*ntile + [0,16)).
-        if (ntile > 0) {
-            if (lane != 31) {
-                const int idx = (int)(c0 - 16 * (ntile - 1) - d_min);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    atomicAdd(&sm_y2[idx + 2 * i], (int)(carry[i] & 0xFFFFu));
-                    atomicAdd(&sm_y2[idx + 2 * i + 1], (int)(carry[i] >> 16));
-                }
-            }
-            const int idx = (int)(c0 - 16 * ntile - d_min);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                uint32_t lo = __byte_perm(W[i], 0, 0x4140), hi = __byte_perm(W[i], 0, 0x4342);
-                // bins below d_min are impossible: they need a row >= nrow
-                if (lo & 0xFFFFu) atomicAdd(&sm_y2[idx + 4 * i], (int)(lo & 0xFFFFu));
-                if (lo >> 16) atomicAdd(&sm_y2[idx + 4 * i + 1], (int)(lo >> 16));
-                if (hi & 0xFFFFu) atomicAdd(&sm_y2[idx + 4 * i + 2], (int)(hi & 0xFFFFu));
-                if (hi >> 16) atomicAdd(&sm_y2[idx + 4 * i + 3], (int)(hi >> 16));
-            }
-        }
-        // ---- M1 counts: this lane's 16 columns
-        int32_t *c1 = a.counts + b * (a.M1 + a.M2) + c0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            atomicAdd(&c1[2 * i], (int)(y1w[i] & 0xFFFFu));
-            atomicAdd(&c1[2 * i + 1], (int)(y1w[i] >> 16));
-        }
-    }
-    __syncthreads();
-    // ---- M2 counts: unwrapped diagonal d -> bin (d - (row0 + ra)) mod M2
-    int32_t *c2 = a.counts + b * (a.M1 + a.M2) + a.M1;
-    const int64_t g0 = a.row0 + ra;
-    int64_t bin0 = (d_min - g0) % a.M2;   // once per CTA
-    if (bin0 < 0) bin0 += a.M2;
-    for (int i = threadIdx.x; i < n_sm; i += blockDim.x) {
-        int v = sm_y2[i];
-        if (v) {
-            int64_t bin = bin0 + i;
-            while (bin >= a.M2) bin -= a.M2;
-            atomicAdd(&c2[bin], v);
-        }
-    }
-}
+constexpr int PM_COLS = 8 * 512;  // columns per CTA group of the packed kernel (fold_tma.cu TCOLS)
 
 // ---------------------------------------------------------------------------
 // finalize: counts -> values, + wrap + extension (partial-fold semantics)
@@ -305,27 +125,6 @@ __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t
     }
 }
 
-int pick_row_chunks(const tm_plan_s *p, int64_t batch, int64_t rows, int64_t n_groups) {
-    // Work items = batch * n_groups * n_rc.  Keep items >= 256 rows; pick n_rc that
-    // minimises the idle fraction of the last wave (2 CTAs per SM).
-    const int64_t slots = (int64_t)p->num_sms * 2;
-    int64_t best = (rows + 8191) / 8192;
-    double best_eff = -1.0;
-    const int64_t n0 = (rows + 8191) / 8192;   // R <= 8192 keeps 16-bit column counters exact
-    for (int64_t n = n0; n <= n0 + 64; ++n) {
-        int64_t R = ((rows + n - 1) / n + 15) / 16 * 16;
-        if (n > n0 && R < 256) break;
-        int64_t nrc = (rows + R - 1) / R;
-        int64_t items = batch * n_groups * nrc;
-        double waves = (double)items / (double)slots;
-        double eff = waves / ((double)((items + slots - 1) / slots));
-        // prefer fewer items (fewer atomics) unless the tail gets clearly better
-        if (eff > best_eff + 0.03) { best_eff = eff; best = nrc; }
-        if (items >= 16 * slots) break;
-    }
-    return (int)best;
-}
-
 // Work split for the persistent TMA kernel (one CTA per SM): the fewest row
 // chunks per (pair, column group) whose item count spreads over the SMs with
 // < 5% imbalance (items are equal-sized), rows per item in [128, 1024].
@@ -360,8 +159,7 @@ int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batc
     const bool aligned = ((uintptr_t)x % 16 == 0) && (ldx % 16 == 0);
     const bool fast = p->fast_fold && aligned && (offset % p->M1 == 0) && (len % p->M1 == 0) &&
                       batch <= (int64_t(1) << 31) / 64;
-    static const bool use_regs = getenv("TM_FOLD_KERNEL") && !strcmp(getenv("TM_FOLD_KERNEL"), "regs");
-    if (fast && len > 0 && !use_regs) {
+    if (fast && len > 0) {
         int64_t R = 0, nrc = 0;
         const int64_t rows = len / p->M1, n_groups = (p->M1 + PM_COLS - 1) / PM_COLS;
         pick_rows_tma(p, batch, rows, n_groups, &R, &nrc);
@@ -380,38 +178,6 @@ int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batc
             TM_CHECK_LAUNCH("tm_fold: fold_finalize");
             return TM_OK;
         }
-    }
-    if (fast && len > 0) {
-        tm_ws_layout L = tm_ws(p, batch);
-        int32_t *counts = (int32_t *)((char *)ws + L.fold_counts);
-        cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)batch * (p->M1 + p->M2) * 4, s);
-        if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: memset");
-        PmArgs a;
-        a.x = (const int8_t *)x; a.ldx = ldx; a.M1 = p->M1; a.M2 = p->M2;
-        a.rows = len / p->M1; a.row0 = offset / p->M1;
-        a.n_groups = (p->M1 + PM_COLS - 1) / PM_COLS;
-        int64_t nrc = pick_row_chunks(p, batch, a.rows, a.n_groups);
-        a.R = ((a.rows + nrc - 1) / nrc + 15) / 16 * 16;
-        a.n_rc = (a.rows + a.R - 1) / a.R;
-        a.counts = counts;
-        int64_t items = batch * a.n_groups * a.n_rc;
-        size_t smem = (size_t)(PM_COLS + a.R) * 4;
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(fold_pm1, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-            attr_set = true;
-        }
-        if (smem > 96 * 1024) { tm_set_error("tm_fold: row chunk too large"); return TM_EUNSUPPORTED; }
-        if (items > 0x7FFFFFFF) { tm_set_error("tm_fold: too many work items"); return TM_EUNSUPPORTED; }
-        fold_pm1<<<(unsigned)items, PM_WARPS * 32, smem, s>>>(a);
-        TM_CHECK_LAUNCH("tm_fold: fold_pm1");
-        int64_t gx = (p->M2 + p->K + 1023) / 1024;
-        { const cudaError_t e_ = launch_pdl(fold_finalize, dim3((unsigned)gx, (unsigned)batch), dim3(256), 0, s,
-                (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, a.row0, a.rows,
-            counts, (int32_t *)y1, ldy1, (int32_t *)y2, ldy2, accumulate, p->block);
-              if (e_ != cudaSuccess) return tm_cuda_status(e_, "tm_fold: fold_finalize"); }
-        TM_CHECK_LAUNCH("tm_fold: fold_finalize");
-        return TM_OK;
     }
     if (p->dtype == TM_F32 && ws && len > 0) {  // strip kernel + fixed-order finalize
         tm_ws_layout L = tm_ws(p, batch);

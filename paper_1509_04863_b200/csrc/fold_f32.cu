@@ -36,6 +36,7 @@ struct F32Args {
     int64_t R, nrc;            // rows per item, row chunks
     int64_t g0m, Rm;           // row0 mod M2, R mod M2 (the finalize's diagonal index of a chunk)
     int block;                 // TM_BLOCK: no wrap, cyclic extension
+    int x_early;               // TM_INPUTS_STABLE: x may be read before the previous launch completes
     int64_t n_strips, n_groups;
     float *parts;              // [batch][nrc][M1 + n_strips (R + 127)]
 };
@@ -50,6 +51,7 @@ __device__ __forceinline__ int64_t part_stride(const F32Args &a) { return part_s
 __global__ void __launch_bounds__(FW * 32) fold_f32_strips(F32Args a) {
     extern __shared__ float emit[];  // [FW][RMAX + 127]
     pdl_trigger();
+    if (!a.x_early) pdl_wait();  // x may come from the launch right before this one
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t item = blockIdx.x;
     const int64_t rc = item % a.nrc;
@@ -223,6 +225,7 @@ int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     a.M1 = p->M1; a.M2 = p->M2; a.K = p->K; a.N = p->N; a.q2 = p->q2;
     a.rows = len / p->M1; a.row0 = offset / p->M1;
     a.block = p->block;
+    a.x_early = (p->flags & TM_INPUTS_STABLE) ? 1 : 0;
     geometry(p, a.rows, &a.R, &a.nrc);
     if (a.R >= a.M2) return TM_EUNSUPPORTED;  // the finalize's two-diagonal bound (M1 M2 > N implies R < M2)
     a.g0m = a.row0 % a.M2;
@@ -233,10 +236,9 @@ int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     const int64_t items = batch * a.n_groups * a.nrc;
     if (items > 0x7FFFFFFF || batch > 65535) return TM_EUNSUPPORTED;
     const size_t smem = (size_t)FW * (RMAX + 127) * 4;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(fold_f32_strips, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
+    {
+        const cudaError_t e = tm_smem_attr((const void *)fold_f32_strips, (int)smem);
+        if (e != cudaSuccess) return tm_cuda_status(e, "fold_f32_strips: shared-memory attribute");
     }
     {
         const cudaError_t e = launch_pdl(fold_f32_strips, dim3((unsigned)items), dim3(FW * 32), smem, s, a);

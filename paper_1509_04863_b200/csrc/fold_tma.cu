@@ -52,15 +52,10 @@ struct TmaArgs {
     int priv_stride;     // words per warp-private anti-diagonal array (512 + 16 ceil(R/16))
     int32_t *counts;     // non-owner: [batch][M1 + M2]
     int32_t *y1, *y2;    // owner outputs
-    // fused mode: NTT warps correlate pair i while the fold warps stream pair i+1
-    FastArgs f;          // template, tables, y pointers, resid (see ntt_core.cuh)
-    int32_t *residues_out;
-    int64_t *k_out;
-    uint32_t crt_inv;
-    int64_t crt_wrap;
     int block;            // TM_BLOCK: no wrap term, cyclic extension
     int xs_bytes;        // bytes reserved for the epilogue's x[0 .. K + q) stage
-    int *work_counter;   // non-NULL: dynamic item assignment (atomic counter, zeroed per launch)
+    int x_early;         // PDL launch may read x (and t) before the previous grid completes
+                         // (plan flag TM_INPUTS_STABLE); 0: every thread waits at entry
     // tensor-core fused mode: 8 warps correlate pair i (tc_core.cuh) while the fold streams pair i+1
     tc::TcArgs tca;
     uint32_t tc_off;     // shared-memory offset of the tensor-core group's region
@@ -178,20 +173,19 @@ __device__ __forceinline__ int32_t comb3(const uint16_t *pv, int stride, int d, 
     return v;
 }
 
-constexpr int ntt_threads(int logl2) { return logl2 > 0 ? (1 << (logl2 - 4)) : 0; }
-
-// NST: ring stages.  LOGL2 > 0 selects the fused kernel: NT = L2/16 extra threads
-// (warps 13..) run the pair NTT correlation (ntt_core.cuh) of each finished pair.
-// MINB = 2 caps registers (<= 78/thread) so that a pair-NTT CTA can share the SM
-// (overlap mode of tm_run).
+// NST: ring stages.  TCM selects the fused kernel: 8 extra warps correlate each
+// finished pair on the tensor cores (tc_core.cuh) while the fold streams the next.
 constexpr int TC_GROUP = 5;  // named barrier of the tensor-core warps
 
-template <int NST, int LOGL2, int MINB = 1, bool TCM = false>
-__global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM ? tc::NTHR : 0), MINB)
+template <int NST, int MINB = 1, bool TCM = false>
+__global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MINB)
     fold_pm1_tma(TmaArgs a) {
-    constexpr bool FUSED = LOGL2 > 0 || TCM;
+    constexpr bool FUSED = TCM;
     extern __shared__ __align__(1024) uint8_t smem[];
-    if constexpr (LOGL2 == 0) pdl_trigger();
+    pdl_trigger();
+    // without TM_INPUTS_STABLE the previous launch on the stream may still be writing
+    // x or t: nothing is read before it has completed (griddepcontrol.wait)
+    if (!a.x_early) pdl_wait();
     uint8_t *ring = smem;
     uint16_t *privb = reinterpret_cast<uint16_t *>(smem + NST * STAGE_BYTES);  // [2][TW][priv_stride]
     uint64_t *full = reinterpret_cast<uint64_t *>(privb + 2 * TW * a.priv_stride);
@@ -199,13 +193,12 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
     uint64_t *pfull = empty + NST;   // [2]: consumers -> epilogue (count TW)
     uint64_t *pempty = pfull + 2;    // [2]: epilogue -> consumers (count NE)
     uint64_t *yready = pempty + 2;   // [2]: y1 + y2 of a pair in global memory (count TW + NE)
-    uint64_t *ydone = yready + 2;    // [2]: NTT warps finished with a pair (count NT / 32)
+    uint64_t *ydone = yready + 2;    // [2]: tensor-core warps finished with a pair (count NTHR / 32)
     int64_t *item_q = reinterpret_cast<int64_t *>(ydone + 2);  // [8] producer -> consumers: item of seq
     int64_t *pitem = item_q + 8;     // [2] consumers -> epilogue / NTT warps: item of a buffer (-1 = end)
     uint4 *xs = reinterpret_cast<uint4 *>(pitem + 2);  // owner epilogue: x[0 .. K + q)
-    uint32_t *nbuf = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(xs) + a.xs_bytes);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int NTW = TCM ? tc::NTHR / 32 : ntt_threads(LOGL2) / 32;
+    constexpr int NTW = TCM ? tc::NTHR / 32 : 0;
     long long t_entry = 0;
     if constexpr (TCM) t_entry = tc::gtime();
     if (threadIdx.x == 0) {
@@ -266,7 +259,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 // the MMAs of both chunks run back to back on the kernel's tail
                 uint8_t *a_alt = nullptr;
 #ifndef TM_NO_RING_A
-                if (a.work_counter == nullptr && b + (int64_t)gridDim.x >= a.n_items && a.tca.NC > a.tca.CCH &&
+                if (b + (int64_t)gridDim.x >= a.n_items && a.tca.NC > a.tca.CCH &&
                     2 * a.tca.CCH >= a.tca.NC &&
                     (uint32_t)(256 * (8 * (a.tca.NC - a.tca.CCH - 1) + 15)) <= (uint32_t)(NST * STAGE_BYTES)) {
                     tc::build_a(a.tca, tsm, a.tca.CCH, a.tca.NC, gt, smem);
@@ -288,37 +281,6 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             return;
         }
     }
-    if constexpr (LOGL2 > 0) {
-        if (warp >= TW + 1 + NE) {
-            // ---------------------------------------------------------- NTT warps
-            constexpr int NT = ntt_threads(LOGL2);
-            using NBar = NamedBar<3, NT>;
-            const int nt = threadIdx.x - (TW + 1 + NE) * 32;
-            uint32_t *Ts2 = nbuf + (1 << LOGL2);
-            uint32_t *Ts1 = Ts2 + (1 << LOGL2);
-            int pb = 0;
-            uint32_t pph = 0;
-            for (;;) {
-                mbar_wait(&yready[pb], pph);
-                const int64_t b = pitem[pb];  // fused mode: items are whole pairs
-                if (b < 0) break;
-                pair_template_to_smem<LOGL2, NBar>(nbuf, Ts2, Ts1, nt, a.f, b);
-                NBar::sync();
-                pair_modulus2<LOGL2, NBar>(nbuf, Ts2, nt, a.f, b);
-                pair_modulus1<LOGL2, NBar>(nbuf, Ts1, nt, a.f, b);
-                if (nt == 0) {  // steps 8-9 (tm_resolve)
-                    const int64_t m1 = a.f.resid[b * 2], m2 = a.f.resid[b * 2 + 1];
-                    a.k_out[b] = tm_resolve(m1, m2, a.M1, a.M2, a.crt_inv, a.N, a.crt_wrap);
-                    if (a.residues_out) { a.residues_out[2 * b] = (int32_t)m1; a.residues_out[2 * b + 1] = (int32_t)m2; }
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&ydone[pb]);
-                if (++pb == 2) { pb = 0; pph ^= 1; }
-            }
-            return;
-        }
-    }
-
     if (warp == TW) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
@@ -326,7 +288,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             uint32_t ph = 0;
             const uint64_t pol = l2_evict_first_policy();
             for (int64_t seq = 0;; ++seq) {
-                int64_t item = a.work_counter ? (int64_t)atomicAdd(a.work_counter, 1) : blockIdx.x + seq * gridDim.x;
+                int64_t item = blockIdx.x + seq * gridDim.x;
                 if (item >= a.n_items) item = -1;
                 item_q[seq & 7] = item;  // published by the arrive on the item's first stage
                 if (item < 0) {          // end: complete one more stage phase with no data
@@ -374,9 +336,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 }
             }
             mbar_wait(&pfull[pb], pph);
-            if constexpr (LOGL2 == 0) {  // before this warp's first y2 store / counts atomic
-                if (!pdl_done) { pdl_wait(); pdl_done = true; }
-            }
+            if (!pdl_done) { pdl_wait(); pdl_done = true; }  // before this warp's first y2 store / counts atomic
             long long te0 = 0;
             if constexpr (TCM) te0 = tc::gtime();
             const int64_t item = pitem[pb];
@@ -418,7 +378,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
                 // gentler per-bin loop below costs the concurrent fold less): runs of 16
                 // consecutive bins per thread with 16-byte loads and stores (pad <= 512:
                 // a diagonal then lies in at most two strips, or strip 0 when d < 0)
-                const bool runs = TCM && a.work_counter == nullptr && item + (int64_t)gridDim.x >= a.n_items &&
+                const bool runs = TCM && item + (int64_t)gridDim.x >= a.n_items &&
                                   pad <= 512 && (q & 15) == 0 && (M1 & 15) == 0 && !a.accumulate &&
                                   ((reinterpret_cast<uintptr_t>(o2) & 15) == 0);
                 if (runs) {
@@ -556,7 +516,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
         mbar_wait(&full[s], ph);  // first stage of the next item (or the end marker)
         const int64_t item = item_q[seq & 7];
         mbar_wait(&pempty[pb], pph ^ 1);
-        if constexpr (FUSED) mbar_wait(&ydone[pb], pph ^ 1);  // bounds the fold's lead over the NTT
+        if constexpr (FUSED) mbar_wait(&ydone[pb], pph ^ 1);  // bounds the fold's lead over the correlation
         if (item < 0) {  // tell the epilogue (and the NTT / tensor-core warps) to stop
 #ifdef TM_CONS_PROF
             if constexpr (TCM) {
@@ -680,9 +640,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM
             }
         }
         const int64_t c0 = it.cs_cta + warp * 512 + 16 * lane;
-        if constexpr (LOGL2 == 0) {
-            if (seq == 0) pdl_wait();  // first global write of this warp (y1 / counts) follows
-        }
+        if (seq == 0) pdl_wait();  // first global write of this warp (y1 / counts) follows
         if (active) {
             // drain: lane l's low block (bins 16 l - 16 ntile + [0,16)) + lane l-1's pending carry
             uint32_t lo[8];
@@ -768,6 +726,7 @@ int setup_args(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, in
     a.n_items = batch * a.n_groups * a.n_rc;
     a.owner = (a.n_groups == 1 && a.n_rc == 1 && offset == 0 && len == p->N) ? 1 : 0;
     a.accumulate = accumulate;
+    a.x_early = (p->flags & TM_INPUTS_STABLE) ? 1 : 0;
     if (R > 1024) return TM_EUNSUPPORTED;
     a.priv_stride = (int)(512 + (R + 15) / 16 * 16);
     a.acc_words = TW * a.priv_stride;
@@ -779,40 +738,31 @@ int setup_args(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, in
     return TM_OK;
 }
 
-size_t smem_bytes(const TmaArgs &a, int nst, int logl2) {
-    size_t b = (size_t)nst * STAGE_BYTES + (size_t)2 * a.acc_words * 2 + (2 * nst + 8) * 8 + 10 * 8 + a.xs_bytes;
-    if (logl2 > 0) b += (size_t)(2 * (1 << logl2) + (1 << (logl2 - 1))) * 4;
-    return b;
+size_t smem_bytes(const TmaArgs &a, int nst) {
+    return (size_t)nst * STAGE_BYTES + (size_t)2 * a.acc_words * 2 + (2 * nst + 8) * 8 + 10 * 8 + a.xs_bytes;
 }
 
-template <int NST, int LOGL2, int MINB = 1, bool TCM = false>
+template <int NST, int MINB = 1, bool TCM = false>
 int launch(const TmaArgs &a, int64_t grid, size_t smem, cudaStream_t s) {
-    auto k = fold_pm1_tma<NST, LOGL2, MINB, TCM>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-        attr = true;
-    }
-    const unsigned nthr = (TW + 1 + NE) * 32 + ntt_threads(LOGL2) + (TCM ? tc::NTHR : 0);
-    const bool no_pdl = !tm_pdl_enabled();  // A/B
-    if constexpr (LOGL2 == 0) {
-        if (!no_pdl) {  // programmatic dependent launch: see pdl_trigger / pdl_wait
-            cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3((unsigned)grid);
-            cfg.blockDim = dim3(nthr);
-            cfg.dynamicSmemBytes = smem;
-            cfg.stream = s;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[0].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            const cudaError_t e = cudaLaunchKernelEx(&cfg, k, a);
-            if (e != cudaSuccess) return tm_cuda_status(e, "fold_pm1_tma (PDL launch)");
-            TM_CHECK_LAUNCH("fold_pm1_tma");
-            return TM_OK;
-        }
+    auto k = fold_pm1_tma<NST, MINB, TCM>;
+    cudaError_t e = tm_smem_attr((const void *)k, 227 * 1024, true);
+    if (e != cudaSuccess) return tm_cuda_status(e, "fold_pm1_tma: shared-memory attribute");
+    const unsigned nthr = (TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0);
+    if (tm_pdl_enabled()) {  // programmatic dependent launch: see pdl_trigger / pdl_wait
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(nthr);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, k, a);
+        if (e != cudaSuccess) return tm_cuda_status(e, "fold_pm1_tma (PDL launch)");
+        TM_CHECK_LAUNCH("fold_pm1_tma");
+        return TM_OK;
     }
     k<<<(unsigned)grid, nthr, smem, s>>>(a);
     TM_CHECK_LAUNCH("fold_pm1_tma");
@@ -848,101 +798,10 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
 #ifndef TM_FOLD_NST
 #define TM_FOLD_NST 4
 #endif
-    const size_t smem = smem_bytes(a, TM_FOLD_NST, 0);
+    const size_t smem = smem_bytes(a, TM_FOLD_NST);
     if (smem > 227 * 1024) return TM_EUNSUPPORTED;
     const int64_t grid = a.n_items < p->num_sms ? a.n_items : p->num_sms;
-    return launch<TM_FOLD_NST, 0>(a, grid, smem, s);
-}
-
-// Overlap mode of tm_run: the owner-mode fold of a chunk of pairs with dynamic item
-// assignment, a 3-stage ring and <= 78 registers, so that pair-NTT CTAs of the
-// previous chunk (another stream) co-reside on the same SMs.
-bool tm_overlap_ok(const tm_plan_s *p, int64_t batch) {
-    // opt-in (TM_OVERLAP=1): measured slower than the serial fold -> pair-NTT sequence
-    // (cfg2: 0.40-0.59 ms vs 0.342 ms per step with 2-6 chunks)
-    static const bool on = getenv("TM_OVERLAP") != nullptr;
-    if (!on) return false;
-    return p->fast_fold && p->fast_corr && p->n_primes == 1 && p->M1 <= TCOLS && p->q1 <= 1024 &&
-           p->logL2 == p->logL1 + 1 && p->L1 == p->M1 && p->nload1 == p->M1 && p->logL2 >= 10 && p->logL2 <= 14 &&
-           batch >= 2 * p->num_sms;
-}
-
-// Tensor-core two-stream overlap mode of tm_run (run.cu): opt-in (TM_OVERLAP=1);
-// measured slower than the fused kernel and than fold -> correlation in sequence
-// (cfg2: 0.36-0.72 ms vs 0.277 ms per step with 4-16 chunks).
-bool tm_overlap_tc_ok(const tm_plan_s *p, int64_t batch) {
-    static const char *env = getenv("TM_OVERLAP");
-    static const bool on = env && env[0] == '1';
-    if (!on) return false;
-    return p->use_tc && p->tc_ok && p->fast_fold && p->M1 <= TCOLS && p->q1 <= 1024 && batch >= 2 * 64 &&
-           p->N % 16 == 0 && p->N == p->M1 * p->q1;
-}
-
-int tm_fold_overlap(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, void *y1, void *y2, void *ws,
-                    int *counter, cudaStream_t s) {
-    if (((uintptr_t)x % 16) || (ldx % 16)) return TM_EUNSUPPORTED;
-    TmaArgs a{};
-    const int64_t R = (p->q1 + 15) / 16 * 16;
-    int rc = setup_args(p, x, ldx, batch, 0, p->N, y1, y2, 0, ws, R, 1, a);
-    if (rc) return rc;
-    if (!a.owner) return TM_EUNSUPPORTED;
-    cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
-    if (e != cudaSuccess) return tm_cuda_status(e, "tm_run: counter reset");
-    a.work_counter = counter;
-    const size_t sm = smem_bytes(a, 3, 0);
-    if (sm > 227 * 1024) return TM_EUNSUPPORTED;
-    const int64_t grid = batch < p->num_sms ? batch : p->num_sms;
-    return launch<3, 0, 2>(a, grid, sm, s);
-}
-
-// The whole of Algorithm 1 in ONE kernel for the paper's shape: whole pairs per
-// item (M1 <= 4096, q <= 1024), one NTT prime, L2 = 2 L1 <= 2^13.  Returns
-// TM_EUNSUPPORTED (nothing enqueued) when the plan/batch does not qualify.
-bool tm_fused_ok(const tm_plan_s *p, int64_t batch) {
-    // opt-in (TM_FUSED=1): measured slower than fold + pair-NTT kernels back to back
-    // (0.414 vs 0.346 ms per cfg2 step): one 512-thread NTT group per SM cannot keep up
-    static const bool on = getenv("TM_FUSED") != nullptr;
-    if (!on) return false;
-    return p->fast_fold && p->fast_corr && p->n_primes == 1 && p->M1 <= TCOLS && p->q1 <= 1024 &&
-           p->logL2 == p->logL1 + 1 && p->L1 == p->M1 && p->nload1 == p->M1 && p->logL2 >= 10 && p->logL2 <= 13 &&
-           batch >= p->num_sms && (TW + 1 + NE) * 32 + ntt_threads(p->logL2) <= 1024;  // one CTA's threads
-}
-
-int tm_fold_corr_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
-                       void *y2, int32_t *resid, int32_t *residues, int64_t *k, void *ws, cudaStream_t s) {
-    if (!tm_fused_ok(p, batch)) return TM_EUNSUPPORTED;
-    if (((uintptr_t)x % 16) || (ldx % 16)) return TM_EUNSUPPORTED;
-    TmaArgs a{};
-    const int64_t R = (p->q1 + 15) / 16 * 16;
-    int rc = setup_args(p, x, ldx, batch, 0, p->N, y1, y2, 0, ws, R, 1, a);
-    if (rc) return rc;
-    if (!a.owner) return TM_EUNSUPPORTED;
-    tm_ntt_tables tabs;
-    tm_ntt_tables_get(p->device, &tabs);
-    FastArgs &f = a.f;
-    f.t = (const int8_t *)t; f.K = p->K;
-    f.twf[0] = tabs.tw2[0][0]; f.twi[0] = tabs.tw2[0][1];
-    f.twf[1] = tabs.tw2[1][0]; f.twi[1] = tabs.tw2[1][1];
-    tm_mont_linv(p->logL2, TM_P1, &f.cL[0], &f.cLs[0]);
-    tm_mont_linv(p->logL1, TM_P1, &f.cL1, &f.cL1s);
-    f.y1 = (const int32_t *)y1; f.y2 = (const int32_t *)y2;
-    f.ldy1 = p->len_y1; f.ldy2 = p->len_y2;
-    f.nload1 = p->nload1; f.nload2 = p->nload2;
-    f.M1 = p->M1; f.M2 = p->M2;
-    f.r1 = nullptr; f.r2 = nullptr;
-    f.resid = resid;
-    a.residues_out = residues;
-    a.k_out = k;
-    a.crt_inv = p->crt_inv;
-    a.crt_wrap = p->crt_wrap;
-    const int64_t grid = batch < p->num_sms ? batch : p->num_sms;
-    switch (p->logL2) {
-        case 10: { const size_t sm = smem_bytes(a, 3, 10); if (sm > 227 * 1024) return TM_EUNSUPPORTED; return launch<3, 10>(a, grid, sm, s); }
-        case 11: { const size_t sm = smem_bytes(a, 3, 11); if (sm > 227 * 1024) return TM_EUNSUPPORTED; return launch<3, 11>(a, grid, sm, s); }
-        case 12: { const size_t sm = smem_bytes(a, 3, 12); if (sm > 227 * 1024) return TM_EUNSUPPORTED; return launch<3, 12>(a, grid, sm, s); }
-        case 13: { const size_t sm = smem_bytes(a, 3, 13); if (sm > 227 * 1024) return TM_EUNSUPPORTED; return launch<3, 13>(a, grid, sm, s); }
-        default: return TM_EUNSUPPORTED;
-    }
+    return launch<TM_FOLD_NST>(a, grid, smem, s);
 }
 
 // The whole of Algorithm 1 in ONE persistent kernel with the tensor-core
@@ -951,7 +810,7 @@ int tm_fold_corr_fused(const tm_plan_s *p, const void *x, int64_t ldx, const voi
 // q <= 1024).  Returns TM_EUNSUPPORTED (nothing enqueued) when the plan/batch
 // does not qualify.
 bool tm_fused_tc_ok(const tm_plan_s *p, int64_t batch) {
-    static const char *env = getenv("TM_FUSED_TC");
+    static const char *env = getenv("TM_FUSED_TC");  // A/B: "0" forces the staged kernels
     static const bool off = env && env[0] == '0';
     if (off) return false;
     return p->use_tc && p->tc_ok && p->fast_fold && p->M1 <= TCOLS && p->q1 <= 1024 && p->N == p->M1 * p->q1 &&
@@ -959,7 +818,7 @@ bool tm_fused_tc_ok(const tm_plan_s *p, int64_t batch) {
 }
 
 int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
-                     void *y2, int32_t *residues, int64_t *k, void *ws, int *counter, cudaStream_t s) {
+                     void *y2, int32_t *residues, int64_t *k, void *ws, cudaStream_t s) {
     if (!tm_fused_tc_ok(p, batch)) return TM_EUNSUPPORTED;
     if (((uintptr_t)x % 16) || (ldx % 16)) return TM_EUNSUPPORTED;
     TmaArgs a{};
@@ -969,15 +828,16 @@ int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void 
     if (!a.owner) return TM_EUNSUPPORTED;
     tm_tc_fill_args(p, y1, y2, t, p->K, nullptr, nullptr, nullptr, residues, k, a.tca);
     a.tca.dbg = tm_tc_dbg_buffer();
-    // y is scratch here: 128-byte rows, dropped from L2 without write-back once correlated
+    // y is scratch here: 128-byte rows, dropped from L2 without write-back once
+    // correlated (TM_KEEP_Y, a test hook, keeps them for inspection)
     a.ldy1 = a.tca.ldy[0] = p->ldy1_run;
     a.ldy2 = a.tca.ldy[1] = p->ldy2_run;
-    a.tca.discard_y = 1;
+    a.tca.discard_y = (p->flags & TM_KEEP_Y) ? 0 : 1;
     // 4-stage ring when the tensor-core region fits next to it, else 3 stages
     constexpr int K4 = 32 / SROWS;   // "4 stages" of 8 rows: the same 128 KB ring in SROWS-row stages
     constexpr int K3 = 24 / SROWS;
-    const size_t base4 = (smem_bytes(a, K4, 0) + 1023) / 1024 * 1024;
-    const size_t base3 = (smem_bytes(a, K3, 0) + 1023) / 1024 * 1024;
+    const size_t base4 = (smem_bytes(a, K4) + 1023) / 1024 * 1024;
+    const size_t base3 = (smem_bytes(a, K3) + 1023) / 1024 * 1024;
     const int nst = (base4 + p->tc_smem <= 227 * 1024) ? K4 : K3;
     const size_t base = nst == K4 ? base4 : base3;
     a.tc_off = (uint32_t)base;
@@ -985,14 +845,7 @@ int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void 
     if (sm > 227 * 1024) return TM_EUNSUPPORTED;
     // whole pairs are equal-sized items: the static round-robin schedule balances
     // them as well as a dynamic counter and needs no per-launch reset
-#ifdef TM_FUSED_DYNAMIC
-    cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int), s);
-    if (e != cudaSuccess) return tm_cuda_status(e, "tm_run: counter reset");
-    a.work_counter = counter;
-#else
-    (void)counter;
-#endif
     const int64_t grid = batch < p->num_sms ? batch : p->num_sms;
-    if (nst == K4) return launch<K4, 0, 1, true>(a, grid, sm, s);
-    return launch<K3, 0, 1, true>(a, grid, sm, s);
+    if (nst == K4) return launch<K4, 1, true>(a, grid, sm, s);
+    return launch<K3, 1, true>(a, grid, sm, s);
 }

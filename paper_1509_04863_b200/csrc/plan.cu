@@ -8,6 +8,10 @@
 #include "tm_internal.cuh"
 
 #include <atomic>
+#include <mutex>
+#include <new>
+#include <set>
+#include <tuple>
 
 static thread_local char g_err[512] = "";
 static std::atomic<unsigned long long> g_launches{0};
@@ -87,7 +91,7 @@ int tm_plan_create_impl(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t 
     if (K < 1) { tm_set_error("tm_plan_create: K=%lld < 1", (long long)K); return TM_EINVAL; }
     if (dtype != TM_I8 && dtype != TM_F32) { tm_set_error("tm_plan_create: bad dtype %d", dtype); return TM_EINVAL; }
     if ((flags & TM_BLOCK) && (flags & TM_ALIAS_REPAIR)) { tm_set_error("tm_plan_create: TM_BLOCK and TM_ALIAS_REPAIR are exclusive"); return TM_EINVAL; }
-    if (flags & ~(TM_BINARY | TM_CORR_NTT | TM_CORR_TC | TM_ALIAS_REPAIR | TM_BLOCK)) { tm_set_error("tm_plan_create: unknown flags 0x%x", flags); return TM_EINVAL; }
+    if (flags & ~(TM_BINARY | TM_CORR_NTT | TM_CORR_TC | TM_ALIAS_REPAIR | TM_BLOCK | TM_INPUTS_STABLE | TM_KEEP_Y)) { tm_set_error("tm_plan_create: unknown flags 0x%x", flags); return TM_EINVAL; }
     if ((flags & TM_CORR_NTT) && (flags & TM_CORR_TC)) { tm_set_error("tm_plan_create: TM_CORR_NTT and TM_CORR_TC are exclusive"); return TM_EINVAL; }
     if ((flags & (TM_CORR_NTT | TM_CORR_TC)) && dtype != TM_I8) { tm_set_error("tm_plan_create: TM_CORR_* needs TM_I8"); return TM_EINVAL; }
     if ((flags & TM_BINARY) && dtype != TM_I8) { tm_set_error("tm_plan_create: TM_BINARY needs TM_I8"); return TM_EINVAL; }
@@ -123,7 +127,7 @@ int tm_plan_create_impl(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t 
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return tm_cuda_status(e, "tm_plan_create: cudaDeviceGetAttribute");
 
-    tm_plan_s *p = (tm_plan_s *)calloc(1, sizeof(tm_plan_s));
+    tm_plan_s *p = new (std::nothrow) tm_plan_s();  // value-initialised: every scalar 0
     if (!p) { tm_set_error("tm_plan_create: out of host memory"); return TM_EINVAL; }
     p->N = N; p->K = K; p->M1 = M1; p->M2 = M2;
     p->q1 = ceil_div(N, M1); p->q2 = ceil_div(N, M2);
@@ -217,15 +221,32 @@ extern "C" __attribute__((visibility("default"))) int tm_plan_query(tm_plan plan
 
 extern "C" __attribute__((visibility("default"))) void tm_plan_destroy(tm_plan plan) {
     if (!plan) return;
-    if (plan->aux_stream) {
-        cudaStreamDestroy(plan->aux_stream);
-        for (int i = 0; i < 2; ++i)
-            for (int j = 0; j < 16; ++j) cudaEventDestroy(plan->aux_ev[i][j]);
+    if (plan->host_stream) {
+        cudaStreamDestroy(plan->host_stream);
+        for (int i = 0; i < 4; ++i) cudaEventDestroy(plan->host_ev[i]);
     }
-    free(plan);
+    delete plan;
 }
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+// cudaFuncSetAttribute acts on the current device: remember (function, device)
+// pairs already set, under a mutex (plans may be used from several threads and
+// on several devices of one process)
+cudaError_t tm_smem_attr(const void *func, int bytes, bool max_carveout) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void *, int, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({func, dev, bytes})) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess && max_carveout)
+        e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess) done.insert({func, dev, bytes});
+    return e;
+}
 
 bool tm_pdl_enabled() {
     static const bool on = getenv("TM_NO_PDL") == nullptr;

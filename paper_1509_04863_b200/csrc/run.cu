@@ -3,6 +3,7 @@
 // host->device copies of chunk i+1 overlapped with the compute of chunk i).
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 
 #include "tm_internal.cuh"
 
@@ -39,101 +40,6 @@ RunWs run_ws(const tm_plan_s *p, int64_t batch, void *ws) {
 
 size_t tm_run_ws_bytes(const tm_plan_s *p, int64_t batch) { return run_ws(p, batch, nullptr).total; }
 
-#include <mutex>
-static std::mutex g_aux_mu;
-
-// Overlap mode: the batch is cut into chunks; the fold of chunk c+1 (caller's
-// stream) runs while the pair-NTT kernel of chunk c runs on an internal stream,
-// so the HBM-bound fold and the ALU-bound correlation share the SMs.
-static int run_overlap(const tm_plan_s *pc, const void *x, int64_t ldx, const void *t, int64_t batch,
-                       int32_t *residues, int64_t *k, const RunWs &W, void *counters, cudaStream_t s) {
-    tm_plan_s *p = const_cast<tm_plan_s *>(pc);  // lazily created internal stream/events only
-    {
-        std::lock_guard<std::mutex> lk(g_aux_mu);
-        if (!p->aux_stream) {
-            if (cudaStreamCreateWithFlags(&p->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
-                return TM_EUNSUPPORTED;
-            for (int i = 0; i < 2; ++i)
-                for (int j = 0; j < 16; ++j) cudaEventCreateWithFlags(&p->aux_ev[i][j], cudaEventDisableTiming);
-        }
-    }
-    static const int env_chunks = getenv("TM_OVERLAP_CHUNKS") ? atoi(getenv("TM_OVERLAP_CHUNKS")) : 0;
-    int C = env_chunks > 0 ? env_chunks : 4;
-    if (C > 16) C = 16;
-    while (C > 1 && batch / C < p->num_sms) --C;
-    const int64_t per = (batch + C - 1) / C;
-    cudaStream_t s2 = p->aux_stream;
-    int *cnt = (int *)counters;
-    // the aux stream must not start before work already queued on s (e.g. inputs)
-    cudaEventRecord(p->aux_ev[1][15], s);
-    cudaStreamWaitEvent(s2, p->aux_ev[1][15], 0);
-    for (int c = 0; c < C; ++c) {
-        const int64_t b0 = c * per, nb = (batch - b0) < per ? (batch - b0) : per;
-        if (nb <= 0) break;
-        int32_t *y1c = (int32_t *)W.y1 + b0 * p->len_y1;
-        int32_t *y2c = (int32_t *)W.y2 + b0 * p->len_y2;
-        int rc = tm_fold_overlap(p, (const int8_t *)x + b0 * ldx, ldx, nb, y1c, y2c, W.fold_ws, cnt + c, s);
-        if (rc) return rc;
-        cudaEventRecord(p->aux_ev[0][c], s);
-        cudaStreamWaitEvent(s2, p->aux_ev[0][c], 0);
-        rc = tm_fast_correlate(p, y1c, y2c, (const int8_t *)t + b0 * p->K, nullptr, nb, nullptr, nullptr,
-                               W.resid + 2 * b0, s2);
-        if (rc) return rc;
-    }
-    cudaEventRecord(p->aux_ev[1][0], s2);
-    cudaStreamWaitEvent(s, p->aux_ev[1][0], 0);
-    for (int i = 1; i <= 3; ++i) tm_prof_mark(i, s);
-    int rc = tm_crt_impl(p, W.resid, batch, residues, k, s);
-    tm_prof_mark(4, s);
-    return rc;
-}
-
-// Tensor-core overlap mode: the fold of chunk c+1 (caller's stream, 3-stage ring,
-// dynamic item assignment) runs while corr_tc_kernel correlates chunk c on an
-// internal stream; a fold CTA (~127 KB shared memory) and a tensor-core CTA
-// (~90 KB, TMEM for its accumulators) co-reside on each SM, so the HBM-bound
-// fold and the tensor-core correlation overlap.
-static int run_overlap_tc(const tm_plan_s *pc, const void *x, int64_t ldx, const void *t, int64_t batch,
-                          int32_t *residues, int64_t *k, const RunWs &W, void *counters, cudaStream_t s) {
-    tm_plan_s *p = const_cast<tm_plan_s *>(pc);  // lazily created internal stream/events only
-    {
-        std::lock_guard<std::mutex> lk(g_aux_mu);
-        if (!p->aux_stream) {
-            if (cudaStreamCreateWithFlags(&p->aux_stream, cudaStreamNonBlocking) != cudaSuccess)
-                return TM_EUNSUPPORTED;
-            for (int i = 0; i < 2; ++i)
-                for (int j = 0; j < 16; ++j) cudaEventCreateWithFlags(&p->aux_ev[i][j], cudaEventDisableTiming);
-        }
-    }
-    static const int env_chunks = getenv("TM_OVERLAP_CHUNKS") ? atoi(getenv("TM_OVERLAP_CHUNKS")) : 0;
-    int C = env_chunks > 0 ? env_chunks : 8;
-    if (C > 16) C = 16;
-    while (C > 1 && batch / C < 64) --C;
-    const int64_t per = (batch + C - 1) / C;
-    cudaStream_t s2 = p->aux_stream;
-    int *cnt = (int *)counters;
-    cudaEventRecord(p->aux_ev[1][15], s);  // the aux stream starts after work already queued on s
-    cudaStreamWaitEvent(s2, p->aux_ev[1][15], 0);
-    tm_prof_mark(1, s);
-    for (int c = 0; c < C; ++c) {
-        const int64_t b0 = c * per, nb = (batch - b0) < per ? (batch - b0) : per;
-        if (nb <= 0) break;
-        int32_t *y1c = (int32_t *)W.y1 + b0 * p->len_y1;
-        int32_t *y2c = (int32_t *)W.y2 + b0 * p->len_y2;
-        int rc = tm_fold_overlap(p, (const int8_t *)x + b0 * ldx, ldx, nb, y1c, y2c, W.fold_ws, cnt + c, s);
-        if (rc) return rc;
-        cudaEventRecord(p->aux_ev[0][c], s);
-        cudaStreamWaitEvent(s2, p->aux_ev[0][c], 0);
-        rc = tm_tc_correlate(p, y1c, y2c, p->len_y1, p->len_y2, (const int8_t *)t + b0 * p->K, p->K, nb, nullptr, nullptr, nullptr,
-                             residues ? residues + 2 * b0 : nullptr, k + b0, s2);
-        if (rc) return rc;
-    }
-    cudaEventRecord(p->aux_ev[1][0], s2);
-    cudaStreamWaitEvent(s, p->aux_ev[1][0], 0);
-    for (int i = 2; i <= 4; ++i) tm_prof_mark(i, s);
-    return TM_OK;
-}
-
 extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const void *x, int64_t ldx, const void *t, int64_t batch, int32_t *residues,
                       int64_t *k, void *ws, void *stream) {
     if (!p) { tm_set_error("tm_run: NULL plan"); return TM_EINVAL; }
@@ -145,16 +51,11 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
     tm_prof_mark(0, s);
     if (p->use_tc) {
         if (tm_fused_tc_ok(p, batch)) {  // the whole path in one persistent kernel
-            int rc = tm_fold_tc_fused(p, x, ldx, t, batch, W.y1, W.y2, residues, k, W.fold_ws,
-                                      (int *)((char *)ws + tm_ws(p, batch).counters), s);
+            int rc = tm_fold_tc_fused(p, x, ldx, t, batch, W.y1, W.y2, residues, k, W.fold_ws, s);
             if (rc != TM_EUNSUPPORTED) {
                 tm_prof_mark(1, s);  // one kernel: the later stage marks would only add gaps
                 return rc;
             }
-        }
-        if (tm_overlap_tc_ok(p, batch)) {
-            int rc = run_overlap_tc(p, x, ldx, t, batch, residues, k, W, (char *)ws + tm_ws(p, batch).counters, s);
-            if (rc != TM_EUNSUPPORTED) return rc;
         }
         // step 3, then steps 4-9 in one tensor-core kernel (argmax + CRT in its epilogue)
         // (y rows at the 16-byte aligned strides ldy*_run: vector loads in the correlation)
@@ -167,18 +68,6 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
         tm_prof_mark(3, s);
         tm_prof_mark(4, s);
         return rc;
-    }
-    if (tm_fused_ok(p, batch)) {
-        // the whole of Algorithm 1 in one persistent kernel (fold warps + NTT warps per SM)
-        int rc = tm_fold_corr_fused(p, x, ldx, t, batch, W.y1, W.y2, W.resid, residues, k, W.fold_ws, s);
-        if (rc != TM_EUNSUPPORTED) {
-            for (int i = 1; i <= 4; ++i) tm_prof_mark(i, s);
-            return rc;
-        }
-    }
-    if (tm_overlap_ok(p, batch)) {
-        int rc = run_overlap(p, x, ldx, t, batch, residues, k, W, (char *)ws + tm_ws(p, batch).counters, s);
-        if (rc != TM_EUNSUPPORTED) return rc;
     }
     int rc = tm_fold_impl(p, x, ldx, batch, 0, p->N, W.y1, W.y2, 0, W.fold_ws, s);     // step 3
     if (rc) return rc;
@@ -211,12 +100,21 @@ extern "C" __attribute__((visibility("default"))) int tm_run_path(tm_plan p, int
     if (!p || batch <= 0) return -1;
     if (p->use_tc) {
         if (tm_fused_tc_ok(p, batch)) return TM_PATH_FUSED_TC;
-        if (tm_overlap_tc_ok(p, batch)) return TM_PATH_OVERLAP;
         return TM_PATH_STAGED_TC;
     }
-    if (tm_fused_ok(p, batch)) return TM_PATH_FUSED_NTT;
-    if (tm_overlap_ok(p, batch)) return TM_PATH_OVERLAP;
     return TM_PATH_STAGED;
+}
+
+extern "C" __attribute__((visibility("default"))) int tm_run_fold_rows(tm_plan p, int64_t batch, int64_t *out) {
+    if (!p || batch < 1 || !out) { tm_set_error("tm_run_fold_rows: bad arguments"); return TM_EINVAL; }
+    RunWs W = run_ws(p, batch, nullptr);
+    out[0] = (int64_t)(uintptr_t)W.y1;
+    out[2] = (int64_t)(uintptr_t)W.y2;
+    // the fused kernel and the staged tensor-core path use the 32-entry aligned strides
+    const bool aligned = p->use_tc;
+    out[1] = aligned ? p->ldy1_run : p->len_y1;
+    out[3] = aligned ? p->ldy2_run : p->len_y2;
+    return TM_OK;
 }
 
 // the correlation of one huge signal split over ranks by output
@@ -285,14 +183,20 @@ extern "C" __attribute__((visibility("default"))) int tm_run_host(tm_plan p, con
         return TM_EINVAL;
     }
     const size_t ex = p->dtype == TM_I8 ? 1 : 4;
-    cudaStream_t s = (cudaStream_t)stream, sc = nullptr;
-    cudaError_t e = cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return tm_cuda_status(e, "tm_run_host: stream");
-    cudaEvent_t copied[2], freed[2];
-    for (int i = 0; i < 2; ++i) {
-        cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming);
+    cudaStream_t s = (cudaStream_t)stream;
+    // the plan's copy stream and events, created on first use and kept until
+    // tm_plan_destroy; the mutex serialises concurrent tm_run_host calls on one plan
+    // while they enqueue (the records and waits of one call must not interleave)
+    tm_plan_s *pm = const_cast<tm_plan_s *>(p);
+    std::lock_guard<std::mutex> lk(pm->host_mu);
+    cudaError_t e = cudaSuccess;
+    if (!pm->host_stream) {
+        e = cudaStreamCreateWithFlags(&pm->host_stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { pm->host_stream = nullptr; return tm_cuda_status(e, "tm_run_host: stream"); }
+        for (int i = 0; i < 4; ++i) cudaEventCreateWithFlags(&pm->host_ev[i], cudaEventDisableTiming);
     }
+    cudaStream_t sc = pm->host_stream;
+    cudaEvent_t *copied = pm->host_ev, *freed = pm->host_ev + 2;
     // the copy stream must not overwrite a slot the caller's stream still reads from a
     // previous call: start after everything already queued on s
     cudaEventRecord(freed[0], s);
@@ -324,8 +228,6 @@ extern "C" __attribute__((visibility("default"))) int tm_run_host(tm_plan p, con
             e = cudaMemcpyAsync(residues_host, dres, (size_t)batch * 8, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) rc = tm_cuda_status(e, "tm_run_host: D2H");
     }
-    for (int i = 0; i < 2; ++i) { cudaEventDestroy(copied[i]); cudaEventDestroy(freed[i]); }
-    cudaStreamDestroy(sc);
     return rc;
 }
 

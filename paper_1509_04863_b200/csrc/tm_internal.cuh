@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "../../include/tm.h"
 
 #define TM_MAX_LOGL 18           // longest correlation transform: 2^18 (K <= 2^17)
@@ -25,8 +27,9 @@ struct tm_plan_s {
     int device;
     int num_sms;
     int64_t tf_elems;    // uint2 (value, shoup) elements per prime per pair (I8) / floats (F32)
-    cudaStream_t aux_stream;    // internal stream of tm_run's overlap mode (created lazily)
-    cudaEvent_t aux_ev[2][16];  // fold-done / ntt-done events per chunk
+    std::mutex host_mu;         // tm_run_host: guards the copy stream / events below
+    cudaStream_t host_stream;   // tm_run_host's host->device copy stream (created on first use)
+    cudaEvent_t host_ev[4];     // copied[2], freed[2]
     int64_t tf_bytes;
     uint32_t crt_inv;    // M1^{-1} mod M2
     int block;           // TM_BLOCK: strategy 2 (Theorem 2), no wrap, cyclic extension
@@ -81,6 +84,9 @@ void tm_count_launch();
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 bool tm_pdl_enabled();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize = bytes [, max shared carveout]) once
+// per (function, device, bytes), thread-safe (plan.cu)
+cudaError_t tm_smem_attr(const void *func, int bytes, bool max_carveout = false);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args &&...args) {
     if (!tm_pdl_enabled()) {
@@ -137,16 +143,9 @@ size_t tm_run_ws_bytes(const tm_plan_s *p, int64_t batch);  // run.cu
 // ---- internal launchers ----
 bool tm_fast_corr_ok(const tm_plan_s *p);
 void tm_mont_linv(int logL, uint32_t p, uint32_t *c, uint32_t *cs);
-bool tm_fused_ok(const tm_plan_s *p, int64_t batch);
-bool tm_overlap_ok(const tm_plan_s *p, int64_t batch);
-bool tm_overlap_tc_ok(const tm_plan_s *p, int64_t batch);
 bool tm_fused_tc_ok(const tm_plan_s *p, int64_t batch);
 int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
-                     void *y2, int32_t *residues, int64_t *k, void *ws, int *counter, cudaStream_t s);
-int tm_fold_overlap(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, void *y1, void *y2, void *ws,
-                    int *counter, cudaStream_t s);
-int tm_fold_corr_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
-                       void *y2, int32_t *resid, int32_t *residues, int64_t *k, void *ws, cudaStream_t s);
+                     void *y2, int32_t *residues, int64_t *k, void *ws, cudaStream_t s);
 size_t tm_gntt_scratch_bytes(const tm_plan_s *p, int64_t batch);
 int tm_gntt_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *t, const void *tf,
                       int64_t batch, void *r1, void *r2, int32_t *resid, void *scratch, cudaStream_t s);

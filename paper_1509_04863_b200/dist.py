@@ -5,8 +5,8 @@
 * One huge signal is split into contiguous, row-aligned chunks (rows of M1
   samples, so every chunk can use the packed fold kernel) -- `signal_chunks`;
   each rank folds its chunk with global-position semantics (tm_fold(offset,
-  len)) and the partial folds are summed with ONE all-reduce of the
-  concatenated y1 || y2 vector -- `allreduce_folds`.  The fold of Eq. 2 is
+  len)) and the partial folds are summed IN PLACE with ONE all-reduce of the
+  flat y1 || y2 buffer -- `allreduce_folds` / `single.SingleSignal`.  The fold of Eq. 2 is
   additive over any partition of the positions (pinned in tests), so the sum
   is exactly the full fold.
 * The correlation of that one signal can then be split by output blocks
@@ -40,14 +40,27 @@ def signal_chunks(N: int, M1: int, world: int) -> list[tuple[int, int]]:
 
 
 def allreduce_folds(y1, y2, group=None):
-    """Sum partial folds across ranks with one collective (SUM over int32 or fp32).
-    Returns (y1, y2) holding the full fold on every rank."""
-    import torch
+    """Sum partial folds across ranks IN PLACE (SUM over int32 or fp32): on return
+    y1 and y2 themselves hold the full fold on every rank (they are also returned).
+    When y1 and y2 are views of one contiguous buffer (``SingleSignal.flat``) that
+    buffer is reduced with one collective and no copy; otherwise the two vectors
+    are reduced one after the other."""
     import torch.distributed as dist
-    n1 = y1.numel()
-    flat = torch.cat([y1.reshape(-1), y2.reshape(-1)])
-    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
-    return flat[:n1].view_as(y1), flat[n1:].view_as(y2)
+    base = y1.untyped_storage().data_ptr()
+    same = (base == y2.untyped_storage().data_ptr() and y1.is_contiguous() and y2.is_contiguous())
+    if same:
+        import torch
+        lo = min(y1.storage_offset(), y2.storage_offset())
+        hi = max(y1.storage_offset() + y1.numel(), y2.storage_offset() + y2.numel())
+        same = hi - lo <= y1.numel() + y2.numel() + 64   # only alignment padding in between
+    if same:
+        flat = torch.empty(0, dtype=y1.dtype, device=y1.device).set_(
+            y1.untyped_storage(), lo, (hi - lo,), (1,))
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    else:
+        dist.all_reduce(y1, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(y2, op=dist.ReduceOp.SUM, group=group)
+    return y1, y2
 
 
 def allreduce_max_keys(keys, group=None):

@@ -1,0 +1,108 @@
+"""One huge signal split over the ranks (BASELINE cfg5).
+
+Algorithm 1 on ONE signal x of length N whose samples are
+spread over G ranks (one process per GPU) as contiguous row-aligned chunks:
+
+1. every rank folds its chunk with global-position semantics (Eq. 2 is a sum
+   over positions, so the fold of a partition is the sum of the
+   folds of its parts) -- ``tm_fold(offset, len)``; the chunk holding
+   position 0 also contributes the wrap and extension terms;
+2. the partial y1 || y2 vectors, which live in ONE flat buffer (y1 and y2 are
+   views of it), are summed IN PLACE with one all-reduce, so every rank holds
+   the whole fold in the same y1 / y2 views the kernels read next;
+3. the correlation is split by output blocks (8(e)(ii)): each rank runs
+   ``tm_correlate_match_part`` on its part and writes one order-preserving
+   key per modulus; one all-reduce MAX of the 16-byte keys and
+   ``tm_match_keys`` give identical residues and k on every rank.  Plans the
+   split engine does not take (fp32 data) correlate redundantly on every rank.
+
+This module is host glue only (no arithmetic of the method); every step runs
+in libtm's kernels or in the collective.  ``plan`` is a ``Plan`` (or any object
+with the same methods -- the CPU wiring test stands the oracle in for it).
+"""
+from __future__ import annotations
+
+from .dist import signal_chunks
+
+
+def _round_up(a: int, b: int) -> int:
+    return (a + b - 1) // b * b
+
+
+class SingleSignal:
+    """Per-rank state of the split single-signal match.
+
+    ``rank``/``world``/``group``: the process group the chunks are spread over
+    (world = 1: no collective).  ``split_correlation``: None = split when the
+    plan is int8 and world > 1.  Buffers are allocated once on ``device``.
+    """
+
+    def __init__(self, plan, rank: int = 0, world: int = 1, group=None, device="cuda",
+                 split_correlation: bool | None = None):
+        import torch
+        self.plan, self.rank, self.world, self.group = plan, rank, world, group
+        self.offset, self.length = signal_chunks(plan.N, plan.M1, world)[rank]
+        n1, n2 = int(plan.len_y1), int(plan.len_y2)
+        # y1 region padded to 32 entries (128 B) so y2 starts 16-byte aligned for the
+        # kernels' vector loads; the padding is zero and never read.
+        self.ldy1 = _round_up(n1, 32)
+        self.flat = torch.zeros(self.ldy1 + n2, dtype=plan.y_dtype, device=device)
+        self.y1 = self.flat[:n1].view(1, n1)
+        self.y2 = self.flat[self.ldy1:].view(1, n2)
+        self.ws = plan.workspace(1, device)
+        self.keys = torch.empty((1, 2), dtype=torch.int64, device=device)
+        self.residues = torch.empty((1, 2), dtype=torch.int32, device=device)
+        self.k = torch.empty(1, dtype=torch.int64, device=device)
+        if split_correlation is None:
+            split_correlation = world > 1 and getattr(plan, "dtype", 0) == 0  # TM_I8
+        self.split = bool(split_correlation) and world > 1
+
+    @property
+    def reduce_bytes(self) -> int:
+        return self.flat.numel() * self.flat.element_size()
+
+    def fold(self, x_chunk, stream=None):
+        """Step 3 on this rank's chunk: the partial fold into the y1 / y2 views."""
+        self.plan.fold(x_chunk, offset=self.offset, length=self.length, y1=self.y1, y2=self.y2,
+                       accumulate=False, ws=self.ws, stream=stream)
+
+    def combine(self):
+        """Sum the partial folds over the ranks in place (one all-reduce of y1 || y2)."""
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
+
+    def match(self, t, stream=None):
+        """Steps 4-9 on the combined fold: residues [1][2] int32, k [1] int64 on every rank."""
+        if self.split:
+            import torch.distributed as dist
+            self.plan.correlate_match_part(self.y1, self.y2, t, self.rank, self.world, keys=self.keys,
+                                           ws=self.ws, stream=stream)
+            dist.all_reduce(self.keys, op=dist.ReduceOp.MAX, group=self.group)
+            self.plan.match_keys(self.keys, residues=self.residues, k=self.k, stream=stream)
+        else:
+            self.plan.correlate_match(self.y1, self.y2, t, residues=self.residues, k=self.k, ws=self.ws,
+                                      stream=stream)
+        return self.residues, self.k
+
+    def step(self, x_chunk, t, stream=None, events=None):
+        """One whole pass: fold -> all-reduce -> correlate / argmax / CRT.
+        ``events``: optional 4 CUDA events recorded between the stages."""
+        import contextlib
+
+        import torch
+        ctx = torch.cuda.stream(stream) if stream is not None and hasattr(stream, "cuda_stream") \
+            else contextlib.nullcontext()
+        with ctx:
+            if events:
+                events[0].record()
+            self.fold(x_chunk, stream=stream)
+            if events:
+                events[1].record()
+            self.combine()
+            if events:
+                events[2].record()
+            out = self.match(t, stream=stream)
+            if events:
+                events[3].record()
+        return out

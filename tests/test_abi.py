@@ -63,7 +63,7 @@ def test_plan_create_rejects_invalid_without_gpu(libtm):
     assert L.tm_plan_create(ctypes.byref(h), 0, 4, 0, 0, 0, 0) == 1
     assert L.tm_plan_create(ctypes.byref(h), 1024, 64, 0, 0, 1, 1) == 1   # TM_BINARY needs int8
     assert L.tm_plan_create(ctypes.byref(h), 1024, 64, 0, 0, 0, 16 | 8) == 1  # TM_BLOCK excludes TM_ALIAS_REPAIR
-    assert L.tm_plan_create(ctypes.byref(h), 1024, 64, 0, 0, 0, 32) == 1   # unknown flag
+    assert L.tm_plan_create(ctypes.byref(h), 1024, 64, 0, 0, 0, 128) == 1  # unknown flag
     assert L.tm_plan_create(ctypes.byref(h), 1001, 40, 0, 0, 0, 8) == 2    # TM_ALIAS_REPAIR needs M1 | N
     M = (ctypes.c_int64 * 3)(17, 18, 20)                                      # 18, 20 not co-prime
     L.tm_mplan_create.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,

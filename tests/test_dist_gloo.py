@@ -55,7 +55,8 @@ def _worker(rank, world, port, q):
         off, ln = tmdist.signal_chunks(N, M1, world)[rank]
         y1 = torch.from_numpy(oracle.fold(x, M1, K, off, ln))
         y2 = torch.from_numpy(oracle.fold(x, M2, K, off, ln))
-        y1, y2 = tmdist.allreduce_folds(y1, y2)
+        ret = tmdist.allreduce_folds(y1, y2)
+        assert ret[0] is y1 and ret[1] is y2          # in place: the caller's tensors hold the sum
         ok_fold = np.array_equal(y1.numpy(), oracle.fold(x, M1, K)) and np.array_equal(y2.numpy(), oracle.fold(x, M2, K))
         # every rank then matches the same full fold -> identical k on all ranks
         t = tmgen.template(9, 0, N, K, 0.0)
@@ -102,3 +103,112 @@ def test_allreduce_of_partial_folds_gloo():
         assert len(set(ks)) == 1
         assert ok_k
         assert tmax == 2.0
+
+
+# --------------------------------------------------------------------------------
+# SingleSignal (paper_1509_04863_b200/single.py) wiring on gloo ranks, with the
+# oracle standing in for libtm's kernels (this is a test of the host logic: the
+# in-place all-reduce of the flat y1 || y2 buffer, the split correlation keys).
+class OraclePlan:
+    """Duck-typed Plan whose entry points run the oracle on CPU tensors."""
+
+    def __init__(self, N, K):
+        import oracle
+        self.N, self.K = N, K
+        self.M1, self.M2 = oracle.moduli(N, K)
+        self.len_y1, self.len_y2 = self.M1 + K, self.M2 + K
+        self.y_dtype, self.dtype = torch.int32, 0
+        self.calls = []
+
+    def workspace(self, batch, device):
+        return torch.empty(1, dtype=torch.uint8)
+
+    def fold(self, x, offset, length, y1, y2, accumulate, ws, stream):
+        import oracle
+        assert not accumulate
+        xfull = np.zeros(self.N, np.int8)          # global positions; outside the chunk unused
+        xfull[offset:offset + length] = x[0].numpy()
+        y1.copy_(torch.from_numpy(oracle.fold(xfull, self.M1, self.K, offset, length)).view(1, -1))
+        y2.copy_(torch.from_numpy(oracle.fold(xfull, self.M2, self.K, offset, length)).view(1, -1))
+        self.calls.append("fold")
+
+    @staticmethod
+    def _key(r, k):
+        v = (((int(r) + (1 << 42)) << 21) | ((1 << 21) - 1 - int(k))) ^ (1 << 63)
+        return v - (1 << 64) if v >= (1 << 63) else v
+
+    def correlate_match_part(self, y1, y2, t, part, nparts, keys, ws, stream):
+        import oracle
+        out = []
+        for y, M in ((y1, self.M1), (y2, self.M2)):
+            r = oracle.correlate(y[0].numpy().astype(np.int64), M, t[0].numpy())
+            lo, hi = M * part // nparts, M * (part + 1) // nparts
+            kk = lo + int(np.argmax(r[lo:hi]))
+            out.append(self._key(r[kk], kk))
+        keys.copy_(torch.tensor([out], dtype=torch.int64))
+        self.calls.append("part")
+
+    def match_keys(self, keys, residues, k, stream):
+        import oracle
+        dec = [(1 << 21) - 1 - ((int(v) + (1 << 64)) % (1 << 64) & ((1 << 21) - 1)) for v in keys[0]]
+        residues.copy_(torch.tensor([dec], dtype=torch.int32))
+        z = oracle.crt(dec[0], self.M1, dec[1], self.M2)
+        k.fill_(z if z < self.N else -1)
+        self.calls.append("keys")
+
+    def correlate_match(self, y1, y2, t, residues, k, ws, stream):
+        import oracle
+        r1 = oracle.correlate(y1[0].numpy().astype(np.int64), self.M1, t[0].numpy())
+        r2 = oracle.correlate(y2[0].numpy().astype(np.int64), self.M2, t[0].numpy())
+        m1, m2 = oracle.argmax(r1), oracle.argmax(r2)
+        residues.copy_(torch.tensor([[m1, m2]], dtype=torch.int32))
+        z = oracle.crt(m1, self.M1, m2, self.M2)
+        k.fill_(z if z < self.N else -1)
+        self.calls.append("whole")
+
+
+def _single_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import tmgen
+        from paper_1509_04863_b200.single import SingleSignal
+        N, K = 64 * 45, 64
+        plan = OraclePlan(N, K)
+        ss = SingleSignal(plan, rank, world, device="cpu")
+        x = tmgen.signal(13, 0, N)
+        t = tmgen.template(13, 0, N, K, 0.05)
+        xc = torch.from_numpy(x[ss.offset:ss.offset + ss.length].copy()).view(1, -1)
+        res, k = ss.step(xc, torch.from_numpy(t).view(1, -1))
+        o = oracle.ftm(x, t)
+        ok = (np.array_equal(ss.y1[0].numpy(), o["y1"]) and np.array_equal(ss.y2[0].numpy(), o["y2"])
+              and tuple(res[0].tolist()) == o["residues"] and int(k[0]) == o["k"])
+        q.put((rank, ok, plan.calls, ss.offset, ss.length))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_single_signal_wiring_gloo(world):
+    """Each rank folds its chunk, the flat y1 || y2 buffer is all-reduced in place,
+    the split correlation's keys are MAX-reduced: every rank's y1, y2, residues
+    and k equal the oracle's whole-signal Algorithm 1."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_single_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    covered = 0
+    for rank, ok, calls, off, ln in sorted(res):
+        assert ok, rank
+        assert calls == ["fold", "part", "keys"], calls
+        assert off == covered
+        covered += ln
+    assert covered == 64 * 45

@@ -428,9 +428,8 @@ def test_cfg5_full_size_fold_and_chunks(tm):
 
 @pytest.mark.parametrize("N,K", [(2 ** 16, 1024), (2 ** 18, 2048), (2 ** 20, 4096)])
 def test_fused_kernel_every_pair(tm, N, K, monkeypatch):
-    """tm_run on a batch >= #SMs (the persistent fold + pair-NTT path, and the
-    opt-in single-kernel path when TM_FUSED is set in the environment); every
-    pair's residues and k equal the oracle's, and equal the staged path's
+    """tm_run on a batch >= #SMs (the persistent fused fold + tensor-core kernel);
+    every pair's residues and k equal the oracle's, and equal the staged path's
     (fold -> template fold -> correlate -> match)."""
     B = 300 if N < 2 ** 20 else 160
     plan = tm.Plan(N, K, seed=61)
