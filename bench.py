@@ -42,6 +42,11 @@ WORKLOADS = {
                   desc="cfg4: N=2^24, K=8192, batch 64, +-1 int8, 20% flips"),
     "cfg4": dict(N=2 ** 24, K=16384, B=64, dtype="int8", noise=0.2, seed=4,
                  desc="cfg4: N=2^24, K=16384, batch 64, +-1 int8, 20% flips"),
+    # SURVEY 8(d) companions of the cfg4 K sweep (the K^2/log K transition)
+    "cfg4c": dict(N=2 ** 24, K=32768, B=64, dtype="int8", noise=0.2, seed=4,
+                  desc="cfg4 companion: N=2^24, K=32768, batch 64, +-1 int8, 20% flips"),
+    "cfg4d": dict(N=2 ** 24, K=65536, B=64, dtype="int8", noise=0.2, seed=4,
+                  desc="cfg4 companion: N=2^24, K=65536, batch 64, +-1 int8, 20% flips"),
     # one signal split into contiguous row-aligned chunks over the ranks (strong scaling)
     "cfg5": dict(N=2 ** 31, K=65536, B=1, dtype="int8", noise=0.05, seed=5, single=True,
                  desc="cfg5: one signal N=2^31 (+-1 int8, 2 GiB), K=65536, 5% flips, split over the GPUs; "

@@ -54,6 +54,8 @@ def lib():
         for n in ("or_correlate_i64", "or_correlate_f64"):
             getattr(L, n).restype = None
             getattr(L, n).argtypes = [_p, _i64, _i64, _p, _p]
+        L.or_correlate_at_i64.restype = None
+        L.or_correlate_at_i64.argtypes = [_p, _i64, _p, _p, _i64, _p]
         for n in ("or_argmax_i64", "or_argmax_f64"):
             getattr(L, n).restype = _i64
             getattr(L, n).argtypes = [_p, _i64]
@@ -178,6 +180,18 @@ def correlate(y: np.ndarray, M: int, t: np.ndarray) -> np.ndarray:
             y = np.concatenate([y, np.zeros(M + K - y.shape[0], np.float64)])
         r = np.zeros(M, np.float64)
         lib().or_correlate_f64(_ptr(y), M, K, _ptr(t), _ptr(r))
+    return r
+
+
+def correlate_at(y: np.ndarray, t: np.ndarray, ks) -> np.ndarray:
+    """r[k] = sum_{i<K} t[i] y[k+i] at the selected outputs ks only (int8 t, int64 y)."""
+    t = _as_input(t)
+    assert _is_int(t)
+    y = np.ascontiguousarray(y, np.int64)
+    ks = np.ascontiguousarray(np.asarray(ks, np.int64))
+    assert ks.size == 0 or (ks.min() >= 0 and ks.max() + t.shape[0] <= y.shape[0])
+    r = np.zeros(ks.shape[0], np.int64)
+    lib().or_correlate_at_i64(_ptr(y), t.shape[0], _ptr(t), _ptr(ks), ks.shape[0], _ptr(r))
     return r
 
 

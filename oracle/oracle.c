@@ -117,6 +117,18 @@ void or_correlate_i64(const int64_t *y, int64_t M, int64_t K,
     }
 }
 
+/* Selected entries of O3, one output at a time: r_k for k = ks[0..nk) with the
+ * same formula and order as or_correlate_i64 (sampled checks where the whole
+ * correlation is too slow for the oracle: K = 2^18, 2^19 at N = 2^31). */
+void or_correlate_at_i64(const int64_t *y, int64_t K, const int8_t *t,
+                         const int64_t *ks, int64_t nk, int64_t *r) {
+    for (int64_t j = 0; j < nk; ++j) {
+        int64_t s = 0;
+        for (int64_t i = 0; i < K; ++i) s += (int64_t)t[i] * y[ks[j] + i];
+        r[j] = s;
+    }
+}
+
 void or_correlate_f64(const double *y, int64_t M, int64_t K,
                       const float *t, double *r) {
     for (int64_t k = 0; k < M; ++k) {

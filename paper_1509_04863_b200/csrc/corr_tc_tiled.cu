@@ -487,7 +487,9 @@ void tm_tc_tiled_plan(tm_plan_s *p) {
     const int lmax = ybound <= 127 ? 1 : ybound <= 2047 ? 2 : ybound <= 32767 ? 3 : ybound <= 524287 ? 4 : 0;
     if (!lmax) return;
     if ((double)p->K * xmax * ybound >= (double)((int64_t)1 << 41)) return;  // packed key range
-    if (p->K > ((int64_t)1 << 17)) return;                                  // per-limb |r| < 2^31
+    // per-limb partial sums accumulate in int32 TMEM: |t| * |limb| <= tmax * 128 (the
+    // signed top limb, or y itself when one limb holds it) over K terms
+    if ((double)p->K * xmax * 128.0 >= (double)((int64_t)1 << 31)) return;
     if (p->M2 >= ((int64_t)1 << KEY_SHIFT)) return;
     p->tct_lmax = lmax;
     p->tct_ok = 1;

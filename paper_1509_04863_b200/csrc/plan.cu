@@ -116,10 +116,9 @@ int tm_plan_create_impl(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t 
     const bool cyc1 = (N % M1 == 0) && ((M1 & (M1 - 1)) == 0);
     int64_t L1 = cyc1 ? M1 : int64_t(1) << ilog2_ceil(M1 + K - 1);
     int64_t L2 = int64_t(1) << ilog2_ceil(M2 + K - 1);
-    if (ilog2_ceil(M2 + K - 1) > TM_MAX_LOGL) {
-        tm_set_error("tm_plan_create: correlation length %lld exceeds this build's 2^%d", (long long)L2, TM_MAX_LOGL);
-        return TM_EUNSUPPORTED;
-    }
+    // the NTT engine's root tables stop at 2^TM_MAX_LOGL; longer correlations
+    // (K > 2^17) run on the tiled tensor-core engine (int8) or the direct fp32 kernel
+    const bool ntt_len_ok = ilog2_ceil(M2 + K - 1) <= TM_MAX_LOGL;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return tm_cuda_status(e, "tm_plan_create: cudaGetDevice");
@@ -152,8 +151,8 @@ int tm_plan_create_impl(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t 
         double tmax = (flags & TM_BINARY) ? 1.0 : 128.0;
         double bound = (double)K * tmax * (double)(p->q1 > p->q2 ? p->q1 : p->q2) * tmax;
         p->n_primes = (bound < (double)(TM_PRIMES[0] / 2) - 1.0) ? 1 : 2;
-        p->fast_corr = tm_fast_corr_ok(p);
-        p->big_corr = !p->fast_corr && p->logL2 > 14;
+        p->fast_corr = ntt_len_ok && tm_fast_corr_ok(p);
+        p->big_corr = ntt_len_ok && !p->fast_corr && p->logL2 > 14;
         if (p->big_corr) {   // u32 natural bit-reversed spectra at L2 (first L1 serve y1)
             p->tf_elems = L2;
             p->tf_bytes = L2 * p->n_primes * 4;
@@ -167,7 +166,7 @@ int tm_plan_create_impl(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t 
         }
         tm_ntt_tables t;
         int rc = tm_ntt_tables_get(dev, &t);
-        if (rc != TM_OK) { free(p); return rc; }
+        if (rc != TM_OK) { delete p; return rc; }
         // correlation engine: tensor cores when eligible (TM_CORR=ntt in the
         // environment forces the NTT for A/B measurements of the default)
         tm_tc_plan(p);
@@ -176,13 +175,20 @@ int tm_plan_create_impl(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t 
         const bool env_ntt = env && strcmp(env, "ntt") == 0;
         if (flags & TM_CORR_TC) {
             if (!p->tc_ok && !p->tct_ok) {
-                free(p);
+                delete p;
                 tm_set_error("tm_plan_create: TM_CORR_TC: plan not eligible for the tensor-core engine");
                 return TM_EUNSUPPORTED;
             }
             p->use_tc = 1;
         } else {
             p->use_tc = (p->tc_ok || p->tct_ok) && !(flags & TM_CORR_NTT) && !env_ntt;
+        }
+        if (!ntt_len_ok && !p->use_tc) {
+            delete p;
+            tm_set_error("tm_plan_create: correlation length 2^%d exceeds the NTT engine's 2^%d and the plan is not "
+                         "eligible for the tiled tensor-core engine (int8 data, |y| <= 524287, M2 < 2^21)",
+                         ilog2_ceil(M2 + K - 1), TM_MAX_LOGL);
+            return TM_EUNSUPPORTED;
         }
         if (p->use_tc) {  // the folded template is the int8 template itself, 16-byte rows
             p->tf_bytes = (K + 15) / 16 * 16;

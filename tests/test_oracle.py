@@ -137,6 +137,22 @@ def test_full_corr_matches_dense_T():
         np.testing.assert_array_equal(oracle.full_corr(x, t), brute_scores(x, t))
 
 
+def test_correlate_at_matches_dense_band():
+    """Selected outputs (or_correlate_at_i64) against a dense numpy Hankel-band
+    matrix T[k, k:k+K] = t (reading C3)."""
+    rng = np.random.default_rng(44)
+    for _ in range(30):
+        K = int(rng.integers(1, 40))
+        M = int(rng.integers(K, 90))
+        y = rng.integers(-500, 500, M + K).astype(np.int64)
+        t = rng.integers(-128, 128, K).astype(np.int8)
+        T = np.zeros((M, M + K), np.int64)
+        for k in range(M):
+            T[k, k:k + K] = t
+        ks = rng.integers(0, M, 12)
+        np.testing.assert_array_equal(oracle.correlate_at(y, t, ks), (T @ y)[ks])
+
+
 def test_correlation_commutation_identity_eq4():
     """Eq. (4), i.e. Thm 1 under strategy 1:
     r[k] = sum_{i<ceil(N/M)} (Tx)[(k+iM) mod N] for every k < M, with (Tx)
