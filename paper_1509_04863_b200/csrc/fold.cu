@@ -127,13 +127,18 @@ __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t
 
 // Work split for the persistent TMA kernel (one CTA per SM): the fewest row
 // chunks per (pair, column group) whose item count spreads over the SMs with
-// < 5% imbalance (items are equal-sized), rows per item in [128, 1024].
+// < 5% imbalance (items are equal-sized), rows per item in [128, TM_FOLD_RMAX]
+// (the per-warp anti-diagonal arrays grow with the rows per item: a smaller
+// bound leaves shared memory for more ring stages, TM_FOLD_NST).
+#ifndef TM_FOLD_RMAX
+#define TM_FOLD_RMAX 1024
+#endif
 void pick_rows_tma(const tm_plan_s *p, int64_t batch, int64_t rows, int64_t n_groups, int64_t *R_out,
                    int64_t *nrc_out) {
     const int64_t slots = p->num_sms;
     int64_t bestR = 0, bestN = 0;
     double best_eff = -1.0;
-    for (int64_t n = (rows + 1023) / 1024; n <= rows; ++n) {
+    for (int64_t n = (rows + TM_FOLD_RMAX - 1) / TM_FOLD_RMAX; n <= rows; ++n) {
         const int64_t R = ((rows + n - 1) / n + 15) / 16 * 16;
         const int64_t nrc = (rows + R - 1) / R;
         if (nrc != n && n > 1) continue;

@@ -42,7 +42,7 @@ def test_plan_beyond_ntt_tables(tm):
     cores; general int8 data at that K (|r| per limb beyond int32) and fp32 have
     their own engines or are rejected with TM_EUNSUPPORTED, never a wrong result."""
     p = tm.Plan(2 ** 31, 2 ** 18)
-    assert p.corr_engine == 1 and p.L2 == 2 ** 20
+    assert p.corr_engine == 1 and p.L2 == 2 ** 19   # > 2^18: beyond the NTT tables
     with pytest.raises(tm.TMError):
         tm.Plan(2 ** 25, 2 ** 18, binary=False)
     with pytest.raises(tm.TMError):
