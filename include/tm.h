@@ -298,6 +298,12 @@ int tm_run_fold_rows(tm_plan plan, int64_t batch, int64_t *out);
  * aligned device memory) on stream, for timing a live read-only bandwidth
  * ceiling with events (bench.py).  Not part of the method. */
 int tm_probe_read_bw(const void *buf, int64_t bytes, void *stream);
+/* tm_probe_read_pattern: the same streaming pass with the fold's access pattern
+ * over a row-major [rows][ldx] byte matrix: items of (column group of `width`
+ * bytes, R rows), column groups fastest (order 0) or row chunks fastest (1),
+ * 32 KB / width rows per stage, `grid` CTAs (0: one per SM).  Instrumentation. */
+int tm_probe_read_pattern(const void *buf, int64_t ldx, int width, int64_t rows, int64_t R, int order, int grid,
+                          void *stream);
 
 /*
  * ---- One huge signal over several GPUs: the correlation split by outputs ----
