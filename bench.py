@@ -47,6 +47,9 @@ WORKLOADS = {
                   desc="cfg4 companion: N=2^24, K=32768, batch 64, +-1 int8, 20% flips"),
     "cfg4d": dict(N=2 ** 24, K=65536, B=64, dtype="int8", noise=0.2, seed=4,
                   desc="cfg4 companion: N=2^24, K=65536, batch 64, +-1 int8, 20% flips"),
+    # PAPER.md Table 2's shape through the fp32 path (four-step FFT, L2 = 2^17)
+    "t2": dict(N=2 ** 26, K=65536, B=8, dtype="float32", noise=0.5, seed=26,
+               desc="Table 2 shape: N=2^26, K=2^16, batch 8, fp32 N(0,1), template noise sigma 0.5"),
     # one signal split into contiguous row-aligned chunks over the ranks (strong scaling)
     "cfg5": dict(N=2 ** 31, K=65536, B=1, dtype="int8", noise=0.05, seed=5, single=True,
                  desc="cfg5: one signal N=2^31 (+-1 int8, 2 GiB), K=65536, 5% flips, split over the GPUs; "

@@ -326,6 +326,26 @@ int tm_correlate_match_part(tm_plan plan, const void *y1, const void *y2, const 
 int tm_match_keys(tm_plan plan, const int64_t *keys, int64_t batch, int32_t *residues, int64_t *k, void *stream);
 
 /*
+ * tm_fold_reduce -- the cross-GPU combine of SURVEY.md 8(f) f4(iii), fused into
+ * the fold's epilogue.  Eq. 2 is a sum over positions, so the fold of
+ * one signal is the sum of the folds of its chunks; this call folds the chunk
+ * [offset, offset + len) of each pair exactly as tm_fold does, but instead of
+ * storing y1, y2 it ADDS them (int32, exact, order-free) into ndst destination
+ * folds at once: dst_y1[d] int32 [batch][len_y1], dst_y2[d] int32 [batch][len_y2]
+ * (host arrays of device pointers; peer-mapped memory of other GPUs, e.g. torch
+ * symmetric-memory buffers, with red.global.add), or, with multicast != 0, ONE
+ * NVLS multicast address each (ndst == 1; multimem.red.add: the switch adds into
+ * the copy on every GPU bound to the multicast object).  The destinations must
+ * hold zero (or other chunks' contributions) beforehand; the caller orders the
+ * ranks around the call (barrier before: destinations zeroed; after: every
+ * chunk added).  TM_I8 plans on the packed fold only (TM_BINARY, M1 | N, M1 a
+ * multiple of 512, row-aligned 16-byte aligned chunks), 1 <= ndst <= 8;
+ * otherwise TM_EINVAL / TM_EUNSUPPORTED before any launch.  ws: tm_workspace_bytes.
+ */
+int tm_fold_reduce(tm_plan plan, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len, int ndst,
+                   void *const *dst_y1, void *const *dst_y2, int multicast, void *ws, void *stream);
+
+/*
  * ---- More than two moduli: Theorem 4 with alpha moduli ----
  * "Any integer m is uniquely specified mod N by its remainders modulo alpha
  * relatively prime integers M_1 .. M_alpha as long as prod M_i >= N" (read as

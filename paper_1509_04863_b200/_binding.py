@@ -23,7 +23,7 @@ EXPORTED_SYMBOLS = (
     "tm_status_string", "tm_last_error", "tm_launch_count", "tm_profile_events", "tm_run_path",
     "tm_correlate_match_part", "tm_match_keys",
     "tm_mplan_create", "tm_mplan_workspace_bytes", "tm_mplan_run", "tm_crt_multi", "tm_mplan_destroy",
-    "tm_run_fold_rows", "tm_probe_read_bw",
+    "tm_run_fold_rows", "tm_probe_read_bw", "tm_probe_read_pattern", "tm_fold_reduce",
 )
 RUN_PATHS = {0: "staged (fold -> NTT/fp32 correlation -> CRT)", 1: "staged (fold -> tensor-core correlation)",
              2: "fused (fold + tensor-core correlation in one kernel)"}
@@ -116,6 +116,10 @@ def lib():
         L.tm_mplan_destroy.argtypes = [_p]
         L.tm_run_fold_rows.restype = ctypes.c_int
         L.tm_run_fold_rows.argtypes = [_p, _i64, ctypes.POINTER(_i64)]
+        L.tm_fold_reduce.restype = ctypes.c_int
+        L.tm_fold_reduce.argtypes = [_p, _p, _i64, _i64, _i64, _i64, ctypes.c_int, _p, _p, ctypes.c_int, _p, _p]
+        L.tm_probe_read_pattern.restype = ctypes.c_int
+        L.tm_probe_read_pattern.argtypes = [_p, _i64, ctypes.c_int, _i64, _i64, ctypes.c_int, ctypes.c_int, _p]
         L.tm_probe_read_bw.restype = ctypes.c_int
         L.tm_probe_read_bw.argtypes = [_p, _i64, _p]
         L.tm_status_string.restype = ctypes.c_char_p
@@ -277,6 +281,24 @@ class Plan:
         _check(lib().tm_fold(self._h, _ptr(x), _ld(x), batch, offset, length, _ptr(y1), _ptr(y2),
                              int(accumulate), _ptr(ws), _stream(stream)), "tm_fold")
         return y1, y2
+
+    def fold_reduce(self, x, dst_y1, dst_y2, offset: int = 0, length: int | None = None, multicast: bool = False,
+                    ws=None, stream=None):
+        """tm_fold_reduce: ADD this chunk's fold into every destination (lists of
+        device pointers (ints) or tensors: peer-mapped buffers, or one multicast
+        address each with multicast=True)."""
+        batch = x.shape[0]
+        length = x.shape[1] if length is None else length
+        d1 = [v if isinstance(v, int) else v.data_ptr() for v in dst_y1]
+        d2 = [v if isinstance(v, int) else v.data_ptr() for v in dst_y2]
+        if len(d1) != len(d2):
+            raise ValueError("dst_y1 and dst_y2 need the same length")
+        a1 = (_p * len(d1))(*d1)
+        a2 = (_p * len(d2))(*d2)
+        if ws is None:
+            ws = self._tmp_ws(batch, x.device, stream)
+        _check(lib().tm_fold_reduce(self._h, _ptr(x), _ld(x), batch, offset, length, len(d1), a1, a2, int(multicast),
+                                    _ptr(ws), _stream(stream)), "tm_fold_reduce")
 
     def fold_template(self, t, tf=None, stream=None):
         import torch

@@ -1,23 +1,45 @@
-// corr_tc_tiled.cu -- the tensor-core correlation (corr_tc.cu, tc_core.cuh)
-// split over many CTAs per pair, for long templates and small batches (cfg4:
-// 64 pairs at K = 16384; cfg5: one pair at K = 65536) where one CTA per pair
-// would leave most SMs idle or not fit in shared memory.
+// corr_tc_tiled.cu -- the tensor-core correlation (Algorithm 1 steps 4-9,
+// PAPER.md P:98-106 read as P:61, reading C3; the P = 128 Toeplitz blocking of
+// corr_tc.cu) split over many CTAs per pair, for long templates and small
+// batches (cfg4: 64 pairs at K = 16384; cfg5: one pair at K = 65536; K up to
+// 2^20) where one CTA per pair would leave most SMs idle or not fit.
 //
-// CTA (pair b, output tile [a0, a0 + NT) blocks, template range [cb, ce)):
-//   D[b'][2 (a - a0) + j] = sum_{c in [cb, ce)} A_c B_c   (P = 128 blocking of
-//   corr_tc.cu), accumulated in TMEM over chunks of <= CCH template blocks;
-//   per chunk the CTA stages the template slice, builds A (16 byte-shifted
-//   copies), and stages the B window = y_j blocks [a0 + c0, a0 + NT + c1 - 1)
-//   once per 4-bit limb (the limb count comes from a scan of the CTA's whole
-//   y window, so every chunk uses the same decomposition).
-// Epilogue: with one template range per pair, the tile's lowest-index maximum
-// per modulus goes to an atomicMax on a packed key (r + 2^42) << 21 | (2^21 -
-// 1 - k) (max r, ties to the lowest k); with several ranges the tile's partial
-// r are added (int64 atomics, exact) into r, and the CTA that completes a
-// tile's last range reduces the tile's final r to the same packed key.
-// tc_tiled_leftover computes the <= 8 outputs k in [128 NA_j, M_j) per
-// modulus (dot products split over K-slices), and tc_tiled_final combines keys
-// and leftovers per pair and does steps 8-9 (tm_resolve).
+// Three kernels, chained with programmatic dependent launch:
+//
+//  tiled_prep  (one pass over y and t, whole GPU)
+//    * B operand planes: every 16-entry piece of y_j is written once per
+//      "plane" in exactly the shared-memory image the MMA reads (chunk column
+//      h, row 2 s + j, 16 bytes), so a CTA's B window is 8 bulk copies:
+//        plane 0          y itself as int8       (pairs whose |y| <= 127)
+//        plane 1 + l      (y >> 4l) & 15         (l = 0 .. lmax-2: low limbs)
+//        plane lmax-1+l   y >> 4l  (signed)      (l = 1 .. lmax-1: top limb of
+//                                                  an (l+1)-limb split)
+//      so y = sum_l 16^l v_l with any limb count nl <= lmax reads planes
+//      {0} (nl = 1) or {1 .. nl-1, lmax + nl - 2}, exact and int8-valued;
+//    * the limbs each 128-entry block needs (max over both moduli), so a CTA
+//      uses the fewest limbs its own window allows;
+//    * the template's A image S[J][s][e] = t(16 J + s + e - 127) (its 16
+//      byte-shifted copies; corr_tc.cu), so an A chunk is ONE bulk copy;
+//    * the partial dot products of the <= 8 leftover outputs k in
+//      [128 NA_j, M_j) per modulus, per prep CTA (no atomics);
+//    * zeroes the keys, tile counters and (several template ranges) the
+//      int64 partial sums the main kernel accumulates into.
+//  corr_tc_tiled  CTA (pair b, output tile [a0, a0 + NT) blocks, template
+//    range [cb, ce)): warp 9 streams (chunk of <= TCCH template blocks, limb)
+//    passes into two A and two B buffers with cp.async.bulk (mbarrier
+//    transaction counts); warp 8 issues the MMAs of a pass as soon as its
+//    bytes have landed and commits them to the buffer's "done" mbarrier,
+//    which frees it for the pass after next; warps 0-7 only run the
+//    epilogue (TMEM -> registers, limbs combined, lowest-index max).  With one
+//    template range per pair the tile's max goes to an atomicMax on a packed
+//    key (r + 2^42) << 21 | (2^21 - 1 - k); with several, each CTA stores its
+//    partial r (int64, plain coalesced stores) and
+//  tiled_reduce  sums the ranges' partials per output in a fixed order (exact),
+//    takes the lowest-index max per pair and modulus (packed-key atomicMax).
+//  tc_tiled_final  per pair: keys + leftovers -> residues -> steps 8-9.
+// NT (output blocks per tile) is 32 or 64: the shared-memory-operand MMA costs
+// ~(4096 + 32 N) / 128 cycles (A read once per MMA, corr_tc.cu), so N = 2 NT =
+// 128 does twice the work of N = 64 in ~1.3x the time.
 #include <algorithm>
 
 #include "tc_core.cuh"
@@ -25,97 +47,203 @@
 namespace {
 using namespace tc;
 
-constexpr int NT_MIN = 32;  // output blocks per tile: NT in {32, 64} (MMA N = 2 NT)
-constexpr int TCCH = 16;  // template blocks per A chunk
+constexpr int TCCH = 16;    // template blocks per A chunk
 constexpr int KEY_SHIFT = 21;
 constexpr int64_t KEY_BIAS = (int64_t)1 << 42;
+constexpr int TNTHR = NTHR + 64;   // 8 epilogue warps, MMA issuer (warp 8), TMA producer (warp 9)
+constexpr int PREP_T = 256;
+constexpr int PREP_MAXCTA = 256;   // prep CTAs per pair (bound for the leftover partials)
 
 struct TiledArgs {
-    TcArgs a;              // y, t, K, M, NA, crt constants (NMC, R, NC unused except NC)
+    TcArgs a;              // y, t, K, M, NA, NC, crt constants
     int n_at, n_cr, CR;    // tiles over output blocks, template ranges, blocks per range
     int at0, n_atp;        // this launch's tiles [at0, at0 + n_atp) (a part of a split correlation)
-    int lmax;
-    unsigned long long *keys;  // [batch][2] (n_cr == 1), zeroed
-    int64_t *racc[2];          // [batch][Mj] partial sums (n_cr > 1), zeroed; or r outputs
-    int write_r;               // n_cr == 1: store r values (staged tm_correlate)
-    unsigned *tile_cnt;        // [batch][n_at] template ranges finished per tile (n_cr > 1), zeroed
-    int64_t *lsum;             // [batch][2 MAXLEFT] leftover dot products, zeroed
+    int lmax, np;          // limb bound of the plan, planes per pair (2 lmax - 1)
+    int64_t S;             // blocks per plane (rows 2 S)
+    int JT;                // A-image rows (J) per pair
+    int n_pcta;            // prep CTAs per pair
+    uint8_t *planes;       // [batch][np][8][2 S][16]
+    uint8_t *aimg;         // [batch][JT][256]
+    uint8_t *bmag;         // [batch][S] limbs block s needs
+    int NT;                    // output blocks per tile
+    unsigned long long *keys;  // [batch][2] packed (max r, lowest k) per modulus
+    void *part;                // [batch][n_cr][M1 + M2] partial r of each template range (n_cr > 1):
+    int part32;                // int32 when every partial provably fits (plan bound), else int64
+    int64_t *r_out[2];         // [batch][Mj] r outputs (staged tm_correlate) or NULL
+    int64_t *lpart;            // [batch][n_pcta][2 MAXLEFT] leftover partial dot products
 };
 
 __device__ __forceinline__ unsigned long long pack_key(int64_t r, int64_t k) {
     return ((unsigned long long)(r + KEY_BIAS) << KEY_SHIFT) | (unsigned long long)(((int64_t)1 << KEY_SHIFT) - 1 - k);
 }
 
-// smem: A [2][256 * (8 (TCCH-1) + 15)] | B [2][8 * 2 (NT + TCCH - 1) * 16] | tp slice | misc.
-// Passes (chunk, limb) alternate between the two A and B buffers, so the
-// staging of pass p + 1 overlaps the MMAs of pass p (mbarrier mdone[p & 1]).
-// An SS MMA costs ~(4096 + 32 N) / 128 cycles (shared-memory operand reads), so
-// N = 128 (NT = 64) does twice the work of N = 64 in 1.33x the time.
-constexpr int A_BYTES = (256 * (8 * (TCCH - 1) + 15) + 127) / 128 * 128;
-template <int NT>
-constexpr int b_bytes() { return (8 * (2 * (NT + TCCH - 1) * 16 + 16) + 127) / 128 * 128; }
-// B chunk-column stride: 32 nrows + 16 bytes, an odd multiple of 16 modulo 128, so
-// the 8 chunk columns a warp's store touches fall in distinct bank quads
-__device__ __forceinline__ uint32_t b_lbo(int nrows) { return 32u * nrows + 16u; }
-constexpr int TP_BYTES = 128 * TCCH + 256;
-template <int NT>
-constexpr int smem_bytes() { return 2 * A_BYTES + 2 * b_bytes<NT>() + TP_BYTES + 64; }
+__host__ __device__ __forceinline__ int nleft_of(int64_t M, int NA) {
+    const int64_t n = M - (int64_t)P * NA;
+    return n > 0 ? (int)n : 0;
+}
 
-// Warp roles: warps 0-7 stage (limb scan, template slices, A copies, B windows,
-// epilogue); warp 8 only issues the MMAs, so that staging pass p + 1 overlaps
-// the tensor core working on pass p (with one warp doing both, the issue loop
-// blocks on the tensor core's queue and staging and MMAs serialise).
-// Named barriers: 1 + (p & 1) "pass p staged" (256 arrive, issuer syncs), 3 the
-// 256 staging threads.
-constexpr int TNTHR = NTHR + 32;
-__device__ __forceinline__ void stagers_sync() { asm volatile("bar.sync 3, %0;" ::"n"(NTHR) : "memory"); }
+__device__ __forceinline__ int limbs_needed(int32_t v) {
+    const uint32_t m = (uint32_t)(v ^ (v >> 31));  // |v| or |v| - 1: fits b + 1 signed bits iff m < 2^b
+    return m <= 127u ? 1 : m <= 2047u ? 2 : m <= 32767u ? 3 : m <= 524287u ? 4 : 5;
+}
 
-// Stage limb l of the B window (y_1 and y_2 blocks s_begin + [0, nrows)) with
-// both moduli's rows in one batch of loads: row r = 2 s + j, warp w takes rows
-// w + 8 u, RB rows in flight per warp (one L2 round trip per pass at NT = 32;
-// the one-CTA kernel's stage_yw walks the moduli one after the other).
-template <int RB>
-__device__ __forceinline__ void stage_window(const TcArgs &a, uint8_t *B, int64_t b, int l, int nl, int64_t s_begin,
-                                             int nrows, int warp, int lane) {
-    const uint32_t lbo = b_lbo(nrows);
-    const int h = lane >> 2, wq = lane & 3;
-    const int32_t *yr0 = a.y[0] + b * a.ldy[0], *yr1 = a.y[1] + b * a.ldy[1];
-    const bool al0 = ((((uintptr_t)yr0) & 15) == 0), al1 = ((((uintptr_t)yr1) & 15) == 0);
-    for (int r0 = warp; r0 < 2 * nrows; r0 += RB * (NTHR / 32)) {
-        int32_t v[RB][4];
+// byte j of t (zero outside [0, K))
+__device__ __forceinline__ uint32_t tbyte(const int8_t *tr, int64_t K, int64_t j) {
+    return (j >= 0 && j < K) ? (uint32_t)(uint8_t)tr[j] : 0u;
+}
+
+// ---------------------------------------------------------------------------
+// prep: planes, block limb counts, A image, leftover partials, zeroing
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
+    pdl_trigger();
+    pdl_wait();  // y and t come from the preceding launches
+    const TcArgs &a = T.a;
+    const int64_t b = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int64_t gtid = (int64_t)blockIdx.x * PREP_T + tid, gstride = (int64_t)gridDim.x * PREP_T;
+    const int8_t *tr = a.t + b * a.ldt;
+    const int nl0 = nleft_of(a.M[0], a.NA[0]), nl1 = nleft_of(a.M[1], a.NA[1]);
+    int64_t lacc[2 * MAXLEFT];
 #pragma unroll
-        for (int u = 0; u < RB; ++u) {
-            const int r = r0 + u * (NTHR / 32), j = r & 1;
-            const int64_t i0 = (int64_t)P * (s_begin + (r >> 1)) + 4 * lane;
-            const int32_t *yr = j ? yr1 : yr0;
-            const int64_t len = a.len[j];
-            v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0;
-            if (r < 2 * nrows && i0 >= 0) {
-                if ((j ? al1 : al0) && i0 + 4 <= len) {
-                    const int4 q = *reinterpret_cast<const int4 *>(yr + i0);
-                    v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
-                } else {
+    for (int q = 0; q < 2 * MAXLEFT; ++q) lacc[q] = 0;
+
+    // ---- zeroing (the keys are max-reduced by the later kernels)
+    if (blockIdx.x == 0 && tid < 2) T.keys[2 * b + tid] = 0;
+
+    // ---- planes + block limb counts + leftovers: thread = 16 entries (block s,
+    // modulus j, chunk column h); 16 consecutive threads cover one block of both moduli
+    const int64_t n16 = T.S * 16;
+    const int64_t pstride = (int64_t)8 * 32 * T.S;  // bytes per plane (8 columns x 2 S rows x 16)
+    uint8_t *pl = T.planes + b * T.np * pstride;
+    // (the loop is warp-uniform: the shuffles below combine 16-lane groups)
+    for (int64_t w0 = gtid - (tid & 31); w0 < n16; w0 += gstride) {
+        const int64_t w = w0 + (tid & 31);
+        const bool valid = w < n16;
+        const int64_t s = w >> 4;
+        const int j = (int)((w >> 3) & 1), h = (int)(w & 7);
+        const int32_t *yr = a.y[j] + b * a.ldy[j];
+        const int64_t i0 = (int64_t)P * s + 16 * h, len = valid ? a.len[j] : 0;
+        int32_t v[16];
+        if (i0 + 16 <= len && ((((uintptr_t)(yr + i0)) & 15) == 0)) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (i0 + e < len) v[u][e] = yr[i0 + e];
-                }
+            for (int q = 0; q < 4; ++q) {
+                const int4 u = *reinterpret_cast<const int4 *>(yr + i0 + 4 * q);
+                v[4 * q] = u.x; v[4 * q + 1] = u.y; v[4 * q + 2] = u.z; v[4 * q + 3] = u.w;
             }
-        }
+        } else {
 #pragma unroll
-        for (int u = 0; u < RB; ++u) {
-            const int r = r0 + u * (NTHR / 32);
-            if (r >= 2 * nrows) break;
-            *reinterpret_cast<uint32_t *>(B + lbo * h + 16 * r + 4 * wq) =
-                nl == 1 ? pack4(v[u][0], v[u][1], v[u][2], v[u][3])
-                        : pack4(limb(v[u][0], l, nl), limb(v[u][1], l, nl), limb(v[u][2], l, nl), limb(v[u][3], l, nl));
+            for (int e = 0; e < 16; ++e) v[e] = (i0 + e < len) ? yr[i0 + e] : 0;
+        }
+        int need = 1;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) need = max(need, limbs_needed(v[e]));
+        // max over the 16 lanes of the block (both moduli, 8 columns)
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
+        if (!valid) continue;
+        if ((tid & 15) == 0) T.bmag[b * T.S + s] = (uint8_t)min(need, 255);
+        const int64_t roff = (int64_t)h * 32 * T.S + 16 * (2 * s + j);
+        for (int p = 0; p < T.np; ++p) {
+            // plane p: 0 -> v; 1 + l (l <= lmax-2) -> (v >> 4l) & 15; lmax - 1 + l -> v >> 4l
+            const int kind = p == 0 ? 0 : (p <= T.lmax - 1 ? 1 : 2);
+            const int sh = kind == 1 ? 4 * (p - 1) : kind == 2 ? 4 * (p - T.lmax + 1) : 0;
+            uint32_t wd[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                int32_t c[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int32_t x = v[4 * q + e] >> sh;
+                    c[e] = kind == 1 ? (x & 15) : x;
+                }
+                wd[q] = pack4(c[0], c[1], c[2], c[3]);
+            }
+            *reinterpret_cast<uint4 *>(pl + p * pstride + roff) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        }
+        // leftover outputs k of modulus j: sum over this piece of t[idx - k] y_j[idx]
+        const int nlj = j ? nl1 : nl0;
+        for (int q = 0; q < nlj; ++q) {
+            const int64_t k = (int64_t)P * a.NA[j] + q;
+            int64_t acc = 0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int64_t i = i0 + e - k;
+                if (i >= 0 && i < a.K) acc += (int64_t)tr[i] * v[e];
+            }
+            lacc[(j ? nl0 : 0) + q] += acc;
         }
     }
+
+    // ---- A image: row (J, sg) = t(16 J + sg + e - 127), e < 16
+    uint8_t *ai = T.aimg + b * (int64_t)T.JT * 256;
+    for (int64_t w = gtid; w < (int64_t)T.JT * 16; w += gstride) {
+        const int64_t J = w >> 4;
+        const int sg = (int)(w & 15);
+        const int64_t base = 16 * J + sg - 127;
+        uint32_t wd[4];
+        const int64_t w0 = base >> 2;  // floor(base / 4)
+        if (w0 >= 0 && 4 * (w0 + 5) <= a.K && ((((uintptr_t)tr) & 3) == 0)) {  // interior: 5 aligned words
+            const uint32_t *tw = reinterpret_cast<const uint32_t *>(tr) + w0;
+            const uint32_t u0 = __ldg(tw), u1 = __ldg(tw + 1), u2 = __ldg(tw + 2), u3 = __ldg(tw + 3),
+                           u4 = __ldg(tw + 4);
+            const int sh = 8 * (int)(base & 3);
+            wd[0] = __funnelshift_r(u0, u1, sh); wd[1] = __funnelshift_r(u1, u2, sh);
+            wd[2] = __funnelshift_r(u2, u3, sh); wd[3] = __funnelshift_r(u3, u4, sh);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                wd[q] = tbyte(tr, a.K, base + 4 * q) | (tbyte(tr, a.K, base + 4 * q + 1) << 8) |
+                        (tbyte(tr, a.K, base + 4 * q + 2) << 16) | (tbyte(tr, a.K, base + 4 * q + 3) << 24);
+        }
+        *reinterpret_cast<uint4 *>(ai + 256 * J + 16 * sg) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    }
+
+    // ---- leftover partials of this CTA (fixed order: warp shuffle, then warps in order)
+    __shared__ int64_t red[PREP_T / 32][2 * MAXLEFT];
+    const int nq = nl0 + nl1;
+    for (int q = 0; q < nq; ++q) {
+        int64_t v = lacc[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((tid & 31) == 0) red[tid >> 5][q] = v;
+    }
+    __syncthreads();
+    if (tid < nq) {
+        int64_t v = 0;
+        for (int w = 0; w < PREP_T / 32; ++w) v += red[w][tid];
+        T.lpart[(b * T.n_pcta + blockIdx.x) * 2 * MAXLEFT + tid] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// main kernel
+// ---------------------------------------------------------------------------
+// smem: A [2][A_BYTES] | B [2][B_BYTES] | full[2] | mdone[2] | TMEM slot | flag
+constexpr int A_BYTES = (256 * (8 * (TCCH - 1) + 15) + 127) / 128 * 128;
+// B chunk-column stride: 32 nrows + 16 bytes (a multiple of 16, as the
+// descriptor needs); rows of a column are contiguous (16 B each)
+__host__ __device__ __forceinline__ uint32_t b_lbo(int nrows) { return 32u * nrows + 16u; }
+template <int NT>
+constexpr int b_bytes() { return (8 * (2 * (NT + TCCH - 1) * 16 + 16) + 127) / 128 * 128; }
+template <int NT>
+constexpr int smem_bytes() { return 2 * A_BYTES + 2 * b_bytes<NT>() + 64; }
+
+__device__ __forceinline__ void mbar_init1(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
 template <int NT>
 __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
     pdl_trigger();
-    pdl_wait();
+    pdl_wait();  // the prep kernel's planes, A image and zeroed keys
     constexpr int B_BYTES = b_bytes<NT>();
     extern __shared__ __align__(1024) uint8_t sm[];
     const TcArgs &a = T.a;
@@ -124,48 +252,26 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
     const int at = T.at0 + blockIdx.x % T.n_atp, cr = blockIdx.x / T.n_atp;
     const int a0 = at * NT;
     const int cb = cr * T.CR, ce = min(a.NC, cb + T.CR);
-    uint8_t *Abuf = sm, *Bbuf = sm + 2 * A_BYTES, *tp = Bbuf + 2 * B_BYTES;
-    uint64_t *mdone = reinterpret_cast<uint64_t *>(tp + TP_BYTES);  // [2]
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(mdone + 2);
-    int *nlflag = reinterpret_cast<int *>(mdone + 3);
-    long long ts[8] = {gtime(), 0, 0, 0, 0, 0, 0, 0};  // instrumentation (a.dbg): phase stamps
-    if (tid == 32) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mdone)));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mdone + 1)));
+    uint8_t *Abuf = sm, *Bbuf = sm + 2 * A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(Bbuf + 2 * B_BYTES);  // [2]
+    uint64_t *mdone = full + 2;                                          // [2]
+    uint64_t *fin = mdone + 2;                                           // every MMA of the CTA done
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(fin + 1);
+    long long ts[4] = {gtime(), 0, 0, 0};  // instrumentation (a.dbg): phase stamps
+    if (tid == 0) {
+        mbar_init1(full); mbar_init1(full + 1); mbar_init1(mdone); mbar_init1(mdone + 1); mbar_init1(fin);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // ---- limb count: scan this CTA's whole y window (blocks [a0 + cb, a0 + NT + ce - 1)),
-    // 16-byte loads with several in flight (a latency-bound scalar scan cost ~30% of the kernel)
-    int fl = 0;
+    // ---- limb count: the most any block of this CTA's window [a0 + cb, a0 + NT + ce - 1) needs
+    int need = 1;
     {
-        const int64_t s0 = a0 + cb, n = NT + (ce - cb) - 1;
-        uint32_t mag = 0;  // OR of v ^ (v >> 31): below 2^b iff every v fits b + 1 signed bits
-        for (int j = 0; j < 2 && tid < NTHR; ++j) {
-            const int32_t *yr = a.y[j] + b * a.ldy[j];
-            const int64_t lo = P * s0, hi = min(P * (s0 + n), a.len[j]);
-            if (hi <= lo) continue;
-            if ((((uintptr_t)(yr + lo)) & 15) == 0) {
-                const int64_t n4 = (hi - lo) >> 2;
-                const int4 *q = reinterpret_cast<const int4 *>(yr + lo);
-#pragma unroll 4
-                for (int64_t i = tid; i < n4; i += NTHR) {
-                    const int4 v = q[i];
-                    mag |= (uint32_t)(v.x ^ (v.x >> 31)) | (uint32_t)(v.y ^ (v.y >> 31)) |
-                           (uint32_t)(v.z ^ (v.z >> 31)) | (uint32_t)(v.w ^ (v.w >> 31));
-                }
-                for (int64_t i = lo + 4 * n4 + tid; i < hi; i += NTHR) mag |= (uint32_t)(yr[i] ^ (yr[i] >> 31));
-            } else {
-#pragma unroll 4
-                for (int64_t i = lo + tid; i < hi; i += NTHR) mag |= (uint32_t)(yr[i] ^ (yr[i] >> 31));
-            }
-        }
-        fl = (mag > 127u ? 1 : 0) | (mag > 2047u ? 2 : 0) | (mag > 32767u ? 4 : 0);
+        const int64_t s0 = (int64_t)a0 + cb, n = NT + (ce - cb) - 1;
+        for (int64_t i = tid; i < n; i += TNTHR)
+            if (s0 + i < T.S) need = max(need, (int)T.bmag[b * T.S + s0 + i]);
     }
-    fl = __syncthreads_or(fl & 1) | (__syncthreads_or(fl & 2) << 1) | (__syncthreads_or(fl & 4) << 2);
-    int nl = (fl & 4) ? 4 : (fl & 2) ? 3 : (fl & 1) ? 2 : 1;
-    if (nl > T.lmax) nl = T.lmax;
-    // TMEM: 2 NT columns per limb, allocated after the scan so that two CTAs fit
-    // per SM whenever 2 NT nl <= 256
+    const int nl = min(T.lmax, 1 + (__syncthreads_or(need >= 2) + __syncthreads_or(need >= 3) +
+                                     __syncthreads_or(need >= 4)));
+    // TMEM: 2 NT columns per limb (two CTAs fit per SM while 2 NT nl <= 256)
     uint32_t ncols = 32;
     while (ncols < (uint32_t)(2 * NT * nl)) ncols *= 2;
     if (warp == 0) {
@@ -173,30 +279,49 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
                      "r"(ncols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    (void)nlflag;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tbase = *tslot;
     ts[1] = gtime();
+    const int npass = ((ce - cb + TCCH - 1) / TCCH) * nl;
 
-    // pass q = (chunk, limb) uses A[chunk & 1], B[q & 1] and commits to mdone[q & 1]
-    // (its (q >> 1)-th phase).  Before staging pass q the stagers wait for pass q - 2,
-    // which (commits being cumulative) also frees the A buffer of chunk - 2.
-    uint32_t pass = 0;
-    if (warp == NTHR / 32) {
+    if (warp == 9) {
+        // ---- TMA producer: pass q = (chunk, limb) into A[chunk & 1], B[q & 1]
+        if (lane == 0) {
+            const int64_t pstride = (int64_t)8 * 32 * T.S;
+            const uint8_t *pl = T.planes + b * T.np * pstride;
+            const uint8_t *ai = T.aimg + b * (int64_t)T.JT * 256;
+            int q = 0, ch = 0;
+            for (int c0 = cb; c0 < ce; c0 += TCCH, ++ch) {
+                const int c1 = min(ce, c0 + TCCH);
+                const int nrows = NT + (c1 - c0) - 1;  // B window: blocks [a0 + c0, a0 + c0 + nrows)
+                const uint32_t lbo = b_lbo(nrows);
+                const uint32_t abytes = 256u * (8 * (c1 - c0 - 1) + 15);
+                for (int l = 0; l < nl; ++l, ++q) {
+                    if (q >= 2) mbar_wait(mdone + (q & 1), ((q - 2) >> 1) & 1u);  // buffers of pass q - 2 free
+                    const int plane = nl == 1 ? 0 : (l < nl - 1 ? 1 + l : T.lmax + nl - 2);
+                    expect_tx(full + (q & 1), (l == 0 ? abytes : 0u) + 8u * 32u * nrows);
+                    if (l == 0) bulk_copy(Abuf + (ch & 1) * A_BYTES, ai + 256 * 8 * (int64_t)c0, abytes, full + (q & 1));
+                    const uint8_t *src = pl + plane * pstride + 32 * ((int64_t)a0 + c0);
+                    uint8_t *B = Bbuf + (q & 1) * B_BYTES;
+                    for (int h = 0; h < 8; ++h)
+                        bulk_copy(B + h * lbo, src + h * 32 * T.S, 32u * nrows, full + (q & 1));
+                }
+            }
+        }
+    } else if (warp == 8) {
         // ---- MMA issuer
-        int ch = 0;
+        int q = 0, ch = 0;
         for (int c0 = cb; c0 < ce; c0 += TCCH, ++ch) {
             const int c1 = min(ce, c0 + TCCH);
             const int nrows = NT + (c1 - c0) - 1;
+            const uint32_t lbo = b_lbo(nrows);
             const uint8_t *A = Abuf + (ch & 1) * A_BYTES;
-            for (int l = 0; l < nl; ++l) {
-                const uint8_t *B = Bbuf + (pass & 1) * B_BYTES;
-                if (pass & 1) asm volatile("bar.sync 2, %0;" ::"n"(TNTHR) : "memory");
-                else asm volatile("bar.sync 1, %0;" ::"n"(TNTHR) : "memory");
+            for (int l = 0; l < nl; ++l, ++q) {
+                mbar_wait(full + (q & 1), (q >> 1) & 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t lbo = b_lbo(nrows);
+                const uint8_t *B = Bbuf + (q & 1) * B_BYTES;
                 const uint64_t ad0 = sdesc(smem_u32(A), 256, 128);
                 const uint64_t bd0 = sdesc(smem_u32(B), lbo, 128);
                 const uint32_t id = idesc_i8(2 * NT);
@@ -209,82 +334,14 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
                         mma_i8(dcol, ad, bd, id, (c != cb || ks) ? 1u : 0u);
                     }
                 }
-                umma_commit(mdone + (pass & 1));
-                ++pass;
+                umma_commit(mdone + (q & 1));
             }
         }
-    } else {
-        // ---- stagers.  The template slice of the next chunk is prefetched into
-        // registers (tw_) while the current chunk is staged.
-        constexpr int TPW = TP_BYTES / 4;
-        uint32_t tw_[(TPW + NTHR - 1) / NTHR];
-        auto load_slice = [&](int c0v) {  // tp'[j] = t[128 c0v + j - 128] (zero outside [0, K))
-            const int8_t *tr = a.t + b * a.ldt;
-            const int64_t base = 128 * (int64_t)c0v - 128;
-            const bool fast = base >= 0 && base + TP_BYTES <= a.K && ((((uintptr_t)(tr + base)) & 3) == 0);
-#pragma unroll
-            for (int u = 0; u < (TPW + NTHR - 1) / NTHR; ++u) {
-                const int i = tid + u * NTHR;
-                if (i >= TPW) break;
-                if (fast) {
-                    tw_[u] = __ldg(reinterpret_cast<const uint32_t *>(tr + base) + i);
-                } else {
-                    uint32_t w = 0;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int64_t j = base + 4 * i + e;
-                        if (j >= 0 && j < a.K) w |= (uint32_t)(uint8_t)tr[j] << (8 * e);
-                    }
-                    tw_[u] = w;
-                }
-            }
-        };
-        load_slice(cb);
-        int ch = 0;
-        for (int c0 = cb; c0 < ce; c0 += TCCH, ++ch) {
-            const int c1 = min(ce, c0 + TCCH);
-            const int nrows = NT + (c1 - c0) - 1;  // B window: blocks [a0 + c0, a0 + c0 + nrows)
-            uint8_t *A = Abuf + (ch & 1) * A_BYTES;
-            for (int l = 0; l < nl; ++l) {
-                uint8_t *B = Bbuf + (pass & 1) * B_BYTES;
-                long long tw = gtime();
-                if (pass >= 2) mbar_wait(mdone + (pass & 1), ((pass - 2) >> 1) & 1u);
-                long long tw2 = gtime();
-                ts[4] += tw2 - tw;
-                if (l == 0) {
-                    stagers_sync();  // every stager is done reading the previous slice
-#pragma unroll
-                    for (int u = 0; u < (TPW + NTHR - 1) / NTHR; ++u)
-                        if (tid + u * NTHR < TPW) reinterpret_cast<uint32_t *>(tp)[tid + u * NTHR] = tw_[u];
-                    stagers_sync();
-                    if (c1 < ce) load_slice(c1);
-                    const int n = (8 * (c1 - c0 - 1) + 15) * 16;
-                    for (int c = tid; c < n; c += NTHR) {
-                        const int J = c >> 4, sg = c & 15;
-                        const int sh = sg + 1, m = sh >> 2, r = 8 * (sh & 3);
-                        const uint32_t *w = reinterpret_cast<const uint32_t *>(tp + 16 * J) + m;
-                        const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
-                        uint4 o;
-                        o.x = __funnelshift_r(w0, w1, r);
-                        o.y = __funnelshift_r(w1, w2, r);
-                        o.z = __funnelshift_r(w2, w3, r);
-                        o.w = __funnelshift_r(w3, w4, r);
-                        reinterpret_cast<uint4 *>(A)[c] = o;
-                    }
-                }
-                ts[5] += gtime() - tw2;  // template slice + A build
-                tw2 = gtime();
-                stage_window<12>(a, B, b, l, nl, (int64_t)a0 + c0, nrows, warp, lane);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                if (pass & 1) asm volatile("bar.arrive 2, %0;" ::"n"(TNTHR) : "memory");
-                else asm volatile("bar.arrive 1, %0;" ::"n"(TNTHR) : "memory");
-                ts[6] += gtime() - tw2;  // B staging
-                ++pass;
-            }
-        }
+        umma_commit(fin);  // tracks every MMA this thread issued
     }
-    mbar_wait(mdone + ((pass - 1) & 1), ((pass - 1) >> 1) & 1u);
+    // every warp: all MMAs complete (fin completes exactly once: parity 0; a wait on
+    // mdone's parity would return at once for a phase not yet begun)
+    mbar_wait(fin, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     ts[2] = gtime();
 
@@ -315,36 +372,19 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
                 for (int j = 0; j < 2; ++j) {
                     const int64_t k = P * ab + brow;
                     if (ab < a.NA[j] && k < a.M[j]) {
-                        if (T.n_cr > 1) {
-                            atomicAdd(reinterpret_cast<unsigned long long *>(T.racc[j] + b * a.M[j] + k),
-                                      (unsigned long long)r[i][j]);
+                        if (T.n_cr > 1) {  // this range's partial r (summed by tiled_reduce)
+                            const int64_t o = (b * T.n_cr + cr) * (a.M1 + a.M2) + (j ? a.M1 : 0) + k;
+                            if (T.part32) reinterpret_cast<int32_t *>(T.part)[o] = (int32_t)r[i][j];
+                            else reinterpret_cast<int64_t *>(T.part)[o] = r[i][j];
                         } else {
-                            if (T.write_r) T.racc[j][b * a.M[j] + k] = r[i][j];
+                            if (T.r_out[j]) T.r_out[j][b * a.M[j] + k] = r[i][j];
                             amax(bv[j], bk[j], r[i][j], k);
                         }
                     }
                 }
             }
         }
-        if (T.n_cr > 1) {
-            // the CTA that completes a tile's last template range reduces its final r
-            __threadfence();
-            stagers_sync();
-            if (tid == 0) *nlflag = (atomicAdd(T.tile_cnt + b * T.n_at + at, 1u) == (unsigned)(T.n_cr - 1));
-            stagers_sync();
-            if (*nlflag) {
-                __threadfence();
-                for (int ar0 = (NT / 2) * hw; ar0 < (NT / 2) * hw + NT / 2; ++ar0) {
-                    const int64_t ab = a0 + ar0;
-#pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const int64_t k = P * ab + brow;
-                        if (ab < a.NA[j] && k < a.M[j]) amax(bv[j], bk[j], __ldcg(T.racc[j] + b * a.M[j] + k), k);
-                    }
-                }
-            }
-        }
-        if (T.n_cr == 1 || *nlflag) {
+        if (T.n_cr == 1) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
 #pragma unroll
@@ -363,69 +403,91 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
         ts[3] = gtime();
         uint32_t smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        ts[7] = ((long long)smid << 32) | ((long long)pass << 8) | nl;
         long long *d = a.dbg + 8 * ((int64_t)blockIdx.y * gridDim.x + blockIdx.x);
-        for (int i = 0; i < 8; ++i) d[i] = ts[i];
+        d[0] = ts[0]; d[1] = ts[1]; d[2] = ts[2]; d[3] = ts[3];
+        d[4] = 0; d[5] = 0; d[6] = 0;
+        d[7] = ((long long)smid << 32) | ((long long)npass << 8) | nl;
     }
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols));
 }
 
-// leftover outputs k in [128 NA_j, M_j) (at most MAXLEFT per modulus): CTA
-// (K-slice, pair) adds its partial dot products into lsum (exact int64)
-constexpr int LSLICE = 1024;  // K-slice per CTA (4 terms per thread: latency-bound loop)
-__global__ void __launch_bounds__(256) tc_tiled_leftover(const TiledArgs T) {
+// several template ranges: r = sum of the ranges' partials (fixed order, exact
+// int64), the lowest-index max per pair and modulus -> packed-key atomicMax.
+// Thread = 4 consecutive outputs of one modulus; CTA = 1024 outputs.
+constexpr int RED_T = 256;
+template <typename PT>
+__global__ void __launch_bounds__(RED_T) tiled_reduce(const TiledArgs T) {
     pdl_trigger();
     pdl_wait();
     const TcArgs &a = T.a;
     const int64_t b = blockIdx.y;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t i0 = (int64_t)blockIdx.x * LSLICE, i1 = min(a.K, i0 + LSLICE);
-    __shared__ int64_t part[8];
-    const int nleft0 = (int)max((int64_t)0, a.M[0] - (int64_t)P * a.NA[0]);
-    const int nleft1 = (int)max((int64_t)0, a.M[1] - (int64_t)P * a.NA[1]);
-    const int8_t *tr = a.t + b * a.ldt;
-    for (int q = 0; q < nleft0 + nleft1; ++q) {
-        const int j = q < nleft0 ? 0 : 1;
-        const int64_t k = (int64_t)P * a.NA[j] + (j ? q - nleft0 : q);
-        const int32_t *yr = a.y[j] + b * a.ldy[j] + k;
-        int64_t sum = 0;
-#pragma unroll 4
-        for (int64_t i = i0 + tid; i < i1; i += 256) sum += (int64_t)tr[i] * yr[i];
+    const int64_t ML = a.M1 + a.M2;
+    int64_t bv[2] = {INT64_MIN, INT64_MIN}, bk[2] = {INT64_MAX, INT64_MAX};
+    const int64_t idx = (int64_t)blockIdx.x * RED_T + threadIdx.x;  // one output per thread
+    const PT *pp = reinterpret_cast<const PT *>(T.part) + b * T.n_cr * ML;
+    if (idx < ML) {
+        const int j = idx >= a.M1 ? 1 : 0;
+        const int64_t k = idx - (j ? a.M1 : 0);
+        const int64_t blk = k / P;
+        // MMA outputs of this launch's tiles only (leftovers: tc_tiled_final; split correlation)
+        if (k < (int64_t)P * a.NA[j] && blk >= (int64_t)T.at0 * T.NT && blk < (int64_t)(T.at0 + T.n_atp) * T.NT) {
+            int64_t r = 0;
+            int c = 0;
+            for (; c + 8 <= T.n_cr; c += 8) {  // eight loads in flight, summed in range order
+                PT v[8];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        if (lane == 0) part[warp] = sum;
-        __syncthreads();
-        if (tid == 0) {
-            int64_t tot = 0;
-            for (int w = 0; w < 8; ++w) tot += part[w];
-            atomicAdd(reinterpret_cast<unsigned long long *>(T.lsum + b * 2 * MAXLEFT + q), (unsigned long long)tot);
+                for (int u = 0; u < 8; ++u) v[u] = __ldcg(pp + (c + u) * ML + idx);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) r += (int64_t)v[u];
+            }
+            for (; c < T.n_cr; ++c) r += (int64_t)__ldcg(pp + c * ML + idx);
+            if (T.r_out[j]) T.r_out[j][b * a.M[j] + k] = r;
+            amax(bv[j], bk[j], r, k);
         }
-        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int64_t ov = __shfl_xor_sync(0xffffffffu, bv[j], o);
+            const int64_t ok = __shfl_xor_sync(0xffffffffu, bk[j], o);
+            amax(bv[j], bk[j], ov, ok);
+        }
+        if (lane == 0 && bk[j] != INT64_MAX) atomicMax(T.keys + 2 * b + j, pack_key(bv[j], bk[j]));
     }
 }
 
-// workspace reset as a PDL kernel (a memset would end the overlap of launches)
-__global__ void tiled_zero(int32_t *p0, int64_t n0, int32_t *p1, int64_t n1, int32_t *p2, int64_t n2) {
-    pdl_trigger();
-    pdl_wait();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1 + n2; i += stride) {
-        if (i < n0) p0[i] = 0;
-        else if (i < n0 + n1) p1[i - n0] = 0;
-        else p2[i - n0 - n1] = 0;
-    }
-}
-
-// per pair: tile keys + leftovers -> residues; steps 8-9 (tm_resolve)
-__global__ void tc_tiled_final(const TiledArgs T, int64_t batch, int32_t *resid, int32_t *residues_out,
-                               int64_t *k_out, int64_t *r_out0, int64_t *r_out1, int64_t *keys_out, int with_left) {
+// per pair (one CTA of FIN_T threads): tile keys + leftovers -> residues; steps 8-9 (tm_resolve)
+constexpr int FIN_T = 256;
+__global__ void __launch_bounds__(FIN_T) tc_tiled_final(const TiledArgs T, int64_t batch, int32_t *resid,
+                                                       int32_t *residues_out, int64_t *k_out, int64_t *keys_out,
+                                                       int with_left) {
     pdl_trigger();
     pdl_wait();
     const TcArgs &a = T.a;
-    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= batch) return;
-    const int nleft0 = (int)max((int64_t)0, a.M[0] - (int64_t)P * a.NA[0]);
-    const int nleft1 = (int)max((int64_t)0, a.M[1] - (int64_t)P * a.NA[1]);
+    const int64_t b = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nleft0 = nleft_of(a.M[0], a.NA[0]), nleft1 = nleft_of(a.M[1], a.NA[1]);
+    const int nq = with_left ? nleft0 + nleft1 : 0;
+    __shared__ int64_t red[FIN_T / 32][2 * MAXLEFT];
+    __shared__ int64_t lsum[2 * MAXLEFT];
+    // leftover dot products: the prep CTAs' partials, summed in a fixed order
+    for (int q = 0; q < nq; ++q) {
+        int64_t r = 0;
+        for (int c = tid; c < T.n_pcta; c += FIN_T) r += T.lpart[(b * T.n_pcta + c) * 2 * MAXLEFT + q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        if (lane == 0) red[warp][q] = r;
+    }
+    __syncthreads();
+    if (tid < nq) {
+        int64_t r = 0;
+        for (int w = 0; w < FIN_T / 32; ++w) r += red[w][tid];
+        lsum[tid] = r;
+    }
+    __syncthreads();
+    if (tid) return;
     int64_t m[2];
     for (int j = 0; j < 2; ++j) {
         int64_t bv = INT64_MIN, bk = INT64_MAX;
@@ -436,10 +498,9 @@ __global__ void tc_tiled_final(const TiledArgs T, int64_t batch, int32_t *resid,
         }
         const int nleft = with_left ? (j ? nleft1 : nleft0) : 0;
         for (int q = 0; q < nleft; ++q) {
-            const int64_t r = T.lsum[b * 2 * MAXLEFT + (j ? nleft0 : 0) + q];
+            const int64_t r = lsum[(j ? nleft0 : 0) + q];
             const int64_t k = (int64_t)P * a.NA[j] + q;
-            int64_t *ro = j ? r_out1 : r_out0;
-            if (ro) ro[b * a.M[j] + k] = r;
+            if (T.r_out[j]) T.r_out[j][b * a.M[j] + k] = r;
             amax(bv, bk, r, k);
         }
         m[j] = bk;
@@ -466,6 +527,49 @@ __global__ void match_keys_kernel(const int64_t *keys, int64_t batch, int64_t M1
     if (k) k[b] = tm_resolve(m[0], m[1], M1, M2, inv, N, wrap);
 }
 
+// geometry shared by the workspace size and the launch
+constexpr size_t PART_BUDGET = (size_t)64 << 20;  // bytes of partial sums (several template ranges)
+// NT = 64 (MMA N = 128: fewer A-operand reads per MAC) when the pairs' tiles fill
+// the SMs without splitting the template range much; NT = 32 otherwise, where the
+// partial sums of more template ranges cost more than the MMAs save (measured,
+// same box: cfg5 one pair K = 65536 42 vs 47 us, 64 pairs K = 16384 94 vs 112 us;
+// 64 pairs K = 32768 / 65536: 172 / 545 vs 135 / 406 us)
+int tiled_nt(const tm_plan_s *p, int64_t batch) {
+    static const char *env = getenv("TM_TILED_NT");  // A/B: "32" or "64"
+    if (env && (atoi(env) == 32 || atoi(env) == 64)) return atoi(env);
+    const int64_t na = std::max(p->M1, p->M2) / P + 1;
+    return batch * ((na + 63) / 64) >= p->num_sms ? 64 : 32;
+}
+struct Geo {
+    int NT, NC, NA[2], n_at, lmax, np, JT, n_pcta, max_cr;
+    int64_t S;
+};
+Geo geometry(const tm_plan_s *p, int64_t batch) {
+    Geo g{};
+    g.NT = tiled_nt(p, batch);
+    g.NC = (int)((p->K + P - 2) / P) + 1;
+    for (int j = 0; j < 2; ++j) {
+        const int64_t M = j ? p->M2 : p->M1;
+        int64_t na = M / P;
+        if (M - na * P > MAXLEFT) ++na;
+        if (na < 1) na = 1;
+        g.NA[j] = (int)na;
+    }
+    const int namax = std::max(g.NA[0], g.NA[1]);
+    g.n_at = (namax + g.NT - 1) / g.NT;
+    g.S = (int64_t)g.n_at * g.NT + g.NC + 1;  // every window row [a0 + c0, a0 + c0 + nrows)
+    g.lmax = std::max(1, p->tct_lmax);
+    g.np = 2 * g.lmax - 1;
+    g.JT = 8 * (g.NC - 1) + 16;
+    const int64_t want = (2 * (int64_t)p->num_sms + batch - 1) / std::max<int64_t>(batch, 1);
+    g.n_pcta = (int)std::min<int64_t>(PREP_MAXCTA, std::max<int64_t>(1, want));
+    // template ranges of >= one A chunk each, and their partial sums within the budget
+    const size_t per = (size_t)std::max<int64_t>(batch, 1) * (size_t)(p->M1 + p->M2) * 8;
+    g.max_cr = std::max(1, std::min((g.NC + TCCH - 1) / TCCH, (int)std::min<size_t>(PART_BUDGET / per, 1 << 20)));
+    return g;
+}
+
+size_t align_up256(size_t v) { return (v + 255) & ~size_t(255); }
 }  // namespace
 
 int tm_tc_match_keys(const tm_plan_s *p, const int64_t *keys, int64_t batch, int32_t *residues, int64_t *k,
@@ -478,7 +582,7 @@ int tm_tc_match_keys(const tm_plan_s *p, const int64_t *keys, int64_t batch, int
 }
 
 // Plan-time eligibility (int8 data whose |y| fits 4 four-bit limbs and whose
-// |r| fits the packed key) and geometry.
+// |r| fits the packed key).
 void tm_tc_tiled_plan(tm_plan_s *p) {
     p->tct_ok = 0;
     if (p->dtype != TM_I8) return;
@@ -496,10 +600,16 @@ void tm_tc_tiled_plan(tm_plan_s *p) {
 }
 
 size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch) {
-    if (!p->tct_ok) return 0;
-    // keys [batch][2] | lsum [batch][2 MAXLEFT] | tile counters [batch][<= 2^KEY_SHIFT / (128 NT)] | racc
-    return 256 + (size_t)batch * (16 + 16 * MAXLEFT + 4 * (((int64_t)1 << KEY_SHIFT) / (P * NT_MIN) + 1)) +
-           (size_t)batch * (p->M1 + p->M2) * 8 + 1024;
+    if (!p->tct_ok || batch < 1) return 0;
+    const Geo g = geometry(p, batch);
+    size_t n = 0;
+    n += align_up256((size_t)batch * 16);                                   // keys
+    n += align_up256(g.max_cr > 1 ? (size_t)batch * g.max_cr * (p->M1 + p->M2) * 8 : 0);  // partial sums
+    n += align_up256((size_t)batch * g.S);                                  // block limb counts
+    n += align_up256((size_t)batch * g.np * 8 * 32 * g.S);                  // B planes
+    n += align_up256((size_t)batch * g.JT * 256);                           // A image
+    n += align_up256((size_t)batch * g.n_pcta * 2 * MAXLEFT * 8);           // leftover partials
+    return n + 256;
 }
 
 // r1/r2 (int64, may be NULL), residues_out/resid (may be NULL), k (may be NULL).
@@ -510,87 +620,84 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     if (!p->tct_ok) return TM_EUNSUPPORTED;
     if (batch == 0) return TM_OK;
     if (batch > 65535) return TM_EUNSUPPORTED;
+    const Geo g = geometry(p, batch);
     TiledArgs T{};
     tm_tc_fill_args(p, y1, y2, t, ldt, nullptr, nullptr, nullptr, nullptr, nullptr, T.a);
     T.a.ldy[0] = ldy1; T.a.ldy[1] = ldy2;
     T.a.dbg = tm_tc_dbg_buffer();
-    // the tiles cover NA_j = the plan's block counts (computed here: tc_ok may be false)
-    const int NC = (int)((p->K + P - 2) / P) + 1;
-    T.a.NC = NC;
-    for (int j = 0; j < 2; ++j) {
-        const int64_t M = j ? p->M2 : p->M1;
-        int64_t na = M / P;
-        if (M - na * P > MAXLEFT) ++na;
-        if (na < 1) na = 1;
-        T.a.NA[j] = (int)na;
-    }
-    T.lmax = p->tct_lmax;
-    const char *env_nt = getenv("TM_TILED_NT");  // A/B: "32" (default, measured faster) or "64"
-    const int NT = (env_nt && atoi(env_nt) == 64) ? 64 : 32;
-    const int namax = T.a.NA[0] > T.a.NA[1] ? T.a.NA[0] : T.a.NA[1];
-    T.n_at = (namax + NT - 1) / NT;
+    T.a.NC = g.NC;
+    T.a.NA[0] = g.NA[0]; T.a.NA[1] = g.NA[1];
+    T.NT = g.NT;
+    T.lmax = g.lmax; T.np = g.np; T.S = g.S; T.JT = g.JT; T.n_pcta = g.n_pcta;
+    T.n_at = g.n_at;
     // split correlation: part `part` of `nparts` takes a contiguous
     // range of output tiles
     T.at0 = (int)((int64_t)T.n_at * part / nparts);
     T.n_atp = (int)((int64_t)T.n_at * (part + 1) / nparts) - T.at0;
     // template ranges: minimise waves x blocks per CTA over 2 resident CTAs per SM
     // (a grid just over one wave doubles the time), fewer ranges on near-ties
-    // (each extra range adds one int64 atomic per output)
-    const int max_cr = std::max(1, (NC + 2 * TCCH - 1) / (2 * TCCH));
+    // (each extra range adds one partial sum per output)
+    // cost model (us): MMA time of the busiest CTA slot, 4 k-steps x ~2 limbs x the
+    // shared-memory-operand MMA ((4096 + 64 NT) / 128 cycles), plus the partial sums'
+    // write + read (several ranges) at ~6 TB/s of L2
+    const int NC = g.NC;
     const int64_t slots = 2 * (int64_t)p->num_sms;
+    const double xmax = (p->flags & TM_BINARY) ? 1.0 : 128.0;
+    const double ybound = xmax * (double)(p->q1 > p->q2 ? p->q1 : p->q2);
+    const double t_block = 4.0 * 2.0 * (4096.0 + 64.0 * g.NT) / 128.0 / 1900.0 * 2.0;  // 2 CTAs share an SM
     int n_cr = 1;
     double best = 1e300;
-    for (int c = 1; c <= max_cr; ++c) {
+    for (int c = 1; c <= g.max_cr; ++c) {
         const int64_t ctas = batch * std::max(T.n_atp, 1) * c;
-        const double cost = (double)((ctas + slots - 1) / slots) * (double)((NC + c - 1) / c);
-        if (cost < best * 0.95) { best = cost; n_cr = c; }
+        const int cr_blocks = (NC + c - 1) / c;
+        const bool p32 = (double)cr_blocks * P * xmax * ybound < 2147483647.0;
+        const double part = c > 1 ? (double)c * batch * (p->M1 + p->M2) * (p32 ? 4.0 : 8.0) * 3.0 / 6.0e6 : 0.0;
+        const double cost = (double)((ctas + slots - 1) / slots) * (double)cr_blocks * t_block + part;
+        if (cost < best * 0.97) { best = cost; n_cr = c; }
     }
     T.CR = (NC + n_cr - 1) / n_cr;
     T.n_cr = (NC + T.CR - 1) / T.CR;
+    T.part32 = (double)T.CR * P * xmax * ybound < 2147483647.0;  // |partial| <= CR P max|t| max|y|
     char *w = (char *)ws;
-    auto carve = [&](size_t bytes) { char *q = w; w += (bytes + 255) / 256 * 256; return q; };
+    auto carve = [&](size_t bytes) { char *q = w; w += align_up256(bytes); return q; };
     T.keys = (unsigned long long *)carve((size_t)batch * 16);
-    T.lsum = (int64_t *)carve((size_t)batch * 16 * MAXLEFT);
-    T.tile_cnt = (unsigned *)carve((size_t)batch * T.n_at * 4);
-    const size_t zero_bytes = (size_t)(w - (char *)ws);  // keys, lsum, counters: one memset
-    int64_t *racc = (int64_t *)carve((size_t)batch * (p->M1 + p->M2) * 8);
-    T.racc[0] = r1 ? (int64_t *)r1 : racc;
-    T.racc[1] = r2 ? (int64_t *)r2 : racc + batch * p->M1;
-    T.write_r = (r1 != nullptr);
+    T.part = (int64_t *)carve(g.max_cr > 1 ? (size_t)batch * g.max_cr * (p->M1 + p->M2) * 8 : 0);
+    T.bmag = (uint8_t *)carve((size_t)batch * g.S);
+    T.planes = (uint8_t *)carve((size_t)batch * g.np * 8 * 32 * g.S);
+    T.aimg = (uint8_t *)carve((size_t)batch * g.JT * 256);
+    T.lpart = (int64_t *)carve((size_t)batch * g.n_pcta * 2 * MAXLEFT * 8);
+    T.r_out[0] = (int64_t *)r1;
+    T.r_out[1] = (int64_t *)r2;
     {
-        const int64_t n0 = (int64_t)(zero_bytes / 4);
-        const int64_t n1 = T.n_cr > 1 ? batch * p->M1 * 2 : 0, n2 = T.n_cr > 1 ? batch * p->M2 * 2 : 0;
-        const int64_t blocks = std::min<int64_t>((n0 + n1 + n2 + 255) / 256, 4 * (int64_t)p->num_sms);
-        const cudaError_t e = launch_pdl(tiled_zero, dim3((unsigned)blocks), dim3(256), 0, s, (int32_t *)ws, n0,
-                                         (int32_t *)T.racc[0], n1, (int32_t *)T.racc[1], n2);
-        if (e != cudaSuccess) return tm_cuda_status(e, "tm_correlate: tiled reset");
-        TM_CHECK_LAUNCH("tm_correlate: tiled reset");
-    }
-    {
-        cudaError_t e = tm_smem_attr((const void *)corr_tc_tiled<32>, (int)smem_bytes<32>());
-        if (e == cudaSuccess) e = tm_smem_attr((const void *)corr_tc_tiled<64>, (int)smem_bytes<64>());
-        if (e != cudaSuccess) return tm_cuda_status(e, "corr_tc_tiled: shared-memory attribute");
+        const cudaError_t e = launch_pdl(tiled_prep, dim3((unsigned)g.n_pcta, (unsigned)batch), dim3(PREP_T), 0, s, T);
+        if (e != cudaSuccess) return tm_cuda_status(e, "tm_correlate: tiled_prep");
+        TM_CHECK_LAUNCH("tm_correlate: tiled_prep");
     }
     const dim3 grid((unsigned)(T.n_atp * T.n_cr), (unsigned)batch);
     if (T.n_atp > 0) {
-        const cudaError_t e = NT == 32 ? launch_pdl(corr_tc_tiled<32>, grid, dim3(TNTHR), smem_bytes<32>(), s, T)
-                                       : launch_pdl(corr_tc_tiled<64>, grid, dim3(TNTHR), smem_bytes<64>(), s, T);
+        cudaError_t e;
+        if (g.NT == 64) {
+            e = tm_smem_attr((const void *)corr_tc_tiled<64>, smem_bytes<64>());
+            if (e == cudaSuccess) e = launch_pdl(corr_tc_tiled<64>, grid, dim3(TNTHR), smem_bytes<64>(), s, T);
+        } else {
+            e = tm_smem_attr((const void *)corr_tc_tiled<32>, smem_bytes<32>());
+            if (e == cudaSuccess) e = launch_pdl(corr_tc_tiled<32>, grid, dim3(TNTHR), smem_bytes<32>(), s, T);
+        }
         if (e != cudaSuccess) return tm_cuda_status(e, "corr_tc_tiled");
         TM_CHECK_LAUNCH("corr_tc_tiled");
+        if (T.n_cr > 1) {
+            const int64_t ML = p->M1 + p->M2;
+            const dim3 gr((unsigned)((ML + RED_T - 1) / RED_T), (unsigned)batch);
+            e = T.part32 ? launch_pdl(tiled_reduce<int32_t>, gr, dim3(RED_T), 0, s, T)
+                         : launch_pdl(tiled_reduce<int64_t>, gr, dim3(RED_T), 0, s, T);
+            if (e != cudaSuccess) return tm_cuda_status(e, "tiled_reduce");
+            TM_CHECK_LAUNCH("tiled_reduce");
+        }
     }
-    const int nleft = (int)(std::max<int64_t>(0, p->M1 - (int64_t)P * T.a.NA[0]) +
-                            std::max<int64_t>(0, p->M2 - (int64_t)P * T.a.NA[1]));
     const int with_left = part == 0;  // the leftover outputs belong to part 0
-    if (nleft > 0 && with_left) {
-        const cudaError_t e = launch_pdl(tc_tiled_leftover, dim3((unsigned)((p->K + LSLICE - 1) / LSLICE), (unsigned)batch),
-                                         dim3(256), 0, s, T);
-        if (e != cudaSuccess) return tm_cuda_status(e, "tc_tiled_leftover");
-        TM_CHECK_LAUNCH("tc_tiled_leftover");
-    }
     {
-        const cudaError_t e = launch_pdl(tc_tiled_final, dim3((unsigned)((batch + 127) / 128)), dim3(128), 0, s, T,
-                                         batch, resid, residues_out, k, (int64_t *)r1, (int64_t *)r2, keys_out,
-                                         with_left);
+        const cudaError_t e = launch_pdl(tc_tiled_final, dim3((unsigned)batch), dim3(FIN_T), 0, s, T, batch, resid,
+                                         residues_out, k, keys_out, with_left);
         if (e != cudaSuccess) return tm_cuda_status(e, "tc_tiled_final");
     }
     TM_CHECK_LAUNCH("tc_tiled_final");

@@ -511,7 +511,7 @@ int tm_correlate_impl(const tm_plan_s *p, const void *y1, const void *y2, const 
                       void *tc_ws) {
     if (batch == 0) return TM_OK;
     if (p->dtype == TM_F32 && tm_fft_f32_ok(p))
-        return tm_fft_f32_correlate(p, y1, y2, tf, batch, r1, r2, resid, s);
+        return tm_fft_f32_correlate(p, y1, y2, tf, batch, r1, r2, resid, gntt_scratch, s);
     if (p->dtype == TM_F32) {
         const int nt1 = (int)((p->M1 + F_TK - 1) / F_TK), nt2 = (int)((p->M2 + F_TK - 1) / F_TK);
         const int nt = nt2;
@@ -566,7 +566,10 @@ extern "C" __attribute__((visibility("default"))) int tm_correlate(tm_plan p, co
     if (!p) { tm_set_error("tm_correlate: NULL plan"); return TM_EINVAL; }
     if (batch < 0) { tm_set_error("tm_correlate: batch < 0"); return TM_EINVAL; }
     if (batch > 0 && (!y1 || !y2 || !tf || !r1 || !r2)) { tm_set_error("tm_correlate: NULL pointer"); return TM_EINVAL; }
-    if (p->big_corr && !ws) { tm_set_error("tm_correlate: workspace required for this plan"); return TM_EINVAL; }
+    if ((p->big_corr || tm_fft_f32_long(p)) && !ws) {
+        tm_set_error("tm_correlate: workspace required for this plan");
+        return TM_EINVAL;
+    }
     void *g = ws ? (char *)ws + tm_ws(p, batch).gntt : nullptr;
     return tm_correlate_impl(p, y1, y2, tf, batch, r1, r2, nullptr, nullptr, g, (cudaStream_t)stream, ws);
 }

@@ -21,6 +21,20 @@
 // tables built in double precision on the host, w_n^j at offset n/2 - 1.
 // Error: O(log2 L) fp32 roundings per output, ~1e-6 of max |r| at cfg3 sizes,
 // inside reading C15's 1e-5 normwise tolerance (test_f32_*, test_cfg3_*).
+//
+// Transforms longer than one CTA's registers (L = 2^15 .. 2^18, i.e. K up to
+// 2^17; Table 2's N = 2^26, K = 2^16 needs L = 2^17): the four-step
+// split L = R S, S = 2^14 segment, R = 2 .. 16, index n = s + S r,
+// frequency k = k2 + R k1 (decimation in frequency):
+//   pass A   b_s[k2] = w_L^(s k2) sum_r x[s + S r] w_R^(r k2)    (R-point DFT per s,
+//            one thread per s, written transposed: segment k2 holds b_.[k2])
+//   pass B   per segment k2: the register-resident length-S DIF (above) gives
+//            X[k2 + R k1] in the kernel's bit-reversed register order;
+// the correlation multiplies by the template spectrum in the same order, then
+// inverts: pass B^-1 (per segment, DIT back to natural s) and pass A^-1
+//   out[s + S r] = sum_k2 c_s[k2] w_L^(-s k2) w_R^(-r k2)
+// with the argmax as order-preserving packed keys (float key, ~index) per pair
+// and modulus.  Twiddles w_L^j come from sincospif of the exact fraction 2j/L.
 #include <cmath>
 #include <mutex>
 #include <vector>
@@ -307,6 +321,190 @@ __global__ void __launch_bounds__(FGeo<LOGL>::NT, 1) fft_corr_f32(FftArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// long transforms: four-step (pass A in global memory, pass B per segment)
+// ---------------------------------------------------------------------------
+constexpr int SEG_LOG = 14, SEG = 1 << SEG_LOG;
+constexpr int LONG_MAX_LOGL = 18;
+
+struct FtlArgs {
+    const float *t;           // templates [batch][ldt] (template mode) or NULL
+    int64_t ldt, K;
+    const float *y1, *y2;     // folded signals (correlation mode)
+    int64_t ldy1, ldy2, nload1, nload2, M1, M2;
+    float2 *seg;              // [batch][R][S] segments (template mode: tf itself)
+    const float2 *tf;         // [batch][R][S] template spectra, register order, scaled 1/L
+    const float2 *twf, *twi;  // length-S tables (ftables)
+    float *r1, *r2;           // [batch][Mj] or NULL
+    unsigned long long *keys; // [batch][2] packed argmax keys (correlation mode)
+    int logL;
+};
+
+// w_L^(+-j) (DIR 0: exp(-2 pi i j / L), 1: exp(+2 pi i j / L)), j reduced mod L
+template <int DIR>
+__device__ __forceinline__ float2 wL(int64_t j, int logL) {
+    const int64_t L = (int64_t)1 << logL;
+    j &= (L - 1);
+    float sn, cs;
+    sincospif((float)(2 * j) / (float)L, &sn, &cs);  // 2j/L exact in fp32 (L <= 2^18)
+    return make_float2(cs, DIR ? sn : -sn);
+}
+
+__device__ __forceinline__ unsigned long long fkey(float v, int64_t i) {
+    uint32_t u = __float_as_uint(v);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // order-preserving
+    return ((unsigned long long)u << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)i);
+}
+
+// pass A, forward: thread = s; TEMPL: x = t_rev (real), else x = y1 + i y2
+template <int LOGR, bool TEMPL>
+__global__ void __launch_bounds__(256) fftl_passA(FtlArgs a) {
+    pdl_trigger();
+    pdl_wait();
+    constexpr int R = 1 << LOGR;
+    const int64_t b = blockIdx.y;
+    const int64_t s = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    const int64_t L = (int64_t)SEG << LOGR;
+    if (!TEMPL && s == 0 && a.keys) { a.keys[2 * b] = 0; a.keys[2 * b + 1] = 0; }
+    float2 x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t n = s + (int64_t)SEG * r;
+        if (TEMPL) {
+            const int64_t src = n == 0 ? 0 : L - n;  // t_rev[n] = t[(L - n) mod L] (reading C3)
+            x[r] = make_float2(src < a.K ? a.t[b * a.ldt + src] : 0.f, 0.f);
+        } else {
+            x[r] = make_float2(n < a.nload1 ? a.y1[b * a.ldy1 + n] : 0.f, n < a.nload2 ? a.y2[b * a.ldy2 + n] : 0.f);
+        }
+    }
+    float2 *o = a.seg + b * L + s;
+#pragma unroll
+    for (int k2 = 0; k2 < R; ++k2) {
+        float2 acc = x[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) acc = cadd(acc, tw_mul<0>(x[r], ((r * k2) & (R - 1)) * (128 / R)));
+        o[(int64_t)SEG * k2] = k2 ? cmul(acc, wL<0>(s * k2, a.logL)) : acc;
+    }
+}
+
+// pass B: per (pair, segment).  TEMPL: forward DIF, store scaled by 1/L in the
+// register order; else forward DIF, times the template spectrum, inverse DIT,
+// store back in natural order.
+template <bool TEMPL>
+__global__ void __launch_bounds__(SEG / E, 1) fftl_passB(FtlArgs a) {
+    pdl_trigger();
+    pdl_wait();
+    using G = FGeo<SEG_LOG>;
+    extern __shared__ float fsm[];
+    float *br = fsm, *bi = fsm + G::L;
+    const int t = threadIdx.x;
+    const int64_t R = (int64_t)1 << (a.logL - SEG_LOG);
+    const int64_t b = blockIdx.y, k2 = blockIdx.x;
+    float2 *sg = a.seg + (b * R + k2) * SEG;
+    float2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = sg[G::idx(0, t, m)];
+    fdif<SEG_LOG>(v, br, bi, t, a.twf);
+    if (TEMPL) {
+        const float sc = 1.0f / (float)((int64_t)1 << a.logL);
+        __syncthreads();  // every thread has read its natural-order inputs
+#pragma unroll
+        for (int m = 0; m < E; ++m) sg[m * G::NT + t] = make_float2(v[m].x * sc, v[m].y * sc);
+        return;
+    }
+    const float2 *T = a.tf + (b * R + k2) * SEG;
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = cmul(v[m], T[m * G::NT + t]);
+    fdit<SEG_LOG>(v, br, bi, t, a.twi);
+#pragma unroll
+    for (int m = 0; m < E; ++m) sg[G::idx(0, t, m)] = v[m];
+}
+
+// pass A, inverse + outputs + argmax: thread = s
+template <int LOGR>
+__global__ void __launch_bounds__(256) fftl_passAinv(FtlArgs a) {
+    pdl_trigger();
+    pdl_wait();
+    constexpr int R = 1 << LOGR;
+    const int64_t b = blockIdx.y;
+    const int64_t s = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    const int64_t L = (int64_t)SEG << LOGR;
+    const float2 *in = a.seg + b * L + s;
+    float2 c[R];
+#pragma unroll
+    for (int k2 = 0; k2 < R; ++k2) {
+        const float2 v = in[(int64_t)SEG * k2];
+        c[k2] = k2 ? cmul(v, wL<1>(s * k2, a.logL)) : v;
+    }
+    unsigned long long best[2] = {0ull, 0ull};
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        float2 acc = c[0];
+#pragma unroll
+        for (int k2 = 1; k2 < R; ++k2) acc = cadd(acc, tw_mul<1>(c[k2], ((r * k2) & (R - 1)) * (128 / R)));
+        const int64_t n = s + (int64_t)SEG * r;  // acc = r1[n] + i r2[n]
+        if (n < a.M1) {
+            if (a.r1) a.r1[b * a.M1 + n] = acc.x;
+            const unsigned long long kk = fkey(acc.x, n);
+            if (kk > best[0]) best[0] = kk;
+        }
+        if (n < a.M2) {
+            if (a.r2) a.r2[b * a.M2 + n] = acc.y;
+            const unsigned long long kk = fkey(acc.y, n);
+            if (kk > best[1]) best[1] = kk;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ov = __shfl_xor_sync(0xffffffffu, best[j], o);
+            if (ov > best[j]) best[j] = ov;
+        }
+        if ((threadIdx.x & 31) == 0 && best[j]) atomicMax(a.keys + 2 * b + j, best[j]);
+    }
+}
+
+__global__ void fftl_keys_to_resid(const unsigned long long *keys, int64_t batch, int32_t *resid) {
+    pdl_trigger();
+    pdl_wait();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < 2 * batch) resid[i] = (int32_t)(0xFFFFFFFFu - (uint32_t)(keys[i] & 0xFFFFFFFFull));
+}
+
+template <int LOGR>
+int launch_long(bool templ, const FtlArgs &A, int64_t batch, int32_t *resid, cudaStream_t s) {
+    const dim3 ga((unsigned)(SEG / 256), (unsigned)batch), gb((unsigned)(1 << LOGR), (unsigned)batch);
+    const size_t smem = (size_t)2 * SEG * 4;
+    cudaError_t e;
+    if (templ) {
+        e = launch_pdl(fftl_passA<LOGR, true>, ga, dim3(256), 0, s, A);
+        if (e == cudaSuccess) e = tm_smem_attr((const void *)fftl_passB<true>, (int)smem);
+        if (e == cudaSuccess) e = launch_pdl(fftl_passB<true>, gb, dim3(SEG / E), smem, s, A);
+    } else {
+        e = launch_pdl(fftl_passA<LOGR, false>, ga, dim3(256), 0, s, A);
+        if (e == cudaSuccess) e = tm_smem_attr((const void *)fftl_passB<false>, (int)smem);
+        if (e == cudaSuccess) e = launch_pdl(fftl_passB<false>, gb, dim3(SEG / E), smem, s, A);
+        if (e == cudaSuccess) e = launch_pdl(fftl_passAinv<LOGR>, ga, dim3(256), 0, s, A);
+        if (e == cudaSuccess && resid)
+            e = launch_pdl(fftl_keys_to_resid, dim3((unsigned)((2 * batch + 255) / 256)), dim3(256), 0, s,
+                           (const unsigned long long *)A.keys, batch, resid);
+    }
+    if (e != cudaSuccess) return tm_cuda_status(e, "fft_f32 (long transform)");
+    TM_CHECK_LAUNCH("fft_f32 (long transform)");
+    return TM_OK;
+}
+
+int dispatch_long(int logL, bool templ, const FtlArgs &A, int64_t batch, int32_t *resid, cudaStream_t s) {
+    switch (logL - SEG_LOG) {
+        case 1: return launch_long<1>(templ, A, batch, resid, s);
+        case 2: return launch_long<2>(templ, A, batch, resid, s);
+        case 3: return launch_long<3>(templ, A, batch, resid, s);
+        case 4: return launch_long<4>(templ, A, batch, resid, s);
+        default: return TM_EUNSUPPORTED;
+    }
+}
+
 std::mutex g_fmu;
 struct FTabs {
     bool ready = false;
@@ -383,8 +581,14 @@ int dispatch(int logL, bool templ, const FftArgs &A, int64_t batch, cudaStream_t
 
 }  // namespace
 
-// float32 plans whose transform length fits the register kernel (L2 <= 2^14)
-bool tm_fft_f32_ok(const tm_plan_s *p) { return p->dtype == TM_F32 && p->logL2 >= 9 && p->logL2 <= FFT_MAX_LOGL; }
+// float32 plans whose transform length fits the register kernel (L2 <= 2^14) or
+// the four-step split (2^15 <= L2 <= 2^18)
+bool tm_fft_f32_ok(const tm_plan_s *p) { return p->dtype == TM_F32 && p->logL2 >= 9 && p->logL2 <= LONG_MAX_LOGL; }
+bool tm_fft_f32_long(const tm_plan_s *p) { return tm_fft_f32_ok(p) && p->logL2 > FFT_MAX_LOGL; }
+size_t tm_fft_f32_scratch_bytes(const tm_plan_s *p, int64_t batch) {
+    if (!tm_fft_f32_long(p)) return 0;
+    return (size_t)batch * (size_t)p->L2 * 8 + (size_t)batch * 16 + 256;
+}
 
 // tf [batch][L2] float2: the template spectrum (tm_fold_template for these plans)
 int tm_fft_f32_template(const tm_plan_s *p, const void *t, int64_t ldt, int64_t batch, void *tf, cudaStream_t s) {
@@ -393,6 +597,14 @@ int tm_fft_f32_template(const tm_plan_s *p, const void *t, int64_t ldt, int64_t 
     FftArgs A{};
     int rc = ftables(p->device, &A.twf, &A.twi);
     if (rc) return rc;
+    if (p->logL2 > FFT_MAX_LOGL) {  // four-step: pass A into tf, pass B in place
+        FtlArgs B{};
+        B.t = (const float *)t; B.ldt = ldt; B.K = p->K;
+        B.seg = (float2 *)tf;
+        B.twf = A.twf; B.twi = A.twi;
+        B.logL = p->logL2;
+        return dispatch_long(p->logL2, true, B, batch, nullptr, s);
+    }
     A.t = (const float *)t; A.ldt = ldt; A.K = p->K;
     A.tf = (float2 *)tf;
     A.nb = batch;
@@ -400,12 +612,28 @@ int tm_fft_f32_template(const tm_plan_s *p, const void *t, int64_t ldt, int64_t 
 }
 
 int tm_fft_f32_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *tf, int64_t batch,
-                         void *r1, void *r2, int32_t *resid, cudaStream_t s) {
+                         void *r1, void *r2, int32_t *resid, void *scratch, cudaStream_t s) {
     if (!tm_fft_f32_ok(p)) return TM_EUNSUPPORTED;
     if (batch > 0x7FFFFFFF) return TM_EUNSUPPORTED;
     FftArgs A{};
     int rc = ftables(p->device, &A.twf, &A.twi);
     if (rc) return rc;
+    if (p->logL2 > FFT_MAX_LOGL) {
+        if (!scratch) { tm_set_error("tm_correlate: workspace required for this plan"); return TM_EINVAL; }
+        if (batch > 65535) return TM_EUNSUPPORTED;
+        FtlArgs B{};
+        B.y1 = (const float *)y1; B.y2 = (const float *)y2;
+        B.ldy1 = p->len_y1; B.ldy2 = p->len_y2;
+        B.nload1 = p->M1 + p->K - 1; B.nload2 = p->M2 + p->K - 1;  // reading C4
+        B.M1 = p->M1; B.M2 = p->M2;
+        B.seg = (float2 *)scratch;
+        B.keys = (unsigned long long *)((char *)scratch + (size_t)batch * p->L2 * 8);
+        B.tf = (const float2 *)tf;
+        B.twf = A.twf; B.twi = A.twi;
+        B.r1 = (float *)r1; B.r2 = (float *)r2;
+        B.logL = p->logL2;
+        return dispatch_long(p->logL2, false, B, batch, resid, s);
+    }
     A.tf = (float2 *)const_cast<void *>(tf);
     A.y1 = (const float *)y1; A.y2 = (const float *)y2;
     A.ldy1 = p->len_y1; A.ldy2 = p->len_y2;

@@ -71,11 +71,30 @@ constexpr int PM_COLS = 8 * 512;  // columns per CTA group of the packed kernel 
 // ---------------------------------------------------------------------------
 // finalize: counts -> values, + wrap + extension (partial-fold semantics)
 // ---------------------------------------------------------------------------
+// Cross-GPU combine fused into this epilogue (tm_fold_reduce):
+// instead of storing its values the kernel ADDS them into n destination folds --
+// peer-mapped buffers of the other ranks (red.global.add) or one NVLS multicast
+// address (multimem.red.add: the switch adds into every bound GPU's copy).
+constexpr int RED_MAX = 8;
+struct RedDst {
+    int n, multicast;
+    int32_t *y1[RED_MAX], *y2[RED_MAX];
+};
+__device__ __forceinline__ void red_out(const RedDst &rd, int which, int64_t off, int32_t v) {
+    for (int d = 0; d < rd.n; ++d) {
+        int32_t *p = (which ? rd.y2[d] : rd.y1[d]) + off;
+        if (rd.multicast)
+            asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+        else
+            asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    }
+}
+
 __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t N, int64_t offset,
                               int64_t len, int64_t M1, int64_t M2, int64_t K, int64_t q2,
                               int64_t row0, int64_t rows, const int32_t *__restrict__ counts,
                               int32_t *__restrict__ y1, int64_t ldy1, int32_t *__restrict__ y2, int64_t ldy2,
-                              int accumulate, int block) {
+                              int accumulate, int block, const RedDst rd) {
     pdl_trigger();
     pdl_wait();  // the counts of this fold
     const int64_t b = blockIdx.y;
@@ -114,6 +133,14 @@ __global__ void fold_finalize(const int8_t *__restrict__ x, int64_t ldx, int64_t
                 if (e >= N) e -= N;
                 ve = block ? v : v - xat(k) + xat(e);
             }
+        }
+        if (rd.n) {  // fused cross-GPU combine: add into every destination fold
+            red_out(rd, 0, b * ldy1 + k, v1);
+            if (k < m2) {
+                red_out(rd, 1, b * ldy2 + k, v);
+                if (k < kk) red_out(rd, 1, b * ldy2 + m2 + k, ve);
+            }
+            continue;
         }
         if (accumulate) o1[k] += v1; else o1[k] = v1;
         if (k < m2) {
@@ -156,11 +183,23 @@ void pick_rows_tma(const tm_plan_s *p, int64_t batch, int64_t rows, int64_t n_gr
 
 int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
                 void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, int64_t R, int64_t n_rc,
-                cudaStream_t s, bool *used_counts);
+                cudaStream_t s, bool *used_counts, bool force_counts);
+
+static int fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
+                     void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, cudaStream_t s,
+                     const RedDst *rd);
 
 int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
                     void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, cudaStream_t s) {
+    return fold_impl(p, x, ldx, batch, offset, len, y1, ldy1, y2, ldy2, accumulate, ws, s, nullptr);
+}
+
+static int fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
+                     void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, cudaStream_t s,
+                     const RedDst *rd) {
     if (batch == 0) return TM_OK;
+    RedDst none{};
+    const RedDst &R_ = rd ? *rd : none;
     const bool aligned = ((uintptr_t)x % 16 == 0) && (ldx % 16 == 0);
     const bool fast = p->fast_fold && aligned && (offset % p->M1 == 0) && (len % p->M1 == 0) &&
                       batch <= (int64_t(1) << 31) / 64;
@@ -170,7 +209,7 @@ int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batc
         pick_rows_tma(p, batch, rows, n_groups, &R, &nrc);
         bool used_counts = false;
         int rc = tm_fold_tma(p, x, ldx, batch, offset, len, y1, ldy1, y2, ldy2, accumulate, ws, R, nrc, s,
-                             &used_counts);
+                             &used_counts, rd != nullptr);
         if (rc != TM_EUNSUPPORTED) {
             if (rc != TM_OK || !used_counts) return rc;
             tm_ws_layout L = tm_ws(p, batch);
@@ -178,11 +217,16 @@ int tm_fold_impl_ld(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batc
             { const cudaError_t e_ = launch_pdl(fold_finalize, dim3((unsigned)gx, (unsigned)batch), dim3(256), 0, s,
                 (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, offset / p->M1, rows,
                 (const int32_t *)((char *)ws + L.fold_counts), (int32_t *)y1, ldy1, (int32_t *)y2, ldy2, accumulate,
-                p->block);
+                p->block, R_);
               if (e_ != cudaSuccess) return tm_cuda_status(e_, "tm_fold: fold_finalize"); }
             TM_CHECK_LAUNCH("tm_fold: fold_finalize");
             return TM_OK;
         }
+    }
+    if (rd) {
+        tm_set_error("tm_fold_reduce: needs the packed +-1 fold (TM_BINARY, M1 | N, M1 %% 512 == 0, row-aligned "
+                     "16-byte aligned chunks)");
+        return TM_EUNSUPPORTED;
     }
     if (p->dtype == TM_F32 && ws && len > 0) {  // strip kernel + fixed-order finalize
         tm_ws_layout L = tm_ws(p, batch);
@@ -227,4 +271,32 @@ extern "C" __attribute__((visibility("default"))) int tm_fold(tm_plan p, const v
         return TM_EINVAL;
     }
     return tm_fold_impl(p, x, ldx, batch, offset, len, y1, y2, accumulate, ws, (cudaStream_t)stream);
+}
+
+extern "C" __attribute__((visibility("default"))) int tm_fold_reduce(tm_plan p, const void *x, int64_t ldx,
+                                                                     int64_t batch, int64_t offset, int64_t len,
+                                                                     int ndst, void *const *dst_y1,
+                                                                     void *const *dst_y2, int multicast, void *ws,
+                                                                     void *stream) {
+    if (!p) { tm_set_error("tm_fold_reduce: NULL plan"); return TM_EINVAL; }
+    if (batch < 0 || offset < 0 || len < 0 || offset + len > p->N) {
+        tm_set_error("tm_fold_reduce: bad batch / chunk");
+        return TM_EINVAL;
+    }
+    if (ndst < 1 || ndst > RED_MAX || (multicast && ndst != 1) || !dst_y1 || !dst_y2 || !ws || (batch > 0 && !x)) {
+        tm_set_error("tm_fold_reduce: need 1 <= ndst <= %d destinations (1 with multicast), ws and x", RED_MAX);
+        return TM_EINVAL;
+    }
+    if (p->dtype != TM_I8) { tm_set_error("tm_fold_reduce: TM_I8 plans only"); return TM_EUNSUPPORTED; }
+    if (batch == 0 || len == 0) return TM_OK;
+    RedDst rd{};
+    rd.n = ndst;
+    rd.multicast = multicast ? 1 : 0;
+    for (int d = 0; d < ndst; ++d) {
+        if (!dst_y1[d] || !dst_y2[d]) { tm_set_error("tm_fold_reduce: NULL destination"); return TM_EINVAL; }
+        rd.y1[d] = (int32_t *)dst_y1[d];
+        rd.y2[d] = (int32_t *)dst_y2[d];
+    }
+    return fold_impl(p, x, ldx, batch, offset, len, nullptr, p->len_y1, nullptr, p->len_y2, 0, ws,
+                     (cudaStream_t)stream, &rd);
 }

@@ -102,6 +102,12 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
 }
 __device__ __forceinline__ void bulk_g2s_ef(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
                                             uint64_t pol) {
+#ifdef TM_NO_EVICT_FIRST  // A/B only
+    (void)pol;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+    return;
+#endif
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(dst)),
@@ -610,8 +616,12 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                             W[4 - alpha + kk] += add;
                         }
                     };
+#ifndef TM_FOLD_NOCOMPUTE
                     if (full_tile) group(std::true_type{});
                     else group(std::false_type{});
+#else  // A/B only: the fold's streaming without its arithmetic (results are wrong)
+                    (void)full_tile;
+#endif
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
@@ -782,10 +792,14 @@ __global__ void zero_i32(int32_t *p, int64_t n) {
 
 int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
                 void *y1, int64_t ldy1, void *y2, int64_t ldy2, int accumulate, void *ws, int64_t R, int64_t n_rc,
-                cudaStream_t s, bool *used_counts) {
+                cudaStream_t s, bool *used_counts, bool force_counts) {
     TmaArgs a{};
     int rc = setup_args(p, x, ldx, batch, offset, len, y1, y2, accumulate, ws, R, n_rc, a);
     if (rc) return rc;
+    if (force_counts && a.owner) {  // tm_fold_reduce: the finalize kernel writes the outputs
+        a.owner = 0;
+        a.xs_bytes = 0;
+    }
     a.ldy1 = ldy1; a.ldy2 = ldy2;
     *used_counts = !a.owner;
     if (!a.owner) {

@@ -273,6 +273,7 @@ tm_ws_layout tm_ws(const tm_plan_s *p, int64_t batch) {
     if (p->dtype == TM_F32) off += align256((size_t)batch * 2 * ((p->M2 + 1023) / 1024) * 8);
     w.gntt = off;
     if (p->big_corr) off += align256(tm_gntt_scratch_bytes(p, batch));
+    off += align256(tm_fft_f32_scratch_bytes(p, batch));  // fp32 four-step FFT segments + keys
     w.counters = off;
     off += 256;
     w.tiled = off;

@@ -86,7 +86,7 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
         rc = tm_fold_template(p, t, batch, W.tf, stream);                            // step 4 (+5 for t)
         if (rc) return rc;
         tm_prof_mark(2, s);
-        rc = tm_correlate_impl(p, W.y1, W.y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, nullptr, s);  // 5-7
+        rc = tm_correlate_impl(p, W.y1, W.y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, W.gntt, s);  // 5-7
         if (rc) return rc;
     }
     tm_prof_mark(3, s);
@@ -166,7 +166,7 @@ extern "C" __attribute__((visibility("default"))) int tm_correlate_match(tm_plan
     } else {
         rc = tm_fold_template(p, t, batch, W.tf, stream);
         if (rc == TM_OK)
-            rc = tm_correlate_impl(p, y1, y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, nullptr, s);
+            rc = tm_correlate_impl(p, y1, y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, W.gntt, s);
     }
     if (rc) return rc;
     return tm_crt_impl(p, W.resid, batch, residues, k, s);

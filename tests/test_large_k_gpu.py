@@ -91,3 +91,16 @@ def test_cfg5_companions_sampled(tm, K):
     z = oracle.crt(int(res[0, 0]), plan.M1, int(res[0, 1]), plan.M2)
     assert k[0] == k_run[0] == (z if z < N else -1)
     print(f"K = {K}: k = {int(k_run[0])}, planted {k0}")
+
+
+@pytest.mark.parametrize("N,K", [(2 ** 20, 16384), (2 ** 22, 32768), (2 ** 26, 65536), (2 ** 24, 131072)])
+def test_f32_four_step_fft(tm, N, K):
+    """fp32 correlations whose transform exceeds one CTA's registers (L2 = 2^15 ..
+    2^18; (2^26, 2^16) is PAPER.md Table 2's shape): the four-step FFT
+    (pass A across 2^14-entry segments, pass B per segment) under reading C15
+    against the oracle's fp64 direct correlation, one pair each."""
+    from test_parity_gpu import check_f32_pairs
+    plan = tm.Plan(N, K, seed=151, dtype="float32")
+    assert plan.L2 > 2 ** 14
+    x_h, t_h, _ = tmgen.batch(151, 0, 1, N, K, 0.5, dtype=np.float32)
+    check_f32_pairs(tm, plan, x_h, t_h, [0])
