@@ -16,6 +16,16 @@ spread over G ranks (one process per GPU) as contiguous row-aligned chunks:
    ``tm_match_keys`` give identical residues and k on every rank.  Plans the
    split engine does not take (fp32 data) correlate redundantly on every rank.
 
+Fused combine (``reducer=``): instead of a fold into the
+local buffer followed by an NCCL all-reduce, every rank's fold epilogue ADDS its
+partial fold into all ranks' buffers at once (``tm_fold_reduce``: red.add into
+peer-mapped symmetric memory, or one multimem.red into an NVLS multicast
+address), so the reduction travels over NVLink while the epilogue runs and no
+separate collective is launched.  Per step: barrier (every rank has zeroed its
+buffer after the previous step) -> fold_reduce -> barrier (every rank's adds
+have landed) -> correlation -> zero the local buffer.  ``SymmReducer`` does this
+with torch symmetric memory; tests substitute a CPU stand-in.
+
 This module is host glue only (no arithmetic of the method); every step runs
 in libtm's kernels or in the collective.  ``plan`` is a ``Plan`` (or any object
 with the same methods -- the CPU wiring test stands the oracle in for it).
@@ -38,7 +48,7 @@ class SingleSignal:
     """
 
     def __init__(self, plan, rank: int = 0, world: int = 1, group=None, device="cuda",
-                 split_correlation: bool | None = None):
+                 split_correlation: bool | None = None, reducer=None):
         import torch
         self.plan, self.rank, self.world, self.group = plan, rank, world, group
         self.offset, self.length = signal_chunks(plan.N, plan.M1, world)[rank]
@@ -46,7 +56,11 @@ class SingleSignal:
         # y1 region padded to 32 entries (128 B) so y2 starts 16-byte aligned for the
         # kernels' vector loads; the padding is zero and never read.
         self.ldy1 = _round_up(n1, 32)
-        self.flat = torch.zeros(self.ldy1 + n2, dtype=plan.y_dtype, device=device)
+        self.reducer = reducer
+        if reducer is None:
+            self.flat = torch.zeros(self.ldy1 + n2, dtype=plan.y_dtype, device=device)
+        else:   # symmetric (peer-visible) buffer, zeroed, owned by the reducer
+            self.flat = reducer.make_flat(self.ldy1 + n2, plan.y_dtype, device, self.ldy1)
         self.y1 = self.flat[:n1].view(1, n1)
         self.y2 = self.flat[self.ldy1:].view(1, n2)
         self.ws = plan.workspace(1, device)
@@ -62,12 +76,23 @@ class SingleSignal:
         return self.flat.numel() * self.flat.element_size()
 
     def fold(self, x_chunk, stream=None):
-        """Step 3 on this rank's chunk: the partial fold into the y1 / y2 views."""
+        """Step 3 on this rank's chunk: the partial fold into the y1 / y2 views, or
+        (fused combine) added into every rank's buffer by the fold's epilogue."""
+        if self.reducer is not None:
+            self.reducer.barrier()   # every rank has zeroed its buffer since it last read it
+            d1, d2, mc = self.reducer.destinations()
+            self.plan.fold_reduce(x_chunk, d1, d2, offset=self.offset, length=self.length, multicast=mc,
+                                  ws=self.ws, stream=stream)
+            return
         self.plan.fold(x_chunk, offset=self.offset, length=self.length, y1=self.y1, y2=self.y2,
                        accumulate=False, ws=self.ws, stream=stream)
 
     def combine(self):
-        """Sum the partial folds over the ranks in place (one all-reduce of y1 || y2)."""
+        """Sum the partial folds over the ranks in place (one all-reduce of y1 || y2);
+        fused combine: wait until every rank's adds have landed."""
+        if self.reducer is not None:
+            self.reducer.barrier()
+            return
         if self.world > 1:
             import torch.distributed as dist
             dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
@@ -105,4 +130,35 @@ class SingleSignal:
             out = self.match(t, stream=stream)
             if events:
                 events[3].record()
+            if self.reducer is not None:
+                self.flat.zero_()   # ready for the next step's adds (ordered by its first barrier)
         return out
+
+
+class SymmReducer:
+    """Fused combine over torch symmetric memory (NVLink peer mappings; NVLS
+    multicast when the system supports it).  One per process group."""
+
+    def __init__(self, group=None, use_multicast: bool = True):
+        import torch.distributed as dist
+        self.group = group if group is not None else dist.group.WORLD
+        self.use_multicast = use_multicast
+        self.handle = None
+
+    def make_flat(self, n, dtype, device, ldy1):
+        import torch.distributed._symmetric_memory as symm
+        flat = symm.empty(n, dtype=dtype, device=device)
+        flat.zero_()
+        self.handle = symm.rendezvous(flat, self.group.group_name)
+        self.ldy1, self.esize = ldy1, flat.element_size()
+        self.handle.barrier(channel=0)
+        return flat
+
+    def destinations(self):
+        h, off2 = self.handle, self.ldy1 * self.esize
+        if self.use_multicast and h.has_multicast_support and h.multicast_ptr:
+            return [h.multicast_ptr], [h.multicast_ptr + off2], True
+        return list(h.buffer_ptrs), [p + off2 for p in h.buffer_ptrs], False
+
+    def barrier(self):
+        self.handle.barrier(channel=0)

@@ -212,3 +212,97 @@ def test_single_signal_wiring_gloo(world):
         assert off == covered
         covered += ln
     assert covered == 64 * 45
+
+
+# --------------------------------------------------------------------------------
+# Fused combine (SingleSignal(reducer=...), tm_fold_reduce):
+# the protocol -- barrier, every rank ADDS its partial fold into every rank's
+# buffer, barrier, correlate, zero -- on gloo ranks with CPU shared-memory buffers
+# standing in for symmetric memory and the oracle standing in for the kernels.
+class SharedCpuReducer:
+    def __init__(self, bufs, rank, lock):
+        self.bufs, self.rank, self.lock = bufs, rank, lock
+
+    def make_flat(self, n, dtype, device, ldy1):
+        assert self.bufs[self.rank].numel() == n
+        self.ldy1 = ldy1
+        return self.bufs[self.rank]
+
+    def destinations(self):
+        return ([b[:self.n1] for b in self.bufs], [b[self.ldy1:] for b in self.bufs], False)
+
+    def barrier(self):
+        dist.barrier()
+
+
+class OracleReducePlan(OraclePlan):
+    def __init__(self, N, K, lock):
+        super().__init__(N, K)
+        self.lock = lock
+
+    def fold_reduce(self, x, d1, d2, offset, length, multicast, ws, stream):
+        import oracle
+        xfull = np.zeros(self.N, np.int8)
+        xfull[offset:offset + length] = x[0].numpy()
+        p1 = torch.from_numpy(oracle.fold(xfull, self.M1, self.K, offset, length)).to(torch.int32)
+        p2 = torch.from_numpy(oracle.fold(xfull, self.M2, self.K, offset, length)).to(torch.int32)
+        with self.lock:  # the device's red.add is atomic; CPU stand-in: one writer at a time
+            for a, b in zip(d1, d2):
+                a.add_(p1)
+                b.add_(p2)
+        self.calls.append("fold_reduce")
+
+
+def _fused_worker(rank, world, port, bufs, lock, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import tmgen
+        from paper_1509_04863_b200.single import SingleSignal
+        N, K = 64 * 45, 64
+        plan = OracleReducePlan(N, K, lock)
+        red = SharedCpuReducer(bufs, rank, lock)
+        red.n1 = plan.len_y1
+        ss = SingleSignal(plan, rank, world, device="cpu", reducer=red)
+        ok = True
+        for seed in (13, 14):   # two steps: the buffers must be re-zeroed between them
+            x = tmgen.signal(seed, 0, N)
+            t = tmgen.template(seed, 0, N, K, 0.05)
+            xc = torch.from_numpy(x[ss.offset:ss.offset + ss.length].copy()).view(1, -1)
+            ss.fold(xc)
+            ss.combine()
+            y1, y2 = ss.y1[0].clone().numpy(), ss.y2[0].clone().numpy()
+            res, k = ss.match(torch.from_numpy(t).view(1, -1))
+            ss.flat.zero_()
+            o = oracle.ftm(x, t)
+            ok &= (np.array_equal(y1, o["y1"]) and np.array_equal(y2, o["y2"]) and
+                   tuple(res[0].tolist()) == o["residues"] and int(k[0]) == o["k"])
+        q.put((rank, ok, plan.calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_single_signal_fused_combine_gloo(world):
+    """Every rank adds its partial fold into every rank's buffer (the fused
+    combine's protocol); after the second barrier each buffer holds the whole
+    fold, and residues and k equal the oracle's, on two consecutive steps."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    lock = ctx.Lock()
+    N, K = 64 * 45, 64
+    n = (64 + K + 31) // 32 * 32 + 65 + K
+    bufs = [torch.zeros(n, dtype=torch.int32).share_memory_() for _ in range(world)]
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, bufs, lock, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, calls in res:
+        assert ok, rank
+        assert calls.count("fold_reduce") == 2 and "part" in calls

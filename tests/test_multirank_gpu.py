@@ -127,3 +127,82 @@ def test_cfg5_ranks_1_2_4_8_identical(tm):
             np.testing.assert_array_equal(a1[0], y1, err_msg=f"G={world} rank {rank} y1")
             np.testing.assert_array_equal(a2[0], y2, err_msg=f"G={world} rank {rank} y2")
             assert r == res and kk == k, (world, rank)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+def test_fold_reduce_emulated_ranks(tm, G):
+    """tm_fold_reduce (the combine fused into the fold epilogue, SURVEY 8(f)
+    f4(iii)): G ranks emulated in one process -- each chunk's fold is ADDED into
+    all G destination buffers (red.global.add); afterwards every buffer holds the
+    whole signal's fold, equal to tm_fold and to the oracle.  N = 2^26, K = 8192."""
+    from paper_1509_04863_b200.dist import signal_chunks
+    N, K, seed = 2 ** 26, 8192, 72
+    plan = tm.Plan(N, K, seed=seed)
+    x, t, _ = plan.generate(0, 1, 0.05)
+    y1, y2 = plan.fold(x)
+    bufs = [(torch.zeros((1, plan.len_y1), dtype=torch.int32, device=DEV),
+             torch.zeros((1, plan.len_y2), dtype=torch.int32, device=DEV)) for _ in range(G)]
+    for off, ln in signal_chunks(N, plan.M1, G):
+        plan.fold_reduce(x[:, off:off + ln], [b[0] for b in bufs], [b[1] for b in bufs], offset=off, length=ln)
+    torch.cuda.synchronize()
+    o = oracle.ftm(tmgen.signal(seed, 0, N), tmgen.template(seed, 0, N, K, 0.05))
+    for a1, a2 in bufs:
+        assert torch.equal(a1, y1) and torch.equal(a2, y2)
+        np.testing.assert_array_equal(a1[0].cpu().numpy(), o["y1"])
+        np.testing.assert_array_equal(a2[0].cpu().numpy(), o["y2"])
+
+
+def _symm_worker(port, q):
+    """One-rank process group + torch symmetric memory: the fused combine through
+    the real symmetric-memory buffers (the NVLS multicast address when this box
+    offers one, else the peer-pointer path)."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    try:
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        import paper_1509_04863_b200 as tm
+        from paper_1509_04863_b200.single import SingleSignal, SymmReducer
+        N, K = 2 ** 26, 8192
+        plan = tm.Plan(N, K, seed=73)
+        x, t, _ = plan.generate(0, 1, 0.05)
+        ref = SingleSignal(plan, 0, 1, device="cuda:0")
+        r0, k0 = ref.step(x, t)
+        out = {}
+        for mc in (True, False):
+            red = SymmReducer(use_multicast=mc)
+            ss = SingleSignal(plan, 0, 1, device="cuda:0", reducer=red)
+            multicast = red.destinations()[2]
+            for _ in range(2):
+                ss.fold(x)
+                ss.combine()
+                same = torch.equal(ss.y1, ref.y1) and torch.equal(ss.y2, ref.y2)
+                r, k = ss.match(t)
+                same &= torch.equal(r, r0) and torch.equal(k, k0)
+                ss.flat.zero_()
+            torch.cuda.synchronize()
+            out["multicast" if multicast else "peer"] = bool(same)
+        q.put(("ok", out))
+    except Exception as e:
+        q.put(("unavailable", repr(e)[:300]))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_fused_combine_symmetric_memory_one_rank(tm):
+    """SingleSignal(reducer=SymmReducer()) on one rank: the fold epilogue adds into
+    the symmetric-memory buffer (multicast when supported), two steps, identical to
+    the plain path.  Skipped if this box offers no symmetric memory."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_symm_worker, args=(_free_port(), q))
+    p.start()
+    status, out = q.get(timeout=600)
+    p.join(timeout=120)
+    if status != "ok":
+        pytest.skip(f"symmetric memory unavailable here: {out}")
+    print("fused combine paths:", out)
+    assert all(out.values()), out
