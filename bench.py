@@ -75,6 +75,9 @@ def parse():
                     help="1: D_{M+K} (P:152, default); 2: Block Phi of Theorem 2 (P:159-177, TM_BLOCK)")
     ap.add_argument("--no-stage-events", action="store_true", help="A/B only: no per-step stage events")
     ap.add_argument("--no-cfg1", action="store_true", help="skip the cfg1 latency sample")
+    ap.add_argument("--fused-reduce", action="store_true",
+                    help="cfg5, world > 1: combine the partial folds in the fold epilogue (tm_fold_reduce into "
+                         "symmetric memory / NVLS multicast, SURVEY 8(f) f4(iii)) instead of an NCCL all-reduce")
     ap.add_argument("--ref-seconds", type=float, default=150.0,
                     help="--impl reference: CPU budget of the timed steps (each step is whole pairs)")
     return ap.parse_args()
@@ -513,7 +516,11 @@ def run_single_signal(args, wl, rank, world, local, dev):
     N, K = wl["N"], wl["K"]
     plan = tm.Plan(N, K, seed=wl["seed"], dtype=wl["dtype"], block=args.strategy == 2, inputs_stable=True)
     stream = torch.cuda.current_stream()
-    ss = SingleSignal(plan, rank, world, device=dev)
+    reducer = None
+    if args.fused_reduce and world > 1:
+        from paper_1509_04863_b200.single import SymmReducer
+        reducer = SymmReducer()
+    ss = SingleSignal(plan, rank, world, device=dev, reducer=reducer)
     off, ln = ss.offset, ss.length
     x, t, k0 = plan.generate(0, 1, wl["noise"], offset=off, length=ln, device=dev)
     torch.cuda.synchronize()
@@ -587,8 +594,12 @@ def run_single_signal(args, wl, rank, world, local, dev):
             "data": "synthetic (seeded counter-based generator, chunks generated on each rank's device)",
             "config": {"workload": wl["desc"], "N": N, "K": K, "M1": plan.M1, "M2": plan.M2, "chunk_samples": ln,
                        "parallelism": f"sequence split over {world} rank(s)"
-                                      + (f" + in-place all-reduce of y1||y2 ({ss.reduce_bytes} B) + correlation "
-                                         f"split by output blocks + all-reduce MAX of 16 B keys" if world > 1 else ""),
+                                      + ((f" + fold epilogue adding y1||y2 ({ss.reduce_bytes} B) into every rank's "
+                                          f"symmetric buffer ({'NVLS multicast' if reducer.destinations()[2] else 'peer'})"
+                                          if reducer is not None else
+                                          f" + in-place all-reduce of y1||y2 ({ss.reduce_bytes} B)")
+                                         + " + correlation split by output blocks + all-reduce MAX of 16 B keys"
+                                         if world > 1 else ""),
                        "l2": "no flush: per-rank input > 126 MB L2"},
             "roofline": roofline_block("hbm", achieved, fold_ms, fold_bytes,
                                        "tm_fold (zero_i32 + fold_pm1_tma + fold_finalize)",

@@ -20,6 +20,7 @@ import tmgen
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
+DEV = "cuda:0"
 
 
 def _free_port():
