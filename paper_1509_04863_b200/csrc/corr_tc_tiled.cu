@@ -70,7 +70,12 @@ struct TiledArgs {
     void *part;                // [batch][n_cr][M1 + M2] partial r of each template range (n_cr > 1):
     int part32;                // int32 when every partial provably fits (plan bound), else int64
     int64_t *r_out[2];         // [batch][Mj] r outputs (staged tm_correlate) or NULL
-    int64_t *lpart;            // [batch][n_pcta][2 MAXLEFT] leftover partial dot products
+    int64_t *lpart;            // [batch][n_pcta][2][MAXLEFT] leftover partial dot products
+    unsigned *done;            // [batch] CTAs of the pair's last kernel finished (zeroed by prep)
+    int n_last;                // CTAs per pair of the last kernel (it runs finish_pair)
+    int32_t *resid, *residues_out;   // finish_pair outputs (may be NULL)
+    int64_t *k_out, *keys_out;
+    int with_left;
 };
 
 __device__ __forceinline__ unsigned long long pack_key(int64_t r, int64_t k) {
@@ -104,12 +109,13 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
     const int64_t gtid = (int64_t)blockIdx.x * PREP_T + tid, gstride = (int64_t)gridDim.x * PREP_T;
     const int8_t *tr = a.t + b * a.ldt;
     const int nl0 = nleft_of(a.M[0], a.NA[0]), nl1 = nleft_of(a.M[1], a.NA[1]);
-    int64_t lacc[2 * MAXLEFT];
+    int64_t lacc0[MAXLEFT], lacc1[MAXLEFT];  // static indices: registers
 #pragma unroll
-    for (int q = 0; q < 2 * MAXLEFT; ++q) lacc[q] = 0;
+    for (int q = 0; q < MAXLEFT; ++q) lacc0[q] = lacc1[q] = 0;
 
-    // ---- zeroing (the keys are max-reduced by the later kernels)
+    // ---- zeroing (the keys are max-reduced by the later kernels; done counts CTAs)
     if (blockIdx.x == 0 && tid < 2) T.keys[2 * b + tid] = 0;
+    if (blockIdx.x == 0 && tid == 0) T.done[b] = 0;
 
     // ---- planes + block limb counts + leftovers: thread = 16 entries (block s,
     // modulus j, chunk column h); 16 consecutive threads cover one block of both moduli
@@ -163,15 +169,18 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
         }
         // leftover outputs k of modulus j: sum over this piece of t[idx - k] y_j[idx]
         const int nlj = j ? nl1 : nl0;
-        for (int q = 0; q < nlj; ++q) {
-            const int64_t k = (int64_t)P * a.NA[j] + q;
-            int64_t acc = 0;
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                const int64_t i = i0 + e - k;
-                if (i >= 0 && i < a.K) acc += (int64_t)tr[i] * v[e];
+        for (int q = 0; q < MAXLEFT; ++q) {
+            if (q < nlj) {
+                const int64_t k = (int64_t)P * a.NA[j] + q;
+                int64_t acc = 0;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const int64_t i = i0 + e - k;
+                    if (i >= 0 && i < a.K) acc += (int64_t)tr[i] * v[e];
+                }
+                if (j) lacc1[q] += acc; else lacc0[q] += acc;
             }
-            lacc[(j ? nl0 : 0) + q] += acc;
         }
     }
 
@@ -200,20 +209,85 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
     }
 
     // ---- leftover partials of this CTA (fixed order: warp shuffle, then warps in order)
+    if (nl0 + nl1 == 0) return;
     __shared__ int64_t red[PREP_T / 32][2 * MAXLEFT];
-    const int nq = nl0 + nl1;
-    for (int q = 0; q < nq; ++q) {
-        int64_t v = lacc[q];
+#pragma unroll
+    for (int q = 0; q < 2 * MAXLEFT; ++q) {
+        int64_t v = q < MAXLEFT ? lacc0[q] : lacc1[q - MAXLEFT];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if ((tid & 31) == 0) red[tid >> 5][q] = v;
     }
     __syncthreads();
-    if (tid < nq) {
+    if (tid < 2 * MAXLEFT) {
         int64_t v = 0;
         for (int w = 0; w < PREP_T / 32; ++w) v += red[w][tid];
         T.lpart[(b * T.n_pcta + blockIdx.x) * 2 * MAXLEFT + tid] = v;
     }
+}
+
+// Steps 7-9 of pair b, run by the CTA that finishes the pair's last kernel (all its
+// threads): the prep CTAs' leftover partials summed in a fixed order, the
+// leftovers merged into the tile keys, residues, k (or the split part's keys).
+__device__ void finish_pair(const TiledArgs &T, int64_t b) {
+    const TcArgs &a = T.a;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int nleft0 = nleft_of(a.M[0], a.NA[0]), nleft1 = nleft_of(a.M[1], a.NA[1]);
+    __shared__ int64_t fred[16][2 * MAXLEFT];
+    __shared__ int64_t lsum[2 * MAXLEFT];
+    if (T.with_left && nleft0 + nleft1) {
+        for (int q = 0; q < 2 * MAXLEFT; ++q) {
+            int64_t r = 0;
+            for (int c = tid; c < T.n_pcta; c += blockDim.x) r += __ldcg(T.lpart + (b * T.n_pcta + c) * 2 * MAXLEFT + q);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+            if (lane == 0) fred[warp][q] = r;
+        }
+        __syncthreads();
+        if (tid < 2 * MAXLEFT) {
+            int64_t r = 0;
+            for (int w = 0; w < nw; ++w) r += fred[w][tid];
+            lsum[tid] = r;
+        }
+        __syncthreads();
+    }
+    if (tid) return;
+    int64_t m[2];
+    for (int j = 0; j < 2; ++j) {
+        int64_t bv = INT64_MIN, bk = INT64_MAX;
+        const unsigned long long key = __ldcg(T.keys + 2 * b + j);
+        if (key) {
+            bk = ((int64_t)1 << KEY_SHIFT) - 1 - (int64_t)(key & (((unsigned long long)1 << KEY_SHIFT) - 1));
+            bv = (int64_t)(key >> KEY_SHIFT) - KEY_BIAS;
+        }
+        const int nleft = T.with_left ? (j ? nleft1 : nleft0) : 0;
+        for (int q = 0; q < nleft; ++q) {
+            const int64_t r = lsum[j * MAXLEFT + q];
+            const int64_t k = (int64_t)P * a.NA[j] + q;
+            if (T.r_out[j]) T.r_out[j][b * a.M[j] + k] = r;
+            amax(bv, bk, r, k);
+        }
+        m[j] = bk;
+        if (T.keys_out)  // split correlation: this part's (max r, lowest k) as an order-preserving int64
+            T.keys_out[2 * b + j] = bk == INT64_MAX ? INT64_MIN : (int64_t)(pack_key(bv, bk) ^ (1ull << 63));
+    }
+    if (T.keys_out) return;
+    if (T.resid) { T.resid[2 * b] = (int32_t)m[0]; T.resid[2 * b + 1] = (int32_t)m[1]; }
+    if (T.residues_out) { T.residues_out[2 * b] = (int32_t)m[0]; T.residues_out[2 * b + 1] = (int32_t)m[1]; }
+    if (T.k_out) T.k_out[b] = tm_resolve(m[0], m[1], a.M1, a.M2, a.crt_inv, a.N, a.crt_wrap);  // steps 8-9
+}
+
+// every CTA of the pair's last kernel calls this after its atomics; the last to
+// arrive runs finish_pair (all threads of the CTA must call it)
+__device__ __forceinline__ void arrive_and_finish(const TiledArgs &T, int64_t b) {
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(T.done + b, 1u) == (unsigned)(T.n_last - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    finish_pair(T, b);
 }
 
 // ---------------------------------------------------------------------------
@@ -409,6 +483,7 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
         d[7] = ((long long)smid << 32) | ((long long)npass << 8) | nl;
     }
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols));
+    if (T.n_cr == 1) arrive_and_finish(T, b);  // this kernel is the pair's last
 }
 
 // several template ranges: r = sum of the ranges' partials (fixed order, exact
@@ -456,61 +531,17 @@ __global__ void __launch_bounds__(RED_T) tiled_reduce(const TiledArgs T) {
         }
         if (lane == 0 && bk[j] != INT64_MAX) atomicMax(T.keys + 2 * b + j, pack_key(bv[j], bk[j]));
     }
+    arrive_and_finish(T, b);
 }
 
 // per pair (one CTA of FIN_T threads): tile keys + leftovers -> residues; steps 8-9 (tm_resolve)
 constexpr int FIN_T = 256;
-__global__ void __launch_bounds__(FIN_T) tc_tiled_final(const TiledArgs T, int64_t batch, int32_t *resid,
-                                                       int32_t *residues_out, int64_t *k_out, int64_t *keys_out,
-                                                       int with_left) {
+// (only when this launch has no tiles -- a part of a split correlation past the
+// last tile: then no main kernel runs to finish the pair)
+__global__ void __launch_bounds__(FIN_T) tc_tiled_final(const TiledArgs T) {
     pdl_trigger();
     pdl_wait();
-    const TcArgs &a = T.a;
-    const int64_t b = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nleft0 = nleft_of(a.M[0], a.NA[0]), nleft1 = nleft_of(a.M[1], a.NA[1]);
-    const int nq = with_left ? nleft0 + nleft1 : 0;
-    __shared__ int64_t red[FIN_T / 32][2 * MAXLEFT];
-    __shared__ int64_t lsum[2 * MAXLEFT];
-    // leftover dot products: the prep CTAs' partials, summed in a fixed order
-    for (int q = 0; q < nq; ++q) {
-        int64_t r = 0;
-        for (int c = tid; c < T.n_pcta; c += FIN_T) r += T.lpart[(b * T.n_pcta + c) * 2 * MAXLEFT + q];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-        if (lane == 0) red[warp][q] = r;
-    }
-    __syncthreads();
-    if (tid < nq) {
-        int64_t r = 0;
-        for (int w = 0; w < FIN_T / 32; ++w) r += red[w][tid];
-        lsum[tid] = r;
-    }
-    __syncthreads();
-    if (tid) return;
-    int64_t m[2];
-    for (int j = 0; j < 2; ++j) {
-        int64_t bv = INT64_MIN, bk = INT64_MAX;
-        const unsigned long long key = T.keys[2 * b + j];
-        if (key) {
-            bk = ((int64_t)1 << KEY_SHIFT) - 1 - (int64_t)(key & (((unsigned long long)1 << KEY_SHIFT) - 1));
-            bv = (int64_t)(key >> KEY_SHIFT) - KEY_BIAS;
-        }
-        const int nleft = with_left ? (j ? nleft1 : nleft0) : 0;
-        for (int q = 0; q < nleft; ++q) {
-            const int64_t r = lsum[(j ? nleft0 : 0) + q];
-            const int64_t k = (int64_t)P * a.NA[j] + q;
-            if (T.r_out[j]) T.r_out[j][b * a.M[j] + k] = r;
-            amax(bv, bk, r, k);
-        }
-        m[j] = bk;
-        if (keys_out)  // split correlation: this part's (max r, lowest k) as an order-preserving int64
-            keys_out[2 * b + j] = bk == INT64_MAX ? INT64_MIN : (int64_t)(pack_key(bv, bk) ^ (1ull << 63));
-    }
-    if (keys_out) return;
-    if (resid) { resid[2 * b] = (int32_t)m[0]; resid[2 * b + 1] = (int32_t)m[1]; }
-    if (residues_out) { residues_out[2 * b] = (int32_t)m[0]; residues_out[2 * b + 1] = (int32_t)m[1]; }
-    if (k_out) k_out[b] = tm_resolve(m[0], m[1], a.M1, a.M2, a.crt_inv, a.N, a.crt_wrap);  // steps 8-9
+    finish_pair(T, blockIdx.x);
 }
 
 // split correlation: all-reduced (MAX) keys -> residues -> steps 8-9
@@ -537,7 +568,8 @@ constexpr size_t PART_BUDGET = (size_t)64 << 20;  // bytes of partial sums (seve
 int tiled_nt(const tm_plan_s *p, int64_t batch) {
     static const char *env = getenv("TM_TILED_NT");  // A/B: "32" or "64"
     if (env && (atoi(env) == 32 || atoi(env) == 64)) return atoi(env);
-    const int64_t na = std::max(p->M1, p->M2) / P + 1;
+    int64_t na = 1;
+    for (int64_t M : {p->M1, p->M2}) na = std::max(na, M / P + (M % P > MAXLEFT ? 1 : 0));
     return batch * ((na + 63) / 64) >= p->num_sms ? 64 : 32;
 }
 struct Geo {
@@ -609,6 +641,7 @@ size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch) {
     n += align_up256((size_t)batch * g.np * 8 * 32 * g.S);                  // B planes
     n += align_up256((size_t)batch * g.JT * 256);                           // A image
     n += align_up256((size_t)batch * g.n_pcta * 2 * MAXLEFT * 8);           // leftover partials
+    n += align_up256((size_t)batch * 4);                                    // done counters
     return n + 256;
 }
 
@@ -666,6 +699,9 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     T.planes = (uint8_t *)carve((size_t)batch * g.np * 8 * 32 * g.S);
     T.aimg = (uint8_t *)carve((size_t)batch * g.JT * 256);
     T.lpart = (int64_t *)carve((size_t)batch * g.n_pcta * 2 * MAXLEFT * 8);
+    T.done = (unsigned *)carve((size_t)batch * 4);
+    T.resid = resid; T.residues_out = residues_out; T.k_out = k; T.keys_out = keys_out;
+    T.with_left = part == 0;  // the leftover outputs belong to part 0
     T.r_out[0] = (int64_t *)r1;
     T.r_out[1] = (int64_t *)r2;
     {
@@ -674,8 +710,11 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         TM_CHECK_LAUNCH("tm_correlate: tiled_prep");
     }
     const dim3 grid((unsigned)(T.n_atp * T.n_cr), (unsigned)batch);
+    const int64_t ML = p->M1 + p->M2;
+    const dim3 gr((unsigned)((ML + RED_T - 1) / RED_T), (unsigned)batch);
+    T.n_last = T.n_cr > 1 ? (int)gr.x : T.n_atp * T.n_cr;
+    cudaError_t e = cudaSuccess;
     if (T.n_atp > 0) {
-        cudaError_t e;
         if (g.NT == 64) {
             e = tm_smem_attr((const void *)corr_tc_tiled<64>, smem_bytes<64>());
             if (e == cudaSuccess) e = launch_pdl(corr_tc_tiled<64>, grid, dim3(TNTHR), smem_bytes<64>(), s, T);
@@ -686,20 +725,15 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         if (e != cudaSuccess) return tm_cuda_status(e, "corr_tc_tiled");
         TM_CHECK_LAUNCH("corr_tc_tiled");
         if (T.n_cr > 1) {
-            const int64_t ML = p->M1 + p->M2;
-            const dim3 gr((unsigned)((ML + RED_T - 1) / RED_T), (unsigned)batch);
             e = T.part32 ? launch_pdl(tiled_reduce<int32_t>, gr, dim3(RED_T), 0, s, T)
                          : launch_pdl(tiled_reduce<int64_t>, gr, dim3(RED_T), 0, s, T);
             if (e != cudaSuccess) return tm_cuda_status(e, "tiled_reduce");
             TM_CHECK_LAUNCH("tiled_reduce");
         }
+        return TM_OK;
     }
-    const int with_left = part == 0;  // the leftover outputs belong to part 0
-    {
-        const cudaError_t e = launch_pdl(tc_tiled_final, dim3((unsigned)batch), dim3(FIN_T), 0, s, T, batch, resid,
-                                         residues_out, k, keys_out, with_left);
-        if (e != cudaSuccess) return tm_cuda_status(e, "tc_tiled_final");
-    }
+    e = launch_pdl(tc_tiled_final, dim3((unsigned)batch), dim3(FIN_T), 0, s, T);
+    if (e != cudaSuccess) return tm_cuda_status(e, "tc_tiled_final");
     TM_CHECK_LAUNCH("tc_tiled_final");
     return TM_OK;
 }
