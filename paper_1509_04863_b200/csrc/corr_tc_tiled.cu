@@ -52,7 +52,7 @@ constexpr int KEY_SHIFT = 21;
 constexpr int64_t KEY_BIAS = (int64_t)1 << 42;
 constexpr int TNTHR = NTHR + 64;   // 8 epilogue warps, MMA issuer (warp 8), TMA producer (warp 9)
 constexpr int PREP_T = 256;
-constexpr int PREP_MAXCTA = 256;   // prep CTAs per pair (bound for the leftover partials)
+constexpr int PREP_MAXCTA = 1024;  // prep CTAs per pair (bound for the leftover partials)
 
 struct TiledArgs {
     TcArgs a;              // y, t, K, M, NA, NC, crt constants
@@ -66,7 +66,8 @@ struct TiledArgs {
     uint8_t *aimg;         // [batch][JT][256]
     uint8_t *bmag;         // [batch][S] limbs block s needs
     int NT;                    // output blocks per tile
-    unsigned long long *keys;  // [batch][2] packed (max r, lowest k) per modulus
+    unsigned long long *ckeys; // [batch][nkey_cta][2] packed (max r, lowest k) per CTA and modulus
+    int nkey_cta;              // CTAs per pair that write ckeys (the pair's last kernel)
     void *part;                // [batch][n_cr][M1 + M2] partial r of each template range (n_cr > 1):
     int part32;                // int32 when every partial provably fits (plan bound), else int64
     int64_t *r_out[2];         // [batch][Mj] r outputs (staged tm_correlate) or NULL
@@ -113,8 +114,7 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
 #pragma unroll
     for (int q = 0; q < MAXLEFT; ++q) lacc0[q] = lacc1[q] = 0;
 
-    // ---- zeroing (the keys are max-reduced by the later kernels; done counts CTAs)
-    if (blockIdx.x == 0 && tid < 2) T.keys[2 * b + tid] = 0;
+    // ---- zeroing (done counts the last kernel's CTAs)
     if (blockIdx.x == 0 && tid == 0) T.done[b] = 0;
 
     // ---- planes + block limb counts + leftovers: thread = 16 entries (block s,
@@ -226,6 +226,29 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
     }
 }
 
+// the CTA's best (max r, lowest k) per modulus -> ckeys[b][slot] (all threads call;
+// bv/bk of threads without outputs are INT64_MIN / INT64_MAX)
+__device__ __forceinline__ void cta_keys(const TiledArgs &T, int64_t b, int slot, int64_t (&bv)[2], int64_t (&bk)[2]) {
+    __shared__ unsigned long long wk[16][2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int64_t ov = __shfl_xor_sync(0xffffffffu, bv[j], o);
+            const int64_t ok = __shfl_xor_sync(0xffffffffu, bk[j], o);
+            amax(bv[j], bk[j], ov, ok);
+        }
+        if (lane == 0) wk[warp][j] = bk[j] == INT64_MAX ? 0ull : pack_key(bv[j], bk[j]);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        unsigned long long m = 0;
+        for (int w = 0; w < nw; ++w) m = wk[w][threadIdx.x] > m ? wk[w][threadIdx.x] : m;
+        T.ckeys[(b * T.nkey_cta + slot) * 2 + threadIdx.x] = m;
+    }
+}
+
 // Steps 7-9 of pair b, run by the CTA that finishes the pair's last kernel (all its
 // threads): the prep CTAs' leftover partials summed in a fixed order, the
 // leftovers merged into the tile keys, residues, k (or the split part's keys).
@@ -236,26 +259,64 @@ __device__ void finish_pair(const TiledArgs &T, int64_t b) {
     __shared__ int64_t fred[16][2 * MAXLEFT];
     __shared__ int64_t lsum[2 * MAXLEFT];
     if (T.with_left && nleft0 + nleft1) {
-        for (int q = 0; q < 2 * MAXLEFT; ++q) {
-            int64_t r = 0;
-            for (int c = tid; c < T.n_pcta; c += blockDim.x) r += __ldcg(T.lpart + (b * T.n_pcta + c) * 2 * MAXLEFT + q);
+        // one L2 round trip: thread c loads prep CTA c's 16 partials at once
+        int64_t v[2 * MAXLEFT];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-            if (lane == 0) fred[warp][q] = r;
+        for (int q = 0; q < 2 * MAXLEFT; ++q) v[q] = 0;
+        for (int c = tid; c < T.n_pcta; c += blockDim.x) {
+            const int4 *src = reinterpret_cast<const int4 *>(T.lpart + (b * T.n_pcta + c) * 2 * MAXLEFT);
+#pragma unroll
+            for (int h = 0; h < MAXLEFT; ++h) {
+                const int4 u = __ldcg(src + h);
+                v[2 * h] += (int64_t)(((uint64_t)(uint32_t)u.y << 32) | (uint32_t)u.x);
+                v[2 * h + 1] += (int64_t)(((uint64_t)(uint32_t)u.w << 32) | (uint32_t)u.z);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 2 * MAXLEFT; ++q) {
+            if ((q < MAXLEFT ? q < nleft0 : q - MAXLEFT < nleft1)) {
+                int64_t r = v[q];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+                if (lane == 0) fred[warp][q] = r;
+            }
         }
         __syncthreads();
         if (tid < 2 * MAXLEFT) {
             int64_t r = 0;
-            for (int w = 0; w < nw; ++w) r += fred[w][tid];
+            if (tid < MAXLEFT ? tid < nleft0 : tid - MAXLEFT < nleft1)
+                for (int w = 0; w < nw; ++w) r += fred[w][tid];
             lsum[tid] = r;
         }
         __syncthreads();
     }
+    // the pair's key per modulus: max over the CTAs' keys (packed keys order like (r, -k))
+    __shared__ unsigned long long fk[16][2];
+    unsigned long long kmax[2] = {0ull, 0ull};
+    for (int c = tid; c < T.nkey_cta; c += blockDim.x) {
+        const ulonglong2 u = __ldcg(reinterpret_cast<const ulonglong2 *>(T.ckeys) + b * T.nkey_cta + c);
+        kmax[0] = u.x > kmax[0] ? u.x : kmax[0];
+        kmax[1] = u.y > kmax[1] ? u.y : kmax[1];
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ov = __shfl_xor_sync(0xffffffffu, kmax[j], o);
+            kmax[j] = ov > kmax[j] ? ov : kmax[j];
+        }
+        if (lane == 0) fk[warp][j] = kmax[j];
+    }
+    __syncthreads();
     if (tid) return;
+    for (int w = 1; w < nw; ++w)
+        for (int j = 0; j < 2; ++j) kmax[j] = fk[w][j] > kmax[j] ? fk[w][j] : kmax[j];
+    kmax[0] = fk[0][0] > kmax[0] ? fk[0][0] : kmax[0];
+    kmax[1] = fk[0][1] > kmax[1] ? fk[0][1] : kmax[1];
     int64_t m[2];
     for (int j = 0; j < 2; ++j) {
         int64_t bv = INT64_MIN, bk = INT64_MAX;
-        const unsigned long long key = __ldcg(T.keys + 2 * b + j);
+        const unsigned long long key = kmax[j];
         if (key) {
             bk = ((int64_t)1 << KEY_SHIFT) - 1 - (int64_t)(key & (((unsigned long long)1 << KEY_SHIFT) - 1));
             bv = (int64_t)(key >> KEY_SHIFT) - KEY_BIAS;
@@ -420,6 +481,7 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
     ts[2] = gtime();
 
     // ---- epilogue (warps 0-7): warp w: TMEM lanes 32 (w & 3) (rows b'), blocks a0 + (NT / 2) (w >> 2) + [0, NT / 2)
+    int64_t mbv[2] = {INT64_MIN, INT64_MIN}, mbk[2] = {INT64_MAX, INT64_MAX};
     if (warp < NTHR / 32) {
         const int qw = warp & 3, hw = warp >> 2;
         const int brow = P - 1 - (32 * qw + lane);
@@ -459,20 +521,12 @@ __global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
             }
         }
         if (T.n_cr == 1) {
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const int64_t ov = __shfl_xor_sync(0xffffffffu, bv[j], o);
-                    const int64_t ok = __shfl_xor_sync(0xffffffffu, bk[j], o);
-                    amax(bv[j], bk[j], ov, ok);
-                }
-                if (lane == 0 && bk[j] != INT64_MAX) atomicMax(T.keys + 2 * b + j, pack_key(bv[j], bk[j]));
-            }
+            mbv[0] = bv[0]; mbv[1] = bv[1]; mbk[0] = bk[0]; mbk[1] = bk[1];
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (T.n_cr == 1) cta_keys(T, b, blockIdx.x, mbv, mbk);
     if (a.dbg && tid == 0) {
         ts[3] = gtime();
         uint32_t smid;
@@ -520,17 +574,7 @@ __global__ void __launch_bounds__(RED_T) tiled_reduce(const TiledArgs T) {
             amax(bv[j], bk[j], r, k);
         }
     }
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const int64_t ov = __shfl_xor_sync(0xffffffffu, bv[j], o);
-            const int64_t ok = __shfl_xor_sync(0xffffffffu, bk[j], o);
-            amax(bv[j], bk[j], ov, ok);
-        }
-        if (lane == 0 && bk[j] != INT64_MAX) atomicMax(T.keys + 2 * b + j, pack_key(bv[j], bk[j]));
-    }
+    cta_keys(T, b, blockIdx.x, bv, bk);
     arrive_and_finish(T, b);
 }
 
@@ -573,7 +617,7 @@ int tiled_nt(const tm_plan_s *p, int64_t batch) {
     return batch * ((na + 63) / 64) >= p->num_sms ? 64 : 32;
 }
 struct Geo {
-    int NT, NC, NA[2], n_at, lmax, np, JT, n_pcta, max_cr;
+    int NT, NC, NA[2], n_at, lmax, np, JT, n_pcta, max_cr, max_keys;
     int64_t S;
 };
 Geo geometry(const tm_plan_s *p, int64_t batch) {
@@ -593,11 +637,13 @@ Geo geometry(const tm_plan_s *p, int64_t batch) {
     g.lmax = std::max(1, p->tct_lmax);
     g.np = 2 * g.lmax - 1;
     g.JT = 8 * (g.NC - 1) + 16;
-    const int64_t want = (2 * (int64_t)p->num_sms + batch - 1) / std::max<int64_t>(batch, 1);
+    const int64_t want = (4 * (int64_t)p->num_sms + batch - 1) / std::max<int64_t>(batch, 1);
     g.n_pcta = (int)std::min<int64_t>(PREP_MAXCTA, std::max<int64_t>(1, want));
     // template ranges of >= one A chunk each, and their partial sums within the budget
     const size_t per = (size_t)std::max<int64_t>(batch, 1) * (size_t)(p->M1 + p->M2) * 8;
     g.max_cr = std::max(1, std::min((g.NC + TCCH - 1) / TCCH, (int)std::min<size_t>(PART_BUDGET / per, 1 << 20)));
+    // CTAs per pair writing keys: the reduce kernel's, or the main kernel's (<= n_at max_cr)
+    g.max_keys = std::max((int)((p->M1 + p->M2 + RED_T - 1) / RED_T), g.n_at * g.max_cr);
     return g;
 }
 
@@ -635,7 +681,7 @@ size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch) {
     if (!p->tct_ok || batch < 1) return 0;
     const Geo g = geometry(p, batch);
     size_t n = 0;
-    n += align_up256((size_t)batch * 16);                                   // keys
+    n += align_up256((size_t)batch * g.max_keys * 16);                      // per-CTA keys
     n += align_up256(g.max_cr > 1 ? (size_t)batch * g.max_cr * (p->M1 + p->M2) * 8 : 0);  // partial sums
     n += align_up256((size_t)batch * g.S);                                  // block limb counts
     n += align_up256((size_t)batch * g.np * 8 * 32 * g.S);                  // B planes
@@ -693,7 +739,10 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     T.part32 = (double)T.CR * P * xmax * ybound < 2147483647.0;  // |partial| <= CR P max|t| max|y|
     char *w = (char *)ws;
     auto carve = [&](size_t bytes) { char *q = w; w += align_up256(bytes); return q; };
-    T.keys = (unsigned long long *)carve((size_t)batch * 16);
+    const int64_t ML_ = p->M1 + p->M2;
+    const int nred_cta = (int)((ML_ + RED_T - 1) / RED_T);
+    T.nkey_cta = T.n_cr > 1 ? nred_cta : std::max(1, T.n_atp * T.n_cr);
+    T.ckeys = (unsigned long long *)carve((size_t)batch * g.max_keys * 16);
     T.part = (int64_t *)carve(g.max_cr > 1 ? (size_t)batch * g.max_cr * (p->M1 + p->M2) * 8 : 0);
     T.bmag = (uint8_t *)carve((size_t)batch * g.S);
     T.planes = (uint8_t *)carve((size_t)batch * g.np * 8 * 32 * g.S);

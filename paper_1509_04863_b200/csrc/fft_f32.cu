@@ -207,6 +207,10 @@ struct FftArgs {
     float *r1, *r2;          // [batch][Mj] or NULL
     int32_t *resid;          // [batch][2] or NULL
     int64_t nb;              // templates (fft_template_f32: two per CTA)
+    int32_t *residues_out;   // [batch][2] or NULL: steps 8-9 fused into the epilogue
+    int64_t *k_out;          // [batch] or NULL
+    int64_t N, crt_wrap;
+    uint32_t crt_inv;
 };
 
 // Two templates per transform (they are real): v = t_rev[b0] + i t_rev[b0 + 1],
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(FGeo<LOGL>::NT, 1) fft_corr_f32(FftArgs a) {
             fmax_idx(b2, i2, v[m].y, i);
         }
     }
-    if (!a.resid) return;
+    if (!a.resid && !a.k_out && !a.residues_out) return;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         fmax_idx(b1, i1, __shfl_xor_sync(0xffffffffu, b1, o), __shfl_xor_sync(0xffffffffu, i1, o));
@@ -317,7 +321,11 @@ __global__ void __launch_bounds__(FGeo<LOGL>::NT, 1) fft_corr_f32(FftArgs a) {
             fmax_idx(b1, i1, __shfl_xor_sync(0xffffffffu, b1, o), __shfl_xor_sync(0xffffffffu, i1, o));
             fmax_idx(b2, i2, __shfl_xor_sync(0xffffffffu, b2, o), __shfl_xor_sync(0xffffffffu, i2, o));
         }
-        if (l == 0) { a.resid[2 * b] = i1; a.resid[2 * b + 1] = i2; }
+        if (l == 0) {
+            if (a.resid) { a.resid[2 * b] = i1; a.resid[2 * b + 1] = i2; }
+            if (a.residues_out) { a.residues_out[2 * b] = i1; a.residues_out[2 * b + 1] = i2; }
+            if (a.k_out) a.k_out[b] = tm_resolve(i1, i2, a.M1, a.M2, a.crt_inv, a.N, a.crt_wrap);  // steps 8-9
+        }
     }
 }
 
@@ -465,15 +473,26 @@ __global__ void __launch_bounds__(256) fftl_passAinv(FtlArgs a) {
     }
 }
 
-__global__ void fftl_keys_to_resid(const unsigned long long *keys, int64_t batch, int32_t *resid) {
+struct FtlOut {
+    int32_t *resid, *residues_out;
+    int64_t *k_out;
+    int64_t N, M1, M2, crt_wrap;
+    uint32_t crt_inv;
+};
+__global__ void fftl_keys_to_resid(const unsigned long long *keys, int64_t batch, FtlOut o) {
     pdl_trigger();
     pdl_wait();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < 2 * batch) resid[i] = (int32_t)(0xFFFFFFFFu - (uint32_t)(keys[i] & 0xFFFFFFFFull));
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    const int32_t m1 = (int32_t)(0xFFFFFFFFu - (uint32_t)(keys[2 * b] & 0xFFFFFFFFull));
+    const int32_t m2 = (int32_t)(0xFFFFFFFFu - (uint32_t)(keys[2 * b + 1] & 0xFFFFFFFFull));
+    if (o.resid) { o.resid[2 * b] = m1; o.resid[2 * b + 1] = m2; }
+    if (o.residues_out) { o.residues_out[2 * b] = m1; o.residues_out[2 * b + 1] = m2; }
+    if (o.k_out) o.k_out[b] = tm_resolve(m1, m2, o.M1, o.M2, o.crt_inv, o.N, o.crt_wrap);  // steps 8-9
 }
 
 template <int LOGR>
-int launch_long(bool templ, const FtlArgs &A, int64_t batch, int32_t *resid, cudaStream_t s) {
+int launch_long(bool templ, const FtlArgs &A, int64_t batch, const FtlOut &out, cudaStream_t s) {
     const dim3 ga((unsigned)(SEG / 256), (unsigned)batch), gb((unsigned)(1 << LOGR), (unsigned)batch);
     const size_t smem = (size_t)2 * SEG * 4;
     cudaError_t e;
@@ -486,21 +505,21 @@ int launch_long(bool templ, const FtlArgs &A, int64_t batch, int32_t *resid, cud
         if (e == cudaSuccess) e = tm_smem_attr((const void *)fftl_passB<false>, (int)smem);
         if (e == cudaSuccess) e = launch_pdl(fftl_passB<false>, gb, dim3(SEG / E), smem, s, A);
         if (e == cudaSuccess) e = launch_pdl(fftl_passAinv<LOGR>, ga, dim3(256), 0, s, A);
-        if (e == cudaSuccess && resid)
-            e = launch_pdl(fftl_keys_to_resid, dim3((unsigned)((2 * batch + 255) / 256)), dim3(256), 0, s,
-                           (const unsigned long long *)A.keys, batch, resid);
+        if (e == cudaSuccess && (out.resid || out.residues_out || out.k_out))
+            e = launch_pdl(fftl_keys_to_resid, dim3((unsigned)((batch + 255) / 256)), dim3(256), 0, s,
+                           (const unsigned long long *)A.keys, batch, out);
     }
     if (e != cudaSuccess) return tm_cuda_status(e, "fft_f32 (long transform)");
     TM_CHECK_LAUNCH("fft_f32 (long transform)");
     return TM_OK;
 }
 
-int dispatch_long(int logL, bool templ, const FtlArgs &A, int64_t batch, int32_t *resid, cudaStream_t s) {
+int dispatch_long(int logL, bool templ, const FtlArgs &A, int64_t batch, const FtlOut &out, cudaStream_t s) {
     switch (logL - SEG_LOG) {
-        case 1: return launch_long<1>(templ, A, batch, resid, s);
-        case 2: return launch_long<2>(templ, A, batch, resid, s);
-        case 3: return launch_long<3>(templ, A, batch, resid, s);
-        case 4: return launch_long<4>(templ, A, batch, resid, s);
+        case 1: return launch_long<1>(templ, A, batch, out, s);
+        case 2: return launch_long<2>(templ, A, batch, out, s);
+        case 3: return launch_long<3>(templ, A, batch, out, s);
+        case 4: return launch_long<4>(templ, A, batch, out, s);
         default: return TM_EUNSUPPORTED;
     }
 }
@@ -603,7 +622,7 @@ int tm_fft_f32_template(const tm_plan_s *p, const void *t, int64_t ldt, int64_t 
         B.seg = (float2 *)tf;
         B.twf = A.twf; B.twi = A.twi;
         B.logL = p->logL2;
-        return dispatch_long(p->logL2, true, B, batch, nullptr, s);
+        return dispatch_long(p->logL2, true, B, batch, FtlOut{}, s);
     }
     A.t = (const float *)t; A.ldt = ldt; A.K = p->K;
     A.tf = (float2 *)tf;
@@ -612,7 +631,8 @@ int tm_fft_f32_template(const tm_plan_s *p, const void *t, int64_t ldt, int64_t 
 }
 
 int tm_fft_f32_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *tf, int64_t batch,
-                         void *r1, void *r2, int32_t *resid, void *scratch, cudaStream_t s) {
+                         void *r1, void *r2, int32_t *resid, void *scratch, cudaStream_t s, int32_t *residues_out,
+                         int64_t *k_out) {
     if (!tm_fft_f32_ok(p)) return TM_EUNSUPPORTED;
     if (batch > 0x7FFFFFFF) return TM_EUNSUPPORTED;
     FftArgs A{};
@@ -632,7 +652,8 @@ int tm_fft_f32_correlate(const tm_plan_s *p, const void *y1, const void *y2, con
         B.twf = A.twf; B.twi = A.twi;
         B.r1 = (float *)r1; B.r2 = (float *)r2;
         B.logL = p->logL2;
-        return dispatch_long(p->logL2, false, B, batch, resid, s);
+        FtlOut out{resid, residues_out, k_out, p->N, p->M1, p->M2, p->crt_wrap, p->crt_inv};
+        return dispatch_long(p->logL2, false, B, batch, out, s);
     }
     A.tf = (float2 *)const_cast<void *>(tf);
     A.y1 = (const float *)y1; A.y2 = (const float *)y2;
@@ -641,5 +662,7 @@ int tm_fft_f32_correlate(const tm_plan_s *p, const void *y1, const void *y2, con
     A.M1 = p->M1; A.M2 = p->M2;
     A.r1 = (float *)r1; A.r2 = (float *)r2;
     A.resid = resid;
+    A.residues_out = residues_out; A.k_out = k_out;
+    A.N = p->N; A.crt_wrap = p->crt_wrap; A.crt_inv = p->crt_inv;
     return dispatch(p->logL2, false, A, batch, s);
 }

@@ -86,6 +86,12 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
         rc = tm_fold_template(p, t, batch, W.tf, stream);                            // step 4 (+5 for t)
         if (rc) return rc;
         tm_prof_mark(2, s);
+        if (p->dtype == TM_F32 && tm_fft_f32_ok(p)) {  // steps 5-9: the CRT in the FFT kernel's epilogue
+            rc = tm_fft_f32_correlate(p, W.y1, W.y2, W.tf, batch, nullptr, nullptr, nullptr, W.gntt, s, residues, k);
+            tm_prof_mark(3, s);
+            tm_prof_mark(4, s);
+            return rc;
+        }
         rc = tm_correlate_impl(p, W.y1, W.y2, W.tf, batch, nullptr, nullptr, W.resid, W.tiles, W.gntt, s);  // 5-7
         if (rc) return rc;
     }

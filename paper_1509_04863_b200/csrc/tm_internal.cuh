@@ -158,7 +158,8 @@ int tm_fft_f32_template(const tm_plan_s *p, const void *t, int64_t ldt, int64_t 
 bool tm_fft_f32_long(const tm_plan_s *p);
 size_t tm_fft_f32_scratch_bytes(const tm_plan_s *p, int64_t batch);
 int tm_fft_f32_correlate(const tm_plan_s *p, const void *y1, const void *y2, const void *tf, int64_t batch,
-                         void *r1, void *r2, int32_t *resid, void *scratch, cudaStream_t s);
+                         void *r1, void *r2, int32_t *resid, void *scratch, cudaStream_t s,
+                         int32_t *residues_out = nullptr, int64_t *k_out = nullptr);
 bool tm_fold_f32_ok(const tm_plan_s *p);
 size_t tm_fold_f32_ws_bytes(const tm_plan_s *p, int64_t batch);
 int tm_fold_f32(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, int64_t offset, int64_t len,
