@@ -46,6 +46,8 @@ struct TmaArgs {
     int64_t row0;        // global row of the chunk's first row
     int64_t R;           // rows per item
     int64_t n_rc, n_groups, n_items;
+    int contig;          // split items as one contiguous range of (pair, group, row) per CTA
+    int64_t n_segs;      // contig: segments (pair, column group) of `rows` rows each
     int owner;           // items are whole pairs of a full fold: write y directly
     int accumulate;
     int acc_words;       // y2 accumulator words reserved in shared memory
@@ -127,8 +129,19 @@ __device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, int sh) { retu
 struct Item {
     int64_t b, gi, ra, nrow, cs_cta, width;
 };
+// contig items: (segment s << 36) | (first row << 12) | rows (<= 4095)
 __device__ __forceinline__ Item decode(const TmaArgs &a, int64_t item) {
     Item it;
+    if (a.contig) {
+        const int64_t sgm = item >> 36;
+        it.gi = sgm % a.n_groups;
+        it.b = sgm / a.n_groups;
+        it.ra = (item >> 12) & 0xFFFFFF;
+        it.nrow = item & 0xFFF;
+        it.cs_cta = it.gi * TCOLS;
+        it.width = (a.M1 - it.cs_cta < TCOLS) ? a.M1 - it.cs_cta : TCOLS;
+        return it;
+    }
     // column groups fastest: CTAs running at the same time read adjacent 4 KB pieces
     // of the same rows (cfg5, 16 groups: 0.412 -> 0.407 ms; row chunks fastest before)
     it.gi = item % a.n_groups;
@@ -293,9 +306,30 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
             int s = 0;
             uint32_t ph = 0;
             const uint64_t pol = l2_evict_first_policy();
+            // contig: this CTA's range [lin, lend) of the (segment, row) space, cut at
+            // segment ends and every R rows (range ends on multiples of 16 rows)
+            const int64_t Tr = a.n_segs * a.rows;
+            auto rb = [&](int64_t c) -> int64_t {
+                return c >= (int64_t)gridDim.x ? Tr : (c * Tr / (int64_t)gridDim.x) / 16 * 16;
+            };
+            int64_t lin = rb(blockIdx.x), lend = rb(blockIdx.x + 1);
             for (int64_t seq = 0;; ++seq) {
-                int64_t item = blockIdx.x + seq * gridDim.x;
-                if (item >= a.n_items) item = -1;
+                int64_t item;
+                if (a.contig) {
+                    if (lin >= lend) {
+                        item = -1;
+                    } else {
+                        const int64_t sg = lin / a.rows, r0 = lin - sg * a.rows;
+                        int64_t nr = a.rows - r0;
+                        if (nr > a.R) nr = a.R;
+                        if (nr > lend - lin) nr = lend - lin;
+                        item = (sg << 36) | (r0 << 12) | nr;
+                        lin += nr;
+                    }
+                } else {
+                    item = blockIdx.x + seq * gridDim.x;
+                    if (item >= a.n_items) item = -1;
+                }
                 item_q[seq & 7] = item;  // published by the arrive on the item's first stage
                 if (item < 0) {          // end: complete one more stage phase with no data
                     mbar_wait(&empty[s], ph ^ 1);
@@ -737,7 +771,7 @@ int setup_args(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, in
     a.owner = (a.n_groups == 1 && a.n_rc == 1 && offset == 0 && len == p->N) ? 1 : 0;
     a.accumulate = accumulate;
     a.x_early = (p->flags & TM_INPUTS_STABLE) ? 1 : 0;
-    if (R > 1024) return TM_EUNSUPPORTED;
+    if (R > 2048) return TM_EUNSUPPORTED;
     a.priv_stride = (int)(512 + (R + 15) / 16 * 16);
     a.acc_words = TW * a.priv_stride;
     tm_ws_layout L = tm_ws(p, batch);
@@ -747,6 +781,11 @@ int setup_args(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, in
     a.xs_bytes = a.owner ? (int)((p->K + R + 15) / 16 * 16) : 0;
     return TM_OK;
 }
+
+#ifndef TM_FOLD_NST
+#define TM_FOLD_NST 4
+#endif
+constexpr int TM_FOLD_NST_DEF = TM_FOLD_NST;
 
 size_t smem_bytes(const TmaArgs &a, int nst) {
     return (size_t)nst * STAGE_BYTES + (size_t)2 * a.acc_words * 2 + (2 * nst + 8) * 8 + 10 * 8 + a.xs_bytes;
@@ -802,6 +841,23 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     }
     a.ldy1 = ldy1; a.ldy2 = ldy2;
     *used_counts = !a.owner;
+    static const char *env_contig = getenv("TM_FOLD_CONTIG");  // A/B: "0" = round-robin row chunks
+    if (!a.owner && !(env_contig && env_contig[0] == '0')) {
+        // split items: each CTA folds one contiguous range of (pair, group, row) --
+        // balanced to 16 rows, with R up to the shared-memory budget -- instead of
+        // round-robin row chunks: fewer, longer items (fewer count atomics and
+        // item hand-offs) without a last-wave imbalance
+        a.contig = 1;
+        a.n_segs = batch * a.n_groups;
+        int64_t Rc = 2048;
+        while (Rc > 16) {
+            a.R = Rc;
+            a.priv_stride = (int)(512 + Rc);
+            a.acc_words = TW * a.priv_stride;
+            if (smem_bytes(a, TM_FOLD_NST_DEF) <= 227 * 1024) break;
+            Rc -= 256;
+        }
+    }
     if (!a.owner) {
         const int64_t n = batch * (p->M1 + p->M2);
         const int64_t blocks = std::min<int64_t>((n + 255) / 256, 4 * (int64_t)p->num_sms);
@@ -809,12 +865,13 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
         if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: counts reset");
         TM_CHECK_LAUNCH("tm_fold: zero_i32");
     }
-#ifndef TM_FOLD_NST
-#define TM_FOLD_NST 4
-#endif
     const size_t smem = smem_bytes(a, TM_FOLD_NST);
     if (smem > 227 * 1024) return TM_EUNSUPPORTED;
-    const int64_t grid = a.n_items < p->num_sms ? a.n_items : p->num_sms;
+    int64_t grid = a.n_items < p->num_sms ? a.n_items : p->num_sms;
+    if (a.contig) {
+        const int64_t units = (a.n_segs * a.rows + 15) / 16;
+        grid = units < p->num_sms ? units : p->num_sms;
+    }
     return launch<TM_FOLD_NST>(a, grid, smem, s);
 }
 
