@@ -842,6 +842,10 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     a.ldy1 = ldy1; a.ldy2 = ldy2;
     *used_counts = !a.owner;
     static const char *env_contig = getenv("TM_FOLD_CONTIG");  // A/B: "0" = round-robin row chunks
+    // ring stages: 5 for rows read as >= 8 separate 4 KB pieces (wide M1: cfg5's 16
+    // column groups, 0.3389 -> 0.3355 ms), 4 otherwise (contiguous 32 KB stages
+    // measured 4-5% slower with 5: cfg4a 0.177 -> 0.185 ms)
+    const int nst = (a.n_groups >= 8 && TM_FOLD_NST_DEF == 4) ? 5 : TM_FOLD_NST_DEF;
     if (!a.owner && !(env_contig && env_contig[0] == '0')) {
         // split items: each CTA folds one contiguous range of (pair, group, row) --
         // balanced to 16 rows, with R up to the shared-memory budget -- instead of
@@ -854,7 +858,7 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
             a.R = Rc;
             a.priv_stride = (int)(512 + Rc);
             a.acc_words = TW * a.priv_stride;
-            if (smem_bytes(a, TM_FOLD_NST_DEF) <= 227 * 1024) break;
+            if (smem_bytes(a, nst) <= 227 * 1024) break;
             Rc -= 256;
         }
     }
@@ -865,13 +869,14 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
         if (e != cudaSuccess) return tm_cuda_status(e, "tm_fold: counts reset");
         TM_CHECK_LAUNCH("tm_fold: zero_i32");
     }
-    const size_t smem = smem_bytes(a, TM_FOLD_NST);
+    const size_t smem = smem_bytes(a, nst);
     if (smem > 227 * 1024) return TM_EUNSUPPORTED;
     int64_t grid = a.n_items < p->num_sms ? a.n_items : p->num_sms;
     if (a.contig) {
         const int64_t units = (a.n_segs * a.rows + 15) / 16;
         grid = units < p->num_sms ? units : p->num_sms;
     }
+    if (nst == 5) return launch<5>(a, grid, smem, s);
     return launch<TM_FOLD_NST>(a, grid, smem, s);
 }
 
