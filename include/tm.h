@@ -284,8 +284,10 @@ int tm_profile_events(void **events, int n);
  * arguments.  TM_PATH_FUSED_TC: one persistent kernel (packed fold warps +
  * tensor-core correlation warps, argmax and CRT in its epilogue);
  * TM_PATH_STAGED_TC: fold kernel, then the tensor-core correlation kernel;
- * TM_PATH_STAGED: fold, then the NTT (or fp32) correlation and the CRT kernel. */
-enum { TM_PATH_STAGED = 0, TM_PATH_STAGED_TC = 1, TM_PATH_FUSED_TC = 2 };
+ * TM_PATH_STAGED: fold, then the NTT (or fp32) correlation and the CRT kernel;
+ * TM_PATH_SMALL: small int8 pairs (N <= 16384, M2 + K <= 4096, K (M1 + M2) <=
+ * 2^21, no engine flag): the whole path in one kernel, one CTA per pair. */
+enum { TM_PATH_STAGED = 0, TM_PATH_STAGED_TC = 1, TM_PATH_FUSED_TC = 2, TM_PATH_SMALL = 3 };
 int tm_run_path(tm_plan plan, int64_t batch);
 /* tm_run_fold_rows: where tm_run(plan, batch, ws) writes the folded rows y1, y2
  * inside ws: out[0] = byte offset of y1 [batch][out[1]] (int32/fp32 entries,

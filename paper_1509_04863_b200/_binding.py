@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = (
     "tm_run_fold_rows", "tm_probe_read_bw", "tm_probe_read_pattern", "tm_fold_reduce",
 )
 RUN_PATHS = {0: "staged (fold -> NTT/fp32 correlation -> CRT)", 1: "staged (fold -> tensor-core correlation)",
-             2: "fused (fold + tensor-core correlation in one kernel)"}
+             2: "fused (fold + tensor-core correlation in one kernel)", 3: "small pair (whole path, one CTA per pair)"}
 
 _i64, _u64, _i32, _u32, _p, _d = (ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32,
                                   ctypes.c_void_p, ctypes.c_double)

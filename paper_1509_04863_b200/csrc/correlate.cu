@@ -61,6 +61,7 @@ int tm_ntt_tables_get(int device, tm_ntt_tables *out) {
     std::lock_guard<std::mutex> lk(g_tab_mu);
     DevTables &D = g_tabs[device];
     if (!D.ready) {
+        TmDeviceGuard guard(device);  // the allocation and upload belong to `device`
         const size_t n = size_t(1) << TM_MAX_LOGL;  // entries per table (sum of n/2 over lengths)
         std::vector<uint32_t> h(16 * n, 0u);  // 8n separate (value | companion) + 8n interleaved
         for (int pi = 0; pi < 2; ++pi) {

@@ -537,6 +537,7 @@ int ftables(int device, const float2 **twf, const float2 **twi) {
     std::lock_guard<std::mutex> lk(g_fmu);
     FTabs &F = g_ftabs[device];
     if (!F.ready) {
+        TmDeviceGuard guard(device);  // tables and __constant__ roots of `device`
         const size_t n = size_t(1) << FFT_MAX_LOGL;
         std::vector<float2> h(2 * n);
         for (int dir = 0; dir < 2; ++dir)

@@ -190,6 +190,11 @@ int tm_plan_create_impl(tm_plan *out, int64_t N, int64_t K, int64_t M, uint64_t 
                          ilog2_ceil(M2 + K - 1), TM_MAX_LOGL);
             return TM_EUNSUPPORTED;
         }
+        {   // the latency path for small pairs (not when an engine was requested explicitly)
+            static const char *env_small = getenv("TM_SMALL");  // A/B: "0" disables
+            p->small_ok = tm_small_ok(p) && !(flags & (TM_CORR_NTT | TM_CORR_TC)) &&
+                          !(env_small && env_small[0] == '0');
+        }
         if (p->use_tc) {  // the folded template is the int8 template itself, 16-byte rows
             p->tf_bytes = (K + 15) / 16 * 16;
             p->tf_elems = p->tf_bytes;

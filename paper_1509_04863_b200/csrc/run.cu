@@ -49,6 +49,11 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
     cudaStream_t s = (cudaStream_t)stream;
     RunWs W = run_ws(p, batch, ws);
     tm_prof_mark(0, s);
+    if (p->small_ok) {  // small pairs: the whole path in one kernel, one CTA per pair
+        const int rc = tm_small_run(p, x, ldx, t, batch, residues, k, s);
+        for (int i = 1; i <= 4; ++i) tm_prof_mark(i, s);
+        return rc;
+    }
     if (p->use_tc) {
         if (tm_fused_tc_ok(p, batch)) {  // the whole path in one persistent kernel
             int rc = tm_fold_tc_fused(p, x, ldx, t, batch, W.y1, W.y2, residues, k, W.fold_ws, s);
@@ -104,6 +109,7 @@ extern "C" __attribute__((visibility("default"))) int tm_run(tm_plan p, const vo
 // Instrumentation: which kernel sequence tm_run(plan, batch) launches.
 extern "C" __attribute__((visibility("default"))) int tm_run_path(tm_plan p, int64_t batch) {
     if (!p || batch <= 0) return -1;
+    if (p->small_ok) return TM_PATH_SMALL;
     if (p->use_tc) {
         if (tm_fused_tc_ok(p, batch)) return TM_PATH_FUSED_TC;
         return TM_PATH_STAGED_TC;

@@ -39,6 +39,7 @@ struct tm_plan_s {
     int tc_ok;           // plan shape eligible for it
     int tc_NA[2], tc_NMC, tc_R, tc_NC, tc_JA, tc_CCH, tc_lmax;
     int tct_ok, tct_lmax;  // tiled tensor-core correlation (corr_tc_tiled.cu) eligible
+    int small_ok;          // tm_run uses the one-kernel small-pair path (small.cu)
     uint32_t tc_ncols, tc_offB, tc_offTp, tc_offMisc, tc_smem;
 };
 
@@ -84,6 +85,15 @@ void tm_count_launch();
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 bool tm_pdl_enabled();
+// makes `dev` current for a scope (per-device one-time setup: tables, constants)
+struct TmDeviceGuard {
+    int prev = -1;
+    explicit TmDeviceGuard(int dev) {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    ~TmDeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize = bytes [, max shared carveout]) once
 // per (function, device, bytes), thread-safe (plan.cu)
 cudaError_t tm_smem_attr(const void *func, int bytes, bool max_carveout = false);
@@ -144,6 +154,9 @@ size_t tm_run_ws_bytes(const tm_plan_s *p, int64_t batch);  // run.cu
 bool tm_fast_corr_ok(const tm_plan_s *p);
 void tm_mont_linv(int logL, uint32_t p, uint32_t *c, uint32_t *cs);
 bool tm_fused_tc_ok(const tm_plan_s *p, int64_t batch);
+bool tm_small_ok(const tm_plan_s *p);   // small.cu: one CTA per pair, the latency path
+int tm_small_run(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, int32_t *residues,
+                 int64_t *k, cudaStream_t s);
 int tm_fold_tc_fused(const tm_plan_s *p, const void *x, int64_t ldx, const void *t, int64_t batch, void *y1,
                      void *y2, int32_t *residues, int64_t *k, void *ws, cudaStream_t s);
 size_t tm_gntt_scratch_bytes(const tm_plan_s *p, int64_t batch);

@@ -889,3 +889,33 @@ def test_multi_moduli_f32(tm):
                 assert int(res[b, j]) == oracle.argmax(r), (b, j)
         z = oracle.crt_multi(res[b].astype(np.int64), M)
         assert int(k[b]) == (z if z < N else -1)
+
+
+@pytest.mark.parametrize("N,K,M,binary,block,repair", [(4096, 256, 0, True, False, False),
+                                                        (4096, 256, 0, True, False, True),
+                                                        (3000, 60, 0, False, False, False),
+                                                        (997, 40, 45, False, False, False),
+                                                        (12, 3, 4, False, False, False),
+                                                        (4096, 256, 0, True, True, False),
+                                                        (16384, 1000, 1024, False, False, False)])
+def test_small_pair_path(tm, N, K, M, binary, block, repair):
+    """The one-kernel small-pair path of tm_run (TM_PATH_SMALL, the latency path of
+    cfg1): residues and k equal the oracle's for strategy 1 (M dividing N or not),
+    the Block strategy, alias repair, +-1 and general int8 data."""
+    B = 9
+    plan = tm.Plan(N, K, M=M, seed=3, binary=binary, block=block, alias_repair=repair)
+    assert plan.run_path(B) == 3
+    rng = np.random.default_rng(N + K)
+    if binary:
+        x_h, t_h, _ = tmgen.batch(3, 0, B, N, K, 0.1)
+    else:
+        x_h = rng.integers(-128, 128, (B, N)).astype(np.int8)
+        t_h = np.stack([x_h[b][(np.arange(K) + 5 * b) % N] for b in range(B)]).astype(np.int8)
+    res, k = plan.run(up(x_h), up(t_h))
+    torch.cuda.synchronize()
+    res, k = res.cpu().numpy(), k.cpu().numpy()
+    for b in range(B):
+        mm = plan.M1 if plan.M1 != plan.K else 0
+        o = (oracle.ftm_block(x_h[b], t_h[b], M=mm, want_vectors=False) if block else
+             oracle.ftm(x_h[b], t_h[b], M=mm, want_vectors=False, alias_repair=repair))
+        assert tuple(res[b]) == o["residues"] and k[b] == o["k"], b
