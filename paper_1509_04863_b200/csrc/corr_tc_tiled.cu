@@ -376,7 +376,10 @@ __device__ __forceinline__ void bulk_copy(void *dst, const void *src, uint32_t b
 }
 
 template <int NT>
-__global__ void __launch_bounds__(TNTHR, 2) corr_tc_tiled(const TiledArgs T) {
+#ifndef TM_TILED_MINB
+#define TM_TILED_MINB 2
+#endif
+__global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const TiledArgs T) {
     pdl_trigger();
     pdl_wait();  // the prep kernel's planes, A image and zeroed keys
     constexpr int B_BYTES = b_bytes<NT>();

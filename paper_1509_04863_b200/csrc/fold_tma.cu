@@ -853,7 +853,10 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
         // item hand-offs) without a last-wave imbalance
         a.contig = 1;
         a.n_segs = batch * a.n_groups;
-        int64_t Rc = 2048;
+#ifndef TM_FOLD_RCAP
+#define TM_FOLD_RCAP 2048
+#endif
+        int64_t Rc = TM_FOLD_RCAP;
         while (Rc > 16) {
             a.R = Rc;
             a.priv_stride = (int)(512 + Rc);
