@@ -119,14 +119,18 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
 
     // ---- planes + block limb counts + leftovers: thread = 16 entries (block s,
     // modulus j, chunk column h); 16 consecutive threads cover one block of both moduli
-    const int64_t n16 = T.S * 16;
+    // blocks this launch's windows read: [at0 NT, (at0 + n_atp) NT + NC) (every block
+    // when the leftovers are computed here: the last part holds them)
+    const int64_t s_lo = (int64_t)T.at0 * T.NT;
+    const int64_t s_hi = min(T.S, (int64_t)(T.at0 + T.n_atp) * T.NT + a.NC + 1);
+    const int64_t n16 = (s_hi - s_lo) * 16;
     const int64_t pstride = (int64_t)8 * 32 * T.S;  // bytes per plane (8 columns x 2 S rows x 16)
     uint8_t *pl = T.planes + b * T.np * pstride;
     // (the loop is warp-uniform: the shuffles below combine 16-lane groups)
     for (int64_t w0 = gtid - (tid & 31); w0 < n16; w0 += gstride) {
         const int64_t w = w0 + (tid & 31);
         const bool valid = w < n16;
-        const int64_t s = w >> 4;
+        const int64_t s = s_lo + (w >> 4);
         const int j = (int)((w >> 3) & 1), h = (int)(w & 7);
         const int32_t *yr = a.y[j] + b * a.ldy[j];
         const int64_t i0 = (int64_t)P * s + 16 * h, len = valid ? a.len[j] : 0;
@@ -555,14 +559,18 @@ __global__ void __launch_bounds__(RED_T) tiled_reduce(const TiledArgs T) {
     const int64_t b = blockIdx.y;
     const int64_t ML = a.M1 + a.M2;
     int64_t bv[2] = {INT64_MIN, INT64_MIN}, bk[2] = {INT64_MAX, INT64_MAX};
-    const int64_t idx = (int64_t)blockIdx.x * RED_T + threadIdx.x;  // one output per thread
+    // one output per thread, over this launch's MMA outputs only (the tiles [at0, at0 +
+    // n_atp) of a split correlation; leftovers: finish_pair): k in [klo, khi_j) per modulus
+    const int64_t klo = (int64_t)P * T.at0 * T.NT, kt = (int64_t)P * (T.at0 + T.n_atp) * T.NT;
+    const int64_t kh0 = min(kt, (int64_t)P * a.NA[0]), kh1 = min(kt, (int64_t)P * a.NA[1]);
+    const int64_t n0 = max((int64_t)0, kh0 - klo), n1 = max((int64_t)0, kh1 - klo);
+    const int64_t e = (int64_t)blockIdx.x * RED_T + threadIdx.x;
     const PT *pp = reinterpret_cast<const PT *>(T.part) + b * T.n_cr * ML;
-    if (idx < ML) {
-        const int j = idx >= a.M1 ? 1 : 0;
-        const int64_t k = idx - (j ? a.M1 : 0);
-        const int64_t blk = k / P;
-        // MMA outputs of this launch's tiles only (leftovers: tc_tiled_final; split correlation)
-        if (k < (int64_t)P * a.NA[j] && blk >= (int64_t)T.at0 * T.NT && blk < (int64_t)(T.at0 + T.n_atp) * T.NT) {
+    if (e < n0 + n1) {
+        const int j = e >= n0 ? 1 : 0;
+        const int64_t k = klo + (j ? e - n0 : e);
+        const int64_t idx = (j ? a.M1 : 0) + k;
+        {
             int64_t r = 0;
             int c = 0;
             for (; c + 8 <= T.n_cr; c += 8) {  // eight loads in flight, summed in range order
@@ -743,7 +751,12 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     char *w = (char *)ws;
     auto carve = [&](size_t bytes) { char *q = w; w += align_up256(bytes); return q; };
     const int64_t ML_ = p->M1 + p->M2;
-    const int nred_cta = (int)((ML_ + RED_T - 1) / RED_T);
+    int64_t nred_out = 0;  // the reduce kernel's outputs: this launch's tiles' MMA outputs
+    {
+        const int64_t klo = (int64_t)P * T.at0 * g.NT, kt = (int64_t)P * (T.at0 + T.n_atp) * g.NT;
+        for (int j = 0; j < 2; ++j) nred_out += std::max<int64_t>(0, std::min<int64_t>(kt, (int64_t)P * g.NA[j]) - klo);
+    }
+    const int nred_cta = (int)std::max<int64_t>(1, (nred_out + RED_T - 1) / RED_T);
     T.nkey_cta = T.n_cr > 1 ? nred_cta : std::max(1, T.n_atp * T.n_cr);
     T.ckeys = (unsigned long long *)carve((size_t)batch * g.max_keys * 16);
     T.part = (int64_t *)carve(g.max_cr > 1 ? (size_t)batch * g.max_cr * (p->M1 + p->M2) * 8 : 0);
@@ -753,7 +766,7 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     T.lpart = (int64_t *)carve((size_t)batch * g.n_pcta * 2 * MAXLEFT * 8);
     T.done = (unsigned *)carve((size_t)batch * 4);
     T.resid = resid; T.residues_out = residues_out; T.k_out = k; T.keys_out = keys_out;
-    T.with_left = part == 0;  // the leftover outputs belong to part 0
+    T.with_left = part == nparts - 1;  // the leftover outputs: the last part (its windows hold their y)
     T.r_out[0] = (int64_t *)r1;
     T.r_out[1] = (int64_t *)r2;
     {
@@ -763,7 +776,7 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     }
     const dim3 grid((unsigned)(T.n_atp * T.n_cr), (unsigned)batch);
     const int64_t ML = p->M1 + p->M2;
-    const dim3 gr((unsigned)((ML + RED_T - 1) / RED_T), (unsigned)batch);
+    const dim3 gr((unsigned)nred_cta, (unsigned)batch);
     T.n_last = T.n_cr > 1 ? (int)gr.x : T.n_atp * T.n_cr;
     cudaError_t e = cudaSuccess;
     if (T.n_atp > 0) {
