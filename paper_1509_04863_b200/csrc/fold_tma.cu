@@ -129,10 +129,12 @@ __device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, int sh) { retu
 struct Item {
     int64_t b, gi, ra, nrow, cs_cta, width;
 };
-// contig items: (segment s << 36) | (first row << 12) | rows (<= 4095)
+// contig items: (segment s << 36) | (first row << 12) | rows (<= 4095); CONTIG =
+// false compiles the round-robin decode only (the fused kernel: whole pairs)
+template <bool CONTIG = true>
 __device__ __forceinline__ Item decode(const TmaArgs &a, int64_t item) {
     Item it;
-    if (a.contig) {
+    if (CONTIG && a.contig) {
         const int64_t sgm = item >> 36;
         it.gi = sgm % a.n_groups;
         it.b = sgm / a.n_groups;
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
             int64_t lin = rb(blockIdx.x), lend = rb(blockIdx.x + 1);
             for (int64_t seq = 0;; ++seq) {
                 int64_t item;
-                if (a.contig) {
+                if (!TCM && a.contig) {
                     if (lin >= lend) {
                         item = -1;
                     } else {
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                     mbar_arrive(&full[s]);
                     break;
                 }
-                const Item it = decode(a, item);
+                const Item it = decode<!TCM>(a, item);
                 const int8_t *base = a.x + it.b * a.ldx + it.ra * a.M1 + it.cs_cta;
                 for (int64_t r0 = 0; r0 < it.nrow; r0 += SROWS) {
                     const int nr = (int)((it.nrow - r0) < SROWS ? (it.nrow - r0) : SROWS);
@@ -369,8 +371,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                 mbar_wait(reinterpret_cast<uint64_t *>(smem + a.tc_off + a.tca.offMisc + tc::MISC_PBEGIN) + pb, pph);
                 const int64_t item0 = pitem[pb];
                 if (item0 >= 0 && a.owner && !a.block) {
-                    const int nx = (int)((a.K + decode(a, item0).nrow + 15) / 16);
-                    const uint4 *src = reinterpret_cast<const uint4 *>(a.x + decode(a, item0).b * a.ldx);
+                    const int nx = (int)((a.K + decode<!TCM>(a, item0).nrow + 15) / 16);
+                    const uint4 *src = reinterpret_cast<const uint4 *>(a.x + decode<!TCM>(a, item0).b * a.ldx);
                     uint4 *dst = reinterpret_cast<uint4 *>(xs);
                     for (int i = et; i < nx; i += NE * 32) dst[i] = src[i];
                 }
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                 }
                 break;
             }
-            const Item it = decode(a, item);
+            const Item it = decode<!TCM>(a, item);
             const int ntile = (int)((it.nrow + 15) / 16);
             const int width = (int)it.width;
             const uint16_t *pv = privb + pb * TW * a.priv_stride;
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
             }
             break;
         }
-        const Item it = decode(a, item);
+        const Item it = decode<!TCM>(a, item);
         const int nrow = (int)it.nrow;
         const int ntile = (nrow + 15) / 16;
         const int width = (int)it.width;
