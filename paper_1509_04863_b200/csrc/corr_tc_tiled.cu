@@ -70,6 +70,8 @@ struct TiledArgs {
     int nkey_cta;              // CTAs per pair that write ckeys (the pair's last kernel)
     void *part;                // [batch][n_cr][M1 + M2] partial r of each template range (n_cr > 1):
     int part32;                // int32 when every partial provably fits (plan bound), else int64
+    int accum;                 // 1: the ranges add their partials into ONE int64 row (red.add) instead
+                               // of storing them (part = [batch][M1 + M2] int64, zeroed by prep)
     int64_t *r_out[2];         // [batch][Mj] r outputs (staged tm_correlate) or NULL
     int64_t *lpart;            // [batch][n_pcta][2][MAXLEFT] leftover partial dot products
     unsigned *done;            // [batch] CTAs of the pair's last kernel finished (zeroed by prep)
@@ -114,7 +116,11 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
 #pragma unroll
     for (int q = 0; q < MAXLEFT; ++q) lacc0[q] = lacc1[q] = 0;
 
-    // ---- zeroing (done counts the last kernel's CTAs)
+    // ---- zeroing (done counts the last kernel's CTAs; the accumulated partial row)
+    if (T.accum) {
+        int64_t *acc = reinterpret_cast<int64_t *>(T.part) + b * (a.M1 + a.M2);
+        for (int64_t i = gtid; i < a.M1 + a.M2; i += gstride) acc[i] = 0;
+    }
     if (blockIdx.x == 0 && tid == 0) T.done[b] = 0;
 
     // ---- planes + block limb counts + leftovers: thread = 16 entries (block s,
@@ -516,9 +522,16 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
                     const int64_t k = P * ab + brow;
                     if (ab < a.NA[j] && k < a.M[j]) {
                         if (T.n_cr > 1) {  // this range's partial r (summed by tiled_reduce)
-                            const int64_t o = (b * T.n_cr + cr) * (a.M1 + a.M2) + (j ? a.M1 : 0) + k;
-                            if (T.part32) reinterpret_cast<int32_t *>(T.part)[o] = (int32_t)r[i][j];
-                            else reinterpret_cast<int64_t *>(T.part)[o] = r[i][j];
+                            if (T.accum) {  // exact: int64 adds commute
+                                unsigned long long *acc = reinterpret_cast<unsigned long long *>(T.part) +
+                                                          b * (a.M1 + a.M2) + (j ? a.M1 : 0) + k;
+                                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(acc),
+                                             "l"((unsigned long long)r[i][j]) : "memory");
+                            } else {
+                                const int64_t o = (b * T.n_cr + cr) * (a.M1 + a.M2) + (j ? a.M1 : 0) + k;
+                                if (T.part32) reinterpret_cast<int32_t *>(T.part)[o] = (int32_t)r[i][j];
+                                else reinterpret_cast<int64_t *>(T.part)[o] = r[i][j];
+                            }
                         } else {
                             if (T.r_out[j]) T.r_out[j][b * a.M[j] + k] = r[i][j];
                             amax(bv[j], bk[j], r[i][j], k);
@@ -573,6 +586,10 @@ __global__ void __launch_bounds__(RED_T) tiled_reduce(const TiledArgs T) {
         {
             int64_t r = 0;
             int c = 0;
+            if (T.accum) {
+                r = __ldcg(reinterpret_cast<const int64_t *>(T.part) + b * ML + idx);
+                c = T.n_cr;
+            }
             for (; c + 8 <= T.n_cr; c += 8) {  // eight loads in flight, summed in range order
                 PT v[8];
 #pragma unroll
@@ -748,6 +765,13 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     T.CR = (NC + n_cr - 1) / n_cr;
     T.n_cr = (NC + T.CR - 1) / T.CR;
     T.part32 = (double)T.CR * P * xmax * ybound < 2147483647.0;  // |partial| <= CR P max|t| max|y|
+    {
+        // several ranges: accumulate the partials with int64 red.add into one row
+        // (exact; cfg5 correlation ~2 us less than storing 17 partial rows and summing
+        // them); TM_TILED_ACC=0 stores and sums instead (A/B)
+        static const char *env_acc = getenv("TM_TILED_ACC");
+        T.accum = (T.n_cr > 1 && !(env_acc && env_acc[0] == '0')) ? 1 : 0;
+    }
     char *w = (char *)ws;
     auto carve = [&](size_t bytes) { char *q = w; w += align_up256(bytes); return q; };
     const int64_t ML_ = p->M1 + p->M2;

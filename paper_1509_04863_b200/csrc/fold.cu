@@ -213,7 +213,10 @@ static int fold_impl(const tm_plan_s *p, const void *x, int64_t ldx, int64_t bat
         if (rc != TM_EUNSUPPORTED) {
             if (rc != TM_OK || !used_counts) return rc;
             tm_ws_layout L = tm_ws(p, batch);
+            // ~4 bins per thread when the grid stays several waves deep (many pairs),
+            // one per thread otherwise (one pair: cfg5, 129 -> 513 CTAs)
             int64_t gx = (p->M2 + p->K + 1023) / 1024;
+            if (gx * batch < 4 * (int64_t)p->num_sms) gx = (p->M2 + p->K + 255) / 256;
             { const cudaError_t e_ = launch_pdl(fold_finalize, dim3((unsigned)gx, (unsigned)batch), dim3(256), 0, s,
                 (const int8_t *)x, ldx, p->N, offset, len, p->M1, p->M2, p->K, p->q2, offset / p->M1, rows,
                 (const int32_t *)((char *)ws + L.fold_counts), (int32_t *)y1, ldy1, (int32_t *)y2, ldy2, accumulate,
