@@ -198,8 +198,8 @@ __device__ __forceinline__ int32_t comb3(const uint16_t *pv, int stride, int d, 
 // finished pair on the tensor cores (tc_core.cuh) while the fold streams the next.
 constexpr int TC_GROUP = 5;  // named barrier of the tensor-core warps
 
-template <int NST, int MINB = 1, bool TCM = false>
-__global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MINB)
+template <int NST, int MINB = 1, bool TCM = false, int NEP = NE>
+__global__ void __launch_bounds__((TW + 1 + NEP) * 32 + (TCM ? tc::NTHR : 0), MINB)
     fold_pm1_tma(TmaArgs a) {
     constexpr bool FUSED = TCM;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -212,8 +212,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
     uint64_t *full = reinterpret_cast<uint64_t *>(privb + 2 * TW * a.priv_stride);
     uint64_t *empty = full + NST;
     uint64_t *pfull = empty + NST;   // [2]: consumers -> epilogue (count TW)
-    uint64_t *pempty = pfull + 2;    // [2]: epilogue -> consumers (count NE)
-    uint64_t *yready = pempty + 2;   // [2]: y1 + y2 of a pair in global memory (count TW + NE)
+    uint64_t *pempty = pfull + 2;    // [2]: epilogue -> consumers (count NEP)
+    uint64_t *yready = pempty + 2;   // [2]: y1 + y2 of a pair in global memory (count TW + NEP)
     uint64_t *ydone = yready + 2;    // [2]: tensor-core warps finished with a pair (count NTHR / 32)
     int64_t *item_q = reinterpret_cast<int64_t *>(ydone + 2);  // [8] producer -> consumers: item of seq
     int64_t *pitem = item_q + 8;     // [2] consumers -> epilogue / NTT warps: item of a buffer (-1 = end)
@@ -234,8 +234,8 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&pfull[b], TW);
-            mbar_init(&pempty[b], NE);
-            mbar_init(&yready[b], TW + NE);
+            mbar_init(&pempty[b], NEP);
+            mbar_init(&yready[b], TW + NEP);
             mbar_init(&ydone[b], NTW > 0 ? NTW : 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -243,11 +243,11 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
     __syncthreads();
 
     if constexpr (TCM) {
-        if (warp >= TW + 1 + NE) {
+        if (warp >= TW + 1 + NEP) {
             // ------------------------------------------------- tensor-core warps
             // steps 4-9 of each finished pair (tc_core.cuh), one pair behind the fold
             using GS = tc::GroupSync<TC_GROUP>;
-            const int gt = threadIdx.x - (TW + 1 + NE) * 32;
+            const int gt = threadIdx.x - (TW + 1 + NEP) * 32;
             uint8_t *tsm = smem + a.tc_off;
             uint32_t *tslot = reinterpret_cast<uint32_t *>(tsm + a.tca.offMisc + 8);
             if (gt < 32) {
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
 
     if (warp > TW) {
         // ------------------------------------------------------------ epilogue
-        const int et = threadIdx.x - (TW + 1) * 32;  // 0 .. NE*32-1
+        const int et = threadIdx.x - (TW + 1) * 32;  // 0 .. NEP*32-1
         int pb = 0;
         uint32_t pph = 0;
         bool pdl_done = false;
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                     const int nx = (int)((a.K + decode<!TCM>(a, item0).nrow + 15) / 16);
                     const uint4 *src = reinterpret_cast<const uint4 *>(a.x + decode<!TCM>(a, item0).b * a.ldx);
                     uint4 *dst = reinterpret_cast<uint4 *>(xs);
-                    for (int i = et; i < nx; i += NE * 32) dst[i] = src[i];
+                    for (int i = et; i < nx; i += NEP * 32) dst[i] = src[i];
                 }
             }
             mbar_wait(&pfull[pb], pph);
@@ -404,9 +404,9 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                         const int nx = (int)((a.K + q + 15) / 16);
                         const uint4 *src = reinterpret_cast<const uint4 *>(a.x + it.b * a.ldx);
                         uint4 *dst = reinterpret_cast<uint4 *>(xs);
-                        for (int i = et; i < nx; i += NE * 32) dst[i] = src[i];
+                        for (int i = et; i < nx; i += NEP * 32) dst[i] = src[i];
                     }
-                    asm volatile("bar.sync 2, %0;" ::"n"(NE * 32) : "memory");
+                    asm volatile("bar.sync 2, %0;" ::"n"(NEP * 32) : "memory");
                 }
                 const int8_t *xb = reinterpret_cast<const int8_t *>(xs);
                 int32_t *o2 = a.y2 + it.b * a.ldy2;
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                                   ((reinterpret_cast<uintptr_t>(o2) & 15) == 0);
                 if (runs) {
                     const int stride = a.priv_stride;
-                    if (et == NE * 32 - 1) {
+                    if (et == NEP * 32 - 1) {
                         // bin M1 = M2 - 1 in closed form: only the diagonal d = -1 (strip 0,
                         // index pad - 1) reaches it; its row g* = 0 < q is one element short,
                         // and the mod-N wrap adds x[q - 1]
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                         if (!a.block) v += xb[q - 1];
                         o2[M1] = v;
                     }
-                    for (int r = et; r < (M1 >> 4); r += NE * 32) {
+                    for (int r = et; r < (M1 >> 4); r += NEP * 32) {
                         const int k0 = r << 4;
                         const int w1 = k0 >> 9, rel = (k0 & 511) + pad;
                         int32_t C[16];
@@ -488,7 +488,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                     }
                 }
 #pragma unroll 2
-                for (int k = runs ? M2 : et; k < M2; k += NE * 32) {  // (runs: every bin is done)
+                for (int k = runs ? M2 : et; k < M2; k += NEP * 32) {  // (runs: every bin is done)
                     // bin k collects the unwrapped diagonals d = k and d = k - M2 (d >= dlo)
                     int32_t C = c3 ? comb3(pv, a.priv_stride, k, pad, nw) : comb_at(pv, a.priv_stride, k, ntile, width);
                     if (k - M2 >= dlo)
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                         if (a.accumulate) o2[M2 + k] += e; else o2[M2 + k] = e;
                     }
                 }
-                asm volatile("bar.sync 2, %0;" ::"n"(NE * 32) : "memory");  // xs reuse
+                asm volatile("bar.sync 2, %0;" ::"n"(NEP * 32) : "memory");  // xs reuse
             } else {
                 int32_t *c2 = a.counts + it.b * (a.M1 + a.M2) + a.M1;
                 const int64_t g0 = a.row0 + it.ra;
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__((TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0), MIN
                 if (bin0 < 0) bin0 += a.M2;
                 const int pad = 16 * ntile, nw = width >> 9;
                 const bool c3 = pad <= 1024;
-                for (int i = et; i < width - dlo; i += NE * 32) {
+                for (int i = et; i < width - dlo; i += NEP * 32) {
                     const int v = c3 ? comb3(pv, a.priv_stride, dlo + i, pad, nw)
                                      : comb_at(pv, a.priv_stride, dlo + i, ntile, width);
                     if (v) {
@@ -793,12 +793,12 @@ size_t smem_bytes(const TmaArgs &a, int nst) {
     return (size_t)nst * STAGE_BYTES + (size_t)2 * a.acc_words * 2 + (2 * nst + 8) * 8 + 10 * 8 + a.xs_bytes;
 }
 
-template <int NST, int MINB = 1, bool TCM = false>
+template <int NST, int MINB = 1, bool TCM = false, int NEP = NE>
 int launch(const TmaArgs &a, int64_t grid, size_t smem, cudaStream_t s) {
-    auto k = fold_pm1_tma<NST, MINB, TCM>;
+    auto k = fold_pm1_tma<NST, MINB, TCM, NEP>;
     cudaError_t e = tm_smem_attr((const void *)k, 227 * 1024, true);
     if (e != cudaSuccess) return tm_cuda_status(e, "fold_pm1_tma: shared-memory attribute");
-    const unsigned nthr = (TW + 1 + NE) * 32 + (TCM ? tc::NTHR : 0);
+    const unsigned nthr = (TW + 1 + NEP) * 32 + (TCM ? tc::NTHR : 0);
     if (tm_pdl_enabled()) {  // programmatic dependent launch: see pdl_trigger / pdl_wait
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)grid);
@@ -847,7 +847,17 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     // ring stages: 5 for rows read as >= 8 separate 4 KB pieces (wide M1: cfg5's 16
     // column groups, 0.3389 -> 0.3355 ms), 4 otherwise (contiguous 32 KB stages
     // measured 4-5% slower with 5: cfg4a 0.177 -> 0.185 ms)
-    const int nst = (a.n_groups >= 8 && TM_FOLD_NST_DEF == 4) ? 5 : TM_FOLD_NST_DEF;
+    int nst = (a.n_groups >= 8 && TM_FOLD_NST_DEF == 4) ? 5 : TM_FOLD_NST_DEF;
+    // dual: two smaller fold CTAs per SM (2-stage rings, 4 epilogue warps, items <= 1024
+    // rows): 16 consumer warps per SM instead of 8
+    // (same box, per step: cfg5 (16 groups) 0.383 -> 0.375 ms, K = 8192 (2 groups)
+    // 0.233 -> 0.223, K = 4096 (1 group) 0.200 -> 0.197, but K = 16384 (4 groups)
+    // 0.277 -> 0.285 and K = 32768 / 65536 (8 / 16 groups of 64 pairs) unchanged:
+    // dual except for 3..7 column groups; TM_FOLD_DUAL=0/1 forces)
+    static const char *env_dual = getenv("TM_FOLD_DUAL");
+    bool dual = !a.owner && (a.n_groups <= 2 || a.n_groups >= 8);
+    if (env_dual) dual = !a.owner && env_dual[0] == '1';
+    if (dual) nst = 2;
     if (!a.owner && !(env_contig && env_contig[0] == '0')) {
         // split items: each CTA folds one contiguous range of (pair, group, row) --
         // balanced to 16 rows, with R up to the shared-memory budget -- instead of
@@ -858,12 +868,13 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
 #ifndef TM_FOLD_RCAP
 #define TM_FOLD_RCAP 2048
 #endif
-        int64_t Rc = TM_FOLD_RCAP;
+        int64_t Rc = dual ? 1024 : TM_FOLD_RCAP;
+        const size_t budget = dual ? (size_t)112 * 1024 : (size_t)227 * 1024;
         while (Rc > 16) {
             a.R = Rc;
             a.priv_stride = (int)(512 + Rc);
             a.acc_words = TW * a.priv_stride;
-            if (smem_bytes(a, nst) <= 227 * 1024) break;
+            if (smem_bytes(a, nst) <= budget) break;
             Rc -= 256;
         }
     }
@@ -876,13 +887,18 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
     }
     const size_t smem = smem_bytes(a, nst);
     if (smem > 227 * 1024) return TM_EUNSUPPORTED;
-    int64_t grid = a.n_items < p->num_sms ? a.n_items : p->num_sms;
+#ifndef TM_FOLD_MINB
+#define TM_FOLD_MINB 1  // A/B: 2 = two (smaller) fold CTAs per SM
+#endif
+    const int64_t slots = (int64_t)p->num_sms * (dual ? 2 : TM_FOLD_MINB);
+    int64_t grid = a.n_items < slots ? a.n_items : slots;
     if (a.contig) {
         const int64_t units = (a.n_segs * a.rows + 15) / 16;
-        grid = units < p->num_sms ? units : p->num_sms;
+        grid = units < slots ? units : slots;
     }
-    if (nst == 5) return launch<5>(a, grid, smem, s);
-    return launch<TM_FOLD_NST>(a, grid, smem, s);
+    if (dual) return launch<2, 2, false, 4>(a, grid, smem, s);
+    if (nst == 5) return launch<5, TM_FOLD_MINB>(a, grid, smem, s);
+    return launch<TM_FOLD_NST, TM_FOLD_MINB>(a, grid, smem, s);
 }
 
 // The whole of Algorithm 1 in ONE persistent kernel with the tensor-core
