@@ -53,6 +53,9 @@ constexpr int64_t KEY_BIAS = (int64_t)1 << 42;
 constexpr int TNTHR = NTHR + 64;   // 8 epilogue warps, MMA issuer (warp 8), TMA producer (warp 9)
 constexpr int PREP_T = 256;
 constexpr int PREP_MAXCTA = 1024;  // prep CTAs per pair (bound for the leftover partials)
+constexpr int SPE = 24;            // sparse single-limb mode: at most this many entries of a pair's y
+                                   // outside [-128, 127] (cfg4, K = 16384: ~5 expected per pair)
+constexpr int SPREC = 1 + 3 * SPE; // ints per sparse record
 
 struct TiledArgs {
     TcArgs a;              // y, t, K, M, NA, NC, crt constants
@@ -65,6 +68,11 @@ struct TiledArgs {
     uint8_t *planes;       // [batch][np][8][2 S][16]
     uint8_t *aimg;         // [batch][JT][256]
     uint8_t *bmag;         // [batch][S] limbs block s needs
+    int sparse;            // 1: pairs with <= SPE entries of y outside int8 use ONE limb (y clamped
+                           // to int8) plus an exact sparse correction (see SparseList)
+    int32_t *spcnt;        // [batch][n_pcta] per prep CTA: its entries outside int8
+    int32_t *sprec;        // [batch][n_pcta][3 SPE] per prep CTA: its first <= SPE (idx, e, j)
+    int32_t *spair;        // [batch][SPREC] the pair's entries, for tiled_reduce (main kernel CTA 0)
     int NT;                    // output blocks per tile
     unsigned long long *ckeys; // [batch][nkey_cta][2] packed (max r, lowest k) per CTA and modulus
     int nkey_cta;              // CTAs per pair that write ckeys (the pair's last kernel)
@@ -100,6 +108,15 @@ __device__ __forceinline__ uint32_t tbyte(const int8_t *tr, int64_t K, int64_t j
     return (j >= 0 && j < K) ? (uint32_t)(uint8_t)tr[j] : 0u;
 }
 
+// blocks this launch's windows read: [at0 NT, (at0 + n_atp) NT + NC] (every block
+// when the leftovers are computed here: the last part holds them)
+__device__ __forceinline__ void plane_range(const TiledArgs &T, int64_t &s_lo, int64_t &s_hi) {
+    s_lo = (int64_t)T.at0 * T.NT;
+    s_hi = min(T.S, (int64_t)(T.at0 + T.n_atp) * T.NT + T.a.NC + 1);
+}
+
+__device__ __forceinline__ int32_t clamp8(int32_t v) { return max(-128, min(127, v)); }
+
 // ---------------------------------------------------------------------------
 // prep: planes, block limb counts, A image, leftover partials, zeroing
 // ---------------------------------------------------------------------------
@@ -109,6 +126,10 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
     const TcArgs &a = T.a;
     const int64_t b = blockIdx.y;
     const int tid = threadIdx.x;
+    __shared__ int sp_n;            // this CTA's entries of y outside int8 (sparse mode)
+    __shared__ int32_t sp_ent[3 * SPE];
+    if (tid == 0) sp_n = 0;
+    __syncthreads();
     const int64_t gtid = (int64_t)blockIdx.x * PREP_T + tid, gstride = (int64_t)gridDim.x * PREP_T;
     const int8_t *tr = a.t + b * a.ldt;
     const int nl0 = nleft_of(a.M[0], a.NA[0]), nl1 = nleft_of(a.M[1], a.NA[1]);
@@ -125,10 +146,8 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
 
     // ---- planes + block limb counts + leftovers: thread = 16 entries (block s,
     // modulus j, chunk column h); 16 consecutive threads cover one block of both moduli
-    // blocks this launch's windows read: [at0 NT, (at0 + n_atp) NT + NC) (every block
-    // when the leftovers are computed here: the last part holds them)
-    const int64_t s_lo = (int64_t)T.at0 * T.NT;
-    const int64_t s_hi = min(T.S, (int64_t)(T.at0 + T.n_atp) * T.NT + a.NC + 1);
+    int64_t s_lo, s_hi;
+    plane_range(T, s_lo, s_hi);
     const int64_t n16 = (s_hi - s_lo) * 16;
     const int64_t pstride = (int64_t)8 * 32 * T.S;  // bytes per plane (8 columns x 2 S rows x 16)
     uint8_t *pl = T.planes + b * T.np * pstride;
@@ -144,7 +163,7 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
         if (i0 + 16 <= len && ((((uintptr_t)(yr + i0)) & 15) == 0)) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const int4 u = *reinterpret_cast<const int4 *>(yr + i0 + 4 * q);
+                const int4 u = __ldg(reinterpret_cast<const int4 *>(yr + i0 + 4 * q));
                 v[4 * q] = u.x; v[4 * q + 1] = u.y; v[4 * q + 2] = u.z; v[4 * q + 3] = u.w;
             }
         } else {
@@ -154,6 +173,39 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
         int need = 1;
 #pragma unroll
         for (int e = 0; e < 16; ++e) need = max(need, limbs_needed(v[e]));
+        if (T.sparse) {  // record the entries outside int8 (invalid lanes hold 0); one atomic per
+                         // warp, none once the CTA has more than SPE (a dense pair)
+            int nexc = 0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) nexc += v[e] != clamp8(v[e]);
+            const int wtot = (int)__reduce_add_sync(0xffffffffu, (unsigned)nexc);
+            if (wtot) {
+                const int lane = tid & 31;
+                int base = 0;
+                if (lane == 0) base = *(volatile int *)&sp_n > SPE ? SPE + 1 : atomicAdd(&sp_n, wtot);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                int pre = nexc;  // inclusive prefix over the lanes
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, pre, o);
+                    if (lane >= o) pre += u;
+                }
+                if (base <= SPE && nexc) {
+                    int q = base + pre - nexc;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        if (v[e] != clamp8(v[e])) {
+                            if (q < SPE) {
+                                sp_ent[3 * q] = (int32_t)(i0 + e);
+                                sp_ent[3 * q + 1] = v[e] - clamp8(v[e]);
+                                sp_ent[3 * q + 2] = j;
+                            }
+                            ++q;
+                        }
+                    }
+                }
+            }
+        }
         // max over the 16 lanes of the block (both moduli, 8 columns)
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
@@ -171,7 +223,7 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int32_t x = v[4 * q + e] >> sh;
-                    c[e] = kind == 1 ? (x & 15) : x;
+                    c[e] = kind == 1 ? (x & 15) : kind == 0 ? clamp8(x) : x;  // plane 0: y clamped to int8
                 }
                 wd[q] = pack4(c[0], c[1], c[2], c[3]);
             }
@@ -218,6 +270,14 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
         *reinterpret_cast<uint4 *>(ai + 256 * J + 16 * sg) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     }
 
+    // ---- this CTA's sparse record (count, then its first <= SPE entries)
+    if (T.sparse) {
+        __syncthreads();
+        const int n = sp_n;
+        if (tid == 0) T.spcnt[b * T.n_pcta + blockIdx.x] = n;
+        if (tid < 3 * min(n, SPE)) T.sprec[(b * T.n_pcta + blockIdx.x) * 3 * SPE + tid] = sp_ent[tid];
+    }
+
     // ---- leftover partials of this CTA (fixed order: warp shuffle, then warps in order)
     if (nl0 + nl1 == 0) return;
     __shared__ int64_t red[PREP_T / 32][2 * MAXLEFT];
@@ -257,6 +317,30 @@ __device__ __forceinline__ void cta_keys(const TiledArgs &T, int64_t b, int slot
         for (int w = 0; w < nw; ++w) m = wk[w][threadIdx.x] > m ? wk[w][threadIdx.x] : m;
         T.ckeys[(b * T.nkey_cta + slot) * 2 + threadIdx.x] = m;
     }
+}
+
+// Sparse single-limb mode.  y = c + e with c = clamp(y, -128, 127) (plane 0) and e
+// nonzero only where y leaves int8.  r_j(k) = sum_idx t(idx - k) y_j(idx) (the
+// staged correlation, reading C3) = [one-limb MMA over c] + sum over the few
+// (idx, e) of e t(idx - k): exact in int64.  When a pair has 1..SPE such entries
+// in the blocks this launch reads (prep records them per prep CTA), every CTA of
+// the pair runs one limb and the kernel that produces the final r (the main
+// kernel's epilogue with one template range, else tiled_reduce) adds the
+// correction.  Entry order in the list is immaterial (exact integer sums).
+struct SparseList {
+    int n;
+    int32_t ent[3 * SPE];  // (idx, e, j)
+};
+// the correction of output k of modulus j
+__device__ __forceinline__ int64_t sparse_corr(const TiledArgs &T, int64_t b, const SparseList &L, int n, int j,
+                                               int64_t k) {
+    const int8_t *tr = T.a.t + b * T.a.ldt;
+    int64_t c = 0;
+    for (int q = 0; q < n; ++q) {
+        const int64_t i = (int64_t)L.ent[3 * q] - k;
+        if (L.ent[3 * q + 2] == j && i >= 0 && i < T.a.K) c += (int64_t)L.ent[3 * q + 1] * tr[i];
+    }
+    return c;
 }
 
 // Steps 7-9 of pair b, run by the CTA that finishes the pair's last kernel (all its
@@ -406,19 +490,50 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
     uint64_t *fin = mdone + 2;                                           // every MMA of the CTA done
     uint32_t *tslot = reinterpret_cast<uint32_t *>(fin + 1);
     long long ts[4] = {gtime(), 0, 0, 0};  // instrumentation (a.dbg): phase stamps
+    __shared__ SparseList spl;
+    __shared__ int wneed[TNTHR / 32], wcnt[TNTHR / 32];
     if (tid == 0) {
         mbar_init1(full); mbar_init1(full + 1); mbar_init1(mdone); mbar_init1(mdone + 1); mbar_init1(fin);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        spl.n = 0;
     }
-    // ---- limb count: the most any block of this CTA's window [a0 + cb, a0 + NT + ce - 1) needs
-    int need = 1;
+    // ---- limb count: the most any block of this CTA's window [a0 + cb, a0 + NT + ce - 1)
+    // needs, and (sparse mode) the pair's entries outside int8, in one round trip
+    int need = 1, cnt = 0;
     {
         const int64_t s0 = (int64_t)a0 + cb, n = NT + (ce - cb) - 1;
         for (int64_t i = tid; i < n; i += TNTHR)
             if (s0 + i < T.S) need = max(need, (int)T.bmag[b * T.S + s0 + i]);
+        if (T.sparse)
+            for (int c = tid; c < T.n_pcta; c += TNTHR) cnt += T.spcnt[b * T.n_pcta + c];
     }
-    const int nl = min(T.lmax, 1 + (__syncthreads_or(need >= 2) + __syncthreads_or(need >= 3) +
-                                     __syncthreads_or(need >= 4)));
+    need = __reduce_max_sync(0xffffffffu, need);
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) { wneed[warp] = need; wcnt[warp] = cnt; }
+    __syncthreads();
+    int nmax = 1, total = 0;
+#pragma unroll
+    for (int w = 0; w < TNTHR / 32; ++w) { nmax = max(nmax, wneed[w]); total += wcnt[w]; }
+    const int nsp = (total >= 1 && total <= SPE) ? total : 0;  // sparse pair: one limb + correction
+    if (nsp) {
+        for (int c = tid; c < T.n_pcta; c += TNTHR) {
+            const int m = T.spcnt[b * T.n_pcta + c];
+            if (m) {
+                const int32_t *rec = T.sprec + (b * T.n_pcta + c) * 3 * SPE;
+                const int o = atomicAdd(&spl.n, m);
+                for (int q = 0; q < 3 * m; ++q) spl.ent[3 * o + q] = rec[q];
+            }
+        }
+        __syncthreads();
+        if (T.n_cr > 1 && blockIdx.x == 0) {  // for tiled_reduce
+            int32_t *dst = T.spair + b * SPREC;
+            if (tid < 3 * nsp) dst[1 + tid] = spl.ent[tid];
+            if (tid == 0) dst[0] = nsp;
+        }
+    } else if (T.sparse && T.n_cr > 1 && blockIdx.x == 0 && tid == 0) {
+        T.spair[b * SPREC] = 0;
+    }
+    const int nl = nsp ? 1 : min(T.lmax, nmax);
     // TMEM: 2 NT columns per limb (two CTAs fit per SM while 2 NT nl <= 256)
     uint32_t ncols = 32;
     while (ncols < (uint32_t)(2 * NT * nl)) ncols *= 2;
@@ -514,6 +629,20 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
                     r[i][1] += (int64_t)v[2 * i + 1] * ((int64_t)1 << (4 * l));
                 }
             }
+            if (nsp && T.n_cr == 1) {  // sparse pair: + sum_q e_q t(idx_q - k)
+                const int8_t *tr = a.t + b * a.ldt;
+                for (int q = 0; q < nsp; ++q) {
+                    const int64_t idx = spl.ent[3 * q];
+                    const int64_t ev = spl.ent[3 * q + 1];
+                    const int jj = spl.ent[3 * q + 2];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int64_t ti = idx - (P * (a0 + ar0 + i) + brow);
+                        const int64_t c = (ti >= 0 && ti < a.K) ? ev * tr[ti] : 0;
+                        if (jj) r[i][1] += c; else r[i][0] += c;
+                    }
+                }
+            }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const int64_t ab = a0 + ar0 + i;
@@ -579,12 +708,15 @@ __global__ void __launch_bounds__(RED_T) tiled_reduce(const TiledArgs T) {
     const int64_t n0 = max((int64_t)0, kh0 - klo), n1 = max((int64_t)0, kh1 - klo);
     const int64_t e = (int64_t)blockIdx.x * RED_T + threadIdx.x;
     const PT *pp = reinterpret_cast<const PT *>(T.part) + b * T.n_cr * ML;
-    if (e < n0 + n1) {
-        const int j = e >= n0 ? 1 : 0;
-        const int64_t k = klo + (j ? e - n0 : e);
+    __shared__ SparseList spl;
+    const int nsp = T.sparse ? __ldcg(T.spair + b * SPREC) : 0;  // written by the main kernel's CTA 0
+    const bool have = e < n0 + n1;
+    const int j = e >= n0 ? 1 : 0;
+    const int64_t k = klo + (j ? e - n0 : e);
+    int64_t r = 0;
+    if (have) {
         const int64_t idx = (j ? a.M1 : 0) + k;
         {
-            int64_t r = 0;
             int c = 0;
             if (T.accum) {
                 r = __ldcg(reinterpret_cast<const int64_t *>(T.part) + b * ML + idx);
@@ -598,9 +730,16 @@ __global__ void __launch_bounds__(RED_T) tiled_reduce(const TiledArgs T) {
                 for (int u = 0; u < 8; ++u) r += (int64_t)v[u];
             }
             for (; c < T.n_cr; ++c) r += (int64_t)__ldcg(pp + c * ML + idx);
-            if (T.r_out[j]) T.r_out[j][b * a.M[j] + k] = r;
-            amax(bv[j], bk[j], r, k);
         }
+    }
+    if (nsp) {  // sparse pair: + sum_q e_q t(idx_q - k)
+        for (int q = threadIdx.x; q < 3 * nsp; q += RED_T) spl.ent[q] = __ldcg(T.spair + b * SPREC + 1 + q);
+        __syncthreads();
+        if (have) r += sparse_corr(T, b, spl, nsp, j, k);
+    }
+    if (have) {
+        if (T.r_out[j]) T.r_out[j][b * a.M[j] + k] = r;
+        amax(bv[j], bk[j], r, k);
     }
     cta_keys(T, b, blockIdx.x, bv, bk);
     arrive_and_finish(T, b);
@@ -712,6 +851,9 @@ size_t tm_tc_tiled_ws_bytes(const tm_plan_s *p, int64_t batch) {
     n += align_up256((size_t)batch * g.max_keys * 16);                      // per-CTA keys
     n += align_up256(g.max_cr > 1 ? (size_t)batch * g.max_cr * (p->M1 + p->M2) * 8 : 0);  // partial sums
     n += align_up256((size_t)batch * g.S);                                  // block limb counts
+    n += align_up256((size_t)batch * g.n_pcta * 4);                         // sparse counts per prep CTA
+    n += align_up256((size_t)batch * g.n_pcta * 3 * SPE * 4);               // sparse entries per prep CTA
+    n += align_up256((size_t)batch * SPREC * 4);                            // sparse list per pair
     n += align_up256((size_t)batch * g.np * 8 * 32 * g.S);                  // B planes
     n += align_up256((size_t)batch * g.JT * 256);                           // A image
     n += align_up256((size_t)batch * g.n_pcta * 2 * MAXLEFT * 8);           // leftover partials
@@ -769,12 +911,11 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         // several ranges: accumulate the partials with int64 red.add into one row
         // (exact; cfg5 correlation ~2 us less than storing 17 partial rows and summing
         // them); TM_TILED_ACC=0 stores and sums instead (A/B)
-        static const char *env_acc = getenv("TM_TILED_ACC");
+        const char *env_acc = getenv("TM_TILED_ACC");  // read per launch (tests flip it)
         T.accum = (T.n_cr > 1 && !(env_acc && env_acc[0] == '0')) ? 1 : 0;
     }
     char *w = (char *)ws;
     auto carve = [&](size_t bytes) { char *q = w; w += align_up256(bytes); return q; };
-    const int64_t ML_ = p->M1 + p->M2;
     int64_t nred_out = 0;  // the reduce kernel's outputs: this launch's tiles' MMA outputs
     {
         const int64_t klo = (int64_t)P * T.at0 * g.NT, kt = (int64_t)P * (T.at0 + T.n_atp) * g.NT;
@@ -785,6 +926,19 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     T.ckeys = (unsigned long long *)carve((size_t)batch * g.max_keys * 16);
     T.part = (int64_t *)carve(g.max_cr > 1 ? (size_t)batch * g.max_cr * (p->M1 + p->M2) * 8 : 0);
     T.bmag = (uint8_t *)carve((size_t)batch * g.S);
+    T.spcnt = (int32_t *)carve((size_t)batch * g.n_pcta * 4);
+    T.sprec = (int32_t *)carve((size_t)batch * g.n_pcta * 3 * SPE * 4);
+    T.spair = (int32_t *)carve((size_t)batch * SPREC * 4);
+    {
+        // sparse single-limb mode: plans that may need >= 2 limbs, except +-1 plans whose
+        // bins (sums of q signs, sd sqrt(q)) leave int8 often (sqrt(q) > 127 / 3: cfg4b,
+        // cfg5 -- there the records and the decision only cost time); TM_TILED_SPARSE=0 /
+        // 1: never / always (A/B)
+        const char *env_sp = getenv("TM_TILED_SPARSE");  // read per launch (tests flip it)
+        const int64_t qmax = p->q1 > p->q2 ? p->q1 : p->q2;
+        T.sparse = g.lmax >= 2 && (!(p->flags & TM_BINARY) || 9 * qmax <= 127 * 127) ? 1 : 0;
+        if (env_sp) T.sparse = (g.lmax >= 2 && env_sp[0] == '1') ? 1 : 0;
+    }
     T.planes = (uint8_t *)carve((size_t)batch * g.np * 8 * 32 * g.S);
     T.aimg = (uint8_t *)carve((size_t)batch * g.JT * 256);
     T.lpart = (int64_t *)carve((size_t)batch * g.n_pcta * 2 * MAXLEFT * 8);
@@ -799,7 +953,6 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         TM_CHECK_LAUNCH("tm_correlate: tiled_prep");
     }
     const dim3 grid((unsigned)(T.n_atp * T.n_cr), (unsigned)batch);
-    const int64_t ML = p->M1 + p->M2;
     const dim3 gr((unsigned)nred_cta, (unsigned)batch);
     T.n_last = T.n_cr > 1 ? (int)gr.x : T.n_atp * T.n_cr;
     cudaError_t e = cudaSuccess;

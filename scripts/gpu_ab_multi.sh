@@ -3,7 +3,7 @@ mkdir -p gpurun_out
 VARS=$1; R=${2:-3}; shift 2
 for i in $(seq $R); do
   for v in $VARS; do
-    if [ "$v" = base ]; then
+    if [ "$v" = base ] || [ "$v" = cur ]; then
       timeout 200 python bench.py --steps 100 --warmup 10 --no-cpu-baseline --e2e-steps 0 --no-cfg1 "$@" > gpurun_out/ab_$v.log 2>&1
     else
       TM_LIB_VARIANT=$v timeout 200 python bench.py --steps 100 --warmup 10 --no-cpu-baseline --e2e-steps 0 --no-cfg1 "$@" > gpurun_out/ab_$v.log 2>&1

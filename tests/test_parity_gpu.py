@@ -340,6 +340,39 @@ def test_tc_one_cta_and_tiled_kernels(tm, N, K, M, B, binary, tiled, monkeypatch
     check_int_pairs(tm, plan, x_h, t_h, range(B))
 
 
+@pytest.mark.parametrize("sparse,acc", [("1", "1"), ("0", "1"), ("1", "0")])
+@pytest.mark.parametrize("N,K,B", [(2 ** 18, 4096, 3), (2 ** 20, 8192, 3), (2 ** 18, 4096, 48)])
+def test_tiled_sparse_single_limb(tm, N, K, B, sparse, acc, monkeypatch):
+    """Sparse single-limb mode of the tiled tensor-core correlation: y = clamp(y,
+    -128, 127) + e with e nonzero at a few entries; pairs with 1..24 such entries
+    run ONE limb over the clamped y plus the exact correction sum e t(idx - k)
+    (corr_tc_tiled.cu sparse_list).  Data: +-1 with a few +127 / -128 spikes (a
+    handful of |y| > 127 bins; pair 2 of each group: 40 spikes, too many -> the
+    limb split).  Shapes give one template range per CTA (epilogue correction)
+    and several (tiled_reduce correction); TM_TILED_SPARSE=0 is the limb-split
+    control.  Several template ranges: the ranges add into one int64 row
+    (TM_TILED_ACC=1, default) or store their partials (TM_TILED_ACC=0) for
+    tiled_reduce.  Bit-exact y, r, residues, k against the oracle."""
+    monkeypatch.setenv("TM_TC_TILED", "1")
+    monkeypatch.setenv("TM_TILED_SPARSE", sparse)
+    monkeypatch.setenv("TM_TILED_ACC", acc)
+    plan = tm.Plan(N, K, seed=11, binary=False, engine="tc")
+    rng = np.random.default_rng(N + K + B + 7)
+    x_h = rng.choice(np.array([-1, 1], np.int8), (B, N))
+    for b in range(B):
+        nsp = 40 if b % 3 == 2 else 4
+        pos = rng.choice(N, nsp, replace=False)
+        x_h[b, pos] = np.where(rng.random(nsp) < 0.5, 127, -128).astype(np.int8)
+    t_h = rng.choice(np.array([-1, 1], np.int8), (B, K))
+    t_h[:, :64] = rng.integers(-128, 128, (B, 64)).astype(np.int8)
+    nexc = []
+    for b in range(min(B, 3)):
+        o = oracle.ftm(x_h[b], t_h[b])
+        nexc.append(int(sum(((y > 127) | (y < -128)).sum() for y in (o["y1"], o["y2"]))))
+    assert nexc[2] > 24 and min(nexc[:2]) >= 1, nexc
+    check_int_pairs(tm, plan, x_h, t_h, range(B) if B <= 3 else [0, 1, 2, B // 2, B - 1])
+
+
 def test_tc_and_ntt_engines_agree_on_cfg2(tm):
     """Every pair of a full cfg2 batch: residues and k from the two exact engines
     are identical (both are pinned to the oracle on sampled pairs above)."""
