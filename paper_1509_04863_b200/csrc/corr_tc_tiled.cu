@@ -52,6 +52,7 @@ constexpr int KEY_SHIFT = 21;
 constexpr int64_t KEY_BIAS = (int64_t)1 << 42;
 constexpr int TNTHR = NTHR + 64;   // 8 epilogue warps, MMA issuer (warp 8), TMA producer (warp 9)
 constexpr int PREP_T = 256;
+constexpr int PREP_MINB = 4;  // resident prep CTAs per SM (<= 64 registers); the grid is one wave
 constexpr int PREP_MAXCTA = 1024;  // prep CTAs per pair (bound for the leftover partials)
 constexpr int SPE = 24;            // sparse single-limb mode: at most this many entries of a pair's y
                                    // outside [-128, 127] (cfg4, K = 16384: ~5 expected per pair)
@@ -120,7 +121,7 @@ __device__ __forceinline__ int32_t clamp8(int32_t v) { return max(-128, min(127,
 // ---------------------------------------------------------------------------
 // prep: planes, block limb counts, A image, leftover partials, zeroing
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
+__global__ void __launch_bounds__(PREP_T, PREP_MINB) tiled_prep(const TiledArgs T) {
     pdl_trigger();
     pdl_wait();  // y and t come from the preceding launches
     const TcArgs &a = T.a;
@@ -133,9 +134,7 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
     const int64_t gtid = (int64_t)blockIdx.x * PREP_T + tid, gstride = (int64_t)gridDim.x * PREP_T;
     const int8_t *tr = a.t + b * a.ldt;
     const int nl0 = nleft_of(a.M[0], a.NA[0]), nl1 = nleft_of(a.M[1], a.NA[1]);
-    int64_t lacc0[MAXLEFT], lacc1[MAXLEFT];  // static indices: registers
-#pragma unroll
-    for (int q = 0; q < MAXLEFT; ++q) lacc0[q] = lacc1[q] = 0;
+    int64_t lacc = 0;  // leftover q = 0 of this thread's modulus (its pieces keep one modulus j)
 
     // ---- zeroing (done counts the last kernel's CTAs; the accumulated partial row)
     if (T.accum) {
@@ -144,7 +143,7 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
     }
     if (blockIdx.x == 0 && tid == 0) T.done[b] = 0;
 
-    // ---- planes + block limb counts + leftovers: thread = 16 entries (block s,
+    // ---- planes + block limb counts: thread = 16 entries (block s,
     // modulus j, chunk column h); 16 consecutive threads cover one block of both moduli
     int64_t s_lo, s_hi;
     plane_range(T, s_lo, s_hi);
@@ -170,14 +169,26 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = (i0 + e < len) ? yr[i0 + e] : 0;
         }
-        int need = 1;
+        uint32_t mm = 0;  // max of |v| or |v| - 1 (limbs_needed)
 #pragma unroll
-        for (int e = 0; e < 16; ++e) need = max(need, limbs_needed(v[e]));
+        for (int e = 0; e < 16; ++e) mm = max(mm, (uint32_t)(v[e] ^ (v[e] >> 31)));
+        int need = limbs_needed((int32_t)mm);
+        // leftover output P NA_j (q = 0; q >= 1: the pass below): this piece's t(idx - k) y_j(idx)
+        if (j ? nl1 : nl0) {
+            const int64_t k = (int64_t)P * a.NA[j];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int64_t i = i0 + e - k;
+                if (i >= 0 && i < a.K) lacc += (int64_t)tr[i] * v[e];
+            }
+        }
         if (T.sparse) {  // record the entries outside int8 (invalid lanes hold 0); one atomic per
                          // warp, none once the CTA has more than SPE (a dense pair)
             int nexc = 0;
+            if (mm > 127u) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) nexc += v[e] != clamp8(v[e]);
+                for (int e = 0; e < 16; ++e) nexc += v[e] != clamp8(v[e]);
+            }
             const int wtot = (int)__reduce_add_sync(0xffffffffu, (unsigned)nexc);
             if (wtot) {
                 const int lane = tid & 31;
@@ -229,21 +240,6 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
             }
             *reinterpret_cast<uint4 *>(pl + p * pstride + roff) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
         }
-        // leftover outputs k of modulus j: sum over this piece of t[idx - k] y_j[idx]
-        const int nlj = j ? nl1 : nl0;
-#pragma unroll
-        for (int q = 0; q < MAXLEFT; ++q) {
-            if (q < nlj) {
-                const int64_t k = (int64_t)P * a.NA[j] + q;
-                int64_t acc = 0;
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const int64_t i = i0 + e - k;
-                    if (i >= 0 && i < a.K) acc += (int64_t)tr[i] * v[e];
-                }
-                if (j) lacc1[q] += acc; else lacc0[q] += acc;
-            }
-        }
     }
 
     // ---- A image: row (J, sg) = t(16 J + sg + e - 127), e < 16
@@ -278,15 +274,35 @@ __global__ void __launch_bounds__(PREP_T) tiled_prep(const TiledArgs T) {
         if (tid < 3 * min(n, SPE)) T.sprec[(b * T.n_pcta + blockIdx.x) * 3 * SPE + tid] = sp_ent[tid];
     }
 
-    // ---- leftover partials of this CTA (fixed order: warp shuffle, then warps in order)
+    // ---- leftover outputs k = P NA_j + q (q < nleft_j): this CTA's share of
+    // sum_idx t(idx - k) y_j(idx) over the blocks this launch reads, one output at a
+    // time (the plane loop above keeps no accumulators); fixed order: warp shuffle,
+    // then warps in order
     if (nl0 + nl1 == 0) return;
     __shared__ int64_t red[PREP_T / 32][2 * MAXLEFT];
+    const int nlm = max(nl0, nl1);
+    for (int jq = 0; jq < 2 * MAXLEFT; ++jq) {
+        const int j = jq / MAXLEFT, q = jq % MAXLEFT;
+        if (q >= nlm) continue;  // uniform; red[][jq] unused (finish_pair reads q < nleft_j)
+        int64_t acc = 0;
+        if (q == 0) {
+            // pieces of modulus j only: the thread's lacc belongs to its own modulus
+            acc = ((gtid >> 3) & 1) == j ? lacc : 0;
+        } else if (q < (j ? nl1 : nl0)) {
+            const int64_t k = (int64_t)P * a.NA[j] + q;
+            const int32_t *yr = a.y[j] + b * a.ldy[j];
+            const int64_t lo = max(k, s_lo * P), hi = min(min(k + a.K, s_hi * P), a.len[j]);
+            for (int64_t pc = (lo >> 4) + gtid; 16 * pc < hi; pc += gstride) {
 #pragma unroll
-    for (int q = 0; q < 2 * MAXLEFT; ++q) {
-        int64_t v = q < MAXLEFT ? lacc0[q] : lacc1[q - MAXLEFT];
+                for (int e = 0; e < 16; ++e) {
+                    const int64_t idx = 16 * pc + e;
+                    if (idx >= lo && idx < hi) acc += (int64_t)tr[idx - k] * __ldg(yr + idx);
+                }
+            }
+        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((tid & 31) == 0) red[tid >> 5][q] = v;
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((tid & 31) == 0) red[tid >> 5][jq] = acc;
     }
     __syncthreads();
     if (tid < 2 * MAXLEFT) {
@@ -804,7 +820,7 @@ Geo geometry(const tm_plan_s *p, int64_t batch) {
     g.lmax = std::max(1, p->tct_lmax);
     g.np = 2 * g.lmax - 1;
     g.JT = 8 * (g.NC - 1) + 16;
-    const int64_t want = (4 * (int64_t)p->num_sms + batch - 1) / std::max<int64_t>(batch, 1);
+    const int64_t want = (int64_t)PREP_MINB * p->num_sms / std::max<int64_t>(batch, 1);
     g.n_pcta = (int)std::min<int64_t>(PREP_MAXCTA, std::max<int64_t>(1, want));
     // template ranges of >= one A chunk each, and their partial sums within the budget
     const size_t per = (size_t)std::max<int64_t>(batch, 1) * (size_t)(p->M1 + p->M2) * 8;
