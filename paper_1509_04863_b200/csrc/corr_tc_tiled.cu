@@ -702,7 +702,13 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
         d[7] = ((long long)smid << 32) | ((long long)npass << 8) | nl;
     }
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols));
-    if (T.n_cr == 1) arrive_and_finish(T, b);  // this kernel is the pair's last
+    if (T.n_cr == 1) {
+        arrive_and_finish(T, b);  // this kernel is the pair's last
+        if (a.dbg && tid == 0) {  // [4]: after the arrival (and, for the last CTA, finish_pair)
+            long long *d = a.dbg + 8 * ((int64_t)blockIdx.y * gridDim.x + blockIdx.x);
+            d[4] = gtime();
+        }
+    }
 }
 
 // several template ranges: r = sum of the ranges' partials (fixed order, exact

@@ -27,7 +27,8 @@ passes = (d[:, 7] >> 8) & 0xFFFFFF
 nl = d[:, 7] & 0xFF
 print(f'CTAs {len(d)}, SMs {len(np.unique(sm))}, passes p50 {np.median(passes)}, nl {np.bincount(nl)}')
 for name, v in [('start', d[:, 0] - t0), ('scan+alloc', d[:, 1] - d[:, 0]), ('loop', d[:, 2] - d[:, 1]),
-                ('epilogue', d[:, 3] - d[:, 2]), ('end', d[:, 3] - t0), ('wait(mma)', d[:, 4]),
-                ('tp+A', d[:, 5]), ('B stage+sync', d[:, 6])]:
+                ('epilogue', d[:, 3] - d[:, 2]), ('end', d[:, 3] - t0),
+                ('arrive+finish', np.where(d[:, 4] > 0, d[:, 4] - d[:, 3], 0)),
+                ('exit', np.where(d[:, 4] > 0, d[:, 4] - t0, 0))]:
     v = v / 1e3
     print(f'{name:14s} us: min {v.min():7.2f} p50 {np.median(v):7.2f} max {v.max():7.2f}')
