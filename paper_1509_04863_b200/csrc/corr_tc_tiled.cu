@@ -82,7 +82,7 @@ struct TiledArgs {
     int accum;                 // 1: the ranges add their partials into ONE int64 row (red.add) instead
                                // of storing them (part = [batch][M1 + M2] int64, zeroed by prep)
     int64_t *r_out[2];         // [batch][Mj] r outputs (staged tm_correlate) or NULL
-    int64_t *lpart;            // [batch][n_pcta][2][MAXLEFT] leftover partial dot products
+    int64_t *lpart;            // [batch][2][MAXLEFT][n_pcta] leftover partial dot products (per prep CTA)
     unsigned *done;            // [batch] CTAs of the pair's last kernel finished (zeroed by prep)
     int n_last;                // CTAs per pair of the last kernel (it runs finish_pair)
     int32_t *resid, *residues_out;   // finish_pair outputs (may be NULL)
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(PREP_T, PREP_MINB) tiled_prep(const TiledArgs 
     if (tid < 2 * MAXLEFT) {
         int64_t v = 0;
         for (int w = 0; w < PREP_T / 32; ++w) v += red[w][tid];
-        T.lpart[(b * T.n_pcta + blockIdx.x) * 2 * MAXLEFT + tid] = v;
+        T.lpart[(b * 2 * MAXLEFT + tid) * T.n_pcta + blockIdx.x] = v;
     }
 }
 
@@ -369,27 +369,17 @@ __device__ void finish_pair(const TiledArgs &T, int64_t b) {
     __shared__ int64_t fred[16][2 * MAXLEFT];
     __shared__ int64_t lsum[2 * MAXLEFT];
     if (T.with_left && nleft0 + nleft1) {
-        // one L2 round trip: thread c loads prep CTA c's 16 partials at once
-        int64_t v[2 * MAXLEFT];
-#pragma unroll
-        for (int q = 0; q < 2 * MAXLEFT; ++q) v[q] = 0;
-        for (int c = tid; c < T.n_pcta; c += blockDim.x) {
-            const int4 *src = reinterpret_cast<const int4 *>(T.lpart + (b * T.n_pcta + c) * 2 * MAXLEFT);
-#pragma unroll
-            for (int h = 0; h < MAXLEFT; ++h) {
-                const int4 u = __ldcg(src + h);
-                v[2 * h] += (int64_t)(((uint64_t)(uint32_t)u.y << 32) | (uint32_t)u.x);
-                v[2 * h + 1] += (int64_t)(((uint64_t)(uint32_t)u.w << 32) | (uint32_t)u.z);
-            }
-        }
-#pragma unroll
+        // per leftover output: the prep CTAs' partials are contiguous (coalesced,
+        // several loads in flight per thread)
         for (int q = 0; q < 2 * MAXLEFT; ++q) {
-            if ((q < MAXLEFT ? q < nleft0 : q - MAXLEFT < nleft1)) {
-                int64_t r = v[q];
+            if (!(q < MAXLEFT ? q < nleft0 : q - MAXLEFT < nleft1)) continue;  // uniform
+            const int64_t *src = T.lpart + (b * 2 * MAXLEFT + q) * T.n_pcta;
+            int64_t r = 0;
+#pragma unroll 4
+            for (int c = tid; c < T.n_pcta; c += blockDim.x) r += __ldcg(src + c);
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-                if (lane == 0) fred[warp][q] = r;
-            }
+            for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+            if (lane == 0) fred[warp][q] = r;
         }
         __syncthreads();
         if (tid < 2 * MAXLEFT) {
@@ -403,6 +393,7 @@ __device__ void finish_pair(const TiledArgs &T, int64_t b) {
     // the pair's key per modulus: max over the CTAs' keys (packed keys order like (r, -k))
     __shared__ unsigned long long fk[16][2];
     unsigned long long kmax[2] = {0ull, 0ull};
+#pragma unroll 4
     for (int c = tid; c < T.nkey_cta; c += blockDim.x) {
         const ulonglong2 u = __ldcg(reinterpret_cast<const ulonglong2 *>(T.ckeys) + b * T.nkey_cta + c);
         kmax[0] = u.x > kmax[0] ? u.x : kmax[0];
