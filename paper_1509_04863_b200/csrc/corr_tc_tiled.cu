@@ -74,6 +74,8 @@ struct TiledArgs {
     int32_t *spcnt;        // [batch][n_pcta] per prep CTA: its entries outside int8
     int32_t *sprec;        // [batch][n_pcta][3 SPE] per prep CTA: its first <= SPE (idx, e, j)
     int32_t *spair;        // [batch][SPREC] the pair's entries, for tiled_reduce (main kernel CTA 0)
+    int tsm;               // > 0: the main kernel stages the template (tsm >= K bytes) in shared memory
+                           // for the sparse correction of a one-range pair
     int NT;                    // output blocks per tile
     unsigned long long *ckeys; // [batch][nkey_cta][2] packed (max r, lowest k) per CTA and modulus
     int nkey_cta;              // CTAs per pair that write ckeys (the pair's last kernel)
@@ -497,6 +499,7 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
     uint64_t *fin = mdone + 2;                                           // every MMA of the CTA done
     uint32_t *tslot = reinterpret_cast<uint32_t *>(fin + 1);
     long long ts[4] = {gtime(), 0, 0, 0};  // instrumentation (a.dbg): phase stamps
+    long long te[2] = {0, 0};                // epilogue sub-phases (thread 0)
     __shared__ SparseList spl;
     __shared__ int wneed[TNTHR / 32], wcnt[TNTHR / 32];
     if (tid == 0) {
@@ -609,9 +612,35 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
         }
         umma_commit(fin);  // tracks every MMA this thread issued
     }
+    // sparse pair, one template range: while the MMAs run, the epilogue warps copy the
+    // template into shared memory for the corrections (random byte reads of t from
+    // L2 in the epilogue measured ~4 us per CTA at cfg4)
+    const int8_t *tcor = a.t + b * a.ldt;
+    if (nsp && T.n_cr == 1 && T.tsm && warp < NTHR / 32) {
+        int8_t *tsh = reinterpret_cast<int8_t *>(sm + smem_bytes<NT>());
+        if (((uintptr_t)tcor & 15) == 0) {
+            for (int64_t i = tid; 16 * i < a.K; i += NTHR)
+                reinterpret_cast<int4 *>(tsh)[i] = __ldg(reinterpret_cast<const int4 *>(tcor) + i);
+        } else {
+            for (int64_t i = tid; i < a.K; i += NTHR) tsh[i] = tcor[i];
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NTHR) : "memory");  // the epilogue warps only
+        tcor = tsh;
+    }
     // every warp: all MMAs complete (fin completes exactly once: parity 0; a wait on
-    // mdone's parity would return at once for a phase not yet begun)
-    mbar_wait(fin, 0);
+    // mdone's parity would return at once for a phase not yet begun).  Warps 0-7
+    // (idle through the loop): warp 0 polls, the others sleep in a named barrier,
+    // so they take no issue slots from the MMA issuer, the producer or the
+    // co-resident CTA's epilogue
+#ifndef TM_TILED_GROUPWAIT
+#define TM_TILED_GROUPWAIT 1
+#endif
+    if (TM_TILED_GROUPWAIT && warp < NTHR / 32) {
+        if (warp == 0) mbar_wait(fin, 0);
+        asm volatile("bar.sync 2, %0;" ::"n"(NTHR) : "memory");
+    } else {
+        mbar_wait(fin, 0);
+    }
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     ts[2] = gtime();
 
@@ -622,6 +651,12 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
         const int brow = P - 1 - (32 * qw + lane);
         const uint32_t taddr = tbase + ((uint32_t)(32 * qw) << 16);
         int64_t bv[2] = {INT64_MIN, INT64_MIN}, bk[2] = {INT64_MAX, INT64_MAX};
+        // per-thread constants (outputs k < 2^21 fit int): output k = kb + P (ar0 + i) is
+        // an MMA output of modulus j iff k < klim_j (block < NA_j and k < M_j)
+        const int kb = P * a0 + brow;
+        const int klim0 = (int)min((int64_t)P * a.NA[0], a.M[0]), klim1 = (int)min((int64_t)P * a.NA[1], a.M[1]);
+        const bool keys_only = T.n_cr == 1 && !T.r_out[0] && !T.r_out[1];
+        unsigned long long *accb = reinterpret_cast<unsigned long long *>(T.part) + b * (a.M1 + a.M2);
         for (int ar0 = (NT / 2) * hw; ar0 < (NT / 2) * hw + NT / 2; ar0 += 8) {
             int64_t r[8][2];
 #pragma unroll
@@ -630,38 +665,47 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
                 int32_t v[16];
                 tmem_ld16(taddr + 2 * NT * l + 2 * ar0, v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (tid == 0 && ar0 == 0 && l == 0) te[0] = gtime();  // (a.dbg) first TMEM load back
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     r[i][0] += (int64_t)v[2 * i] * ((int64_t)1 << (4 * l));
                     r[i][1] += (int64_t)v[2 * i + 1] * ((int64_t)1 << (4 * l));
                 }
             }
+            const int k0 = kb + P * ar0;  // output of (ar0 + i): k0 + P i
             if (nsp && T.n_cr == 1) {  // sparse pair: + sum_q e_q t(idx_q - k)
-                const int8_t *tr = a.t + b * a.ldt;
+                const int8_t *tr = tcor;
+                const int Kt = (int)a.K;
                 for (int q = 0; q < nsp; ++q) {
-                    const int64_t idx = spl.ent[3 * q];
-                    const int64_t ev = spl.ent[3 * q + 1];
+                    const int idx = spl.ent[3 * q];
+                    const int32_t ev = spl.ent[3 * q + 1];
                     const int jj = spl.ent[3 * q + 2];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const int64_t ti = idx - (P * (a0 + ar0 + i) + brow);
-                        const int64_t c = (ti >= 0 && ti < a.K) ? ev * tr[ti] : 0;
+                        const int ti = idx - (k0 + P * i);
+                        const int64_t c = (unsigned)ti < (unsigned)Kt ? (int64_t)ev * tr[ti] : 0;
                         if (jj) r[i][1] += c; else r[i][0] += c;
                     }
                 }
             }
+            if (keys_only) {  // one template range: the lowest-index max (k increases along the loop)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int k = k0 + P * i;
+                    if (k < klim0 && r[i][0] > bv[0]) { bv[0] = r[i][0]; bk[0] = k; }
+                    if (k < klim1 && r[i][1] > bv[1]) { bv[1] = r[i][1]; bk[1] = k; }
+                }
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const int64_t ab = a0 + ar0 + i;
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
-                    const int64_t k = P * ab + brow;
-                    if (ab < a.NA[j] && k < a.M[j]) {
+                    const int k = k0 + P * i;
+                    if (k < (j ? klim1 : klim0)) {
                         if (T.n_cr > 1) {  // this range's partial r (summed by tiled_reduce)
                             if (T.accum) {  // exact: int64 adds commute
-                                unsigned long long *acc = reinterpret_cast<unsigned long long *>(T.part) +
-                                                          b * (a.M1 + a.M2) + (j ? a.M1 : 0) + k;
-                                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(acc),
+                                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(accb + (j ? a.M1 : 0) + k),
                                              "l"((unsigned long long)r[i][j]) : "memory");
                             } else {
                                 const int64_t o = (b * T.n_cr + cr) * (a.M1 + a.M2) + (j ? a.M1 : 0) + k;
@@ -679,6 +723,7 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
         if (T.n_cr == 1) {
             mbv[0] = bv[0]; mbv[1] = bv[1]; mbk[0] = bk[0]; mbk[1] = bk[1];
         }
+        if (tid == 0) te[1] = gtime();  // (a.dbg) thread 0's epilogue outputs done
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -689,7 +734,7 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         long long *d = a.dbg + 8 * ((int64_t)blockIdx.y * gridDim.x + blockIdx.x);
         d[0] = ts[0]; d[1] = ts[1]; d[2] = ts[2]; d[3] = ts[3];
-        d[4] = 0; d[5] = 0; d[6] = 0;
+        d[4] = 0; d[5] = te[0]; d[6] = te[1];
         d[7] = ((long long)smid << 32) | ((long long)npass << 8) | nl;
     }
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols));
@@ -917,6 +962,10 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         const double cost = (double)((ctas + slots - 1) / slots) * (double)cr_blocks * t_block + part;
         if (cost < best * 0.97) { best = cost; n_cr = c; }
     }
+    {
+        static const char *env_ncr = getenv("TM_TILED_NCR");  // A/B: force the template-range count
+        if (env_ncr && atoi(env_ncr) >= 1) n_cr = std::min(atoi(env_ncr), g.max_cr);
+    }
     T.CR = (NC + n_cr - 1) / n_cr;
     T.n_cr = (NC + T.CR - 1) / T.CR;
     T.part32 = (double)T.CR * P * xmax * ybound < 2147483647.0;  // |partial| <= CR P max|t| max|y|
@@ -951,6 +1000,9 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         const int64_t qmax = p->q1 > p->q2 ? p->q1 : p->q2;
         T.sparse = g.lmax >= 2 && (!(p->flags & TM_BINARY) || 9 * qmax <= 127 * 127) ? 1 : 0;
         if (env_sp) T.sparse = (g.lmax >= 2 && env_sp[0] == '1') ? 1 : 0;
+        // the template staged in shared memory for one-range sparse corrections: <= 16 KB
+        // (NT = 32 keeps two CTAs per SM)
+        T.tsm = (T.sparse && p->K <= 16384) ? (int)((p->K + 15) / 16 * 16) : 0;
     }
     T.planes = (uint8_t *)carve((size_t)batch * g.np * 8 * 32 * g.S);
     T.aimg = (uint8_t *)carve((size_t)batch * g.JT * 256);
@@ -971,11 +1023,13 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     cudaError_t e = cudaSuccess;
     if (T.n_atp > 0) {
         if (g.NT == 64) {
-            e = tm_smem_attr((const void *)corr_tc_tiled<64>, smem_bytes<64>());
-            if (e == cudaSuccess) e = launch_pdl(corr_tc_tiled<64>, grid, dim3(TNTHR), smem_bytes<64>(), s, T);
+            const int sb = smem_bytes<64>() + T.tsm;
+            e = tm_smem_attr((const void *)corr_tc_tiled<64>, sb);
+            if (e == cudaSuccess) e = launch_pdl(corr_tc_tiled<64>, grid, dim3(TNTHR), sb, s, T);
         } else {
-            e = tm_smem_attr((const void *)corr_tc_tiled<32>, smem_bytes<32>());
-            if (e == cudaSuccess) e = launch_pdl(corr_tc_tiled<32>, grid, dim3(TNTHR), smem_bytes<32>(), s, T);
+            const int sb = smem_bytes<32>() + T.tsm;
+            e = tm_smem_attr((const void *)corr_tc_tiled<32>, sb);
+            if (e == cudaSuccess) e = launch_pdl(corr_tc_tiled<32>, grid, dim3(TNTHR), sb, s, T);
         }
         if (e != cudaSuccess) return tm_cuda_status(e, "corr_tc_tiled");
         TM_CHECK_LAUNCH("corr_tc_tiled");

@@ -28,6 +28,8 @@ nl = d[:, 7] & 0xFF
 print(f'CTAs {len(d)}, SMs {len(np.unique(sm))}, passes p50 {np.median(passes)}, nl {np.bincount(nl)}')
 for name, v in [('start', d[:, 0] - t0), ('scan+alloc', d[:, 1] - d[:, 0]), ('loop', d[:, 2] - d[:, 1]),
                 ('epilogue', d[:, 3] - d[:, 2]), ('end', d[:, 3] - t0),
+                ('epi: 1st TMEM ld', np.where(d[:, 5] > 0, d[:, 5] - d[:, 2], 0)),
+                ('epi: outputs done', np.where(d[:, 6] > 0, d[:, 6] - d[:, 2], 0)),
                 ('arrive+finish', np.where(d[:, 4] > 0, d[:, 4] - d[:, 3], 0)),
                 ('exit', np.where(d[:, 4] > 0, d[:, 4] - t0, 0))]:
     v = v / 1e3
