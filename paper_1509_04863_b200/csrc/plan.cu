@@ -10,6 +10,7 @@
 #include <atomic>
 #include <mutex>
 #include <new>
+#include <map>
 #include <set>
 #include <tuple>
 
@@ -245,17 +246,21 @@ static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 // pairs already set, under a mutex (plans may be used from several threads and
 // on several devices of one process)
 cudaError_t tm_smem_attr(const void *func, int bytes, bool max_carveout) {
+    // the attribute is a per-(function, device) maximum: only ever raised (setting a
+    // smaller value for one launch would break a later, larger launch)
     static std::mutex mu;
-    static std::set<std::tuple<const void *, int, int>> done;
+    static std::map<std::pair<const void *, int>, int> set_to;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(mu);
-    if (done.count({func, dev, bytes})) return cudaSuccess;
+    const auto key = std::make_pair(func, dev);
+    const auto it = set_to.find(key);
+    if (it != set_to.end() && it->second >= bytes) return cudaSuccess;
     e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e == cudaSuccess && max_carveout)
         e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    if (e == cudaSuccess) done.insert({func, dev, bytes});
+    if (e == cudaSuccess) set_to[key] = bytes;
     return e;
 }
 
