@@ -839,7 +839,9 @@ int tiled_nt(const tm_plan_s *p, int64_t batch) {
     if (env && (atoi(env) == 32 || atoi(env) == 64)) return atoi(env);
     int64_t na = 1;
     for (int64_t M : {p->M1, p->M2}) na = std::max(na, M / P + (M % P > MAXLEFT ? 1 : 0));
-    return batch * ((na + 63) / 64) >= p->num_sms ? 64 : 32;
+    // (>= 0.85 of the SMs: one CTA per SM at MMA N = 128 beats two per SM at N = 64; cfg4 K =
+    // 16384, 128 tiles: correlation 67 -> 63 us)
+    return batch * ((na + 63) / 64) * 20 >= (int64_t)p->num_sms * 17 ? 64 : 32;
 }
 struct Geo {
     int NT, NC, NA[2], n_at, lmax, np, JT, n_pcta, max_cr, max_keys;
@@ -954,7 +956,11 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     const double t_block = 4.0 * 2.0 * (4096.0 + 64.0 * g.NT) / 128.0 / 1900.0 * 2.0;  // 2 CTAs share an SM
     int n_cr = 1;
     double best = 1e300;
-    for (int c = 1; c <= g.max_cr; ++c) {
+    // tiles alone (nearly) filling the SMs: one range, no partial sums (the cost model's
+    // two-CTAs-per-SM time overstates one CTA per SM: cfg4 K = 16384 NT = 64, 1 vs 2 ranges
+    // 63 vs 110 us)
+    const bool one_range = batch * std::max(T.n_atp, 1) * 20 >= (int64_t)p->num_sms * 17;
+    for (int c = 1; c <= (one_range ? 1 : g.max_cr); ++c) {
         const int64_t ctas = batch * std::max(T.n_atp, 1) * c;
         const int cr_blocks = (NC + c - 1) / c;
         const bool p32 = (double)cr_blocks * P * xmax * ybound < 2147483647.0;
