@@ -215,10 +215,10 @@ int tm_tc_any_ld(const tm_plan_s *p, const void *y1, const void *y2, int64_t ldy
     const char *env = getenv("TM_TC_TILED");  // tests / A-B: "0" never, "1" whenever eligible
     const bool force = env && env[0] == '1', never = env && env[0] == '0';
     // one CTA per pair when it fits, except for long templates on fewer pairs than
-    // SMs (measured, 64 pairs: K = 16384 tiled 114 us vs one-CTA 134 us; K = 8192
-    // 73 vs 58; K = 4096 55 vs 35); the tiled kernel also takes the plans the
-    // one-CTA kernel cannot (cfg5: K = 65536)
-    const bool tiled_wins = batch < p->num_sms && p->K >= 12288;
+    // SMs (measured, 64 pairs, late round 2: K = 8192 tiled 45 us vs one-CTA 59 us
+    // (0.2197 vs 0.2240 ms per step); K = 4096 44 vs 37 us); the tiled kernel also
+    // takes the plans the one-CTA kernel cannot (cfg5: K = 65536)
+    const bool tiled_wins = batch < p->num_sms && p->K >= 8192;
     if (p->tct_ok && ws && !never && (force || !p->tc_ok || tiled_wins))
         return tm_tc_tiled_correlate(p, y1, y2, ldy1, ldy2, t, ldt, batch, r1, r2, resid, residues_out, k,
                                      (char *)ws + tm_ws(p, batch).tiled, s);
