@@ -674,19 +674,29 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
             }
             const int k0 = kb + P * ar0;  // output of (ar0 + i): k0 + P i
             if (nsp && T.n_cr == 1) {  // sparse pair: + sum_q e_q t(idx_q - k)
+                // |y| <= 524287 (tm_tc_tiled_plan: <= 4 limbs), so |e t| < 2^26 and the
+                // <= SPE = 24 terms of an output sum exactly in int32: one IMAD per term
+                // and modulus, no branches
                 const int8_t *tr = tcor;
                 const int Kt = (int)a.K;
+                int32_t c0[8], c1[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) c0[i] = c1[i] = 0;
                 for (int q = 0; q < nsp; ++q) {
-                    const int idx = spl.ent[3 * q];
+                    const int ti0 = spl.ent[3 * q] - k0;
                     const int32_t ev = spl.ent[3 * q + 1];
-                    const int jj = spl.ent[3 * q + 2];
+                    const bool jj = spl.ent[3 * q + 2] != 0;
+                    const int32_t e0 = jj ? 0 : ev, e1 = jj ? ev : 0;
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const int ti = idx - (k0 + P * i);
-                        const int64_t c = (unsigned)ti < (unsigned)Kt ? (int64_t)ev * tr[ti] : 0;
-                        if (jj) r[i][1] += c; else r[i][0] += c;
+                        const int ti = ti0 - P * i;
+                        const int32_t tv = (unsigned)ti < (unsigned)Kt ? (int32_t)tr[ti] : 0;
+                        c0[i] += e0 * tv;
+                        c1[i] += e1 * tv;
                     }
                 }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) { r[i][0] += c0[i]; r[i][1] += c1[i]; }
             }
             if (keys_only) {  // one template range: the lowest-index max (k increases along the loop)
 #pragma unroll
@@ -735,7 +745,7 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
         long long *d = a.dbg + 8 * ((int64_t)blockIdx.y * gridDim.x + blockIdx.x);
         d[0] = ts[0]; d[1] = ts[1]; d[2] = ts[2]; d[3] = ts[3];
         d[4] = 0; d[5] = te[0]; d[6] = te[1];
-        d[7] = ((long long)smid << 32) | ((long long)npass << 8) | nl;
+        d[7] = ((long long)smid << 32) | ((long long)min(nsp, 255) << 24) | ((long long)(npass & 0xFFFF) << 8) | nl;
     }
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols));
     if (T.n_cr == 1) {
@@ -749,8 +759,16 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
 
 // several template ranges: r = sum of the ranges' partials (fixed order, exact
 // int64), the lowest-index max per pair and modulus -> packed-key atomicMax.
-// Thread = 4 consecutive outputs of one modulus; CTA = 1024 outputs.
+// Thread = RED_E consecutive outputs; the thread's and then the CTA's best output
+// as one packed key (pack_key orders like (r, -k), so a u64 max is the
+// lowest-index max: half the shuffles of an (r, k) pair reduction).  The kernel is
+// a chain of latencies (cfg5: a 1 MB read); RED_E = 4 (fewer arrivals, fewer keys
+// for finish_pair) measured 2.5 us slower per cfg5 step than RED_E = 1.
 constexpr int RED_T = 256;
+#ifndef TM_RED_E
+#define TM_RED_E 1
+#endif
+constexpr int RED_E = TM_RED_E;
 template <typename PT>
 __global__ void __launch_bounds__(RED_T) tiled_reduce(const TiledArgs T) {
     pdl_trigger();
@@ -758,48 +776,84 @@ __global__ void __launch_bounds__(RED_T) tiled_reduce(const TiledArgs T) {
     const TcArgs &a = T.a;
     const int64_t b = blockIdx.y;
     const int64_t ML = a.M1 + a.M2;
-    int64_t bv[2] = {INT64_MIN, INT64_MIN}, bk[2] = {INT64_MAX, INT64_MAX};
-    // one output per thread, over this launch's MMA outputs only (the tiles [at0, at0 +
-    // n_atp) of a split correlation; leftovers: finish_pair): k in [klo, khi_j) per modulus
+    // over this launch's MMA outputs only (the tiles [at0, at0 + n_atp) of a split
+    // correlation; leftovers: finish_pair): k in [klo, khi_j) per modulus
     const int64_t klo = (int64_t)P * T.at0 * T.NT, kt = (int64_t)P * (T.at0 + T.n_atp) * T.NT;
     const int64_t kh0 = min(kt, (int64_t)P * a.NA[0]), kh1 = min(kt, (int64_t)P * a.NA[1]);
     const int64_t n0 = max((int64_t)0, kh0 - klo), n1 = max((int64_t)0, kh1 - klo);
-    const int64_t e = (int64_t)blockIdx.x * RED_T + threadIdx.x;
+    const int64_t e0 = ((int64_t)blockIdx.x * RED_T + threadIdx.x) * RED_E;
     const PT *pp = reinterpret_cast<const PT *>(T.part) + b * T.n_cr * ML;
     __shared__ SparseList spl;
     const int nsp = T.sparse ? __ldcg(T.spair + b * SPREC) : 0;  // written by the main kernel's CTA 0
-    const bool have = e < n0 + n1;
-    const int j = e >= n0 ? 1 : 0;
-    const int64_t k = klo + (j ? e - n0 : e);
-    int64_t r = 0;
-    if (have) {
-        const int64_t idx = (j ? a.M1 : 0) + k;
-        {
+    int64_t r[RED_E];
+    int64_t idx[RED_E];
+#pragma unroll
+    for (int u = 0; u < RED_E; ++u) {
+        const int64_t e = e0 + u;
+        const int j = e >= n0 ? 1 : 0;
+        const int64_t k = klo + (j ? e - n0 : e);
+        idx[u] = e < n0 + n1 ? (j ? a.M1 : 0) + k : -1;
+        r[u] = 0;
+    }
+    if (T.accum) {
+#pragma unroll
+        for (int u = 0; u < RED_E; ++u)
+            if (idx[u] >= 0) r[u] = __ldcg(reinterpret_cast<const int64_t *>(T.part) + b * ML + idx[u]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < RED_E; ++u) {
+            if (idx[u] < 0) continue;
             int c = 0;
-            if (T.accum) {
-                r = __ldcg(reinterpret_cast<const int64_t *>(T.part) + b * ML + idx);
-                c = T.n_cr;
-            }
             for (; c + 8 <= T.n_cr; c += 8) {  // eight loads in flight, summed in range order
                 PT v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = __ldcg(pp + (c + u) * ML + idx);
+                for (int q = 0; q < 8; ++q) v[q] = __ldcg(pp + (c + q) * ML + idx[u]);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) r += (int64_t)v[u];
+                for (int q = 0; q < 8; ++q) r[u] += (int64_t)v[q];
             }
-            for (; c < T.n_cr; ++c) r += (int64_t)__ldcg(pp + c * ML + idx);
+            for (; c < T.n_cr; ++c) r[u] += (int64_t)__ldcg(pp + c * ML + idx[u]);
         }
     }
     if (nsp) {  // sparse pair: + sum_q e_q t(idx_q - k)
         for (int q = threadIdx.x; q < 3 * nsp; q += RED_T) spl.ent[q] = __ldcg(T.spair + b * SPREC + 1 + q);
         __syncthreads();
-        if (have) r += sparse_corr(T, b, spl, nsp, j, k);
+#pragma unroll
+        for (int u = 0; u < RED_E; ++u)
+            if (idx[u] >= 0) {
+                const int j = idx[u] >= a.M1 ? 1 : 0;
+                r[u] += sparse_corr(T, b, spl, nsp, j, idx[u] - (j ? a.M1 : 0));
+            }
     }
-    if (have) {
-        if (T.r_out[j]) T.r_out[j][b * a.M[j] + k] = r;
-        amax(bv[j], bk[j], r, k);
+    unsigned long long key[2] = {0ull, 0ull};  // 0: no output (every real key is > 0)
+#pragma unroll
+    for (int u = 0; u < RED_E; ++u) {
+        if (idx[u] < 0) continue;
+        const int j = idx[u] >= a.M1 ? 1 : 0;
+        const int64_t k = idx[u] - (j ? a.M1 : 0);
+        if (T.r_out[j]) T.r_out[j][b * a.M[j] + k] = r[u];
+        const unsigned long long kk = pack_key(r[u], k);
+        if (j) key[1] = kk > key[1] ? kk : key[1];  // (no dynamic register-array index)
+        else key[0] = kk > key[0] ? kk : key[0];
     }
-    cta_keys(T, b, blockIdx.x, bv, bk);
+    __shared__ unsigned long long wk[RED_T / 32][2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        unsigned long long m = key[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ov = __shfl_xor_sync(0xffffffffu, m, o);
+            m = ov > m ? ov : m;
+        }
+        if (lane == 0) wk[warp][j] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        unsigned long long m = 0;
+#pragma unroll
+        for (int w = 0; w < RED_T / 32; ++w) m = wk[w][threadIdx.x] > m ? wk[w][threadIdx.x] : m;
+        T.ckeys[(b * T.nkey_cta + blockIdx.x) * 2 + threadIdx.x] = m;
+    }
     arrive_and_finish(T, b);
 }
 
@@ -989,7 +1043,7 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
         const int64_t klo = (int64_t)P * T.at0 * g.NT, kt = (int64_t)P * (T.at0 + T.n_atp) * g.NT;
         for (int j = 0; j < 2; ++j) nred_out += std::max<int64_t>(0, std::min<int64_t>(kt, (int64_t)P * g.NA[j]) - klo);
     }
-    const int nred_cta = (int)std::max<int64_t>(1, (nred_out + RED_T - 1) / RED_T);
+    const int nred_cta = (int)std::max<int64_t>(1, (nred_out + RED_T * RED_E - 1) / (RED_T * RED_E));
     T.nkey_cta = T.n_cr > 1 ? nred_cta : std::max(1, T.n_atp * T.n_cr);
     T.ckeys = (unsigned long long *)carve((size_t)batch * g.max_keys * 16);
     T.part = (int64_t *)carve(g.max_cr > 1 ? (size_t)batch * g.max_cr * (p->M1 + p->M2) * 8 : 0);

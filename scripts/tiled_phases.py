@@ -23,7 +23,8 @@ d = dbg.cpu().numpy().reshape(nmax, 8)
 d = d[d[:, 0] != 0]
 t0 = d[:, 0].min()
 sm = d[:, 7] >> 32
-passes = (d[:, 7] >> 8) & 0xFFFFFF
+passes = (d[:, 7] >> 8) & 0xFFFF
+nsp = (d[:, 7] >> 24) & 0xFF
 nl = d[:, 7] & 0xFF
 print(f'CTAs {len(d)}, SMs {len(np.unique(sm))}, passes p50 {np.median(passes)}, nl {np.bincount(nl)}')
 for name, v in [('start', d[:, 0] - t0), ('scan+alloc', d[:, 1] - d[:, 0]), ('loop', d[:, 2] - d[:, 1]),
@@ -34,3 +35,8 @@ for name, v in [('start', d[:, 0] - t0), ('scan+alloc', d[:, 1] - d[:, 0]), ('lo
                 ('exit', np.where(d[:, 4] > 0, d[:, 4] - t0, 0))]:
     v = v / 1e3
     print(f'{name:14s} us: min {v.min():7.2f} p50 {np.median(v):7.2f} max {v.max():7.2f}')
+epi = (d[:, 3] - d[:, 2]) / 1e3
+for lo, hi in [(0, 0), (1, 4), (5, 9), (10, 14), (15, 19), (20, 24)]:
+    m = (nsp >= lo) & (nsp <= hi)
+    if m.any():
+        print(f'nsp {lo:2d}..{hi:2d}: {m.sum():4d} CTAs, epilogue us p50 {np.median(epi[m]):6.2f} max {epi[m].max():6.2f}')
