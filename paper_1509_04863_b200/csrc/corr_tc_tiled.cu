@@ -76,6 +76,8 @@ struct TiledArgs {
     int32_t *spair;        // [batch][SPREC] the pair's entries, for tiled_reduce (main kernel CTA 0)
     int tsm;               // > 0: the main kernel stages the template (tsm >= K bytes) in shared memory
                            // for the sparse correction of a one-range pair
+    int csm;               // > 0: the epilogue warps also compute those corrections while the MMAs
+                           // run, into csm bytes of shared memory after the template (NTHR NT int32)
     int NT;                    // output blocks per tile
     unsigned long long *ckeys; // [batch][nkey_cta][2] packed (max r, lowest k) per CTA and modulus
     int nkey_cta;              // CTAs per pair that write ckeys (the pair's last kernel)
@@ -626,6 +628,39 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
         }
         asm volatile("bar.sync 1, %0;" ::"n"(NTHR) : "memory");  // the epilogue warps only
         tcor = tsh;
+        if (T.csm) {
+            // the corrections of this thread's NT outputs (the epilogue's (ar0, i, j) order),
+            // exact in int32 (see the epilogue), while the tensor pipe runs the loop; the
+            // epilogue then only adds them
+            int32_t *cb = reinterpret_cast<int32_t *>(sm + smem_bytes<NT>() + T.tsm);
+            const int qw = warp & 3, hw = warp >> 2;
+            const int kb = P * a0 + P - 1 - (32 * qw + lane);
+            const int Kt = (int)a.K;
+            for (int it = 0; it < NT / 16; ++it) {
+                const int k0 = kb + P * ((NT / 2) * hw + 8 * it);
+                int32_t c0[8], c1[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) c0[i] = c1[i] = 0;
+                for (int q = 0; q < nsp; ++q) {
+                    const int ti0 = spl.ent[3 * q] - k0;
+                    const int32_t ev = spl.ent[3 * q + 1];
+                    const bool jj = spl.ent[3 * q + 2] != 0;
+                    const int32_t e0 = jj ? 0 : ev, e1 = jj ? ev : 0;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int ti = ti0 - P * i;
+                        const int32_t tv = (unsigned)ti < (unsigned)Kt ? (int32_t)tsh[ti] : 0;
+                        c0[i] += e0 * tv;
+                        c1[i] += e1 * tv;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    cb[((it * 8 + i) * 2) * NTHR + tid] = c0[i];
+                    cb[((it * 8 + i) * 2 + 1) * NTHR + tid] = c1[i];
+                }
+            }
+        }
     }
     // every warp: all MMAs complete (fin completes exactly once: parity 0; a wait on
     // mdone's parity would return at once for a phase not yet begun).  Warps 0-7
@@ -673,7 +708,15 @@ __global__ void __launch_bounds__(TNTHR, TM_TILED_MINB) corr_tc_tiled(const Tile
                 }
             }
             const int k0 = kb + P * ar0;  // output of (ar0 + i): k0 + P i
-            if (nsp && T.n_cr == 1) {  // sparse pair: + sum_q e_q t(idx_q - k)
+            if (nsp && T.n_cr == 1 && T.csm) {  // corrections computed during the loop
+                const int32_t *cb = reinterpret_cast<const int32_t *>(sm + smem_bytes<NT>() + T.tsm);
+                const int it = (ar0 - (NT / 2) * hw) / 8;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    r[i][0] += cb[((it * 8 + i) * 2) * NTHR + tid];
+                    r[i][1] += cb[((it * 8 + i) * 2 + 1) * NTHR + tid];
+                }
+            } else if (nsp && T.n_cr == 1) {  // sparse pair: + sum_q e_q t(idx_q - k)
                 // |y| <= 524287 (tm_tc_tiled_plan: <= 4 limbs), so |e t| < 2^26 and the
                 // <= SPE = 24 terms of an output sum exactly in int32: one IMAD per term
                 // and modulus, no branches
@@ -1079,15 +1122,25 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     }
     const dim3 grid((unsigned)(T.n_atp * T.n_cr), (unsigned)batch);
     const dim3 gr((unsigned)nred_cta, (unsigned)batch);
+    // corrections during the loop: one-range sparse plans whose grid has at most one CTA
+    // per SM anyway (the buffer would otherwise cost the second resident CTA)
+    T.csm = 0;
+#ifndef TM_NO_CSM
+    if (T.tsm && T.n_cr == 1 && (int64_t)grid.x * batch <= p->num_sms) {
+        const int csm = NTHR * g.NT * 4;
+        const int base = (g.NT == 64 ? smem_bytes<64>() : smem_bytes<32>()) + T.tsm;
+        if (base + csm + 4096 <= 227 * 1024) T.csm = csm;  // (+ the static shared memory)
+    }
+#endif
     T.n_last = T.n_cr > 1 ? (int)gr.x : T.n_atp * T.n_cr;
     cudaError_t e = cudaSuccess;
     if (T.n_atp > 0) {
         if (g.NT == 64) {
-            const int sb = smem_bytes<64>() + T.tsm;
+            const int sb = smem_bytes<64>() + T.tsm + T.csm;
             e = tm_smem_attr((const void *)corr_tc_tiled<64>, sb);
             if (e == cudaSuccess) e = launch_pdl(corr_tc_tiled<64>, grid, dim3(TNTHR), sb, s, T);
         } else {
-            const int sb = smem_bytes<32>() + T.tsm;
+            const int sb = smem_bytes<32>() + T.tsm + T.csm;
             e = tm_smem_attr((const void *)corr_tc_tiled<32>, sb);
             if (e == cudaSuccess) e = launch_pdl(corr_tc_tiled<32>, grid, dim3(TNTHR), sb, s, T);
         }
