@@ -180,10 +180,32 @@ __global__ void __launch_bounds__(PREP_T, PREP_MINB) tiled_prep(const TiledArgs 
         // leftover output P NA_j (q = 0; q >= 1: the pass below): this piece's t(idx - k) y_j(idx)
         if (j ? nl1 : nl0) {
             const int64_t k = (int64_t)P * a.NA[j];
+            const int64_t ilo = i0 - k;  // template index of the piece's first entry
+            if (ilo >= 0 && ilo + 16 <= a.K) {
+                // the whole piece inside the template: 16 taps t[ilo, ilo + 16), summed in
+                // int32 (|t v| < 2^26: 4-limb plan bound) -- the partial-overlap loop below
+                // cost a quarter of this kernel's instructions (ncu, cfg4)
+                uint32_t tw[4];
+                const int8_t *tp = tr + ilo;
+                if ((((uintptr_t)tp) & 15) == 0) {
+                    const uint4 u = __ldg(reinterpret_cast<const uint4 *>(tp));
+                    tw[0] = u.x; tw[1] = u.y; tw[2] = u.z; tw[3] = u.w;
+                } else {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                const int64_t i = i0 + e - k;
-                if (i >= 0 && i < a.K) lacc += (int64_t)tr[i] * v[e];
+                    for (int q = 0; q < 4; ++q)
+                        tw[q] = (uint32_t)(uint8_t)tp[4 * q] | ((uint32_t)(uint8_t)tp[4 * q + 1] << 8) |
+                                ((uint32_t)(uint8_t)tp[4 * q + 2] << 16) | ((uint32_t)(uint8_t)tp[4 * q + 3] << 24);
+                }
+                int32_t s32 = 0;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) s32 += (int32_t)(int8_t)(tw[e >> 2] >> (8 * (e & 3))) * v[e];
+                lacc += s32;
+            } else if (ilo + 16 > 0 && ilo < a.K) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const int64_t i = ilo + e;
+                    if (i >= 0 && i < a.K) lacc += (int64_t)tr[i] * v[e];
+                }
             }
         }
         if (T.sparse) {  // record the entries outside int8 (invalid lanes hold 0); one atomic per
@@ -227,22 +249,30 @@ __global__ void __launch_bounds__(PREP_T, PREP_MINB) tiled_prep(const TiledArgs 
         if (!valid) continue;
         if ((tid & 15) == 0) T.bmag[b * T.S + s] = (uint8_t)min(need, 255);
         const int64_t roff = (int64_t)h * 32 * T.S + 16 * (2 * s + j);
-        for (int p = 0; p < T.np; ++p) {
-            // plane p: 0 -> v; 1 + l (l <= lmax-2) -> (v >> 4l) & 15; lmax - 1 + l -> v >> 4l
-            const int kind = p == 0 ? 0 : (p <= T.lmax - 1 ? 1 : 2);
-            const int sh = kind == 1 ? 4 * (p - 1) : kind == 2 ? 4 * (p - T.lmax + 1) : 0;
+        // plane p: 0 -> v clamped to int8; 1 + l (l <= lmax-2) -> (v >> 4l) & 15;
+        // lmax - 1 + l (l >= 1) -> v >> 4l (pack4 keeps the low byte); one loop per kind
+        {
             uint32_t wd[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                int32_t c[4];
+            for (int q = 0; q < 4; ++q)
+                wd[q] = pack4(clamp8(v[4 * q]), clamp8(v[4 * q + 1]), clamp8(v[4 * q + 2]), clamp8(v[4 * q + 3]));
+            *reinterpret_cast<uint4 *>(pl + roff) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        }
+        for (int l = 0; l < T.lmax - 1; ++l) {
+            const int sh = 4 * l;
+            uint32_t wd[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int32_t x = v[4 * q + e] >> sh;
-                    c[e] = kind == 1 ? (x & 15) : kind == 0 ? clamp8(x) : x;  // plane 0: y clamped to int8
-                }
-                wd[q] = pack4(c[0], c[1], c[2], c[3]);
-            }
-            *reinterpret_cast<uint4 *>(pl + p * pstride + roff) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+            for (int q = 0; q < 4; ++q)
+                wd[q] = pack4(v[4 * q] >> sh, v[4 * q + 1] >> sh, v[4 * q + 2] >> sh, v[4 * q + 3] >> sh) & 0x0F0F0F0Fu;
+            *reinterpret_cast<uint4 *>(pl + (1 + l) * pstride + roff) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        }
+        for (int l = 1; l < T.lmax; ++l) {
+            const int sh = 4 * l;
+            uint32_t wd[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                wd[q] = pack4(v[4 * q] >> sh, v[4 * q + 1] >> sh, v[4 * q + 2] >> sh, v[4 * q + 3] >> sh);
+            *reinterpret_cast<uint4 *>(pl + (T.lmax - 1 + l) * pstride + roff) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
         }
     }
 
