@@ -78,6 +78,10 @@ def parse():
     ap.add_argument("--fused-reduce", action="store_true",
                     help="cfg5, world > 1: combine the partial folds in the fold epilogue (tm_fold_reduce into "
                          "symmetric memory / NVLS multicast, SURVEY 8(f) f4(iii)) instead of an NCCL all-reduce")
+    ap.add_argument("--pipeline", type=int, default=0,
+                    help="staged paths on one GPU: buffer sets of the two-stream step pipeline (tm.Pipeline / "
+                         "SingleSignal(depth=)); 1 = every step strictly on one stream; 0 = the measured-best "
+                         "default (3 for the single signal, 2 for batches)")
     ap.add_argument("--ref-seconds", type=float, default=150.0,
                     help="--impl reference: CPU budget of the timed steps (each step is whole pairs)")
     return ap.parse_args()
@@ -344,16 +348,32 @@ def main():
     k = torch.empty(B, dtype=torch.int64, device=dev)
     torch.cuda.synchronize()
 
+    path = plan.run_path(B)
+    # staged paths: consecutive steps pipelined over two streams (the fold of step i+1
+    # concurrent with the correlation of step i; tm.Pipeline).  The fused path
+    # overlaps the two inside its one kernel.
+    if args.pipeline == 0:
+        args.pipeline = 2
+    pipe = tm.Pipeline(plan, B, depth=args.pipeline, device=dev) if args.pipeline > 1 and path in (0, 1) else None
+
     def step():
-        plan.run(x, t, residues=residues, k=k, ws=ws, stream=stream)
+        if pipe is not None:
+            pipe.step(x, t, stream=stream)
+        else:
+            plan.run(x, t, residues=residues, k=k, ws=ws, stream=stream)
+
+    def drain():
+        if pipe is not None:
+            pipe.drain(stream)
 
     for _ in range(max(args.warmup, 3)):
         step()
+    drain()
     torch.cuda.synchronize()
 
     # ---- timed region: K steps.  Stage events (tm_profile_events) on every
     # EV_EVERY-th step only: each event record costs ~2.7 us of GPU time.
-    path = plan.run_path(B)
+    # (pipelined: the sampled steps run tm_run on the caller's stream, which records the marks)
     nev = 2 if path == 2 else 5   # fused: before / after the one kernel
     ev_steps = [i for i in range(args.steps) if i % EV_EVERY == 0] if not args.no_stage_events else []
     ev = {i: [torch.cuda.Event(enable_timing=True) for _ in range(nev)] for i in ev_steps}
@@ -371,12 +391,14 @@ def main():
         h0 = time.perf_counter()
         for i in range(args.steps):
             if i in ev:
+                drain()   # the sampled step runs alone, in order on the caller's stream
                 keep = tm.profile_events(ev[i])
-                step()
+                plan.run(x, t, residues=residues, k=k, ws=ws, stream=stream)
                 tm.profile_events(None)
             else:
                 step()
         host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
+        drain()
         stop.record(stream)
         torch.cuda.synchronize()
     launches = tm.launch_count() - launches0
@@ -406,8 +428,14 @@ def main():
     for i in range(args.steps):
         step()
         bnd[i + 1].record(stream)
+    drain()
     torch.cuda.synchronize()
     per_step = [bnd[i].elapsed_time(bnd[i + 1]) for i in range(args.steps)]
+    if pipe is not None:   # the pipelined steps' results equal the one-stream tm_run's
+        rp, kp = pipe._slots[pipe.last_slot]["residues"], pipe._slots[pipe.last_slot]["k"]
+        if ev:
+            assert torch.equal(kp, k) and torch.equal(rp, residues), "pipelined step differs from tm_run"
+        residues, k = rp, kp
     ceiling = read_ceiling(tm, x, stream)
 
     # ---- end to end through tm_run_host: pinned host inputs, H2D + compute + D2H per step
@@ -481,10 +509,13 @@ def main():
                    "l2": f"no flush: per-step input {B * N * bx / 2**30:.2f} GiB > 126 MB L2"},
         "roofline": roofline_block("hbm", achieved, fold_ms, fold_bytes, kernel, traffic, ceiling),
         "run_path": tm.RUN_PATHS.get(path, str(path)),
+        "pipeline": (f"depth {args.pipeline}: the fold of step i+1 (caller's stream) concurrent with the correlation "
+                     f"of step i (side stream), tm.Pipeline" if pipe is not None else "none (one stream)"),
         "stage_ms": ({"fused_kernel": stage_mean[0]} if nev == 2 else
                      {"fold": stage_mean[0], "fold_template": stage_mean[1], "correlate_argmax": stage_mean[2],
                       "crt": stage_mean[3]}),
-        "stage_events": f"on {len(ev)} of {args.steps} timed steps (every {EV_EVERY}th)",
+        "stage_events": f"on {len(ev)} of {args.steps} timed steps (every {EV_EVERY}th)"
+                        + ("; a sampled step runs tm_run alone on the caller's stream after a drain" if pipe else ""),
         "host_enqueue_ms_per_step": host_ms,
         "step_hbm_frac": (B * N * bx / (ms_max / args.steps * 1e-3) / 1e9) / peak,
         "step_hbm": {kk: B * N * bx / (ms_max / args.steps * 1e-3) / 1e9 / v
@@ -522,13 +553,17 @@ def run_single_signal(args, wl, rank, world, local, dev):
     if args.fused_reduce and world > 1:
         from paper_1509_04863_b200.single import SymmReducer
         reducer = SymmReducer()
-    ss = SingleSignal(plan, rank, world, device=dev, reducer=reducer)
+    # one GPU: consecutive signals pipelined over two streams (SingleSignal(depth=)); with
+    # ranks every step stays on one stream, the collectives between its stages
+    depth = (args.pipeline or 3) if world == 1 and reducer is None else 1
+    ss = SingleSignal(plan, rank, world, device=dev, reducer=reducer, depth=depth)
     off, ln = ss.offset, ss.length
     x, t, k0 = plan.generate(0, 1, wl["noise"], offset=off, length=ln, device=dev)
     torch.cuda.synchronize()
 
     for _ in range(max(args.warmup, 3)):
         ss.step(x, t, stream=stream)
+    ss.drain(stream)
     torch.cuda.synchronize()
     # stage events on every EV_EVERY-th timed step only (an event between two launches
     # ends their PDL overlap: with events at every step the cfg5 step read 0.376 ms
@@ -546,7 +581,13 @@ def run_single_signal(args, wl, rank, world, local, dev):
     with ClockSampler(local) as clocks:
         start.record(stream)
         for i in range(args.steps):
-            ss.step(x, t, stream=stream, events=ev.get(i))
+            if i in ev:   # the sampled step runs alone (pipelined: no other step's kernels beside it)
+                ss.drain(stream)
+                ss.step(x, t, stream=stream, events=ev[i])
+                ss.drain(stream)
+            else:
+                ss.step(x, t, stream=stream)
+        ss.drain(stream)
         stop.record(stream)
         torch.cuda.synchronize()
     launches = tm.launch_count() - l0
@@ -563,6 +604,7 @@ def run_single_signal(args, wl, rank, world, local, dev):
     for i in range(args.steps):
         ss.step(x, t, stream=stream)
         bnd[i + 1].record(stream)
+    ss.drain(stream)
     torch.cuda.synchronize()
     per_step = [bnd[i].elapsed_time(bnd[i + 1]) for i in range(args.steps)]
     res_dev, k_dev = ss.residues.clone(), ss.k.clone()
@@ -583,6 +625,7 @@ def run_single_signal(args, wl, rank, world, local, dev):
         for _ in range(args.e2e_steps):
             xd.copy_(xh, non_blocking=True)
             _, kk = ss.step(xd, t, stream=stream)
+            ss.drain(stream)   # (pipelined: k is written on the side stream)
             kh.copy_(kk, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -616,12 +659,15 @@ def run_single_signal(args, wl, rank, world, local, dev):
                                           f" + in-place all-reduce of y1||y2 ({ss.reduce_bytes} B)")
                                          + " + correlation split by output blocks + all-reduce MAX of 16 B keys"
                                          if world > 1 else ""),
+                       "pipeline": (f"depth {depth}: the fold of step i+1 (caller's stream) concurrent with the "
+                                    f"correlation of step i (side stream)" if depth > 1 else "none (one stream)"),
                        "l2": "no flush: per-rank input > 126 MB L2"},
             "roofline": roofline_block("hbm", achieved, fold_ms, fold_bytes,
                                        "tm_fold (zero_i32 + fold_pm1_tma + fold_finalize)",
                                        traffic_of(args.workload) if world == 1 else None, ceiling),
             "stage_ms": {"fold": st[0], "allreduce": st[1], "correlate_match": st[2]},
-            "stage_events": f"on {len(ev)} of {args.steps} timed steps (every {EV_EVERY}th)",
+            "stage_events": f"on {len(ev)} of {args.steps} timed steps (every {EV_EVERY}th)"
+                            + ("; a sampled step runs alone, drained before and after" if depth > 1 else ""),
             "step_ms": step_stats(per_step, ms_max / args.steps),
             "step_hbm": {k: step_bytes / (ms_max / args.steps * 1e-3) / 1e9 / v
                          for k, v in peak_denominators(ceiling).items()},

@@ -14,7 +14,8 @@ import os
 
 from ._binding import (TM_BINARY, TM_CORR_NTT, TM_CORR_TC, TM_F32, TM_I8, Plan, TMError, lib, lib_path,  # noqa: F401
                        EXPORTED_SYMBOLS, RUN_PATHS, MultiPlan, crt_multi, launch_count, profile_events, probe_read_bw)
+from .pipeline import Pipeline  # noqa: F401
 from .single import SingleSignal  # noqa: F401
 
 __all__ = ["Plan", "MultiPlan", "crt_multi", "TMError", "TM_I8", "TM_F32", "TM_BINARY", "TM_CORR_NTT", "TM_CORR_TC", "lib", "lib_path", "EXPORTED_SYMBOLS",
-           "launch_count", "profile_events", "probe_read_bw", "SingleSignal"]
+           "launch_count", "profile_events", "probe_read_bw", "SingleSignal", "Pipeline"]

@@ -58,31 +58,42 @@ t_st = timeit(staged_one_stream)
 same_st = bool(torch.equal(KK[0], k_ref))
 
 out = [f"N={N} K={K} B={B} {dtype}: tm_run {t_run:.4f} ms, fold+correlate_match one stream {t_st:.4f} (k same {same_st})"]
-for prio in (0, -1):
-    s1 = torch.cuda.Stream(priority=prio)
-    folded = [torch.cuda.Event() for _ in range(2)]
-    done = [torch.cuda.Event() for _ in range(2)]
+def variant(nbuf, fold_prio, corr_prio):
+    global s0
+    sf = torch.cuda.Stream(priority=fold_prio)
+    s1 = torch.cuda.Stream(priority=corr_prio)
+    while len(Y1) < nbuf:
+        Y1.append(torch.empty_like(Y1[0])); Y2.append(torch.empty_like(Y2[0]))
+        WF.append(plan.workspace(B)); WC.append(plan.workspace(B))
+        R.append(torch.empty_like(R[0])); KK.append(torch.empty_like(KK[0]))
+    folded = [torch.cuda.Event() for _ in range(nbuf)]
+    done = [torch.cuda.Event() for _ in range(nbuf)]
     state = {"i": 0}
     for d in done:
         d.record(s1)
 
     def step():
-        b = state["i"] & 1
+        b = state["i"] % nbuf
         state["i"] += 1
-        s0.wait_event(done[b])  # buffers b are free once step i-2's correlation has read them
-        plan.fold(x, y1=Y1[b], y2=Y2[b], ws=WF[b], stream=s0)
-        folded[b].record(s0)
+        sf.wait_event(done[b])  # buffers b are free once step i-nbuf's correlation has read them
+        plan.fold(x, y1=Y1[b], y2=Y2[b], ws=WF[b], stream=sf)
+        folded[b].record(sf)
         s1.wait_event(folded[b])
         plan.correlate_match(Y1[b], Y2[b], t, residues=R[b], k=KK[b], ws=WC[b], stream=s1)
         done[b].record(s1)
 
     def drain():
-        s0.wait_event(done[0])
-        s0.wait_event(done[1])
+        for d in done:
+            s0.wait_event(d)
 
     for kk in KK:
         kk.fill_(-7)
+    sf.wait_stream(s0)
     t_p = timeit(step, drain)
-    same = bool(torch.equal(KK[0], k_ref) and torch.equal(KK[1], k_ref))
-    out.append(f"pipelined (side stream priority {prio}) {t_p:.4f} ms (k same {same})")
-print("; ".join(out), flush=True)
+    same = all(bool(torch.equal(kk, k_ref)) for kk in KK[:nbuf])
+    out.append(f"pipelined nbuf {nbuf} fold prio {fold_prio} corr prio {corr_prio}: {t_p:.4f} ms (k same {same})")
+
+
+for nb, fp, cp in ((2, 0, 0), (3, 0, 0), (2, -1, 0), (3, -1, 0), (2, 0, -1)):
+    variant(nb, fp, cp)
+print("\n  ".join(out), flush=True)

@@ -190,6 +190,52 @@ def _single_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _single_depth_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import tmgen
+        from paper_1509_04863_b200.single import SingleSignal
+        N, K = 64 * 30, 64
+        ss = SingleSignal(OraclePlan(N, K), rank, world, device="cpu", depth=2)
+        ok, held = True, []
+        for i in range(3):          # three different signals through two rotating buffer sets
+            x = tmgen.signal(21 + i, 0, N)
+            t = tmgen.template(21 + i, 0, N, K, 0.05)
+            xc = torch.from_numpy(x[ss.offset:ss.offset + ss.length].copy()).view(1, -1)
+            res, k = ss.step(xc, torch.from_numpy(t).view(1, -1))
+            o = oracle.ftm(x, t)
+            ok = ok and (np.array_equal(ss.y1[0].numpy(), o["y1"]) and np.array_equal(ss.y2[0].numpy(), o["y2"])
+                         and tuple(res[0].tolist()) == o["residues"] and int(k[0]) == o["k"])
+            held.append((k, o["k"]))
+        # step 1's result (slot 1) is still intact after step 2 wrote slot 0
+        ok = ok and int(held[1][0][0]) == held[1][1] and held[0][0] is held[2][0]
+        ss.drain()
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_single_signal_depth_rotates_buffers_gloo():
+    """SingleSignal(depth=2) on two gloo ranks: the buffer sets rotate, every step's
+    all-reduce and keys use the current set, and a result stays valid until its
+    set comes round again."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_single_depth_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_single_signal_wiring_gloo(world):
     """Each rank folds its chunk, the flat y1 || y2 buffer is all-reduced in place,
