@@ -23,7 +23,10 @@
  *   - A failed match is data, not an error: k = -1 (NO_MATCH, reading C9 of
  *     DESIGN.md) with the residues still reported.
  *   - Plans are immutable after creation; one plan may be used concurrently
- *     on several streams.
+ *     on several streams, each call with its own workspace and output
+ *     buffers (the Python Pipeline / SingleSignal(depth=) rely on this: the
+ *     tm_fold of step i+1 on one stream beside the tm_correlate_match of
+ *     step i on another).
  *
  * Element types
  *   TM_I8 : x, t int8;  y1, y2 int32 (exact);  r1, r2 int64 (exact).

@@ -7,6 +7,9 @@ timeout 600 python bench.py > gpurun_out/bench_cfg5_final.json 2> gpurun_out/ben
 for w in cfg2 cfg3 cfg4a cfg4b cfg4 cfg4c cfg4d t2 cfg1; do
   timeout 400 python bench.py --workload $w --no-cfg1 > gpurun_out/bench_${w}_final.json 2> gpurun_out/bench_${w}_final.err; echo "$w $(python scripts/show_bench.py gpurun_out/bench_${w}_final.json | cut -c1-170)"
 done
+for w in cfg5 cfg4 cfg3; do
+  timeout 400 python bench.py --workload $w --pipeline 1 --no-cfg1 --no-cpu-baseline > gpurun_out/bench_${w}_onestream_final.json 2> gpurun_out/bench_${w}_onestream_final.err; echo "$w one stream $(python scripts/show_bench.py gpurun_out/bench_${w}_onestream_final.json | cut -c1-170)"
+done
 timeout 900 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_reference_final.json 2> gpurun_out/bench_reference_final.err; echo "ref rc $?"
 timeout 600 python scripts/table1.py > gpurun_out/table1.json 2> gpurun_out/table1.err; echo "table1 rc $?"
 timeout 600 python scripts/table2.py > gpurun_out/table2.json 2> gpurun_out/table2.err; echo "table2 rc $?"
