@@ -890,7 +890,11 @@ int tm_fold_tma(const tm_plan_s *p, const void *x, int64_t ldx, int64_t batch, i
 #ifndef TM_FOLD_MINB
 #define TM_FOLD_MINB 1  // A/B: 2 = two (smaller) fold CTAs per SM
 #endif
-    const int64_t slots = (int64_t)p->num_sms * (dual ? 2 : TM_FOLD_MINB);
+    int64_t slots = (int64_t)p->num_sms * (dual ? 2 : TM_FOLD_MINB);
+    {   // A/B: cap on the fold's CTAs (SMs left half free for a concurrently resident correlation)
+        const char *env_cap = getenv("TM_FOLD_SLOTS");
+        if (env_cap && atoll(env_cap) > 0 && atoll(env_cap) < slots) slots = atoll(env_cap);
+    }
     int64_t grid = a.n_items < slots ? a.n_items : slots;
     if (a.contig) {
         const int64_t units = (a.n_segs * a.rows + 15) / 16;
