@@ -852,7 +852,8 @@ __global__ void __launch_bounds__(RED_T) tiled_reduce(const TiledArgs T) {
     // over this launch's MMA outputs only (the tiles [at0, at0 + n_atp) of a split
     // correlation; leftovers: finish_pair): k in [klo, khi_j) per modulus
     const int64_t klo = (int64_t)P * T.at0 * T.NT, kt = (int64_t)P * (T.at0 + T.n_atp) * T.NT;
-    const int64_t kh0 = min(kt, (int64_t)P * a.NA[0]), kh1 = min(kt, (int64_t)P * a.NA[1]);
+    // (NA_j counts a last partial block with more than MAXLEFT outputs: its outputs end at M_j)
+    const int64_t kh0 = min(kt, min((int64_t)P * a.NA[0], a.M[0])), kh1 = min(kt, min((int64_t)P * a.NA[1], a.M[1]));
     const int64_t n0 = max((int64_t)0, kh0 - klo), n1 = max((int64_t)0, kh1 - klo);
     const int64_t e0 = ((int64_t)blockIdx.x * RED_T + threadIdx.x) * RED_E;
     const PT *pp = reinterpret_cast<const PT *>(T.part) + b * T.n_cr * ML;
@@ -1114,7 +1115,8 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     int64_t nred_out = 0;  // the reduce kernel's outputs: this launch's tiles' MMA outputs
     {
         const int64_t klo = (int64_t)P * T.at0 * g.NT, kt = (int64_t)P * (T.at0 + T.n_atp) * g.NT;
-        for (int j = 0; j < 2; ++j) nred_out += std::max<int64_t>(0, std::min<int64_t>(kt, (int64_t)P * g.NA[j]) - klo);
+        for (int j = 0; j < 2; ++j)
+            nred_out += std::max<int64_t>(0, std::min<int64_t>(kt, std::min<int64_t>((int64_t)P * g.NA[j], j ? p->M2 : p->M1)) - klo);
     }
     const int nred_cta = (int)std::max<int64_t>(1, (nred_out + RED_T * RED_E - 1) / (RED_T * RED_E));
     T.nkey_cta = T.n_cr > 1 ? nred_cta : std::max(1, T.n_atp * T.n_cr);

@@ -319,6 +319,29 @@ def test_tc_engine_limbs_and_ragged_shapes(tm, N, K, M, B):
     check_int_pairs(tm, plan, x_h, t_h, range(B))
 
 
+@pytest.mark.parametrize("N,K,M,B,binary", [(558 * 3900, 3900, 0, 2, False),    # M1, M2 leave 60 / 61 outputs
+                                            (3000 * 5000, 5000, 0, 3, True),     # in a last partial block
+                                            (3024528, 5919, 6812, 2, False)])
+def test_tiled_ragged_last_block_several_template_ranges(tm, N, K, M, B, binary):
+    """Tiled tensor-core correlation with several template ranges (K of a few thousand
+    on few pairs) and M_j not a multiple of 128: the last partial block's outputs end at
+    M_j.  (Regression: tiled_reduce took P * NA_j as the limit, so outputs k in [M_j,
+    P * NA_j) of pair b were compared in the argmax and written over the first outputs
+    of pair b + 1 -- found by scripts/sweep_wide.py, seeds 97 / 50.)  Run twice: the
+    overwrite raced with pair b + 1's own stores."""
+    plan = tm.Plan(N, K, M=M, seed=9, binary=binary)
+    assert plan.corr_engine == 1
+    rng = np.random.default_rng(N + K)
+    if binary:
+        x_h = (1 - 2 * rng.integers(0, 2, (B, N))).astype(np.int8)
+    else:
+        x_h = rng.integers(-128, 128, (B, N)).astype(np.int8)
+    k0 = rng.integers(0, N, B)
+    t_h = np.stack([x_h[b][(k0[b] + np.arange(K)) % N] for b in range(B)]).astype(np.int8)
+    for _ in range(2):
+        check_int_pairs(tm, plan, x_h, t_h, range(B))
+
+
 @pytest.mark.parametrize("tiled", ["0", "1"])
 @pytest.mark.parametrize("N,K,M,B,binary", [(2 ** 14, 200, 0, 3, False), (4096, 256, 0, 8, True),
                                             (2 ** 18, 4096, 0, 3, True), (2 ** 20, 8192, 0, 2, True),
