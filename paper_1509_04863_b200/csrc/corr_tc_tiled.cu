@@ -1120,6 +1120,10 @@ int tm_tc_tiled_correlate(const tm_plan_s *p, const void *y1, const void *y2, in
     }
     const int nred_cta = (int)std::max<int64_t>(1, (nred_out + RED_T * RED_E - 1) / (RED_T * RED_E));
     T.nkey_cta = T.n_cr > 1 ? nred_cta : std::max(1, T.n_atp * T.n_cr);
+    // a part of a split correlation without tiles launches neither the main kernel nor
+    // tiled_reduce: nobody writes CTA keys, so finish_pair must read none (it took one
+    // uninitialised key of the workspace for a real one)
+    if (T.n_atp == 0) T.nkey_cta = 0;
     T.ckeys = (unsigned long long *)carve((size_t)batch * g.max_keys * 16);
     T.part = (int64_t *)carve(g.max_cr > 1 ? (size_t)batch * g.max_cr * (p->M1 + p->M2) * 8 : 0);
     T.bmag = (uint8_t *)carve((size_t)batch * g.S);

@@ -758,8 +758,12 @@ def test_split_correlation_parts_max_equals_whole(tm, nparts):
     x, t = up(x_h), up(t_h)
     y1, y2 = plan.fold(x)
     keys = None
+    ws = plan.workspace(B)
     for part in range(nparts):
-        kp = plan.correlate_match_part(y1, y2, t, part, nparts)
+        # a workspace full of stale bytes: nothing may be read before it is written
+        # (regression: a part without tiles took an unwritten CTA key for a real one)
+        ws.fill_(0x7F)
+        kp = plan.correlate_match_part(y1, y2, t, part, nparts, ws=ws)
         keys = kp.clone() if keys is None else torch.maximum(keys, kp)
     res, k = plan.match_keys(keys)
     res_w, k_w = plan.correlate_match(y1, y2, t)
@@ -769,6 +773,36 @@ def test_split_correlation_parts_max_equals_whole(tm, nparts):
     for b in range(B):
         o = oracle.ftm(x_h[b], t_h[b], want_vectors=False)
         assert tuple(res[b].tolist()) == o["residues"] and int(k[b]) == o["k"]
+
+
+@pytest.mark.parametrize("N,K,M1,nparts", [(167073, 661, 2304, 7), (128 * 9 * 150, 1000, 128 * 9, 5),
+                                           (128 * 40 * 90 - 77, 5000, 128 * 40, 3)])
+def test_split_correlation_general_int8_stale_workspace(tm, N, K, M1, nparts):
+    """The split correlation on general int8 data (several limbs / the sparse single-limb
+    mode), more parts than tiles, M1 a multiple of 128 (one leftover output for M2), every
+    call on a workspace full of stale bytes -- scripts/sweep_extra.py's shapes."""
+    B = 2
+    plan = tm.Plan(N, K, M=M1, seed=3, binary=False)
+    rng = np.random.default_rng(N)
+    x_h = rng.integers(-8, 9, (B, N)).astype(np.int8)
+    k0 = rng.integers(0, N, B)
+    t_h = np.stack([x_h[b][(k0[b] + np.arange(K)) % N] for b in range(B)]).astype(np.int8)
+    x, t = up(x_h), up(t_h)
+    y1, y2 = plan.fold(x)
+    ws = plan.workspace(B)
+    keys = None
+    for part in range(nparts):
+        ws.fill_(0x7F)
+        kp = plan.correlate_match_part(y1, y2, t, part, nparts, ws=ws)
+        keys = kp.clone() if keys is None else torch.maximum(keys, kp)
+    res, k = plan.match_keys(keys)
+    ws.fill_(0x7F)
+    res_w, k_w = plan.correlate_match(y1, y2, t, ws=ws)
+    torch.cuda.synchronize()
+    for b in range(B):
+        o = oracle.ftm(x_h[b], t_h[b], M=M1, want_vectors=False)
+        assert tuple(res[b].tolist()) == o["residues"] and int(k[b]) == o["k"], b
+        assert tuple(res_w[b].tolist()) == o["residues"] and int(k_w[b]) == o["k"], b
 
 
 # ------------------------------------------------------------- randomized sweep
