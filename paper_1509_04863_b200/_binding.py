@@ -169,6 +169,17 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
+# test hook (TM_WS_POISON=1): every workspace the binding allocates starts as 0x7F bytes,
+# so a kernel reading workspace memory it has not written shows up in the parity tests
+_POISON = bool(os.environ.get("TM_WS_POISON"))
+
+
+def _poisoned(buf):
+    if _POISON:
+        buf.fill_(0x7F)
+    return buf
+
+
 def _scratch(nbytes: int, device, stream):
     """A temporary device buffer used by a launch on `stream`: allocated while
     `stream` is current and recorded on it, so the caching allocator does not hand
@@ -180,6 +191,8 @@ def _scratch(nbytes: int, device, stream):
         st = stream
     with torch.cuda.stream(st):
         buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+        if _POISON:
+            buf.fill_(0x7F)
     buf.record_stream(st)
     return buf
 
@@ -234,7 +247,7 @@ class Plan:
     def workspace(self, batch: int, device="cuda"):
         import torch
         n = lib().tm_workspace_bytes(self._h, batch)
-        return torch.empty(max(int(n), 1), dtype=torch.uint8, device=device)
+        return _poisoned(torch.empty(max(int(n), 1), dtype=torch.uint8, device=device))
 
     def _tmp_ws(self, batch: int, device, stream):
         return _scratch(lib().tm_workspace_bytes(self._h, batch), device, stream)
@@ -451,7 +464,7 @@ class MultiPlan:
     def workspace(self, batch: int, device="cuda"):
         import torch
         n = lib().tm_mplan_workspace_bytes(self._h, batch)
-        return torch.empty(max(int(n), 1), dtype=torch.uint8, device=device)
+        return _poisoned(torch.empty(max(int(n), 1), dtype=torch.uint8, device=device))
 
     def run(self, x, t, residues=None, k=None, ws=None, stream=None):
         """Steps 3-7 per modulus, then Garner's CRT: (residues [batch][alpha], k [batch])."""

@@ -27,3 +27,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:"til
 C="python bench.py --workload cfg2 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-cfg1"
 $C > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fold_pm1_tma" -s 3 -c 1 -o gpurun_out/tr_cfg2 $C > gpurun_out/tr_cfg2.log 2>&1; echo "ncu full cfg2 rc $?"
+# randomized parity sweeps against the oracle on the same build (bounded)
+timeout 420 python scripts/sweep_many.py 0 4000 > gpurun_out/sweep_many.log 2>&1; echo "sweep many: $(tail -1 gpurun_out/sweep_many.log)"
+timeout 400 python scripts/sweep_wide.py 0 1200 > gpurun_out/sweep_wide.log 2>&1; echo "sweep wide: $(tail -1 gpurun_out/sweep_wide.log)"
+timeout 300 python scripts/sweep_extra.py 400 > gpurun_out/sweep_extra.log 2>&1; echo "sweep extra: $(tail -1 gpurun_out/sweep_extra.log)"
