@@ -171,12 +171,16 @@ def _ptr(t):
 
 # test hook (TM_WS_POISON=1): every workspace the binding allocates starts as 0x7F bytes,
 # so a kernel reading workspace memory it has not written shows up in the parity tests
+# (TM_WS_POISON=0xFF etc. picks the byte)
 _POISON = bool(os.environ.get("TM_WS_POISON"))
+_POISON_BYTE = (int(os.environ.get("TM_WS_POISON") or "0", 0) & 0xFF) if _POISON else 0
+if _POISON and _POISON_BYTE <= 1:
+    _POISON_BYTE = 0x7F
 
 
 def _poisoned(buf):
     if _POISON:
-        buf.fill_(0x7F)
+        buf.fill_(_POISON_BYTE)
     return buf
 
 
@@ -192,7 +196,7 @@ def _scratch(nbytes: int, device, stream):
     with torch.cuda.stream(st):
         buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
         if _POISON:
-            buf.fill_(0x7F)
+            buf.fill_(_POISON_BYTE)
     buf.record_stream(st)
     return buf
 

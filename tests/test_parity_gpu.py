@@ -760,9 +760,10 @@ def test_split_correlation_parts_max_equals_whole(tm, nparts):
     keys = None
     ws = plan.workspace(B)
     for part in range(nparts):
-        # a workspace full of stale bytes: nothing may be read before it is written
+        # a workspace full of stale 0xFF bytes (as a key: the largest r): nothing may be read
+        # before it is written
         # (regression: a part without tiles took an unwritten CTA key for a real one)
-        ws.fill_(0x7F)
+        ws.fill_(0xFF)
         kp = plan.correlate_match_part(y1, y2, t, part, nparts, ws=ws)
         keys = kp.clone() if keys is None else torch.maximum(keys, kp)
     res, k = plan.match_keys(keys)
@@ -780,7 +781,7 @@ def test_split_correlation_parts_max_equals_whole(tm, nparts):
 def test_split_correlation_general_int8_stale_workspace(tm, N, K, M1, nparts):
     """The split correlation on general int8 data (several limbs / the sparse single-limb
     mode), more parts than tiles, M1 a multiple of 128 (one leftover output for M2), every
-    call on a workspace full of stale bytes -- scripts/sweep_extra.py's shapes."""
+    call on a workspace full of stale 0xFF bytes -- scripts/sweep_extra.py's shapes."""
     B = 2
     plan = tm.Plan(N, K, M=M1, seed=3, binary=False)
     rng = np.random.default_rng(N)
@@ -792,11 +793,11 @@ def test_split_correlation_general_int8_stale_workspace(tm, N, K, M1, nparts):
     ws = plan.workspace(B)
     keys = None
     for part in range(nparts):
-        ws.fill_(0x7F)
+        ws.fill_(0xFF)
         kp = plan.correlate_match_part(y1, y2, t, part, nparts, ws=ws)
         keys = kp.clone() if keys is None else torch.maximum(keys, kp)
     res, k = plan.match_keys(keys)
-    ws.fill_(0x7F)
+    ws.fill_(0xFF)
     res_w, k_w = plan.correlate_match(y1, y2, t, ws=ws)
     torch.cuda.synchronize()
     for b in range(B):
