@@ -60,6 +60,14 @@ METRIC = "signal Gsamples/s matched (1/2/4/8 B200) and % of HBM roofline; match 
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
+def sample_steps(steps: int):
+    """Timed steps that carry stage events: every EV_EVERY-th (at least two samples when
+    steps >= 4), never step 0 (the first step after the warm-up's synchronize is not
+    representative of the steady state)."""
+    every = min(EV_EVERY, max(2, steps // 2))
+    return [i for i in range(steps) if i % every == every - 1] or [steps - 1]
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -375,7 +383,7 @@ def main():
     # EV_EVERY-th step only: each event record costs ~2.7 us of GPU time.
     # (pipelined: the sampled steps run tm_run on the caller's stream, which records the marks)
     nev = 2 if path == 2 else 5   # fused: before / after the one kernel
-    ev_steps = [i for i in range(args.steps) if i % EV_EVERY == 0] if not args.no_stage_events else []
+    ev_steps = sample_steps(args.steps) if not args.no_stage_events else []
     ev = {i: [torch.cuda.Event(enable_timing=True) for _ in range(nev)] for i in ev_steps}
     for e5 in ev.values():  # torch creates the CUDA event lazily on first record
         for e in e5:
@@ -514,7 +522,7 @@ def main():
         "stage_ms": ({"fused_kernel": stage_mean[0]} if nev == 2 else
                      {"fold": stage_mean[0], "fold_template": stage_mean[1], "correlate_argmax": stage_mean[2],
                       "crt": stage_mean[3]}),
-        "stage_events": f"on {len(ev)} of {args.steps} timed steps (every {EV_EVERY}th)"
+        "stage_events": f"on {len(ev)} of {args.steps} timed steps (steps {sorted(ev)[:3]}...)"
                         + ("; a sampled step runs tm_run alone on the caller's stream after a drain" if pipe else ""),
         "host_enqueue_ms_per_step": host_ms,
         "step_hbm_frac": (B * N * bx / (ms_max / args.steps * 1e-3) / 1e9) / peak,
@@ -568,7 +576,7 @@ def run_single_signal(args, wl, rank, world, local, dev):
     # stage events on every EV_EVERY-th timed step only (an event between two launches
     # ends their PDL overlap: with events at every step the cfg5 step read 0.376 ms
     # instead of 0.357); the per-step spread comes from a second pass below
-    ev_steps = [i for i in range(args.steps) if i % EV_EVERY == 0]
+    ev_steps = sample_steps(args.steps)
     ev = {i: [torch.cuda.Event(enable_timing=True) for _ in range(4)] for i in ev_steps}
     for e4 in ev.values():  # torch creates the CUDA event lazily on first record
         for e in e4:
@@ -666,7 +674,7 @@ def run_single_signal(args, wl, rank, world, local, dev):
                                        "tm_fold (zero_i32 + fold_pm1_tma + fold_finalize)",
                                        traffic_of(args.workload) if world == 1 else None, ceiling),
             "stage_ms": {"fold": st[0], "allreduce": st[1], "correlate_match": st[2]},
-            "stage_events": f"on {len(ev)} of {args.steps} timed steps (every {EV_EVERY}th)"
+            "stage_events": f"on {len(ev)} of {args.steps} timed steps (steps {sorted(ev)[:3]}...)"
                             + ("; a sampled step runs alone, drained before and after" if depth > 1 else ""),
             "step_ms": step_stats(per_step, ms_max / args.steps),
             "step_hbm": {k: step_bytes / (ms_max / args.steps * 1e-3) / 1e9 / v
